@@ -1,0 +1,71 @@
+/* chimera_ck.h -- the C-ABI boundary of the Chimera-B200 build (libchimera.so).
+ *
+ * The reference (`pipesim`, /root/reference/proj) is a C++ library with no FFI; its
+ * public surface is the headers in proj/include/pipesim/.  This build keeps those
+ * C++ headers verbatim in include/pipesim/ (drop-in) and puts a thin extern "C"
+ * layer under them so that any host language (and our Python mirror) can bind
+ * plain pointers and sizes.  Each entry point names the reference interface it
+ * replaces.  See INTEGRATION.md for the bindings a reference user adds.
+ *
+ * Conventions:
+ *   - status: 0 ok, 2 invalid input (InvalidConfigError), 3 internal error
+ *     (CUDA/NCCL failure, missing activation, deadlock timeout);
+ *   - ck_last_error() returns the message of the calling thread's last failure;
+ *   - strings returned through `char**` are malloc'd: release with ck_free();
+ *   - the caller owns host buffers; a context (ck_toy_*, ck_gpt_*) owns all device
+ *     memory; one host thread drives a context (calls are not thread-safe).
+ *   - no torch types cross this boundary.
+ */
+#ifndef CHIMERA_CK_H
+#define CHIMERA_CK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CK_API __attribute__((visibility("default")))
+#else
+#define CK_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ common */
+CK_API const char* ck_last_error(void);
+CK_API void ck_free(void* p);
+
+/* ------------------------------------------------- host schedule layer (C++) */
+/* schedgen::generate (proj/include/pipesim/schedgen.hpp:92) + to_json(.., indent)
+ * (proj/include/pipesim/core.hpp:182).  JSON is the reference wire format. */
+CK_API int pipesim_generate(const char* config_json, const char* profile_json, int indent,
+                     char** out_json);
+/* validate_config (core.hpp:173); violations joined by '\n' (empty = valid). */
+CK_API int pipesim_validate_config(const char* config_json, const char* profile_json, char** out);
+/* analysis::validate_dependencies (analysis.hpp:41). */
+CK_API int pipesim_validate_dependencies(const char* schedule_json, char** out);
+/* analysis::bubble_ratio_per_worker (analysis.hpp:53) on the zero-comm timing. */
+CK_API int pipesim_bubble_ratio_per_worker(const char* schedule_json, const char* profile_json,
+                                    int64_t* num, int64_t* den, int cap);
+/* analysis::memory_profile (analysis.hpp:59). */
+CK_API int pipesim_memory_profile(const char* schedule_json, const char* profile_json, int* act_counts,
+                           int* weight_counts, double* act_bytes, double* weight_bytes,
+                           int* peak_worker, double* peak_bytes, int cap);
+/* dessim::simulate (dessim.hpp:58) + memory_trace peaks; policy 0 end-of-iteration,
+ * 1 eager-sync, 2 eager-sync-opt. */
+CK_API int pipesim_simulate(const char* schedule_json, const char* profile_json, int policy,
+                     int zero_comm, double eager_overhead, char** out_json);
+/* perfmodel::replicas_per_stage / critical_path / predict_T (perfmodel.hpp:61-75). */
+CK_API int pipesim_replicas_per_stage(const char* config_json);
+CK_API int pipesim_critical_path(const char* schedule_json, const char* profile_json, int* C_f,
+                          int* C_b);
+CK_API int pipesim_predict_T(const char* config_json, const char* profile_json, double* T);
+/* Issue order used by the executors: (worker, index) sorted by unit-tick start,
+ * the reference oracle's replay order (proj/src/oracle.cpp:312-327). */
+CK_API int pipesim_replay_order(const char* schedule_json, int* worker, int* index, int cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHIMERA_CK_H */
