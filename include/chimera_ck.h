@@ -65,6 +65,23 @@ CK_API int pipesim_predict_T(const char* config_json, const char* profile_json, 
  * the reference oracle's replay order (proj/src/oracle.cpp:312-327). */
 CK_API int pipesim_replay_order(const char* schedule_json, int* worker, int* index, int cap);
 
+/* ------------------------------------------ ToyModel executor (sm_100a, fp64) */
+/* oracle::run_iteration_traced (proj/include/pipesim/oracle.hpp:72): one iteration of
+ * the schedule on the current GPU; params are flat per stage [W_s (out x in), b_s];
+ * peak_stash[w] = peak live activation stashes of worker w (replica 0). */
+CK_API int ck_toy_run_iteration(const char* schedule_json, const int* dims, int n_dims,
+                                const double* params_in, const double* inputs,
+                                const double* targets, int batch, double lr, double* params_out,
+                                int* peak_stash, int cap);
+/* oracle::make_model / make_batch (oracle.hpp:44-45), host-side, bit-identical. */
+CK_API int ck_toy_make_model(const int* dims, int n_dims, uint64_t seed, double* params);
+CK_API int ck_toy_make_batch(const int* dims, int n_dims, int size, uint64_t seed,
+                             double* inputs, double* targets);
+/* oracle::sequential_sgd (oracle.hpp:56): plain mini-batch SGD on the GPU. */
+CK_API int ck_toy_sequential_sgd(const int* dims, int n_dims, const double* params_in,
+                                 const double* inputs, const double* targets, int batch,
+                                 double lr, double* params_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,77 @@
+// Shared CUDA helpers for the Chimera-B200 kernels (sm_100a only).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "capi_util.hpp"
+
+#define CK_CUDA(expr)                                                                   \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      throw chimera::capi::InternalError(std::string(#expr) + ": " + cudaGetErrorString(_e) + \
+                                         " (" __FILE__ ":" + std::to_string(__LINE__) + ")"); \
+  } while (0)
+
+namespace chimera::cuda {
+
+constexpr int kNumSMs = 148;  // B200
+
+inline int ceil_div(long long a, long long b) { return int((a + b - 1) / b); }
+
+// The product path refuses to run anywhere but on an sm_100 device.
+inline void require_sm100() {
+  int dev = 0;
+  CK_CUDA(cudaGetDevice(&dev));
+  cudaDeviceProp p{};
+  CK_CUDA(cudaGetDeviceProperties(&p, dev));
+  if (p.major != 10)
+    throw chimera::capi::InternalError("Chimera-B200 kernels require an sm_100 (B200) device, got sm_" +
+                                       std::to_string(p.major * 10 + p.minor));
+}
+
+__device__ __forceinline__ float bf2f(__nv_bfloat16 x) { return __bfloat162float(x); }
+__device__ __forceinline__ __nv_bfloat16 f2bf(float x) { return __float2bfloat16_rn(x); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum for blockDim.x a multiple of 32 (<= 1024); `scratch` >= 32 floats.
+__device__ __forceinline__ float block_sum(float v, float* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  v = lane < nwarps ? scratch[lane] : 0.f;
+  return warp_sum(v);
+}
+__device__ __forceinline__ float block_max(float v, float* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  v = lane < nwarps ? scratch[lane] : -INFINITY;
+  return warp_max(v);
+}
+
+}  // namespace chimera::cuda

@@ -1,0 +1,75 @@
+"""ToyModel parity on the GPU: the sm_100a executor vs the reference oracle.
+
+Inputs are acceptance criterion 6's (proj/tests/acceptance.cpp:259-303): dims
+{4,4,5,3,3}-style, make_model seed 42, batch seeds 100+it, lr 0.05, 3 iterations.
+Stated tolerance: max relative weight difference <= 1e-5 after 3
+iterations; achieved bound with fp64 kernels is 1e-10.  Per-worker stash peaks must
+equal analysis::memory_profile().act_counts exactly.
+"""
+import json
+
+import numpy as np
+import pytest
+
+from paper_2107_06925_b200 import pipesim as P
+from paper_2107_06925_b200 import toy
+
+TOL = 1e-10
+
+
+def test_host_generators_bit_exact(golden):
+    g = golden("toy_oracle.json")["generators"]
+    assert np.array_equal(toy.make_model(g["dims"], 42), np.array(g["model42"]))
+    x, t = toy.make_batch(g["dims"], 16, 100)
+    assert np.array_equal(x, np.array(g["batch100_inputs"]))
+    assert np.array_equal(t, np.array(g["batch100_targets"]))
+
+
+@pytest.mark.gpu
+def test_criterion6_cases_vs_reference_fixtures(golden, toy_oracle):
+    for case in golden("toy_oracle.json")["cases"]:
+        c, dims = case["config"], case["dims"]
+        text = P.generate_json(P.PipelineConfig(**c), None, -1)
+        params = toy.make_model(dims, case["model_seed"])
+        batch = c["B"] * c["N"] * c["W"]
+        for it, seed in enumerate(case["batch_seeds"]):
+            x, t = toy.make_batch(dims, batch, seed)
+            params, peaks = toy.run_iteration(text, dims, params, x, t, case["lr"])
+            want = np.array(case["params_after"][it])
+            assert toy_oracle.max_relative_diff(dims, params, want) <= TOL, (c, it)
+        assert peaks == case["peak_stash"] == P.memory_profile(text)["act_counts"]
+        assert toy_oracle.max_relative_diff(dims, params, np.array(case["sequential_after3"])) <= 1e-6
+
+
+@pytest.mark.gpu
+def test_sequential_sgd_gpu(toy_oracle):
+    dims = [4, 5, 4, 3]
+    p = toy.make_model(dims, 7)
+    x, t = toy.make_batch(dims, 12, 3)
+    got = toy.sequential_sgd(dims, p, x, t, 12, 0.1)
+    want = toy_oracle.sequential_sgd(dims, p, x, t, 12, 0.1)
+    assert toy_oracle.max_relative_diff(dims, got, want) <= TOL
+
+
+@pytest.mark.gpu
+def test_wide_toy_chimera_d8(toy_oracle):
+    # larger dims and f = 2: 4 pipelines x 2 replicas, D = 8
+    cfg = P.PipelineConfig("chimera", 8, 2, 16, 4, 2)
+    dims = [64] * 9
+    text = P.generate_json(cfg, None, -1)
+    p0 = toy.make_model(dims, 3)
+    x, t = toy.make_batch(dims, cfg.mini_batch(), 5)
+    got, peaks = toy.run_iteration(text, dims, p0, x, t, 0.05)
+    want, wpeaks = toy_oracle.run_iteration(json.loads(text), dims, p0, x, t, 0.05)
+    assert toy_oracle.max_relative_diff(dims, got, want) <= TOL
+    assert peaks == wpeaks
+
+
+def test_bad_batch_size_is_invalid():
+    # raised before any device work: runs on CPU too
+    cfg = P.PipelineConfig("chimera", 4, 1, 4, 2, 1)
+    dims = [4, 4, 5, 3, 3]
+    p = toy.make_model(dims, 1)
+    x, t = toy.make_batch(dims, 3, 1)
+    with pytest.raises(P.InvalidConfigError):
+        toy.run_iteration(P.generate_json(cfg, None, -1), dims, p, x, t, 0.1)
