@@ -82,6 +82,15 @@ CK_API int ck_toy_sequential_sgd(const int* dims, int n_dims, const double* para
                                  const double* inputs, const double* targets, int batch,
                                  double lr, double* params_out);
 
+/* ------------------------------------------------------ kernel launchers (device ptrs) */
+/* tcgen05/TMA GEMM with fused epilogue (cuda/gemm.cu).  epi: 0 bf16 store (+bias),
+ * 1 bias+GELU (out=U, out2=gelu(U)), 2 bias+residual(aux), 3 x gelu'(aux), 4 fp32 +=,
+ * 5 fp32 store.  a_mn/b_mn select MN-major operands (see cuda/gemm.cuh). */
+CK_API int ck_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, const void* A,
+                        long long lda, const void* B, long long ldb, void* out, long long ldo,
+                        const void* bias, const void* aux, long long ld_aux, void* out2,
+                        long long ld_out2, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

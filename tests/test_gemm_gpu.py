@@ -1,0 +1,66 @@
+"""tcgen05/TMA GEMM vs a plain fp32 PyTorch reference of the same op.
+
+bf16 inputs, fp32 accumulation: fp32 outputs must match the fp32 reference to
+1e-3 relative (accumulation-order noise only); bf16 outputs to one bf16 ulp (2^-8).
+"""
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2107_06925_b200 import kernels as K  # noqa: E402
+
+SHAPES = [(128, 128, 64), (256, 384, 192), (4096, 3072, 1024), (300, 200, 136), (632, 5120, 1280),
+          (1000, 1000, 72)]
+
+
+def _rand(*shape):
+    return (torch.randn(*shape, device="cuda") * 0.5).to(torch.bfloat16)
+
+
+def _rel(a, b):
+    return ((a.float() - b.float()).norm() / b.float().norm().clamp_min(1e-30)).item()
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
+@pytest.mark.parametrize("M,N,K", SHAPES)
+def test_layouts_f32(a_mn, b_mn, M, N, K):
+    A = _rand(K, M) if a_mn else _rand(M, K)
+    B = _rand(K, N) if b_mn else _rand(N, K)
+    Af = A.float().t() if a_mn else A.float()
+    Bf = B.float() if b_mn else B.float().t()
+    ref = Af @ Bf
+    out = torch.full((M, N), float("nan"), device="cuda")
+    K.gemm("f32", A, B, out, a_mn=a_mn, b_mn=b_mn)
+    torch.cuda.synchronize()
+    assert _rel(out, ref) < 1e-3
+    acc = torch.ones(M, N, device="cuda")
+    K.gemm("acc_f32", A, B, acc, a_mn=a_mn, b_mn=b_mn)
+    assert _rel(acc, ref + 1) < 1e-3
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES[:4])
+def test_fused_epilogues(M, N, K):
+    A, B = _rand(M, K), _rand(N, K)
+    bias = _rand(N)
+    ref = A.float() @ B.float().t() + bias.float()
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    K.gemm("bf16", A, B, out, bias=bias)
+    assert _rel(out, ref) < 8e-3
+    resid = _rand(M, N)
+    K.gemm("bias_resid", A, B, out, bias=bias, aux=resid)
+    assert _rel(out, ref + resid.float()) < 8e-3
+    g = torch.empty_like(out)
+    K.gemm("bias_gelu", A, B, out, bias=bias, out2=g)
+    assert _rel(out, ref) < 8e-3
+    assert _rel(g, torch.nn.functional.gelu(out.float(), approximate="tanh")) < 8e-3
+    # dgrad with fused gelu': D = dY W (W MN-major), scaled by gelu'(U)
+    Wt = _rand(N, K)  # as [rows = reduction N, cols = K]
+    dY = _rand(M, N)
+    U = _rand(M, K)
+    d = torch.empty(M, K, device="cuda", dtype=torch.bfloat16)
+    K.gemm("gelu_bwd", dY, Wt, d, b_mn=True, aux=U)
+    u = U.float().requires_grad_()
+    gl = torch.nn.functional.gelu(u, approximate="tanh")
+    (gp,) = torch.autograd.grad(gl.sum(), u)
+    assert _rel(d, (dY.float() @ Wt.float()) * gp) < 8e-3
