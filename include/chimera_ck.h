@@ -91,6 +91,30 @@ CK_API int ck_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, const 
                         const void* bias, const void* aux, long long ld_aux, void* out2,
                         long long ld_out2, void* stream);
 
+/* LayerNorm (eps 1e-5), rows of h (h % 256 == 0); stats fp32. */
+CK_API int ck_layernorm_fwd(const void* x, const void* g, const void* b, void* y, float* mean,
+                            float* rstd, int M, int h, void* stream);
+CK_API int ck_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd,
+                            const void* g, const void* dres, void* dx, float* dgamma,
+                            float* dbeta, int M, int h, void* stream);
+/* token + position embedding and its scatter-add backward (fp32 grads). */
+CK_API int ck_embed_fwd(const int32_t* tok, const void* wte, const void* wpe, void* x, int M,
+                        int seq, int h, void* stream);
+CK_API int ck_embed_bwd(const int32_t* tok, const void* dx, float* dwte, float* dwpe, int M,
+                        int seq, int h, void* stream);
+/* in-place softmax cross-entropy forward+backward over the first V of Vp columns. */
+CK_API int ck_xent_fwd_bwd(void* logits, long long ld, const int32_t* labels, int M, int V, int Vp,
+                           float grad_scale, float loss_scale, float* loss_sum, void* stream);
+CK_API int ck_bias_grad(const void* dy, float* db, int M, int N, void* stream);
+CK_API int ck_sgd_update(float* w32, void* w16, float* const* grads, int copies, long long n,
+                         float lr, void* stream);
+/* flash attention, head dim 64, over packed qkv [B*seq, 3*H*64]. */
+CK_API int ck_attn_fwd(const void* qkv, void* out, float* lse, int B, int seq, int H, int causal,
+                       void* stream);
+CK_API int ck_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
+                       void* dqkv, float* scratch, int B, int seq, int H, int causal, void* stream);
+CK_API long long ck_attn_bwd_scratch_floats(int B, int seq, int H);
+
 #ifdef __cplusplus
 }
 #endif

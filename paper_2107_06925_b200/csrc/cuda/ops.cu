@@ -1,0 +1,418 @@
+// HBM-bound kernels of the transformer stage: LayerNorm fwd/bwd, embedding, softmax
+// cross-entropy (fused forward + backward, in place), bias gradients, SGD update.
+// Roofline: bytes moved / measured HBM bandwidth.  Design rules applied: 16-byte
+// vector accesses, one warp per row for row-wise ops (statistics stay in registers:
+// two-pass exact mean/variance with no re-read), column reductions accumulated in
+// registers across many rows before one atomic per column per CTA.
+#include "chimera_ck.h"
+#include "common.cuh"
+#include "ops.cuh"
+
+namespace chimera::ops {
+
+namespace {
+
+using cuda::ceil_div;
+
+struct Vec8 {  // 8 bf16 <-> 8 fp32
+  float f[8];
+  __device__ __forceinline__ void load(const bf16* p) {
+    const uint4 q = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float2 v = __bfloat1622float2(h[t]);
+      f[2 * t] = v.x, f[2 * t + 1] = v.y;
+    }
+  }
+  __device__ __forceinline__ void store(bf16* p) const {
+    uint4 q;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) h[t] = __floats2bfloat162_rn(f[2 * t], f[2 * t + 1]);
+    *reinterpret_cast<uint4*>(p) = q;
+  }
+};
+
+// ------------------------------------------------------------------ LayerNorm --
+// One warp per row; lane owns VPL chunks of 8 columns: column = (c * 32 + lane) * 8.
+template <int VPL>
+__global__ void __launch_bounds__(256) k_ln_fwd(const bf16* __restrict__ x, const bf16* __restrict__ g,
+                                                const bf16* __restrict__ b, bf16* __restrict__ y,
+                                                float* __restrict__ mean, float* __restrict__ rstd, int M) {
+  constexpr int h = VPL * 256;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const bf16* xr = x + (long long)row * h;
+  Vec8 v[VPL];
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < VPL; ++c) {
+    v[c].load(xr + (c * 32 + lane) * 8);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) s += v[c].f[t];
+  }
+  const float mu = cuda::warp_sum(s) * (1.f / h);
+  float ss = 0.f;
+#pragma unroll
+  for (int c = 0; c < VPL; ++c)
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const float d = v[c].f[t] - mu;
+      ss += d * d;
+    }
+  const float rs = rsqrtf(cuda::warp_sum(ss) * (1.f / h) + 1e-5f);
+#pragma unroll
+  for (int c = 0; c < VPL; ++c) {
+    const int col = (c * 32 + lane) * 8;
+    Vec8 gg, bb, o;
+    gg.load(g + col);
+    bb.load(b + col);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) o.f[t] = (v[c].f[t] - mu) * rs * gg.f[t] + bb.f[t];
+    o.store(y + (long long)row * h + col);
+  }
+  if (lane == 0) mean[row] = mu, rstd[row] = rs;
+}
+
+template <int VPL>
+__global__ void __launch_bounds__(256) k_ln_bwd(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                                                const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                const bf16* __restrict__ g, const bf16* __restrict__ dres,
+                                                bf16* __restrict__ dx, float* __restrict__ dgamma,
+                                                float* __restrict__ dbeta, int M) {
+  constexpr int h = VPL * 256;
+  extern __shared__ float red[];  // [8 warps][2][h]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float acc_g[VPL][8], acc_b[VPL][8];
+  Vec8 gam[VPL];
+#pragma unroll
+  for (int c = 0; c < VPL; ++c) {
+    gam[c].load(g + (c * 32 + lane) * 8);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) acc_g[c][t] = acc_b[c][t] = 0.f;
+  }
+  for (int row = blockIdx.x * 8 + warp; row < M; row += gridDim.x * 8) {
+    const float mu = mean[row], rs = rstd[row];
+    Vec8 dv[VPL], xv[VPL];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int c = 0; c < VPL; ++c) {
+      const int col = (c * 32 + lane) * 8;
+      dv[c].load(dy + (long long)row * h + col);
+      xv[c].load(x + (long long)row * h + col);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const float xh = (xv[c].f[t] - mu) * rs;
+        const float gg = dv[c].f[t] * gam[c].f[t];
+        s1 += gg;
+        s2 += gg * xh;
+        acc_g[c][t] += dv[c].f[t] * xh;
+        acc_b[c][t] += dv[c].f[t];
+        xv[c].f[t] = xh;
+      }
+    }
+    s1 = cuda::warp_sum(s1) * (1.f / h);
+    s2 = cuda::warp_sum(s2) * (1.f / h);
+#pragma unroll
+    for (int c = 0; c < VPL; ++c) {
+      const int col = (c * 32 + lane) * 8;
+      Vec8 r, o;
+      if (dres) r.load(dres + (long long)row * h + col);
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        o.f[t] = rs * (dv[c].f[t] * gam[c].f[t] - s1 - xv[c].f[t] * s2) + (dres ? r.f[t] : 0.f);
+      o.store(dx + (long long)row * h + col);
+    }
+  }
+  // reduce the per-lane column partials over the 8 warps, then one atomic per column
+#pragma unroll
+  for (int c = 0; c < VPL; ++c)
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int col = (c * 32 + lane) * 8 + t;
+      red[(warp * 2) * h + col] = acc_g[c][t];
+      red[(warp * 2 + 1) * h + col] = acc_b[c][t];
+    }
+  __syncthreads();
+  for (int col = threadIdx.x; col < h; col += blockDim.x) {
+    float sg = 0.f, sb = 0.f;
+    for (int w = 0; w < 8; ++w) sg += red[(w * 2) * h + col], sb += red[(w * 2 + 1) * h + col];
+    atomicAdd(dgamma + col, sg);
+    atomicAdd(dbeta + col, sb);
+  }
+}
+
+// ------------------------------------------------------------------ embedding --
+__global__ void k_embed_fwd(const int32_t* __restrict__ tok, const bf16* __restrict__ wte,
+                            const bf16* __restrict__ wpe, bf16* __restrict__ x, int M, int seq, int h) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const bf16* a = wte + (long long)tok[row] * h;
+  const bf16* p = wpe + (long long)(row % seq) * h;
+  for (int col = lane * 8; col < h; col += 256) {
+    Vec8 u, v;
+    u.load(a + col);
+    v.load(p + col);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) u.f[t] += v.f[t];
+    u.store(x + (long long)row * h + col);
+  }
+}
+
+__global__ void k_embed_bwd(const int32_t* __restrict__ tok, const bf16* __restrict__ dx,
+                            float* __restrict__ dwte, float* __restrict__ dwpe, int M, int seq, int h) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= M) return;
+  float* a = dwte + (long long)tok[row] * h;
+  float* p = dwpe + (long long)(row % seq) * h;
+  for (int col = lane * 8; col < h; col += 256) {
+    Vec8 u;
+    u.load(dx + (long long)row * h + col);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) atomicAdd(a + col + t, u.f[t]), atomicAdd(p + col + t, u.f[t]);
+  }
+}
+
+// -------------------------------------------------------------- cross-entropy --
+// One CTA per row.  Pass 1: online max / sum-exp over the valid V columns (16-byte
+// loads); pass 2: in-place gradient.  Vp % 8 == 0.
+__global__ void __launch_bounds__(512) k_xent(bf16* __restrict__ logits, long long ld,
+                                              const int32_t* __restrict__ labels, int V, int Vp,
+                                              float grad_scale, float loss_scale, float* __restrict__ loss_sum) {
+  __shared__ float scratch[32];
+  const int row = blockIdx.x;
+  bf16* lr = logits + (long long)row * ld;
+  float m = -INFINITY, s = 0.f;
+  for (int c = threadIdx.x * 8; c < Vp; c += blockDim.x * 8) {
+    Vec8 v;
+    v.load(lr + c);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      if (c + t >= V) break;
+      const float x = v.f[t];
+      if (x > m) s = s * __expf(m - x) + 1.f, m = x;
+      else s += __expf(x - m);
+    }
+  }
+  const float gm = cuda::block_max(m, scratch);
+  s = (m == -INFINITY) ? 0.f : s * __expf(m - gm);
+  const float gs = cuda::block_sum(s, scratch);
+  const float lse = gm + __logf(gs);
+  const int lab = labels[row];
+  const float x_lab = __bfloat162float(lr[lab]);
+  __syncthreads();  // everyone has read lr[lab] before it is overwritten
+  for (int c = threadIdx.x * 8; c < Vp; c += blockDim.x * 8) {
+    Vec8 v;
+    v.load(lr + c);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int j = c + t;
+      v.f[t] = j < V ? (__expf(v.f[t] - lse) - (j == lab ? 1.f : 0.f)) * grad_scale : 0.f;
+    }
+    v.store(lr + c);
+  }
+  if (threadIdx.x == 0) atomicAdd(loss_sum, (lse - x_lab) * loss_scale);
+}
+
+// ------------------------------------------------------------------ bias grad --
+// 128 threads x 2 columns = 256 columns per CTA, rows split in chunks of 256.
+__global__ void k_bias_grad(const bf16* __restrict__ dy, float* __restrict__ db, int M, int N) {
+  const int col = blockIdx.x * 256 + threadIdx.x * 2;
+  if (col >= N) return;
+  const int r0 = blockIdx.y * 256, r1 = min(M, r0 + 256);
+  float a = 0.f, b = 0.f;
+  for (int r = r0; r < r1; ++r) {
+    const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dy + (long long)r * N + col));
+    a += v.x, b += v.y;
+  }
+  atomicAdd(db + col, a);
+  if (col + 1 < N) atomicAdd(db + col + 1, b);
+}
+
+// -------------------------------------------------------------------- update --
+struct GradPtrs {
+  float* p[8];
+};
+
+__global__ void k_sgd(float* __restrict__ w32, bf16* __restrict__ w16, GradPtrs g, int copies,
+                      long long n, float lr) {
+  for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 4; i < n;
+       i += (long long)gridDim.x * blockDim.x * 4) {
+    if (i + 4 <= n) {
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c = 0; c < copies; ++c) {
+        float4* q = reinterpret_cast<float4*>(g.p[c] + i);
+        const float4 v = *q;
+        s.x += v.x, s.y += v.y, s.z += v.z, s.w += v.w;
+        *q = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      float4 w = *reinterpret_cast<float4*>(w32 + i);
+      w.x -= lr * s.x, w.y -= lr * s.y, w.z -= lr * s.z, w.w -= lr * s.w;
+      *reinterpret_cast<float4*>(w32 + i) = w;
+      __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(w16 + i);
+      o[0] = __floats2bfloat162_rn(w.x, w.y);
+      o[1] = __floats2bfloat162_rn(w.z, w.w);
+    } else {
+      for (long long j = i; j < n; ++j) {
+        float s = 0.f;
+        for (int c = 0; c < copies; ++c) s += g.p[c][j], g.p[c][j] = 0.f;
+        w32[j] -= lr * s;
+        w16[j] = __float2bfloat16_rn(w32[j]);
+      }
+    }
+  }
+}
+
+__global__ void k_reduce(float* __restrict__ dst, GradPtrs g, int copies, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int c = 0; c < copies; ++c) s += g.p[c][i];
+    dst[i] = s;
+  }
+}
+
+__global__ void k_cast(const float* __restrict__ s, bf16* __restrict__ d, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    d[i] = __float2bfloat16_rn(s[i]);
+}
+
+int grid_for(long long n, int per_thread) {
+  const long long b = (n / per_thread + 255) / 256;
+  return int(b < 148LL * 16 ? (b < 1 ? 1 : b) : 148LL * 16);
+}
+
+}  // namespace
+
+void layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* mean, float* rstd,
+                   int M, int h, cudaStream_t st) {
+  const int grid = ceil_div(M, 8);
+  switch (h) {
+#define CK_LN(V) case V * 256: k_ln_fwd<V><<<grid, 256, 0, st>>>(x, g, b, y, mean, rstd, M); break;
+    CK_LN(1) CK_LN(2) CK_LN(3) CK_LN(4) CK_LN(5) CK_LN(6) CK_LN(8)
+#undef CK_LN
+    default: throw chimera::capi::InternalError("layernorm: unsupported hidden size");
+  }
+  CK_CUDA(cudaGetLastError());
+}
+
+void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* g,
+                   const bf16* dres, bf16* dx, float* dgamma, float* dbeta, int M, int h,
+                   cudaStream_t st) {
+  const int grid = std::min(ceil_div(M, 8), 2 * cuda::kNumSMs);
+  const size_t smem = size_t(16) * h * sizeof(float);
+  switch (h) {
+#define CK_LN(V)                                                                                   \
+  case V * 256: {                                                                                  \
+    static bool attr = false;                                                                      \
+    if (!attr) {                                                                                   \
+      CK_CUDA(cudaFuncSetAttribute(k_ln_bwd<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * V * 256 * 4)); \
+      attr = true;                                                                                 \
+    }                                                                                              \
+    k_ln_bwd<V><<<grid, 256, smem, st>>>(dy, x, mean, rstd, g, dres, dx, dgamma, dbeta, M);        \
+    break;                                                                                         \
+  }
+    CK_LN(1) CK_LN(2) CK_LN(3) CK_LN(4) CK_LN(5) CK_LN(6) CK_LN(8)
+#undef CK_LN
+    default: throw chimera::capi::InternalError("layernorm: unsupported hidden size");
+  }
+  CK_CUDA(cudaGetLastError());
+}
+
+void embed_fwd(const int32_t* tok, const bf16* wte, const bf16* wpe, bf16* x, int M, int seq, int h,
+               cudaStream_t st) {
+  k_embed_fwd<<<ceil_div(M, 8), 256, 0, st>>>(tok, wte, wpe, x, M, seq, h);
+  CK_CUDA(cudaGetLastError());
+}
+
+void embed_bwd(const int32_t* tok, const bf16* dx, float* dwte, float* dwpe, int M, int seq, int h,
+               cudaStream_t st) {
+  k_embed_bwd<<<ceil_div(M, 8), 256, 0, st>>>(tok, dx, dwte, dwpe, M, seq, h);
+  CK_CUDA(cudaGetLastError());
+}
+
+void xent_fwd_bwd(bf16* logits, long long ld, const int32_t* labels, int M, int V, int Vp,
+                  float grad_scale, float loss_scale, float* loss_sum, cudaStream_t st) {
+  k_xent<<<M, 512, 0, st>>>(logits, ld, labels, V, Vp, grad_scale, loss_scale, loss_sum);
+  CK_CUDA(cudaGetLastError());
+}
+
+void bias_grad(const bf16* dy, float* db, int M, int N, cudaStream_t st) {
+  k_bias_grad<<<dim3(ceil_div(N, 256), ceil_div(M, 256)), 128, 0, st>>>(dy, db, M, N);
+  CK_CUDA(cudaGetLastError());
+}
+
+void sgd_update(float* w32, bf16* w16, float* const* grads, int copies, long long n, float lr,
+                cudaStream_t st) {
+  if (copies < 1 || copies > 8) throw chimera::capi::InternalError("sgd: 1..8 gradient copies");
+  GradPtrs g{};
+  for (int c = 0; c < copies; ++c) g.p[c] = grads[c];
+  k_sgd<<<grid_for(n, 4), 256, 0, st>>>(w32, w16, g, copies, n, lr);
+  CK_CUDA(cudaGetLastError());
+}
+
+void reduce_copies(float* dst, float* const* srcs, int copies, long long n, cudaStream_t st) {
+  if (copies < 1 || copies > 8) throw chimera::capi::InternalError("reduce: 1..8 copies");
+  GradPtrs g{};
+  for (int c = 0; c < copies; ++c) g.p[c] = srcs[c];
+  k_reduce<<<grid_for(n, 1), 256, 0, st>>>(dst, g, copies, n);
+  CK_CUDA(cudaGetLastError());
+}
+
+void cast_f32_bf16(const float* src, bf16* dst, long long n, cudaStream_t st) {
+  k_cast<<<grid_for(n, 1), 256, 0, st>>>(src, dst, n);
+  CK_CUDA(cudaGetLastError());
+}
+
+}  // namespace chimera::ops
+
+// ----------------------------------------------------------- C-ABI launchers --
+extern "C" {
+using chimera::ops::bf16;
+
+CK_API int ck_layernorm_fwd(const void* x, const void* g, const void* b, void* y, float* mean,
+                            float* rstd, int M, int h, void* st) {
+  return chimera::capi::guarded([&] {
+    chimera::ops::layernorm_fwd((const bf16*)x, (const bf16*)g, (const bf16*)b, (bf16*)y, mean, rstd,
+                                M, h, (cudaStream_t)st);
+  });
+}
+CK_API int ck_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd,
+                            const void* g, const void* dres, void* dx, float* dg, float* db, int M,
+                            int h, void* st) {
+  return chimera::capi::guarded([&] {
+    chimera::ops::layernorm_bwd((const bf16*)dy, (const bf16*)x, mean, rstd, (const bf16*)g,
+                                (const bf16*)dres, (bf16*)dx, dg, db, M, h, (cudaStream_t)st);
+  });
+}
+CK_API int ck_embed_fwd(const int32_t* tok, const void* wte, const void* wpe, void* x, int M, int seq,
+                        int h, void* st) {
+  return chimera::capi::guarded([&] {
+    chimera::ops::embed_fwd(tok, (const bf16*)wte, (const bf16*)wpe, (bf16*)x, M, seq, h, (cudaStream_t)st);
+  });
+}
+CK_API int ck_embed_bwd(const int32_t* tok, const void* dx, float* dwte, float* dwpe, int M, int seq,
+                        int h, void* st) {
+  return chimera::capi::guarded([&] {
+    chimera::ops::embed_bwd(tok, (const bf16*)dx, dwte, dwpe, M, seq, h, (cudaStream_t)st);
+  });
+}
+CK_API int ck_xent_fwd_bwd(void* logits, long long ld, const int32_t* labels, int M, int V, int Vp,
+                           float grad_scale, float loss_scale, float* loss_sum, void* st) {
+  return chimera::capi::guarded([&] {
+    chimera::ops::xent_fwd_bwd((bf16*)logits, ld, labels, M, V, Vp, grad_scale, loss_scale, loss_sum,
+                               (cudaStream_t)st);
+  });
+}
+CK_API int ck_bias_grad(const void* dy, float* db, int M, int N, void* st) {
+  return chimera::capi::guarded([&] { chimera::ops::bias_grad((const bf16*)dy, db, M, N, (cudaStream_t)st); });
+}
+CK_API int ck_sgd_update(float* w32, void* w16, float* const* grads, int copies, long long n, float lr,
+                         void* st) {
+  return chimera::capi::guarded([&] {
+    chimera::ops::sgd_update(w32, (bf16*)w16, grads, copies, n, lr, (cudaStream_t)st);
+  });
+}
+}

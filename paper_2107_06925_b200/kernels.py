@@ -37,3 +37,57 @@ def gemm(epi, A, B, out, *, a_mn=False, b_mn=False, M=None, N=None, K=None, bias
                              aux.stride(0) if aux is not None else 0, _p(out2),
                              out2.stride(0) if out2 is not None else 0, _stream(stream)))
     return out
+
+_fp = C.POINTER(C.c_float)
+_lib.register("ck_layernorm_fwd", _i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp])
+_lib.register("ck_layernorm_bwd", _i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp])
+_lib.register("ck_embed_fwd", _i, [_vp, _vp, _vp, _vp, _i, _i, _i, _vp])
+_lib.register("ck_embed_bwd", _i, [_vp, _vp, _vp, _vp, _i, _i, _i, _vp])
+_lib.register("ck_xent_fwd_bwd", _i, [_vp, _ll, _vp, _i, _i, _i, C.c_float, C.c_float, _vp, _vp])
+_lib.register("ck_bias_grad", _i, [_vp, _vp, _i, _i, _vp])
+_lib.register("ck_sgd_update", _i, [_vp, _vp, _vp, _i, _ll, C.c_float, _vp])
+_lib.register("ck_attn_fwd", _i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp])
+_lib.register("ck_attn_bwd", _i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp])
+_lib.register("ck_attn_bwd_scratch_floats", _ll, [_i, _i, _i])
+
+
+def layernorm_fwd(x, g, b, y, mean, rstd, stream=None):
+    M, h = x.shape
+    check(lib().ck_layernorm_fwd(_p(x), _p(g), _p(b), _p(y), _p(mean), _p(rstd), M, h, _stream(stream)))
+
+
+def layernorm_bwd(dy, x, mean, rstd, g, dres, dx, dgamma, dbeta, stream=None):
+    M, h = x.shape
+    check(lib().ck_layernorm_bwd(_p(dy), _p(x), _p(mean), _p(rstd), _p(g), _p(dres), _p(dx), _p(dgamma),
+                                 _p(dbeta), M, h, _stream(stream)))
+
+
+def embed_fwd(tok, wte, wpe, x, seq, stream=None):
+    check(lib().ck_embed_fwd(_p(tok), _p(wte), _p(wpe), _p(x), x.shape[0], seq, x.shape[1], _stream(stream)))
+
+
+def embed_bwd(tok, dx, dwte, dwpe, seq, stream=None):
+    check(lib().ck_embed_bwd(_p(tok), _p(dx), _p(dwte), _p(dwpe), dx.shape[0], seq, dx.shape[1],
+                             _stream(stream)))
+
+
+def xent(logits, labels, V, grad_scale, loss_scale, loss_sum, stream=None):
+    M, Vp = logits.shape
+    check(lib().ck_xent_fwd_bwd(_p(logits), logits.stride(0), _p(labels), M, V, Vp, grad_scale, loss_scale,
+                                _p(loss_sum), _stream(stream)))
+
+
+def bias_grad(dy, db, stream=None):
+    check(lib().ck_bias_grad(_p(dy), _p(db), dy.shape[0], dy.shape[1], _stream(stream)))
+
+
+def attn_fwd(qkv, out, lse, B, seq, H, causal=True, stream=None):
+    check(lib().ck_attn_fwd(_p(qkv), _p(out), _p(lse), B, seq, H, int(causal), _stream(stream)))
+
+
+def attn_bwd(qkv, out, dout, lse, dqkv, B, seq, H, causal=True, stream=None):
+    import torch
+    n = lib().ck_attn_bwd_scratch_floats(B, seq, H)
+    scratch = torch.empty(n, device=qkv.device, dtype=torch.float32)
+    check(lib().ck_attn_bwd(_p(qkv), _p(out), _p(dout), _p(lse), _p(dqkv), _p(scratch), B, seq, H,
+                            int(causal), _stream(stream)))
