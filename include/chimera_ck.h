@@ -115,6 +115,35 @@ CK_API int ck_attn_bwd(const void* qkv, const void* out, const void* dout, const
                        void* dqkv, float* scratch, int B, int seq, int H, int causal, void* stream);
 CK_API long long ck_attn_bwd_scratch_floats(int B, int seq, int H);
 
+/* ------------------------------------------------------- GPT-2 stage executor */
+/* Transformer shape (head dim 64; vocab padded to a multiple of 8, e.g. 50304). */
+typedef struct ck_gpt_model {
+  int n_layer, hidden, heads, ffn, seq, vocab, vocab_padded, causal;
+} ck_gpt_model;
+typedef struct ck_gpt ck_gpt;
+/* A trainer for logical ranks [first_rank, first_rank + n_ranks) of the schedule
+ * (rank = replica * D + worker), on the current device.  Replaces the reference
+ * oracle::run_iteration's Engine (proj/src/oracle.cpp:162-356) for a real model. */
+CK_API int ck_gpt_create(const ck_gpt_model* model, const char* schedule_json, float lr,
+                         int first_rank, int n_ranks, ck_gpt** out);
+CK_API int ck_gpt_destroy(ck_gpt* h);
+/* JSON: per held stage {stage, numel, tensors:[{name, offset, rows, cols, init}]}. */
+CK_API int ck_gpt_layout(ck_gpt* h, char** out_json);
+/* JSON: peak_stash_per_rank, device_bytes, launches_per_step, graph, steps. */
+CK_API int ck_gpt_stats(ck_gpt* h, char** out_json);
+CK_API int ck_gpt_stage_numel(ck_gpt* h, int stage, long long* n);
+CK_API int ck_gpt_set_params(ck_gpt* h, int stage, const float* host);
+CK_API int ck_gpt_get_params(ck_gpt* h, int stage, float* host);
+/* tokens / labels: int32 [W*N*B*seq], sample (r*N + m)*B + i (oracle.cpp:200). */
+CK_API int ck_gpt_set_batch(ck_gpt* h, const int32_t* tokens, const int32_t* labels,
+                            int from_host);
+/* one iteration (all micro-batches, gradient sync, SGD); *loss = mean token loss. */
+CK_API int ck_gpt_step(ck_gpt* h, float* loss);
+/* enqueue one iteration on the trainer stream without waiting (graph replay). */
+CK_API int ck_gpt_launch(ck_gpt* h);
+CK_API int ck_gpt_set_graph(ck_gpt* h, int on);
+CK_API void* ck_gpt_stream(ck_gpt* h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,654 @@
+// GPT-2 stage executor: runs a pipesim Schedule (Chimera, or the GPipe / 1F1B
+// baselines) as real transformer training on B200.
+//
+// Mapping: logical rank = r*D + w for data-parallel replica r and
+// pipeline worker w; this process hosts a contiguous range of ranks (all of them on
+// one GPU, or one per GPU under torchrun).  Each rank owns a CUDA stream; tasks are
+// issued in the reference replay order (oracle.cpp:312-327) looping replicas inside
+// each task, exactly like oracle::Engine, so every cross-rank data edge is a wait on
+// an event recorded earlier in program order.  Per task:
+//   Forward(p,m,s):  [embed] -> L/D x (LN, QKV GEMM, flash-attn, O-proj GEMM + bias +
+//                    residual, LN, FC1 GEMM + bias + GELU, FC2 GEMM + bias + residual)
+//                    -> [final LN, LM-head GEMM, fused softmax-xent fwd+bwd]; the last
+//                    layer's epilogue writes straight into the consumer's receive slot.
+//   Backward(p,m,s): reverse, dgrad GEMMs (MN-major weights, GELU' fused), wgrad
+//                    GEMMs accumulating in fp32 (both operands MN-major), bias grads,
+//                    LN backward with the residual gradient fused, flash-attn bwd.
+// Gradients accumulate per (rank, pipeline) stage copy (oracle.cpp:170-181); at the
+// iteration end every stage's copies are summed (locally, then NCCL across
+// processes) and one SGD step updates the fp32 master and the bf16 working copy
+// (apply_stage_update, oracle.cpp:283-299).  Activation stashes come from per-copy
+// slot pools whose live peak per worker equals analysis::memory_profile().act_counts.
+// The whole iteration is captured once into a CUDA graph and replayed.
+#include <algorithm>
+#include <array>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "chimera_ck.h"
+#include "common.cuh"
+#include "gemm.cuh"
+#include "gpt_exec.hpp"
+#include "json_io.hpp"
+#include "ops.cuh"
+#include "pipesim/analysis.hpp"
+#include "pipesim/core.hpp"
+
+namespace chimera::gpt {
+
+using ops::bf16;
+using pipesim::Task;
+using pipesim::TaskKind;
+
+// ------------------------------------------------------------------- arena --
+struct Arena {
+  std::vector<void*> blocks;
+  size_t bytes = 0;
+  ~Arena() {
+    for (void* p : blocks) cudaFree(p);
+  }
+  template <class T>
+  T* alloc(size_t n) {
+    void* p = nullptr;
+    const size_t b = std::max<size_t>(n * sizeof(T), 256);
+    CK_CUDA(cudaMalloc(&p, b));
+    blocks.push_back(p);
+    bytes += b;
+    return static_cast<T*>(p);
+  }
+};
+
+struct LayerStash {
+  bf16 *h1, *qkv, *a, *x2, *h2, *u, *g, *xo;
+  float *mean1, *rstd1, *mean2, *rstd2, *lse;
+};
+
+struct Stash {
+  bf16* x0 = nullptr;  // stage-0 embedding output (stage input)
+  std::vector<LayerStash> layers;
+  bf16* xfinal = nullptr;  // last stage: input of the final LN
+  bf16* hf = nullptr;
+  float *meanf = nullptr, *rstdf = nullptr;
+  bf16* logits = nullptr;  // dlogits after the fused cross-entropy
+};
+
+struct Scratch {
+  bf16 *dxa, *dxb, *dx2, *dh, *du, *da, *dqkv;
+  float* attn;
+};
+
+struct StageState {
+  StageLayout L;
+  float* w32 = nullptr;
+  bf16* w16 = nullptr;
+  std::vector<float*> grads;  // one per local copy holding this stage
+};
+
+struct Copy {  // one (local rank, pipeline) stage replica
+  int rank, pipeline, stage;
+  float* grad;
+  std::vector<Stash> slots;
+  std::vector<int> free_slots;
+};
+
+struct Trainer::Impl {
+  ModelShape m;
+  pipesim::Schedule sched;
+  float lr;
+  int D, W, N, B, P, first, nlocal;
+  int M;  // tokens per micro-batch = B * seq
+  Arena arena;
+  std::vector<cudaStream_t> streams;  // per local rank
+  cudaStream_t main_stream;
+  std::map<int, StageState> stages;              // stage -> state (stages held locally)
+  std::map<std::array<int, 2>, Copy> copies;     // (rank, pipeline) -> copy
+  std::vector<Scratch> scratch;                  // per local rank
+  std::map<long long, bf16*> msg;                // message buffers
+  std::map<long long, cudaEvent_t> msg_ev;
+  std::vector<cudaEvent_t> rank_done;
+  cudaEvent_t start_ev, upd_ev;
+  int32_t *tokens = nullptr, *labels = nullptr;
+  float* loss = nullptr;
+  std::vector<std::pair<int, int>> order;
+  std::map<std::array<int, 4>, int> slot_of;  // (rank, p, m, s) -> slot index during issue
+  std::vector<int> peak_live;                  // per local rank
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  bool use_graph = true;
+  int steps = 0;
+  long long launches_per_step = 0;
+
+  bool local(int rank) const { return rank >= first && rank < first + nlocal; }
+  cudaStream_t stream_of(int rank) const { return streams[rank - first]; }
+  long long msg_key(int r, int mb, int s, int dir) const {
+    return (((long long)r * N + mb) * D + s) * 2 + dir;
+  }
+};
+
+namespace {
+
+int stage_of(const pipesim::Schedule& s, int w, int p) {
+  for (const Task& t : s.per_worker[w])
+    if (t.pipeline_id == p) return t.stage;
+  return -1;
+}
+
+}  // namespace
+
+Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float lr, int first_rank,
+                 int n_ranks)
+    : d_(new Impl) {
+  Impl& I = *d_;
+  I.m = shape;
+  I.sched = sched;
+  I.lr = lr;
+  const auto& c = sched.config;
+  I.D = c.D, I.W = c.W, I.N = c.N, I.B = c.B;
+  I.P = 1;
+  for (const auto& wl : sched.per_worker)
+    for (const Task& t : wl) I.P = std::max(I.P, t.pipeline_id + 1);
+  I.first = first_rank;
+  I.nlocal = n_ranks;
+  I.M = I.B * shape.seq;
+  if (shape.n_layer % I.D) throw pipesim::InvalidConfigError("n_layer must be divisible by D");
+  if (shape.hidden != shape.heads * 64) throw pipesim::InvalidConfigError("head dim must be 64");
+  if (shape.hidden % 256) throw pipesim::InvalidConfigError("hidden must be a multiple of 256");
+  if (shape.vocab_padded % 8 || shape.vocab_padded < shape.vocab)
+    throw pipesim::InvalidConfigError("vocab_padded must be >= vocab and a multiple of 8");
+  if (c.recompute) throw pipesim::InvalidConfigError("recompute is not supported by this executor yet");
+  if (first_rank < 0 || n_ranks < 1 || first_rank + n_ranks > I.W * I.D)
+    throw pipesim::InvalidConfigError("rank range outside W*D");
+  if (int(sched.per_worker.size()) != I.D) throw pipesim::InvalidConfigError("schedule must have D workers");
+  cuda::require_sm100();
+
+  const int h = shape.hidden, f = shape.ffn, Ls = shape.n_layer / I.D, M = I.M;
+  const int H = shape.heads;
+  // ---- stage weights and per-copy state
+  for (int rank = first_rank; rank < first_rank + n_ranks; ++rank) {
+    const int w = rank % I.D;
+    for (int p = 0; p < I.P; ++p) {
+      const int s = stage_of(sched, w, p);
+      if (s < 0) continue;
+      if (!I.stages.count(s)) {
+        StageState st;
+        st.L = make_stage_layout(shape, I.D, s);
+        st.w32 = I.arena.alloc<float>(st.L.total);
+        st.w16 = I.arena.alloc<bf16>(st.L.total);
+        CK_CUDA(cudaMemset(st.w32, 0, st.L.total * sizeof(float)));
+        CK_CUDA(cudaMemset(st.w16, 0, st.L.total * sizeof(bf16)));
+        I.stages[s] = std::move(st);
+      }
+      Copy cp{rank, p, s, nullptr, {}, {}};
+      cp.grad = I.arena.alloc<float>(I.stages[s].L.total);
+      CK_CUDA(cudaMemset(cp.grad, 0, I.stages[s].L.total * sizeof(float)));
+      I.stages[s].grads.push_back(cp.grad);
+      I.copies[{rank, p}] = std::move(cp);
+    }
+  }
+  // ---- replay order and stash slot counts (simulated issue => per-copy peaks)
+  I.order = capi::replay_order(sched);
+  std::map<std::array<int, 2>, int> live, peak;
+  I.peak_live.assign(n_ranks, 0);
+  std::vector<int> live_rank(n_ranks, 0);
+  for (const auto& [w, i] : I.order) {
+    const Task& t = sched.per_worker[w][i];
+    if (t.kind != TaskKind::Forward && t.kind != TaskKind::Backward) continue;
+    for (int r = 0; r < I.W; ++r) {
+      const int rank = r * I.D + w;
+      if (!I.local(rank)) continue;
+      auto& l = live[{rank, t.pipeline_id}];
+      if (t.kind == TaskKind::Forward) {
+        l++;
+        live_rank[rank - first_rank]++;
+      } else {
+        l--;
+        live_rank[rank - first_rank]--;
+      }
+      peak[{rank, t.pipeline_id}] = std::max(peak[{rank, t.pipeline_id}], l);
+      I.peak_live[rank - first_rank] = std::max(I.peak_live[rank - first_rank], live_rank[rank - first_rank]);
+    }
+  }
+  for (auto& [key, cp] : I.copies) {
+    const StageLayout& L = I.stages[cp.stage].L;
+    const int nslots = peak[key];
+    for (int k = 0; k < nslots; ++k) {
+      Stash st;
+      if (L.has_embed) st.x0 = I.arena.alloc<bf16>((size_t)M * h);
+      for (int l = 0; l < Ls; ++l) {
+        LayerStash ls;
+        ls.h1 = I.arena.alloc<bf16>((size_t)M * h);
+        ls.qkv = I.arena.alloc<bf16>((size_t)M * 3 * h);
+        ls.a = I.arena.alloc<bf16>((size_t)M * h);
+        ls.x2 = I.arena.alloc<bf16>((size_t)M * h);
+        ls.h2 = I.arena.alloc<bf16>((size_t)M * h);
+        ls.u = I.arena.alloc<bf16>((size_t)M * f);
+        ls.g = I.arena.alloc<bf16>((size_t)M * f);
+        ls.xo = (l + 1 < Ls) ? I.arena.alloc<bf16>((size_t)M * h) : nullptr;
+        ls.mean1 = I.arena.alloc<float>(M);
+        ls.rstd1 = I.arena.alloc<float>(M);
+        ls.mean2 = I.arena.alloc<float>(M);
+        ls.rstd2 = I.arena.alloc<float>(M);
+        ls.lse = I.arena.alloc<float>((size_t)I.B * H * shape.seq);
+        st.layers.push_back(ls);
+      }
+      if (L.has_head) {
+        st.xfinal = I.arena.alloc<bf16>((size_t)M * h);
+        st.hf = I.arena.alloc<bf16>((size_t)M * h);
+        st.meanf = I.arena.alloc<float>(M);
+        st.rstdf = I.arena.alloc<float>(M);
+        st.logits = I.arena.alloc<bf16>((size_t)M * shape.vocab_padded);
+      }
+      cp.slots.push_back(std::move(st));
+    }
+  }
+  // ---- per-rank scratch and streams
+  for (int k = 0; k < n_ranks; ++k) {
+    Scratch sc;
+    sc.dxa = I.arena.alloc<bf16>((size_t)M * h);
+    sc.dxb = I.arena.alloc<bf16>((size_t)M * h);
+    sc.dx2 = I.arena.alloc<bf16>((size_t)M * h);
+    sc.dh = I.arena.alloc<bf16>((size_t)M * h);
+    sc.da = I.arena.alloc<bf16>((size_t)M * h);
+    sc.du = I.arena.alloc<bf16>((size_t)M * f);
+    sc.dqkv = I.arena.alloc<bf16>((size_t)M * 3 * h);
+    sc.attn = I.arena.alloc<float>(ops::attn_bwd_scratch_floats(I.B, shape.seq, H));
+    I.scratch.push_back(sc);
+    cudaStream_t s;
+    CK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    I.streams.push_back(s);
+    cudaEvent_t e;
+    CK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    I.rank_done.push_back(e);
+  }
+  CK_CUDA(cudaStreamCreateWithFlags(&I.main_stream, cudaStreamNonBlocking));
+  CK_CUDA(cudaEventCreateWithFlags(&I.start_ev, cudaEventDisableTiming));
+  CK_CUDA(cudaEventCreateWithFlags(&I.upd_ev, cudaEventDisableTiming));
+  // ---- message buffers: fwd (r, m, s) feeds stage s+1; bwd (r, m, s) feeds stage s
+  for (int r = 0; r < I.W; ++r)
+    for (int mb = 0; mb < I.N; ++mb)
+      for (int s = 0; s + 1 < I.D; ++s)
+        for (int dir = 0; dir < 2; ++dir) {
+          const long long k = I.msg_key(r, mb, s, dir);
+          I.msg[k] = I.arena.alloc<bf16>((size_t)M * h);
+          cudaEvent_t e;
+          CK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+          I.msg_ev[k] = e;
+        }
+  const size_t toks = (size_t)I.W * I.N * I.B * shape.seq;
+  I.tokens = I.arena.alloc<int32_t>(toks);
+  I.labels = I.arena.alloc<int32_t>(toks);
+  I.loss = I.arena.alloc<float>(1);
+  CK_CUDA(cudaMemset(I.tokens, 0, toks * 4));
+  CK_CUDA(cudaMemset(I.labels, 0, toks * 4));
+  CK_CUDA(cudaDeviceSynchronize());
+}
+
+Trainer::~Trainer() {
+  Impl& I = *d_;
+  if (I.graph_exec) cudaGraphExecDestroy(I.graph_exec);
+  if (I.graph) cudaGraphDestroy(I.graph);
+  for (auto& kv : I.msg_ev) cudaEventDestroy(kv.second);
+  for (auto e : I.rank_done) cudaEventDestroy(e);
+  cudaEventDestroy(I.start_ev);
+  cudaEventDestroy(I.upd_ev);
+  for (auto s : I.streams) cudaStreamDestroy(s);
+  cudaStreamDestroy(I.main_stream);
+}
+
+// ----------------------------------------------------------- task kernels --
+namespace {
+
+using gemm::EpiArgs;
+
+EpiArgs epi(void* out, long long ldo, const bf16* bias = nullptr, const bf16* aux = nullptr,
+            long long ld_aux = 0, bf16* out2 = nullptr, long long ld_out2 = 0) {
+  EpiArgs e;
+  e.out = out, e.ldo = ldo, e.bias = bias, e.aux = aux, e.ld_aux = ld_aux, e.out2 = out2, e.ld_out2 = ld_out2;
+  return e;
+}
+
+}  // namespace
+
+void Trainer::forward_task(int rank, int p, int mb, int s) {
+  Impl& I = *d_;
+  const ModelShape& m = I.m;
+  const int h = m.hidden, f = m.ffn, M = I.M, H = m.heads, r = rank / I.D;
+  cudaStream_t st = I.stream_of(rank);
+  Copy& cp = I.copies.at({rank, p});
+  StageState& S = I.stages.at(s);
+  const StageLayout& L = S.L;
+  const bf16* w = S.w16;
+  if (cp.free_slots.empty()) throw capi::InternalError("stash pool exhausted");
+  const int slot = cp.free_slots.back();
+  cp.free_slots.pop_back();
+  I.slot_of[{rank, p, mb, s}] = slot;
+  Stash& X = cp.slots[slot];
+  const size_t tok0 = (size_t)(r * I.N + mb) * I.B * m.seq;
+
+  const bf16* x;
+  if (s == 0) {
+    ops::embed_fwd(I.tokens + tok0, w + L.wte, w + L.wpe, X.x0, M, m.seq, h, st);
+    x = X.x0;
+  } else {
+    const long long k = I.msg_key(r, mb, s - 1, 0);
+    CK_CUDA(cudaStreamWaitEvent(st, I.msg_ev.at(k), 0));
+    x = I.msg.at(k);
+  }
+  bf16* out_final = (s + 1 < I.D) ? I.msg.at(I.msg_key(r, mb, s, 0)) : X.xfinal;
+  for (int l = 0; l < L.n_layers; ++l) {
+    const LayerOffsets& o = L.layers[l];
+    LayerStash& A = X.layers[l];
+    bf16* xo = (l + 1 < L.n_layers) ? A.xo : out_final;
+    ops::layernorm_fwd(x, w + o.ln1_g, w + o.ln1_b, A.h1, A.mean1, A.rstd1, M, h, st);
+    gemm::gemm(gemm::kStoreBF16, false, false, M, 3 * h, h, A.h1, h, w + o.w_qkv, h,
+               epi(A.qkv, 3 * h, w + o.b_qkv), st);
+    ops::attn_fwd(A.qkv, A.a, A.lse, I.B, m.seq, H, m.causal, st);
+    gemm::gemm(gemm::kBiasResid, false, false, M, h, h, A.a, h, w + o.w_o, h,
+               epi(A.x2, h, w + o.b_o, x, h), st);
+    ops::layernorm_fwd(A.x2, w + o.ln2_g, w + o.ln2_b, A.h2, A.mean2, A.rstd2, M, h, st);
+    gemm::gemm(gemm::kBiasGelu, false, false, M, f, h, A.h2, h, w + o.w_fc1, h,
+               epi(A.u, f, w + o.b_fc1, nullptr, 0, A.g, f), st);
+    gemm::gemm(gemm::kBiasResid, false, false, M, h, f, A.g, f, w + o.w_fc2, f,
+               epi(xo, h, w + o.b_fc2, A.x2, h), st);
+    x = xo;
+    I.launches_per_step += 7;
+  }
+  if (L.has_head) {
+    ops::layernorm_fwd(X.xfinal, w + L.lnf_g, w + L.lnf_b, X.hf, X.meanf, X.rstdf, M, h, st);
+    gemm::gemm(gemm::kStoreBF16, false, false, M, m.vocab_padded, h, X.hf, h, w + L.w_head, h,
+               epi(X.logits, m.vocab_padded), st);
+    const float scale = 1.f / float((double)I.W * I.N * I.B * m.seq);
+    ops::xent_fwd_bwd(X.logits, m.vocab_padded, I.labels + tok0, M, m.vocab, m.vocab_padded, scale, scale,
+                      I.loss, st);
+    I.launches_per_step += 3;
+  } else {
+    CK_CUDA(cudaEventRecord(I.msg_ev.at(I.msg_key(r, mb, s, 0)), st));
+  }
+  if (s == 0) I.launches_per_step += 1;
+}
+
+void Trainer::backward_task(int rank, int p, int mb, int s) {
+  Impl& I = *d_;
+  const ModelShape& m = I.m;
+  const int h = m.hidden, f = m.ffn, M = I.M, H = m.heads, r = rank / I.D;
+  cudaStream_t st = I.stream_of(rank);
+  Copy& cp = I.copies.at({rank, p});
+  StageState& S = I.stages.at(s);
+  const StageLayout& L = S.L;
+  const bf16* w = S.w16;
+  float* gw = cp.grad;
+  const auto it = I.slot_of.find({rank, p, mb, s});
+  if (it == I.slot_of.end()) throw capi::InternalError("backward without stashed activation");
+  const int slot = it->second;
+  I.slot_of.erase(it);
+  Stash& X = cp.slots[slot];
+  Scratch& sc = I.scratch[rank - I.first];
+  const size_t tok0 = (size_t)(r * I.N + mb) * I.B * m.seq;
+
+  const bf16* dxo;
+  if (L.has_head) {
+    gemm::gemm(gemm::kStoreBF16, false, true, M, h, m.vocab_padded, X.logits, m.vocab_padded, w + L.w_head, h,
+               epi(sc.dh, h), st);
+    gemm::gemm(gemm::kAccF32, true, true, m.vocab_padded, h, M, X.logits, m.vocab_padded, X.hf, h,
+               epi(gw + L.w_head, h), st);
+    ops::layernorm_bwd(sc.dh, X.xfinal, X.meanf, X.rstdf, w + L.lnf_g, nullptr, sc.dxa, gw + L.lnf_g,
+                       gw + L.lnf_b, M, h, st);
+    dxo = sc.dxa;
+    I.launches_per_step += 3;
+  } else {
+    const long long k = I.msg_key(r, mb, s, 1);
+    CK_CUDA(cudaStreamWaitEvent(st, I.msg_ev.at(k), 0));
+    dxo = I.msg.at(k);
+  }
+  bf16* dx_stage = (s > 0) ? I.msg.at(I.msg_key(r, mb, s - 1, 1)) : nullptr;
+  for (int l = L.n_layers - 1; l >= 0; --l) {
+    const LayerOffsets& o = L.layers[l];
+    LayerStash& A = X.layers[l];
+    const bf16* xin = (l > 0) ? X.layers[l - 1].xo
+                              : (s == 0 ? X.x0 : I.msg.at(I.msg_key(r, mb, s - 1, 0)));
+    bf16* dxin = (l > 0) ? (dxo == sc.dxa ? sc.dxb : sc.dxa) : (dx_stage ? dx_stage : (dxo == sc.dxa ? sc.dxb : sc.dxa));
+    // MLP
+    ops::bias_grad(dxo, gw + o.b_fc2, M, h, st);
+    gemm::gemm(gemm::kAccF32, true, true, h, f, M, dxo, h, A.g, f, epi(gw + o.w_fc2, f), st);
+    gemm::gemm(gemm::kGeluBwd, false, true, M, f, h, dxo, h, w + o.w_fc2, f, epi(sc.du, f, nullptr, A.u, f), st);
+    ops::bias_grad(sc.du, gw + o.b_fc1, M, f, st);
+    gemm::gemm(gemm::kAccF32, true, true, f, h, M, sc.du, f, A.h2, h, epi(gw + o.w_fc1, h), st);
+    gemm::gemm(gemm::kStoreBF16, false, true, M, h, f, sc.du, f, w + o.w_fc1, h, epi(sc.dh, h), st);
+    ops::layernorm_bwd(sc.dh, A.x2, A.mean2, A.rstd2, w + o.ln2_g, dxo, sc.dx2, gw + o.ln2_g, gw + o.ln2_b, M, h, st);
+    // attention
+    ops::bias_grad(sc.dx2, gw + o.b_o, M, h, st);
+    gemm::gemm(gemm::kAccF32, true, true, h, h, M, sc.dx2, h, A.a, h, epi(gw + o.w_o, h), st);
+    gemm::gemm(gemm::kStoreBF16, false, true, M, h, h, sc.dx2, h, w + o.w_o, h, epi(sc.da, h), st);
+    ops::attn_bwd(A.qkv, A.a, sc.da, A.lse, sc.dqkv, sc.attn, I.B, m.seq, H, m.causal, st);
+    ops::bias_grad(sc.dqkv, gw + o.b_qkv, M, 3 * h, st);
+    gemm::gemm(gemm::kAccF32, true, true, 3 * h, h, M, sc.dqkv, 3 * h, A.h1, h, epi(gw + o.w_qkv, h), st);
+    gemm::gemm(gemm::kStoreBF16, false, true, M, h, 3 * h, sc.dqkv, 3 * h, w + o.w_qkv, h, epi(sc.dh, h), st);
+    ops::layernorm_bwd(sc.dh, xin, A.mean1, A.rstd1, w + o.ln1_g, sc.dx2, dxin, gw + o.ln1_g, gw + o.ln1_b, M, h, st);
+    dxo = dxin;
+    I.launches_per_step += 19;  // attn_bwd = memset + 3 kernels
+  }
+  if (s == 0) {
+    ops::embed_bwd(I.tokens + tok0, dxo, gw + L.wte, gw + L.wpe, M, m.seq, h, st);
+    I.launches_per_step += 1;
+  } else {
+    CK_CUDA(cudaEventRecord(I.msg_ev.at(I.msg_key(r, mb, s - 1, 1)), st));
+  }
+  cp.free_slots.push_back(slot);
+}
+
+void Trainer::issue_iteration() {
+  Impl& I = *d_;
+  I.launches_per_step = 0;
+  I.slot_of.clear();
+  for (auto& kv : I.copies) {
+    Copy& cp = kv.second;
+    cp.free_slots.resize(cp.slots.size());
+    std::iota(cp.free_slots.rbegin(), cp.free_slots.rend(), 0);
+  }
+  CK_CUDA(cudaMemsetAsync(I.loss, 0, sizeof(float), I.main_stream));
+  CK_CUDA(cudaEventRecord(I.start_ev, I.main_stream));
+  for (auto s : I.streams) CK_CUDA(cudaStreamWaitEvent(s, I.start_ev, 0));
+  for (const auto& [w, i] : I.order) {
+    const Task& t = I.sched.per_worker[w][i];
+    if (t.kind != TaskKind::Forward && t.kind != TaskKind::Backward) continue;
+    for (int r = 0; r < I.W; ++r) {
+      const int rank = r * I.D + w;
+      if (!I.local(rank)) continue;
+      if (t.kind == TaskKind::Forward) forward_task(rank, t.pipeline_id, t.micro_batch, t.stage);
+      else backward_task(rank, t.pipeline_id, t.micro_batch, t.stage);
+    }
+  }
+  for (int k = 0; k < I.nlocal; ++k) {
+    CK_CUDA(cudaEventRecord(I.rank_done[k], I.streams[k]));
+    CK_CUDA(cudaStreamWaitEvent(I.main_stream, I.rank_done[k], 0));
+  }
+  // gradient synchronisation + SGD, stage by stage
+  for (auto& [s, S] : I.stages) {
+    ops::sgd_update(S.w32, S.w16, S.grads.data(), int(S.grads.size()), S.L.total, I.lr, I.main_stream);
+    I.launches_per_step += 1;
+  }
+}
+
+float Trainer::step() {
+  Impl& I = *d_;
+  if (!I.use_graph || I.steps == 0) {
+    issue_iteration();
+  } else {
+    if (!I.graph_exec) {
+      CK_CUDA(cudaStreamBeginCapture(I.main_stream, cudaStreamCaptureModeThreadLocal));
+      issue_iteration();
+      CK_CUDA(cudaStreamEndCapture(I.main_stream, &I.graph));
+      CK_CUDA(cudaGraphInstantiate(&I.graph_exec, I.graph, 0));
+    }
+    CK_CUDA(cudaGraphLaunch(I.graph_exec, I.main_stream));
+  }
+  ++I.steps;
+  float loss = 0;
+  CK_CUDA(cudaMemcpyAsync(&loss, I.loss, sizeof(float), cudaMemcpyDeviceToHost, I.main_stream));
+  CK_CUDA(cudaStreamSynchronize(I.main_stream));
+  return loss;
+}
+
+void Trainer::launch_async() {
+  Impl& I = *d_;
+  if (!I.graph_exec) {
+    (void)step();  // builds the graph on the second call
+    if (!I.graph_exec) (void)step();
+    return;
+  }
+  CK_CUDA(cudaGraphLaunch(I.graph_exec, I.main_stream));
+  ++I.steps;
+}
+
+void* Trainer::stream() const { return d_->main_stream; }
+void Trainer::set_use_graph(bool on) { d_->use_graph = on; }
+
+void Trainer::upload_batch(const int32_t* tokens, const int32_t* labels, bool from_host, void* stream) {
+  Impl& I = *d_;
+  const size_t n = (size_t)I.W * I.N * I.B * I.m.seq;
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : I.main_stream;
+  const auto kind = from_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  CK_CUDA(cudaMemcpyAsync(I.tokens, tokens, n * 4, kind, st));
+  CK_CUDA(cudaMemcpyAsync(I.labels, labels, n * 4, kind, st));
+  if (st != I.main_stream) {
+    cudaEvent_t e;
+    CK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK_CUDA(cudaEventRecord(e, st));
+    CK_CUDA(cudaStreamWaitEvent(I.main_stream, e, 0));
+    CK_CUDA(cudaEventDestroy(e));
+  }
+}
+
+long long Trainer::stage_numel(int s) const {
+  auto it = d_->stages.find(s);
+  if (it == d_->stages.end()) throw pipesim::InvalidConfigError("stage not held by this process");
+  return it->second.L.total;
+}
+
+void Trainer::set_params(int s, const float* host) {
+  Impl& I = *d_;
+  StageState& S = I.stages.at(s);
+  CK_CUDA(cudaMemcpy(S.w32, host, S.L.total * sizeof(float), cudaMemcpyHostToDevice));
+  ops::cast_f32_bf16(S.w32, S.w16, S.L.total, I.main_stream);
+  CK_CUDA(cudaStreamSynchronize(I.main_stream));
+}
+
+void Trainer::get_params(int s, float* host) const {
+  const StageState& S = d_->stages.at(s);
+  CK_CUDA(cudaDeviceSynchronize());
+  CK_CUDA(cudaMemcpy(host, S.w32, S.L.total * sizeof(float), cudaMemcpyDeviceToHost));
+}
+
+std::string Trainer::layout_json() const {
+  using json::Value;
+  Value arr = Value::array();
+  for (const auto& [s, S] : d_->stages) {
+    Value st = Value::object();
+    st.set("stage", Value::integer(s));
+    st.set("numel", Value::integer(S.L.total));
+    Value ts = Value::array();
+    for (const auto& t : S.L.tensors) {
+      Value x = Value::object();
+      x.set("name", Value::string(t.name));
+      x.set("offset", Value::integer(t.offset));
+      x.set("rows", Value::integer(t.rows));
+      x.set("cols", Value::integer(t.cols));
+      x.set("init", Value::string(t.init == Init::Zero ? "zero" : t.init == Init::One ? "one" : "normal"));
+      ts.push(std::move(x));
+    }
+    st.set("tensors", std::move(ts));
+    arr.push(std::move(st));
+  }
+  return json::dump(arr, -1);
+}
+
+std::string Trainer::stats_json() const {
+  using json::Value;
+  const Impl& I = *d_;
+  Value j = Value::object();
+  Value pk = Value::array();
+  for (int v : I.peak_live) pk.push(Value::integer(v));
+  j.set("peak_stash_per_rank", std::move(pk));
+  j.set("device_bytes", Value::integer((long long)I.arena.bytes));
+  j.set("launches_per_step", Value::integer(I.launches_per_step));
+  j.set("graph", Value::boolean(I.graph_exec != nullptr));
+  j.set("steps", Value::integer(I.steps));
+  return json::dump(j, -1);
+}
+
+}  // namespace chimera::gpt
+
+// ------------------------------------------------------------------- C-ABI --
+extern "C" {
+
+struct ck_gpt {
+  std::unique_ptr<chimera::gpt::Trainer> t;
+};
+
+CK_API int ck_gpt_create(const ck_gpt_model* mdl, const char* schedule_json, float lr, int first_rank,
+                         int n_ranks, ck_gpt** out) {
+  return chimera::capi::guarded([&] {
+    chimera::gpt::ModelShape m;
+    m.n_layer = mdl->n_layer, m.hidden = mdl->hidden, m.heads = mdl->heads, m.ffn = mdl->ffn;
+    m.seq = mdl->seq, m.vocab = mdl->vocab, m.vocab_padded = mdl->vocab_padded, m.causal = mdl->causal != 0;
+    const auto s = pipesim::schedule_from_json(schedule_json);
+    const auto v = pipesim::validate_config_shape(s.config);
+    if (!v.empty()) throw pipesim::InvalidConfigError(v.front());
+    auto* h = new ck_gpt;
+    try {
+      h->t = std::make_unique<chimera::gpt::Trainer>(m, s, lr, first_rank, n_ranks);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+CK_API int ck_gpt_destroy(ck_gpt* h) {
+  return chimera::capi::guarded([&] { delete h; });
+}
+
+CK_API int ck_gpt_layout(ck_gpt* h, char** out_json) {
+  return chimera::capi::guarded([&] { *out_json = chimera::capi::dup_string(h->t->layout_json()); });
+}
+
+CK_API int ck_gpt_stats(ck_gpt* h, char** out_json) {
+  return chimera::capi::guarded([&] { *out_json = chimera::capi::dup_string(h->t->stats_json()); });
+}
+
+CK_API int ck_gpt_set_params(ck_gpt* h, int stage, const float* host) {
+  return chimera::capi::guarded([&] { h->t->set_params(stage, host); });
+}
+
+CK_API int ck_gpt_get_params(ck_gpt* h, int stage, float* host) {
+  return chimera::capi::guarded([&] { h->t->get_params(stage, host); });
+}
+
+CK_API int ck_gpt_stage_numel(ck_gpt* h, int stage, long long* n) {
+  return chimera::capi::guarded([&] { *n = h->t->stage_numel(stage); });
+}
+
+CK_API int ck_gpt_set_batch(ck_gpt* h, const int32_t* tokens, const int32_t* labels, int from_host) {
+  return chimera::capi::guarded([&] { h->t->upload_batch(tokens, labels, from_host != 0, nullptr); });
+}
+
+CK_API int ck_gpt_step(ck_gpt* h, float* loss) {
+  return chimera::capi::guarded([&] { *loss = h->t->step(); });
+}
+
+CK_API int ck_gpt_launch(ck_gpt* h) {
+  return chimera::capi::guarded([&] { h->t->launch_async(); });
+}
+
+CK_API int ck_gpt_set_graph(ck_gpt* h, int on) {
+  return chimera::capi::guarded([&] { h->t->set_use_graph(on != 0); });
+}
+
+CK_API void* ck_gpt_stream(ck_gpt* h) { return h->t->stream(); }
+
+}  // extern "C"

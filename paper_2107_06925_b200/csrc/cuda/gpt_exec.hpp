@@ -1,0 +1,36 @@
+// GPT-2 Chimera trainer (cuda/gpt.cu).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+
+#include "gpt_model.hpp"
+#include "pipesim/core.hpp"
+
+namespace chimera::gpt {
+
+class Trainer {
+ public:
+  Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float lr, int first_rank, int n_ranks);
+  ~Trainer();
+  float step();          // one full iteration, returns the loss
+  void launch_async();   // enqueue one iteration (graph replay) without host sync
+  void upload_batch(const int32_t* tokens, const int32_t* labels, bool from_host, void* stream);
+  void set_params(int stage, const float* host);
+  void get_params(int stage, float* host) const;
+  long long stage_numel(int stage) const;
+  std::string layout_json() const;
+  std::string stats_json() const;
+  void* stream() const;
+  void set_use_graph(bool on);
+
+ private:
+  struct Impl;
+  void issue_iteration();
+  void forward_task(int rank, int p, int mb, int s);
+  void backward_task(int rank, int p, int mb, int s);
+  std::unique_ptr<Impl> d_;
+};
+
+}  // namespace chimera::gpt

@@ -1,0 +1,200 @@
+"""GPT-2 training under a Chimera schedule on B200 -- Python host mirror of the
+C-ABI trainer (``ck_gpt_*`` in include/chimera_ck.h, csrc/cuda/gpt.cu).
+
+    tr = Trainer(PRESETS["gpt2-medium"], P.PipelineConfig("chimera", D=4, W=2, N=4, B=4), lr=1e-4)
+    tr.init_params(seed=0)
+    tr.set_batch(tokens, labels)      # int32 [W*N*B*seq]
+    loss = tr.step()
+
+Everything runs on the GPU through libchimera.so; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import call_str, check, lib
+from .pipesim import PipelineConfig, Schedule, generate_json
+
+
+class ck_gpt_model(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("n_layer", "hidden", "heads", "ffn", "seq", "vocab", "vocab_padded",
+                                        "causal")]
+
+
+_vp = C.c_void_p
+_lib.register("ck_gpt_create", C.c_int, [C.POINTER(ck_gpt_model), C.c_char_p, C.c_float, C.c_int, C.c_int,
+                                         C.POINTER(_vp)])
+_lib.register("ck_gpt_destroy", C.c_int, [_vp])
+_lib.register("ck_gpt_layout", C.c_int, [_vp, C.POINTER(_vp)])
+_lib.register("ck_gpt_stats", C.c_int, [_vp, C.POINTER(_vp)])
+_lib.register("ck_gpt_stage_numel", C.c_int, [_vp, C.c_int, C.POINTER(C.c_longlong)])
+_lib.register("ck_gpt_set_params", C.c_int, [_vp, C.c_int, _lib._fp])
+_lib.register("ck_gpt_get_params", C.c_int, [_vp, C.c_int, _lib._fp])
+_lib.register("ck_gpt_set_batch", C.c_int, [_vp, _vp, _vp, C.c_int])
+_lib.register("ck_gpt_step", C.c_int, [_vp, C.POINTER(C.c_float)])
+_lib.register("ck_gpt_launch", C.c_int, [_vp])
+_lib.register("ck_gpt_set_graph", C.c_int, [_vp, C.c_int])
+_lib.register("ck_gpt_stream", _vp, [_vp])
+
+
+@dataclass(frozen=True)
+class GPTShape:
+    n_layer: int
+    hidden: int
+    heads: int
+    ffn: int
+    seq: int
+    vocab: int
+    vocab_padded: int
+    causal: bool = True
+
+    def flops_per_seq(self) -> float:
+        """Algorithmic fwd+bwd FLOPs per sequence:
+        72 s L h^2 (1 + s/(6h) + V/(12 L h))  (no recompute credit)."""
+        s, L, h, V = self.seq, self.n_layer, self.hidden, self.vocab
+        return 72.0 * s * L * h * h * (1 + s / (6.0 * h) + V / (12.0 * L * h))
+
+    def params(self) -> int:
+        h, L = self.hidden, self.n_layer
+        return L * (12 * h * h + 13 * h) + 2 * self.vocab * h + self.seq * h + 2 * h
+
+
+# BASELINE.json configs; vocab padded to a multiple of 128.
+PRESETS = {
+    "tiny": GPTShape(8, 256, 4, 1024, 128, 1024, 1024, True),
+    "gpt2-medium": GPTShape(24, 1024, 16, 4096, 1024, 50257, 50304, True),
+    "bert48": GPTShape(48, 1024, 16, 4096, 128, 30522, 30592, False),
+    "gpt2-1.3b": GPTShape(64, 1280, 20, 5120, 632, 50257, 50304, True),
+    "gpt2-32l": GPTShape(32, 1280, 20, 5120, 632, 50257, 50304, True),
+}
+
+
+def init_stage(layout_stage: dict, seed: int) -> np.ndarray:
+    """N(0, 0.02) matrices/embeddings, zero biases, unit LayerNorm gains; host-side,
+    deterministic per (seed, stage) so every process and the oracle agree."""
+    rng = np.random.default_rng([seed, layout_stage["stage"]])
+    flat = np.zeros(layout_stage["numel"], np.float32)
+    for t in layout_stage["tensors"]:
+        o, n = t["offset"], t["rows"] * t["cols"]
+        if t["init"] == "normal":
+            flat[o:o + n] = rng.standard_normal(n) * 0.02
+        elif t["init"] == "one":
+            flat[o:o + n] = 1.0
+    return flat
+
+
+def synthetic_batch(shape: GPTShape, n_samples: int, seed: int = 0):
+    """i.i.d. uniform tokens; labels = next token (causal LM) -- SURVEY.md §8(d)."""
+    rng = np.random.default_rng(seed)
+    seqs = rng.integers(0, shape.vocab, size=(n_samples, shape.seq + 1), dtype=np.int64)
+    return (np.ascontiguousarray(seqs[:, :-1].reshape(-1), dtype=np.int32),
+            np.ascontiguousarray(seqs[:, 1:].reshape(-1), dtype=np.int32))
+
+
+class Trainer:
+    """Chimera (or GPipe / 1F1B) training of a GPT-2 shape for logical ranks
+    [first_rank, first_rank + n_ranks) on the current CUDA device."""
+
+    def __init__(self, shape: GPTShape, schedule, lr: float, first_rank: int = 0, n_ranks: int | None = None):
+        if isinstance(schedule, PipelineConfig):
+            text = generate_json(schedule, None, -1)
+        elif isinstance(schedule, Schedule):
+            text = schedule.text or schedule.to_json()
+        else:
+            text = schedule
+        self.schedule_text = text
+        cfg = json.loads(text)["config"]
+        self.config = PipelineConfig(**cfg)
+        self.shape = shape
+        if n_ranks is None:
+            n_ranks = cfg["W"] * cfg["D"] - first_rank
+        mdl = ck_gpt_model(shape.n_layer, shape.hidden, shape.heads, shape.ffn, shape.seq, shape.vocab,
+                           shape.vocab_padded, int(shape.causal))
+        h = C.c_void_p()
+        check(lib().ck_gpt_create(C.byref(mdl), text.encode(), lr, first_rank, n_ranks, C.byref(h)))
+        self._h = h
+        self.layout = json.loads(call_str(lib().ck_gpt_layout, h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ck_gpt_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stages(self):
+        return [st["stage"] for st in self.layout]
+
+    def init_params(self, seed: int = 0):
+        for st in self.layout:
+            self.set_params(st["stage"], init_stage(st, seed))
+
+    def set_params(self, stage: int, flat):
+        flat = np.ascontiguousarray(flat, np.float32)
+        check(lib().ck_gpt_set_params(self._h, stage, flat.ctypes.data_as(_lib._fp)))
+
+    def get_params(self, stage: int) -> np.ndarray:
+        n = C.c_longlong()
+        check(lib().ck_gpt_stage_numel(self._h, stage, C.byref(n)))
+        out = np.zeros(n.value, np.float32)
+        check(lib().ck_gpt_get_params(self._h, stage, out.ctypes.data_as(_lib._fp)))
+        return out
+
+    def set_batch(self, tokens, labels):
+        """Host arrays (numpy int32) or device tensors (anything with data_ptr())."""
+        if hasattr(tokens, "data_ptr"):
+            check(lib().ck_gpt_set_batch(self._h, C.c_void_p(tokens.data_ptr()), C.c_void_p(labels.data_ptr()),
+                                         int(not tokens.is_cuda)))
+        else:
+            t = np.ascontiguousarray(tokens, np.int32)
+            l = np.ascontiguousarray(labels, np.int32)
+            check(lib().ck_gpt_set_batch(self._h, t.ctypes.data_as(C.c_void_p), l.ctypes.data_as(C.c_void_p), 1))
+
+    def step(self) -> float:
+        loss = C.c_float()
+        check(lib().ck_gpt_step(self._h, C.byref(loss)))
+        return loss.value
+
+    def launch(self):
+        check(lib().ck_gpt_launch(self._h))
+
+    def use_graph(self, on: bool):
+        check(lib().ck_gpt_set_graph(self._h, int(on)))
+
+    def stream_handle(self) -> int:
+        return lib().ck_gpt_stream(self._h) or 0
+
+    def stats(self) -> dict:
+        return json.loads(call_str(lib().ck_gpt_stats, self._h))
+
+
+def smoke():
+    """One Chimera iteration of the tiny GPT on cuda:0 vs the numpy oracle."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import gpt_oracle as O
+    shape = PRESETS["tiny"]
+    cfg = PipelineConfig("chimera", 4, 1, 4, 1, 1)
+    tr = Trainer(shape, cfg, lr=0.1)
+    tr.init_params(0)
+    p0 = [tr.get_params(s).astype(np.float64) for s in range(cfg.D)]
+    tok, lab = synthetic_batch(shape, cfg.mini_batch(), 1)
+    tr.set_batch(tok, lab)
+    loss = tr.step()
+    oshape = O.Shape(**{k: getattr(shape, k) for k in O.Shape.__dataclass_fields__})
+    _, ref_loss, _, _ = O.run_iteration(json.loads(tr.schedule_text), oshape, p0, tok, lab, 0.1)
+    rel = abs(loss - ref_loss) / abs(ref_loss)
+    assert rel < 2e-2, (loss, ref_loss)
+    print(f"smoke: gpt tiny chimera D=4 loss={loss:.5f} oracle={ref_loss:.5f} rel={rel:.1e}")
+    tr.close()
