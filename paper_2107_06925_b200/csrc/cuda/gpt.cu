@@ -22,6 +22,7 @@
 // The whole iteration is captured once into a CUDA graph and replayed.
 #include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -258,7 +259,9 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
     sc.attn = I.arena.alloc<float>(ops::attn_bwd_scratch_floats(I.B, shape.seq, H));
     I.scratch.push_back(sc);
     cudaStream_t s;
-    CK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    // CK_SERIALIZE=1: every rank issues on one stream (debug: rules out cross-stream races)
+    if (k > 0 && std::getenv("CK_SERIALIZE")) s = I.streams[0];
+    else CK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     I.streams.push_back(s);
     cudaEvent_t e;
     CK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -295,7 +298,8 @@ Trainer::~Trainer() {
   for (auto e : I.rank_done) cudaEventDestroy(e);
   cudaEventDestroy(I.start_ev);
   cudaEventDestroy(I.upd_ev);
-  for (auto s : I.streams) cudaStreamDestroy(s);
+  for (size_t k = 0; k < I.streams.size(); ++k)
+    if (k == 0 || I.streams[k] != I.streams[0]) cudaStreamDestroy(I.streams[k]);
   cudaStreamDestroy(I.main_stream);
 }
 
@@ -532,7 +536,9 @@ long long Trainer::stage_numel(int s) const {
 void Trainer::set_params(int s, const float* host) {
   Impl& I = *d_;
   StageState& S = I.stages.at(s);
-  CK_CUDA(cudaMemcpy(S.w32, host, S.L.total * sizeof(float), cudaMemcpyHostToDevice));
+  // Stream-ordered upload: a pageable cudaMemcpy may return before its DMA lands and
+  // would not order against the non-blocking trainer stream.
+  CK_CUDA(cudaMemcpyAsync(S.w32, host, S.L.total * sizeof(float), cudaMemcpyHostToDevice, I.main_stream));
   ops::cast_f32_bf16(S.w32, S.w16, S.L.total, I.main_stream);
   CK_CUDA(cudaStreamSynchronize(I.main_stream));
 }

@@ -146,6 +146,8 @@ void run(const Schedule* sched, const std::vector<int>& dims, const double* para
   CK_CUDA(cudaMemset(d_grads.p, 0, (size_t)W * P * L.n * sizeof(double)));
   CK_CUDA(cudaMemcpy(d_in.p, inputs, (size_t)batch * dims[0] * sizeof(double), cudaMemcpyHostToDevice));
   CK_CUDA(cudaMemcpy(d_tg.p, targets, (size_t)batch * dims[D] * sizeof(double), cudaMemcpyHostToDevice));
+  // pageable uploads may still be in flight: order them before the non-blocking streams
+  CK_CUDA(cudaDeviceSynchronize());
 
   if (!sched) {  // sequential SGD: one stream, all stages on the whole batch
     DeviceBuf acts((size_t)(D + 1) * batch * maxd), gy((size_t)batch * maxd), gx((size_t)batch * maxd),

@@ -141,13 +141,13 @@ class Trainer:
 
     def set_params(self, stage: int, flat):
         flat = np.ascontiguousarray(flat, np.float32)
-        check(lib().ck_gpt_set_params(self._h, stage, flat.ctypes.data_as(_lib._fp)))
+        check(lib().ck_gpt_set_params(self._h, stage, flat))
 
     def get_params(self, stage: int) -> np.ndarray:
         n = C.c_longlong()
         check(lib().ck_gpt_stage_numel(self._h, stage, C.byref(n)))
         out = np.zeros(n.value, np.float32)
-        check(lib().ck_gpt_get_params(self._h, stage, out.ctypes.data_as(_lib._fp)))
+        check(lib().ck_gpt_get_params(self._h, stage, out))
         return out
 
     def set_batch(self, tokens, labels):
