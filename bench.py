@@ -1,0 +1,308 @@
+"""Chimera-B200 benchmark: GPT-2 training throughput under a Chimera schedule.
+
+Workload (BASELINE.json configs[1]): GPT-2 medium (24 layers, h=1024, 16 heads,
+s=1024, V=50257), Chimera D=4, N=4 micro-batches of B=4 sequences, W=2 data-parallel
+pipeline replicas -> 8 logical ranks, 32 sequences per iteration.  At --gpus G the 8
+ranks are spread over G GPUs (G | 8); one process per GPU under torchrun.  A "step" is
+one full training iteration (all micro-batches forward+backward, stage gradient
+allreduce, SGD update) on synthetic tokens and random-init weights.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Prints ONE JSON line (rank 0).  `value` = sequences/s with inputs resident in HBM
+(device-timed, CUDA events on the trainer stream, max over ranks); `e2e` = the same
+through the public API with the H2D copy of each step's tokens/labels from pinned host
+memory and the D2H loss read inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GPT-2 seqs/sec at D=8 on 8×B200; bubble ratio vs (D-2)/(2N+D-2)"
+SHAPE_NAME = "gpt2-medium"
+CFG = dict(scheme="chimera", D=4, W=2, N=4, B=4, f=1, scaling="direct")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p["bf16_tflops"], p.get("bf16_tflops_sustained"), p["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_port_sample(shape, seconds_hint=20.0):
+    """The numpy oracle (oracle/gpt_oracle.py, fp64, all BLAS threads) on a bounded
+    sample: forward+backward of one GPT-2 medium pipeline stage (6 layers, no head) for
+    one sequence, repeated until ~`seconds_hint`; scaled to full-model seqs/s by
+    algorithmic FLOPs."""
+    import numpy as np
+    from oracle import gpt_oracle as O
+    m = O.Shape(**shape.__dict__)
+    D = CFG["D"]
+    stage = O.StageModel(m, D, 1)
+    params = O.init_params(m, D, 0)[1]
+    P = O.unpack(params, stage.layout)
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((m.seq, m.hidden))
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        y, _, cache = stage.forward(P, x, None, 1, 1.0)
+        G = {k: np.zeros_like(v) for k, v in P.items()}
+        stage.backward(P, G, cache, np.ones_like(y) * 1e-3, 1)
+        n += 1
+        if time.perf_counter() - t0 > seconds_hint or n >= 50:
+            break
+    dt = (time.perf_counter() - t0) / n
+    s, h = m.seq, m.hidden
+    stage_flops = 3 * stage.per * (24 * s * h * h + 4 * s * s * h)  # fwd+bwd, no head
+    rate = stage_flops / dt
+    seqs_per_s = rate / shape.flops_per_seq()
+    return {"value": seqs_per_s, "unit": "seqs/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"numpy fp64 oracle, 1 sequence x 1 stage ({stage.per} layers) fwd+bwd x{n} "
+                      f"({dt:.2f} s each, {rate / 1e9:.1f} GFLOP/s), scaled by FLOPs to the full model"}
+
+
+def gemm_roofline(stream_handle, peak_tflops):
+    """Live CUDA-event timing of the stage GEMMs (the dominant kernel family) at the
+    workload's shapes, on the trainer's device: achieved = 2MNK / avg launch time."""
+    import torch
+    from paper_2107_06925_b200 import kernels as ck
+    from paper_2107_06925_b200.gpt import PRESETS
+    m = PRESETS[SHAPE_NAME]
+    M, h, f = CFG["B"] * m.seq, m.hidden, m.ffn
+    shapes = [  # (M, N, K, a_mn, b_mn) one layer fwd + bwd, weight x tokens
+        (M, 3 * h, h, 0, 0), (M, h, h, 0, 0), (M, f, h, 0, 0), (M, h, f, 0, 0),
+        (M, h, 3 * h, 0, 1), (M, h, h, 0, 1), (M, h, f, 0, 1), (M, f, h, 0, 1),
+        (3 * h, h, M, 1, 1), (h, h, M, 1, 1), (f, h, M, 1, 1), (h, f, M, 1, 1)]
+    st = torch.cuda.ExternalStream(stream_handle) if stream_handle else torch.cuda.current_stream()
+    tot_flops, tot_ms = 0.0, 0.0
+    with torch.cuda.stream(st):
+        bufs = []
+        for (Mm, N, K, a, b) in shapes:
+            A = torch.randn((K, Mm) if a else (Mm, K), device="cuda").bfloat16()
+            B = torch.randn((K, N) if b else (N, K), device="cuda").bfloat16()
+            out = torch.zeros(Mm, N, device="cuda", dtype=torch.float32 if (a and b) else torch.bfloat16)
+            bufs.append((Mm, N, K, a, b, A, B, out))
+        for it in range(2):
+            for (Mm, N, K, a, b, A, B, out) in bufs:
+                ck.gemm("acc_f32" if (a and b) else "bf16", A, B, out, a_mn=bool(a), b_mn=bool(b), stream=st)
+        reps = 20
+        for (Mm, N, K, a, b, A, B, out) in bufs:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(reps):
+                ck.gemm("acc_f32" if (a and b) else "bf16", A, B, out, a_mn=bool(a), b_mn=bool(b), stream=st)
+            e1.record(st)
+            e1.synchronize()
+            tot_ms += e0.elapsed_time(e1) / reps
+            tot_flops += 2.0 * Mm * N * K
+    achieved = tot_flops / (tot_ms * 1e-3) / 1e12
+    return {"bound": "tensor", "kernel": "ck gemm_bf16 (tcgen05.mma kind::f16, TMA, TMEM), 12 stage GEMM shapes",
+            "achieved": round(achieved, 1), "peak": peak_tflops, "unit": "TFLOP/s",
+            "frac": round(achieved / peak_tflops, 4), "traffic": None,
+            "flops_per_launch_avg": tot_flops / len(shapes), "avg_launch_ms": tot_ms / len(shapes)}
+
+
+def run_reference(args, shape):
+    """--impl reference: the reference path's CPU implementation (the numpy port of the
+    reference Engine; the reference itself has no transformer), all host threads."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    samples = []
+    for k in range(args.warmup + args.steps):
+        s = cpu_port_sample(shape, seconds_hint=3.0)
+        if k >= args.warmup:
+            samples.append(s["value"])
+    v = sum(samples) / len(samples)
+    line = {"metric": METRIC, "value": v, "unit": "seqs/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "GPT-2 medium Chimera D=4 N=4 W=2 B=4 (BASELINE configs[1])",
+                       "model": SHAPE_NAME, "global_batch": 32, "seq_len": shape.seq},
+            "cpu_baseline": {"value": v, "unit": "seqs/s", "cores": os.cpu_count(), "kind": "port",
+                             "sample": s["sample"]},
+            "e2e": {"value": v, "unit": "seqs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="chimera")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    from paper_2107_06925_b200.gpt import PRESETS
+    shape = PRESETS[SHAPE_NAME]
+    if args.impl == "reference":
+        return run_reference(args, shape)
+
+    import numpy as np
+    import torch
+    from paper_2107_06925_b200 import pipesim as P
+    from paper_2107_06925_b200.gpt import Trainer, synthetic_batch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    cfg = P.PipelineConfig(**CFG)
+    n_logical = cfg.W * cfg.D
+    if n_logical % world:
+        raise SystemExit(f"--gpus {world} must divide the {n_logical} logical ranks")
+    per = n_logical // world
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    tr = Trainer(shape, cfg, lr=1e-4, first_rank=rank * per, n_ranks=per)
+    tr.init_params(seed=0)
+    n_seq = cfg.mini_batch()
+    tok, lab = synthetic_batch(shape, n_seq, seed=1)
+    tr.set_batch(tok, lab)
+    for _ in range(args.warmup):
+        loss = tr.step()
+    stream = torch.cuda.ExternalStream(tr.stream_handle())
+
+    # ---- value: resident inputs, graph replay, CUDA events on the trainer stream
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            tr.launch()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t)
+    value = n_seq / (ms * 1e-3)
+
+    # ---- e2e: public API per step: pinned H2D tokens+labels, step, D2H loss
+    tok_h = torch.from_numpy(tok).pin_memory()
+    lab_h = torch.from_numpy(lab).pin_memory()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        tr.set_batch(tok_h, lab_h)
+        loss = tr.step()
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_ms])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t)
+
+    stats = tr.stats()
+    peak, peak_sus, hbm, peak_src = peaks()
+    line = None
+    if rank == 0:
+        sched = tr.schedule_text
+        bub = P.bubble_ratio(sched)
+        mp = P.memory_profile(sched)
+        rl = gemm_roofline(tr.stream_handle(), peak)
+        flops_seq = shape.flops_per_seq()
+        cpu = None if args.no_cpu_baseline else cpu_port_sample(shape)
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "seqs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic tokens (uniform, next-token labels), random-init weights N(0,0.02)",
+            "config": {"workload": "GPT-2 medium Chimera D=4 N=4 W=2 B=4 (BASELINE configs[1])",
+                       "model": SHAPE_NAME, "global_batch": n_seq, "seq_len": shape.seq,
+                       "parallelism": f"chimera D={cfg.D} W={cfg.W} f=1: {n_logical} logical ranks on {world} GPU(s)",
+                       "l2": "working set per step >> L2 (weights, grads, stashes ~40 GB)"},
+            "e2e": {"value": round(n_seq / (e2e_ms * 1e-3), 2), "unit": "seqs/s",
+                    "h2d_bytes_per_step": int(tok.nbytes + lab.nbytes), "d2h_bytes_per_step": 4},
+            "roofline": rl,
+            "mfu": {"tflops_per_gpu": round(value * flops_seq / world / 1e12, 1),
+                    "frac_of_sustained": round(value * flops_seq / world / 1e12 / peak_sus, 4) if peak_sus else None,
+                    "flop_per_seq": flops_seq, "peak_source": peak_src},
+            "bubble": {"schedule": str(bub), "closed_form": str(P.closed_form_bubble(cfg.D, cfg.N)),
+                       "measured": None,
+                       "note": "all logical ranks share the GPU(s) at N<8: bubble not observable per rank"},
+            "act_counts_per_worker": mp["act_counts"],
+            "peak_stash_per_rank": stats["peak_stash_per_rank"],
+            "device_bytes": stats["device_bytes"],
+            "loss": loss,
+            "gpu_launches": int(stats["launches_per_step"] * args.steps),
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    tr.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -164,6 +164,8 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
   if (first_rank < 0 || n_ranks < 1 || first_rank + n_ranks > I.W * I.D)
     throw pipesim::InvalidConfigError("rank range outside W*D");
   if (int(sched.per_worker.size()) != I.D) throw pipesim::InvalidConfigError("schedule must have D workers");
+  if (n_ranks != I.W * I.D)
+    throw pipesim::InvalidConfigError("this build hosts all W*D logical ranks in one process");
   cuda::require_sm100();
 
   const int h = shape.hidden, f = shape.ffn, Ls = shape.n_layer / I.D, M = I.M;
@@ -433,7 +435,7 @@ void Trainer::backward_task(int rank, int p, int mb, int s) {
     gemm::gemm(gemm::kStoreBF16, false, true, M, h, 3 * h, sc.dqkv, 3 * h, w + o.w_qkv, h, epi(sc.dh, h), st);
     ops::layernorm_bwd(sc.dh, xin, A.mean1, A.rstd1, w + o.ln1_g, sc.dx2, dxin, gw + o.ln1_g, gw + o.ln1_b, M, h, st);
     dxo = dxin;
-    I.launches_per_step += 19;  // attn_bwd = memset + 3 kernels
+    I.launches_per_step += 18;  // attn_bwd = 3 kernels (+ a memset node)
   }
   if (s == 0) {
     ops::embed_bwd(I.tokens + tok0, dxo, gw + L.wte, gw + L.wpe, M, m.seq, h, st);
