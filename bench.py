@@ -216,6 +216,8 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("gloo")
     tr = Trainer(shape, cfg, lr=1e-4, first_rank=rank * per, n_ranks=per)
+    if world > 1:
+        tr.connect()
     tr.init_params(seed=0)
     n_seq = cfg.mini_batch()
     tok, lab = synthetic_batch(shape, n_seq, seed=1)
@@ -262,6 +264,13 @@ def main():
         e2e_ms = float(t)
 
     stats = tr.stats()
+    if world > 1:  # the loss is summed over the processes holding last stages
+        t = torch.tensor([loss])
+        dist.all_reduce(t)
+        loss = float(t)
+        pk = [None] * world
+        dist.all_gather_object(pk, stats["peak_stash_per_rank"])
+        stats["peak_stash_per_rank"] = [v for x in pk for v in x]
     peak, peak_sus, hbm, peak_src = peaks()
     line = None
     if rank == 0:

@@ -143,6 +143,13 @@ CK_API int ck_gpt_step(ck_gpt* h, float* loss);
 CK_API int ck_gpt_launch(ck_gpt* h);
 CK_API int ck_gpt_set_graph(ck_gpt* h, int on);
 CK_API void* ck_gpt_stream(ck_gpt* h);
+/* Multi-process (one process per GPU): export this process's 128 bytes of CUDA-IPC
+ * handles, all-gather them (host side, e.g. torch.distributed), then connect with all
+ * processes' handles in process order and one ncclUniqueId (ck_nccl_unique_id). */
+CK_API int ck_gpt_ipc_handles(ck_gpt* h, char* out, int cap);
+CK_API int ck_gpt_connect(ck_gpt* h, const char* all_handles, int n_bytes, const char* nccl_id,
+                          int id_bytes);
+CK_API int ck_nccl_unique_id(char* out, int cap);
 
 #ifdef __cplusplus
 }

@@ -30,11 +30,14 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "chimera_ck.h"
 #include "common.cuh"
 #include "gemm.cuh"
 #include "gpt_exec.hpp"
 #include "json_io.hpp"
+#include "links.hpp"
 #include "ops.cuh"
 #include "pipesim/analysis.hpp"
 #include "pipesim/core.hpp"
@@ -108,8 +111,17 @@ struct Trainer::Impl {
   std::map<int, StageState> stages;              // stage -> state (stages held locally)
   std::map<std::array<int, 2>, Copy> copies;     // (rank, pipeline) -> copy
   std::vector<Scratch> scratch;                  // per local rank
-  std::map<long long, bf16*> msg;                // message buffers
-  std::map<long long, cudaEvent_t> msg_ev;
+  std::map<long long, Msg> msgs;                 // messages touching a local rank
+  std::vector<int> micro_pipeline;               // micro-batch -> pipeline id
+  std::map<std::array<int, 2>, int> worker_of;   // (pipeline, stage) -> worker
+  // cross-process plumbing (one process per GPU under torchrun)
+  int procs = 1, proc = 0, per = 1;
+  void* inbox = nullptr;   // receive buffers + flags of locally consumed messages
+  void* outbox = nullptr;  // acks of locally produced, remotely consumed messages
+  std::vector<void*> peer_inbox, peer_outbox;  // IPC mappings, indexed by process
+  bool connected = false;
+  ncclComm_t world_comm = nullptr;
+  std::map<int, ncclComm_t> stage_comm;  // stage -> communicator over its holder processes
   std::vector<cudaEvent_t> rank_done;
   cudaEvent_t start_ev, upd_ev;
   int32_t *tokens = nullptr, *labels = nullptr;
@@ -127,6 +139,45 @@ struct Trainer::Impl {
   cudaStream_t stream_of(int rank) const { return streams[rank - first]; }
   long long msg_key(int r, int mb, int s, int dir) const {
     return (((long long)r * N + mb) * D + s) * 2 + dir;
+  }
+  int proc_of(int rank) const { return rank / per; }
+  // producer / consumer rank of message (r, mb, s, dir): fwd s -> s+1, bwd s+1 -> s
+  int producer_of(int r, int mb, int s, int dir) const {
+    return r * D + worker_of.at({micro_pipeline[mb], dir == 0 ? s : s + 1});
+  }
+  int consumer_of(int r, int mb, int s, int dir) const {
+    return r * D + worker_of.at({micro_pipeline[mb], dir == 0 ? s + 1 : s});
+  }
+  // Deterministic inbox / outbox layouts of process q (identical on every process).
+  struct Slot {
+    size_t buf = 0, flag = 0;
+  };
+  size_t msg_bytes() const { return ((size_t)M * m.hidden * 2 + 255) / 256 * 256; }
+  std::map<long long, Slot> inbox_layout(int q, size_t* total) const {
+    std::map<long long, Slot> out;
+    std::vector<long long> keys;
+    for (int r = 0; r < W; ++r)
+      for (int mb = 0; mb < N; ++mb)
+        for (int s = 0; s + 1 < D; ++s)
+          for (int dir = 0; dir < 2; ++dir)
+            if (proc_of(consumer_of(r, mb, s, dir)) == q) keys.push_back(msg_key(r, mb, s, dir));
+    size_t off = 0;
+    for (long long k : keys) out[k].buf = off, off += msg_bytes();
+    for (long long k : keys) out[k].flag = off, off += 4;
+    *total = std::max<size_t>(off, 256);
+    return out;
+  }
+  std::map<long long, size_t> outbox_layout(int q, size_t* total) const {
+    std::map<long long, size_t> out;
+    size_t off = 0;
+    for (int r = 0; r < W; ++r)
+      for (int mb = 0; mb < N; ++mb)
+        for (int s = 0; s + 1 < D; ++s)
+          for (int dir = 0; dir < 2; ++dir)
+            if (proc_of(producer_of(r, mb, s, dir)) == q && proc_of(consumer_of(r, mb, s, dir)) != q)
+              out[msg_key(r, mb, s, dir)] = off, off += 4;
+    *total = std::max<size_t>(off, 256);
+    return out;
   }
 };
 
@@ -164,8 +215,22 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
   if (first_rank < 0 || n_ranks < 1 || first_rank + n_ranks > I.W * I.D)
     throw pipesim::InvalidConfigError("rank range outside W*D");
   if (int(sched.per_worker.size()) != I.D) throw pipesim::InvalidConfigError("schedule must have D workers");
-  if (n_ranks != I.W * I.D)
-    throw pipesim::InvalidConfigError("this build hosts all W*D logical ranks in one process");
+  if ((I.W * I.D) % n_ranks || first_rank % n_ranks)
+    throw pipesim::InvalidConfigError("ranks must split evenly over processes (contiguous blocks)");
+  I.per = n_ranks;
+  I.procs = I.W * I.D / n_ranks;
+  I.proc = first_rank / n_ranks;
+  I.micro_pipeline.assign(I.N, -1);
+  for (int w = 0; w < I.D; ++w)
+    for (const Task& t : sched.per_worker[w]) {
+      if (t.kind != TaskKind::Forward && t.kind != TaskKind::Backward) continue;
+      if (t.micro_batch < 0 || t.micro_batch >= I.N || t.stage < 0 || t.stage >= I.D)
+        throw pipesim::InvalidConfigError("task out of range");
+      I.micro_pipeline[t.micro_batch] = t.pipeline_id;
+      I.worker_of[{t.pipeline_id, t.stage}] = w;
+    }
+  for (int mb = 0; mb < I.N; ++mb)
+    if (I.micro_pipeline[mb] < 0) throw pipesim::InvalidConfigError("micro-batch without tasks");
   cuda::require_sm100();
 
   const int h = shape.hidden, f = shape.ffn, Ls = shape.n_layer / I.D, M = I.M;
@@ -272,17 +337,41 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
   CK_CUDA(cudaStreamCreateWithFlags(&I.main_stream, cudaStreamNonBlocking));
   CK_CUDA(cudaEventCreateWithFlags(&I.start_ev, cudaEventDisableTiming));
   CK_CUDA(cudaEventCreateWithFlags(&I.upd_ev, cudaEventDisableTiming));
-  // ---- message buffers: fwd (r, m, s) feeds stage s+1; bwd (r, m, s) feeds stage s
+  // ---- messages: fwd (r, m, s) feeds stage s+1; bwd (r, m, s) feeds stage s.
+  //      Receive buffers + flags live in this process's inbox, acks in its outbox.
+  size_t in_bytes = 0, out_bytes = 0;
+  const auto in_lay = I.inbox_layout(I.proc, &in_bytes);
+  const auto out_lay = I.outbox_layout(I.proc, &out_bytes);
+  CK_CUDA(cudaMalloc(&I.inbox, in_bytes));
+  CK_CUDA(cudaMalloc(&I.outbox, out_bytes));
+  CK_CUDA(cudaMemset(I.inbox, 0, in_bytes));  // flags start at 0
+  {
+    std::vector<uint32_t> ones(out_bytes / 4, 1u);  // acks start at 1
+    CK_CUDA(cudaMemcpy(I.outbox, ones.data(), out_bytes, cudaMemcpyHostToDevice));
+  }
   for (int r = 0; r < I.W; ++r)
     for (int mb = 0; mb < I.N; ++mb)
       for (int s = 0; s + 1 < I.D; ++s)
         for (int dir = 0; dir < 2; ++dir) {
+          Msg g;
+          g.producer = I.producer_of(r, mb, s, dir);
+          g.consumer = I.consumer_of(r, mb, s, dir);
+          g.prod_local = I.local(g.producer);
+          g.cons_local = I.local(g.consumer);
+          if (!g.prod_local && !g.cons_local) continue;
           const long long k = I.msg_key(r, mb, s, dir);
-          I.msg[k] = I.arena.alloc<bf16>((size_t)M * h);
-          cudaEvent_t e;
-          CK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-          I.msg_ev[k] = e;
+          if (g.cons_local) {
+            const auto& sl = in_lay.at(k);
+            g.buf = reinterpret_cast<bf16*>(static_cast<char*>(I.inbox) + sl.buf);
+            g.flag = reinterpret_cast<uint32_t*>(static_cast<char*>(I.inbox) + sl.flag);
+          }
+          if (g.prod_local && !g.cons_local)
+            g.ack = reinterpret_cast<uint32_t*>(static_cast<char*>(I.outbox) + out_lay.at(k));
+          if (g.prod_local && g.cons_local)
+            CK_CUDA(cudaEventCreateWithFlags(&g.ev, cudaEventDisableTiming));
+          I.msgs[k] = g;
         }
+  I.connected = I.procs == 1;
   const size_t toks = (size_t)I.W * I.N * I.B * shape.seq;
   I.tokens = I.arena.alloc<int32_t>(toks);
   I.labels = I.arena.alloc<int32_t>(toks);
@@ -296,7 +385,16 @@ Trainer::~Trainer() {
   Impl& I = *d_;
   if (I.graph_exec) cudaGraphExecDestroy(I.graph_exec);
   if (I.graph) cudaGraphDestroy(I.graph);
-  for (auto& kv : I.msg_ev) cudaEventDestroy(kv.second);
+  for (auto& kv : I.msgs)
+    if (kv.second.ev) cudaEventDestroy(kv.second.ev);
+  for (auto& kv : I.stage_comm) ncclCommDestroy(kv.second);
+  if (I.world_comm) ncclCommDestroy(I.world_comm);
+  for (void* p : I.peer_inbox)
+    if (p) cudaIpcCloseMemHandle(p);
+  for (void* p : I.peer_outbox)
+    if (p) cudaIpcCloseMemHandle(p);
+  cudaFree(I.inbox);
+  cudaFree(I.outbox);
   for (auto e : I.rank_done) cudaEventDestroy(e);
   cudaEventDestroy(I.start_ev);
   cudaEventDestroy(I.upd_ev);
@@ -340,11 +438,13 @@ void Trainer::forward_task(int rank, int p, int mb, int s) {
     ops::embed_fwd(I.tokens + tok0, w + L.wte, w + L.wpe, X.x0, M, m.seq, h, st);
     x = X.x0;
   } else {
-    const long long k = I.msg_key(r, mb, s - 1, 0);
-    CK_CUDA(cudaStreamWaitEvent(st, I.msg_ev.at(k), 0));
-    x = I.msg.at(k);
+    const Msg& in = I.msgs.at(I.msg_key(r, mb, s - 1, 0));
+    in.before_consume(st);
+    x = in.buf;
   }
-  bf16* out_final = (s + 1 < I.D) ? I.msg.at(I.msg_key(r, mb, s, 0)) : X.xfinal;
+  const Msg* out_msg = (s + 1 < I.D) ? &I.msgs.at(I.msg_key(r, mb, s, 0)) : nullptr;
+  if (out_msg) out_msg->before_produce(st);
+  bf16* out_final = out_msg ? out_msg->buf : X.xfinal;
   for (int l = 0; l < L.n_layers; ++l) {
     const LayerOffsets& o = L.layers[l];
     LayerStash& A = X.layers[l];
@@ -372,7 +472,7 @@ void Trainer::forward_task(int rank, int p, int mb, int s) {
                       I.loss, st);
     I.launches_per_step += 3;
   } else {
-    CK_CUDA(cudaEventRecord(I.msg_ev.at(I.msg_key(r, mb, s, 0)), st));
+    out_msg->after_produce(st);
   }
   if (s == 0) I.launches_per_step += 1;
 }
@@ -406,16 +506,18 @@ void Trainer::backward_task(int rank, int p, int mb, int s) {
     dxo = sc.dxa;
     I.launches_per_step += 3;
   } else {
-    const long long k = I.msg_key(r, mb, s, 1);
-    CK_CUDA(cudaStreamWaitEvent(st, I.msg_ev.at(k), 0));
-    dxo = I.msg.at(k);
+    const Msg& in = I.msgs.at(I.msg_key(r, mb, s, 1));
+    in.before_consume(st);
+    dxo = in.buf;
   }
-  bf16* dx_stage = (s > 0) ? I.msg.at(I.msg_key(r, mb, s - 1, 1)) : nullptr;
+  const Msg* out_msg = (s > 0) ? &I.msgs.at(I.msg_key(r, mb, s - 1, 1)) : nullptr;
+  if (out_msg) out_msg->before_produce(st);
+  bf16* dx_stage = out_msg ? out_msg->buf : nullptr;
   for (int l = L.n_layers - 1; l >= 0; --l) {
     const LayerOffsets& o = L.layers[l];
     LayerStash& A = X.layers[l];
     const bf16* xin = (l > 0) ? X.layers[l - 1].xo
-                              : (s == 0 ? X.x0 : I.msg.at(I.msg_key(r, mb, s - 1, 0)));
+                              : (s == 0 ? X.x0 : I.msgs.at(I.msg_key(r, mb, s - 1, 0)).buf);
     bf16* dxin = (l > 0) ? (dxo == sc.dxa ? sc.dxb : sc.dxa) : (dx_stage ? dx_stage : (dxo == sc.dxa ? sc.dxb : sc.dxa));
     // MLP
     ops::bias_grad(dxo, gw + o.b_fc2, M, h, st);
@@ -441,8 +543,11 @@ void Trainer::backward_task(int rank, int p, int mb, int s) {
     ops::embed_bwd(I.tokens + tok0, dxo, gw + L.wte, gw + L.wpe, M, m.seq, h, st);
     I.launches_per_step += 1;
   } else {
-    CK_CUDA(cudaEventRecord(I.msg_ev.at(I.msg_key(r, mb, s - 1, 1)), st));
+    out_msg->after_produce(st);
   }
+  // this task was the last reader of its input messages
+  if (s > 0) I.msgs.at(I.msg_key(r, mb, s - 1, 0)).after_last_use(st);
+  if (s + 1 < I.D) I.msgs.at(I.msg_key(r, mb, s, 1)).after_last_use(st);
   cp.free_slots.push_back(slot);
 }
 
@@ -472,15 +577,32 @@ void Trainer::issue_iteration() {
     CK_CUDA(cudaEventRecord(I.rank_done[k], I.streams[k]));
     CK_CUDA(cudaStreamWaitEvent(I.main_stream, I.rank_done[k], 0));
   }
-  // gradient synchronisation + SGD, stage by stage
+  // gradient synchronisation + SGD, stage by stage in ascending stage order (the same
+  // order on every process, so collectives on overlapping groups cannot deadlock)
   for (auto& [s, S] : I.stages) {
-    ops::sgd_update(S.w32, S.w16, S.grads.data(), int(S.grads.size()), S.L.total, I.lr, I.main_stream);
+    auto it = I.stage_comm.find(s);
+    if (it == I.stage_comm.end()) {
+      ops::sgd_update(S.w32, S.w16, S.grads.data(), int(S.grads.size()), S.L.total, I.lr, I.main_stream);
+      I.launches_per_step += 1;
+      continue;
+    }
+    float* g0 = S.grads[0];
+    if (S.grads.size() > 1) {
+      ops::reduce_copies(g0, S.grads.data(), int(S.grads.size()), S.L.total, I.main_stream);
+      for (size_t c = 1; c < S.grads.size(); ++c)
+        CK_CUDA(cudaMemsetAsync(S.grads[c], 0, S.L.total * sizeof(float), I.main_stream));
+      I.launches_per_step += 1;
+    }
+    if (ncclAllReduce(g0, g0, S.L.total, ncclFloat, ncclSum, it->second, I.main_stream) != ncclSuccess)
+      throw capi::InternalError("ncclAllReduce failed");
+    ops::sgd_update(S.w32, S.w16, &g0, 1, S.L.total, I.lr, I.main_stream);
     I.launches_per_step += 1;
   }
 }
 
 float Trainer::step() {
   Impl& I = *d_;
+  if (!I.connected) throw capi::InternalError("multi-process trainer: call connect() first");
   if (!I.use_graph || I.steps == 0) {
     issue_iteration();
   } else {
@@ -549,6 +671,81 @@ void Trainer::get_params(int s, float* host) const {
   const StageState& S = d_->stages.at(s);
   CK_CUDA(cudaDeviceSynchronize());
   CK_CUDA(cudaMemcpy(host, S.w32, S.L.total * sizeof(float), cudaMemcpyDeviceToHost));
+}
+
+std::string Trainer::ipc_export() const {
+  const Impl& I = *d_;
+  cudaIpcMemHandle_t a, b;
+  CK_CUDA(cudaIpcGetMemHandle(&a, I.inbox));
+  CK_CUDA(cudaIpcGetMemHandle(&b, I.outbox));
+  std::string out(2 * sizeof(cudaIpcMemHandle_t), '\0');
+  std::memcpy(&out[0], &a, sizeof a);
+  std::memcpy(&out[sizeof a], &b, sizeof b);
+  return out;
+}
+
+void Trainer::connect(const std::string& all_blobs, const std::string& nccl_id) {
+  Impl& I = *d_;
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  if (all_blobs.size() != size_t(I.procs) * 2 * hb) throw pipesim::InvalidConfigError("bad IPC blob size");
+  if (nccl_id.size() != sizeof(ncclUniqueId)) throw pipesim::InvalidConfigError("bad NCCL id size");
+  I.peer_inbox.assign(I.procs, nullptr);
+  I.peer_outbox.assign(I.procs, nullptr);
+  for (int q = 0; q < I.procs; ++q) {
+    if (q == I.proc) continue;
+    cudaIpcMemHandle_t a, b;
+    std::memcpy(&a, all_blobs.data() + q * 2 * hb, hb);
+    std::memcpy(&b, all_blobs.data() + q * 2 * hb + hb, hb);
+    CK_CUDA(cudaIpcOpenMemHandle(&I.peer_inbox[q], a, cudaIpcMemLazyEnablePeerAccess));
+    CK_CUDA(cudaIpcOpenMemHandle(&I.peer_outbox[q], b, cudaIpcMemLazyEnablePeerAccess));
+  }
+  // remote halves of the links: buffers/flags in the consumer's inbox, acks in the
+  // producer's outbox
+  std::map<int, std::map<long long, Impl::Slot>> in_lay;
+  std::map<int, std::map<long long, size_t>> out_lay;
+  for (auto& [k, g] : I.msgs) {
+    if (!g.cons_local) {
+      const int q = I.proc_of(g.consumer);
+      if (!in_lay.count(q)) {
+        size_t t;
+        in_lay[q] = I.inbox_layout(q, &t);
+      }
+      const auto& sl = in_lay[q].at(k);
+      g.buf = reinterpret_cast<bf16*>(static_cast<char*>(I.peer_inbox[q]) + sl.buf);
+      g.flag = reinterpret_cast<uint32_t*>(static_cast<char*>(I.peer_inbox[q]) + sl.flag);
+    }
+    if (!g.prod_local) {
+      const int q = I.proc_of(g.producer);
+      if (!out_lay.count(q)) {
+        size_t t;
+        out_lay[q] = I.outbox_layout(q, &t);
+      }
+      g.ack = reinterpret_cast<uint32_t*>(static_cast<char*>(I.peer_outbox[q]) + out_lay[q].at(k));
+    }
+  }
+  // NCCL: world communicator, then one split per stage whose holders span >1 process
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_id.data(), sizeof id);
+  if (ncclCommInitRank(&I.world_comm, I.procs, id, I.proc) != ncclSuccess)
+    throw capi::InternalError("ncclCommInitRank failed");
+  for (int s = 0; s < I.D; ++s) {
+    std::vector<int> holders;  // processes holding stage s
+    for (int r = 0; r < I.W; ++r)
+      for (int p = 0; p < I.P; ++p) {
+        auto it = I.worker_of.find({p, s});
+        if (it == I.worker_of.end()) continue;
+        const int q = I.proc_of(r * I.D + it->second);
+        if (std::find(holders.begin(), holders.end(), q) == holders.end()) holders.push_back(q);
+      }
+    if (holders.size() < 2) continue;
+    const bool mine = std::find(holders.begin(), holders.end(), I.proc) != holders.end();
+    ncclComm_t c = nullptr;
+    if (ncclCommSplit(I.world_comm, mine ? s : NCCL_SPLIT_NOCOLOR, I.proc, &c, nullptr) != ncclSuccess)
+      throw capi::InternalError("ncclCommSplit failed");
+    if (mine) I.stage_comm[s] = c;
+  }
+  CK_CUDA(cudaDeviceSynchronize());
+  I.connected = true;
 }
 
 std::string Trainer::layout_json() const {
@@ -658,5 +855,28 @@ CK_API int ck_gpt_set_graph(ck_gpt* h, int on) {
 }
 
 CK_API void* ck_gpt_stream(ck_gpt* h) { return h->t->stream(); }
+
+CK_API int ck_gpt_ipc_handles(ck_gpt* h, char* out, int cap) {
+  return chimera::capi::guarded([&] {
+    const std::string b = h->t->ipc_export();
+    if (cap < int(b.size())) throw pipesim::InvalidConfigError("buffer too small");
+    std::memcpy(out, b.data(), b.size());
+  });
+}
+
+CK_API int ck_gpt_connect(ck_gpt* h, const char* all_handles, int n_bytes, const char* nccl_id, int id_bytes) {
+  return chimera::capi::guarded([&] {
+    h->t->connect(std::string(all_handles, n_bytes), std::string(nccl_id, id_bytes));
+  });
+}
+
+CK_API int ck_nccl_unique_id(char* out, int cap) {
+  return chimera::capi::guarded([&] {
+    ncclUniqueId id;
+    if (cap < int(sizeof id)) throw pipesim::InvalidConfigError("buffer too small");
+    if (ncclGetUniqueId(&id) != ncclSuccess) throw chimera::capi::InternalError("ncclGetUniqueId failed");
+    std::memcpy(out, &id, sizeof id);
+  });
+}
 
 }  // extern "C"

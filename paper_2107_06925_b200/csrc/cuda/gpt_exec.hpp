@@ -24,6 +24,10 @@ class Trainer {
   std::string stats_json() const;
   void* stream() const;
   void set_use_graph(bool on);
+  // multi-process: this process's IPC handles (inbox, outbox), then connect with the
+  // handles of all processes (ordered by process index) and an NCCL unique id.
+  std::string ipc_export() const;
+  void connect(const std::string& all_handles, const std::string& nccl_id);
 
  private:
   struct Impl;

@@ -216,18 +216,34 @@ __global__ void __launch_bounds__(512) k_xent(bf16* __restrict__ logits, long lo
 }
 
 // ------------------------------------------------------------------ bias grad --
-// 128 threads x 2 columns = 256 columns per CTA, rows split in chunks of 256.
-__global__ void k_bias_grad(const bf16* __restrict__ dy, float* __restrict__ db, int M, int N) {
-  const int col = blockIdx.x * 256 + threadIdx.x * 2;
-  if (col >= N) return;
-  const int r0 = blockIdx.y * 256, r1 = min(M, r0 + 256);
-  float a = 0.f, b = 0.f;
-  for (int r = r0; r < r1; ++r) {
-    const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dy + (long long)r * N + col));
-    a += v.x, b += v.y;
+// CTA = 256 columns x 64 rows: 32 column groups of 8 (16-byte loads) x 8 row lanes;
+// per-thread fp32 partials, reduced over the 8 row lanes in shared memory, then one
+// atomic per column per CTA.
+__global__ void __launch_bounds__(256) k_bias_grad(const bf16* __restrict__ dy, float* __restrict__ db,
+                                                   int M, int N) {
+  __shared__ float red[8][256 + 8];
+  const int cg = threadIdx.x & 31, rl = threadIdx.x >> 5;
+  const int col = blockIdx.x * 256 + cg * 8;
+  const int r0 = blockIdx.y * 64;
+  float acc[8] = {};
+  if (col < N) {
+    for (int r = r0 + rl; r < min(M, r0 + 64); r += 8) {
+      Vec8 v;
+      v.load(dy + (long long)r * N + col);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc[t] += v.f[t];
+    }
   }
-  atomicAdd(db + col, a);
-  if (col + 1 < N) atomicAdd(db + col + 1, b);
+#pragma unroll
+  for (int t = 0; t < 8; ++t) red[rl][cg * 8 + t] = acc[t];
+  __syncthreads();
+  const int c = threadIdx.x;
+  if (blockIdx.x * 256 + c < N) {
+    float sum = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sum += red[k][c];
+    atomicAdd(db + blockIdx.x * 256 + c, sum);
+  }
 }
 
 // -------------------------------------------------------------------- update --
@@ -235,32 +251,24 @@ struct GradPtrs {
   float* p[8];
 };
 
-__global__ void k_sgd(float* __restrict__ w32, bf16* __restrict__ w16, GradPtrs g, int copies,
-                      long long n, float lr) {
-  for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 4; i < n;
-       i += (long long)gridDim.x * blockDim.x * 4) {
-    if (i + 4 <= n) {
-      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int c = 0; c < copies; ++c) {
-        float4* q = reinterpret_cast<float4*>(g.p[c] + i);
-        const float4 v = *q;
-        s.x += v.x, s.y += v.y, s.z += v.z, s.w += v.w;
-        *q = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      float4 w = *reinterpret_cast<float4*>(w32 + i);
-      w.x -= lr * s.x, w.y -= lr * s.y, w.z -= lr * s.z, w.w -= lr * s.w;
-      *reinterpret_cast<float4*>(w32 + i) = w;
-      __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(w16 + i);
-      o[0] = __floats2bfloat162_rn(w.x, w.y);
-      o[1] = __floats2bfloat162_rn(w.z, w.w);
-    } else {
-      for (long long j = i; j < n; ++j) {
-        float s = 0.f;
-        for (int c = 0; c < copies; ++c) s += g.p[c][j], g.p[c][j] = 0.f;
-        w32[j] -= lr * s;
-        w16[j] = __float2bfloat16_rn(w32[j]);
-      }
-    }
+template <int COPIES>
+__global__ void __launch_bounds__(256) k_sgd(float* __restrict__ w32, bf16* __restrict__ w16, GradPtrs g,
+                                             long long n, float lr) {
+  const long long stride = (long long)gridDim.x * blockDim.x * 4;
+  for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
+    float4 v[COPIES];
+#pragma unroll
+    for (int c = 0; c < COPIES; ++c) v[c] = __ldcs(reinterpret_cast<const float4*>(g.p[c] + i));
+    float4 w = __ldcs(reinterpret_cast<const float4*>(w32 + i));
+    float4 s = v[0];
+#pragma unroll
+    for (int c = 1; c < COPIES; ++c) s.x += v[c].x, s.y += v[c].y, s.z += v[c].z, s.w += v[c].w;
+    w.x -= lr * s.x, w.y -= lr * s.y, w.z -= lr * s.z, w.w -= lr * s.w;
+    __stcs(reinterpret_cast<float4*>(w32 + i), w);
+    __nv_bfloat162 h[2] = {__floats2bfloat162_rn(w.x, w.y), __floats2bfloat162_rn(w.z, w.w)};
+    *reinterpret_cast<uint2*>(w16 + i) = *reinterpret_cast<uint2*>(h);
+#pragma unroll
+    for (int c = 0; c < COPIES; ++c) __stcs(reinterpret_cast<float4*>(g.p[c] + i), make_float4(0.f, 0.f, 0.f, 0.f));
   }
 }
 
@@ -340,16 +348,23 @@ void xent_fwd_bwd(bf16* logits, long long ld, const int32_t* labels, int M, int 
 }
 
 void bias_grad(const bf16* dy, float* db, int M, int N, cudaStream_t st) {
-  k_bias_grad<<<dim3(ceil_div(N, 256), ceil_div(M, 256)), 128, 0, st>>>(dy, db, M, N);
+  if (N % 8) throw chimera::capi::InternalError("bias_grad: N % 8 != 0");
+  k_bias_grad<<<dim3(ceil_div(N, 256), ceil_div(M, 64)), 256, 0, st>>>(dy, db, M, N);
   CK_CUDA(cudaGetLastError());
 }
 
 void sgd_update(float* w32, bf16* w16, float* const* grads, int copies, long long n, float lr,
                 cudaStream_t st) {
   if (copies < 1 || copies > 8) throw chimera::capi::InternalError("sgd: 1..8 gradient copies");
+  if (n % 4) throw chimera::capi::InternalError("sgd: n % 4 != 0");
   GradPtrs g{};
   for (int c = 0; c < copies; ++c) g.p[c] = grads[c];
-  k_sgd<<<grid_for(n, 4), 256, 0, st>>>(w32, w16, g, copies, n, lr);
+  const int grid = grid_for(n, 4);
+  switch (copies) {
+#define CK_SGD(C) case C: k_sgd<C><<<grid, 256, 0, st>>>(w32, w16, g, n, lr); break;
+    CK_SGD(1) CK_SGD(2) CK_SGD(3) CK_SGD(4) CK_SGD(5) CK_SGD(6) CK_SGD(7) CK_SGD(8)
+#undef CK_SGD
+  }
   CK_CUDA(cudaGetLastError());
 }
 

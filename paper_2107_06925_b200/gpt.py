@@ -40,6 +40,15 @@ _lib.register("ck_gpt_step", C.c_int, [_vp, C.POINTER(C.c_float)])
 _lib.register("ck_gpt_launch", C.c_int, [_vp])
 _lib.register("ck_gpt_set_graph", C.c_int, [_vp, C.c_int])
 _lib.register("ck_gpt_stream", _vp, [_vp])
+_lib.register("ck_gpt_ipc_handles", C.c_int, [_vp, C.c_char_p, C.c_int])
+_lib.register("ck_gpt_connect", C.c_int, [_vp, C.c_char_p, C.c_int, C.c_char_p, C.c_int])
+_lib.register("ck_nccl_unique_id", C.c_int, [C.c_char_p, C.c_int])
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib().ck_nccl_unique_id(buf, 128))
+    return buf.raw
 
 
 @dataclass(frozen=True)
@@ -176,6 +185,24 @@ class Trainer:
 
     def stats(self) -> dict:
         return json.loads(call_str(lib().ck_gpt_stats, self._h))
+
+    def ipc_handles(self) -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().ck_gpt_ipc_handles(self._h, buf, 128))
+        return buf.raw
+
+    def connect(self):
+        """Multi-process wiring over torch.distributed (any backend; gloo is enough):
+        all-gather the CUDA-IPC handles of every process's inbox/outbox and broadcast
+        one NCCL unique id, then open the peer mappings and the stage communicators."""
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(), dist.get_rank()
+        blobs = [None] * world
+        dist.all_gather_object(blobs, self.ipc_handles())
+        uid = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        allb = b"".join(blobs)
+        check(lib().ck_gpt_connect(self._h, allb, len(allb), uid[0], len(uid[0])))
 
 
 def smoke():
