@@ -263,19 +263,42 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t)
 
+    # ---- one profiled (eager) iteration: per-task GPU spans -> measured bubble
+    if world > 1:
+        dist.barrier()
+    prof = tr.profile_step()
+    tasks = prof["tasks"]
+    if world > 1:
+        allt = [None] * world
+        dist.all_gather_object(allt, tasks)
+        tasks = [t for x in allt for t in x]
+
     stats = tr.stats()
     if world > 1:  # the loss is summed over the processes holding last stages
         t = torch.tensor([loss])
         dist.all_reduce(t)
         loss = float(t)
-        pk = [None] * world
-        dist.all_gather_object(pk, stats["peak_stash_per_rank"])
-        stats["peak_stash_per_rank"] = [v for x in pk for v in x]
+        for key in ("peak_stash_per_rank", "peak_stash_bytes_per_rank"):
+            pk = [None] * world
+            dist.all_gather_object(pk, stats[key])
+            stats[key] = [v for x in pk for v in x]
     peak, peak_sus, hbm, peak_src = peaks()
     line = None
     if rank == 0:
         sched = tr.schedule_text
         bub = P.bubble_ratio(sched)
+        from fractions import Fraction
+        from paper_2107_06925_b200.gpt import measured_bubble, timeline_json
+        fwd = [t["end_ms"] - t["start_ms"] for t in tasks if t["kind"] == "Forward"]
+        bwd = [t["end_ms"] - t["start_ms"] for t in tasks if t["kind"] == "Backward"]
+        ratio = (sum(bwd) / len(bwd)) / (sum(fwd) / len(fwd))
+        prof_m = P.CostProfile(backward_ratio=float(Fraction(ratio).limit_denominator(16)))
+        bub_at_ratio = P.bubble_ratio(P.generate_json(cfg, prof_m, -1), prof_m)
+        one_rank_per_gpu = per == 1
+        mb = measured_bubble({"tasks": tasks}) if one_rank_per_gpu else None
+        if os.environ.get("CK_TIMELINE"):
+            with open(os.environ["CK_TIMELINE"], "w") as fh:
+                fh.write(timeline_json({"tasks": tasks}, sched))
         mp = P.memory_profile(sched)
         rl = gemm_roofline(tr.stream_handle(), peak)
         flops_seq = shape.flops_per_seq()
@@ -295,11 +318,17 @@ def main():
             "mfu": {"tflops_per_gpu": round(value * flops_seq / world / 1e12, 1),
                     "frac_of_sustained": round(value * flops_seq / world / 1e12 / peak_sus, 4) if peak_sus else None,
                     "flop_per_seq": flops_seq, "peak_source": peak_src},
-            "bubble": {"schedule": str(bub), "closed_form": str(P.closed_form_bubble(cfg.D, cfg.N)),
-                       "measured": None,
-                       "note": "all logical ranks share the GPU(s) at N<8: bubble not observable per rank"},
+            "bubble": {"measured": (round(sum(mb["per_rank"].values()) / len(mb["per_rank"]), 4) if mb else None),
+                       "measured_per_rank": ([round(v, 4) for v in mb["per_rank"].values()] if mb else None),
+                       "closed_form_(D-2)/(2N+D-2)": str(P.closed_form_bubble(cfg.D, cfg.N)),
+                       "reference_schedule_at_B/F=2": str(bub),
+                       "measured_B/F": round(ratio, 3),
+                       "reference_schedule_at_measured_B/F": str(bub_at_ratio),
+                       "note": (None if one_rank_per_gpu else
+                                f"{per} logical ranks share each GPU: per-rank bubble not observable")},
             "act_counts_per_worker": mp["act_counts"],
             "peak_stash_per_rank": stats["peak_stash_per_rank"],
+            "peak_stash_bytes_per_rank": stats["peak_stash_bytes_per_rank"],
             "device_bytes": stats["device_bytes"],
             "loss": loss,
             "gpu_launches": int(stats["launches_per_step"] * args.steps),

@@ -139,6 +139,10 @@ CK_API int ck_gpt_set_batch(ck_gpt* h, const int32_t* tokens, const int32_t* lab
                             int from_host);
 /* one iteration (all micro-batches, gradient sync, SGD); *loss = mean token loss. */
 CK_API int ck_gpt_step(ck_gpt* h, float* loss);
+/* one eager iteration with CUDA-event timestamps around every task on its rank's
+ * stream: JSON {iteration_ms, tasks:[{rank, kind, pipeline, micro, stage, start_ms,
+ * end_ms}]} relative to the iteration start on this process. */
+CK_API int ck_gpt_profile_step(ck_gpt* h, char** out_json);
 /* enqueue one iteration on the trainer stream without waiting (graph replay). */
 CK_API int ck_gpt_launch(ck_gpt* h);
 CK_API int ck_gpt_set_graph(ck_gpt* h, int on);

@@ -129,9 +129,27 @@ struct Trainer::Impl {
   std::vector<std::pair<int, int>> order;
   std::map<std::array<int, 4>, int> slot_of;  // (rank, p, m, s) -> slot index during issue
   std::vector<int> peak_live;                  // per local rank
+  std::map<std::array<int, 2>, long long> slot_bytes;  // (rank, pipeline) -> bytes of one stash
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   bool use_graph = true;
+  // profiled iteration: timing events around every task on its rank's stream
+  bool profiling = false;
+  struct TaskSpan {
+    int rank, kind, pipeline, micro, stage;
+    cudaEvent_t a, b;
+  };
+  std::vector<TaskSpan> spans;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_next = 0;
+  cudaEvent_t timed_event() {
+    if (ev_next == ev_pool.size()) {
+      cudaEvent_t e;
+      CK_CUDA(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_next++];
+  }
   int steps = 0;
   long long launches_per_step = 0;
 
@@ -283,6 +301,7 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
   for (auto& [key, cp] : I.copies) {
     const StageLayout& L = I.stages[cp.stage].L;
     const int nslots = peak[key];
+    const size_t before = I.arena.bytes;
     for (int k = 0; k < nslots; ++k) {
       Stash st;
       if (L.has_embed) st.x0 = I.arena.alloc<bf16>((size_t)M * h);
@@ -312,6 +331,7 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
       }
       cp.slots.push_back(std::move(st));
     }
+    I.slot_bytes[key] = nslots ? (long long)((I.arena.bytes - before) / nslots) : 0;
   }
   // ---- per-rank scratch and streams
   for (int k = 0; k < n_ranks; ++k) {
@@ -396,6 +416,7 @@ Trainer::~Trainer() {
   cudaFree(I.inbox);
   cudaFree(I.outbox);
   for (auto e : I.rank_done) cudaEventDestroy(e);
+  for (auto e : I.ev_pool) cudaEventDestroy(e);
   cudaEventDestroy(I.start_ev);
   cudaEventDestroy(I.upd_ev);
   for (size_t k = 0; k < I.streams.size(); ++k)
@@ -569,8 +590,18 @@ void Trainer::issue_iteration() {
     for (int r = 0; r < I.W; ++r) {
       const int rank = r * I.D + w;
       if (!I.local(rank)) continue;
+      Impl::TaskSpan sp{rank, int(t.kind), t.pipeline_id, t.micro_batch, t.stage, nullptr, nullptr};
+      if (I.profiling) {
+        sp.a = I.timed_event();
+        CK_CUDA(cudaEventRecord(sp.a, I.stream_of(rank)));
+      }
       if (t.kind == TaskKind::Forward) forward_task(rank, t.pipeline_id, t.micro_batch, t.stage);
       else backward_task(rank, t.pipeline_id, t.micro_batch, t.stage);
+      if (I.profiling) {
+        sp.b = I.timed_event();
+        CK_CUDA(cudaEventRecord(sp.b, I.stream_of(rank)));
+        I.spans.push_back(sp);
+      }
     }
   }
   for (int k = 0; k < I.nlocal; ++k) {
@@ -619,6 +650,49 @@ float Trainer::step() {
   CK_CUDA(cudaMemcpyAsync(&loss, I.loss, sizeof(float), cudaMemcpyDeviceToHost, I.main_stream));
   CK_CUDA(cudaStreamSynchronize(I.main_stream));
   return loss;
+}
+
+std::string Trainer::profile_step() {
+  Impl& I = *d_;
+  if (!I.connected) throw capi::InternalError("multi-process trainer: call connect() first");
+  I.spans.clear();
+  I.ev_next = 0;
+  cudaEvent_t t0 = I.timed_event();
+  CK_CUDA(cudaEventRecord(t0, I.main_stream));
+  I.profiling = true;
+  try {
+    issue_iteration();
+  } catch (...) {
+    I.profiling = false;
+    throw;
+  }
+  I.profiling = false;
+  cudaEvent_t t1 = I.timed_event();
+  CK_CUDA(cudaEventRecord(t1, I.main_stream));
+  CK_CUDA(cudaStreamSynchronize(I.main_stream));
+  ++I.steps;
+  using json::Value;
+  Value arr = Value::array();
+  for (const auto& sp : I.spans) {
+    float a = 0, b = 0;
+    CK_CUDA(cudaEventElapsedTime(&a, t0, sp.a));
+    CK_CUDA(cudaEventElapsedTime(&b, t0, sp.b));
+    Value x = Value::object();
+    x.set("rank", Value::integer(sp.rank));
+    x.set("kind", Value::string(sp.kind == int(TaskKind::Forward) ? "Forward" : "Backward"));
+    x.set("pipeline", Value::integer(sp.pipeline));
+    x.set("micro", Value::integer(sp.micro));
+    x.set("stage", Value::integer(sp.stage));
+    x.set("start_ms", Value::number(a));
+    x.set("end_ms", Value::number(b));
+    arr.push(std::move(x));
+  }
+  float tot = 0;
+  CK_CUDA(cudaEventElapsedTime(&tot, t0, t1));
+  Value j = Value::object();
+  j.set("iteration_ms", Value::number(tot));
+  j.set("tasks", std::move(arr));
+  return json::dump(j, -1);
 }
 
 void Trainer::launch_async() {
@@ -779,6 +853,15 @@ std::string Trainer::stats_json() const {
   for (int v : I.peak_live) pk.push(Value::integer(v));
   j.set("peak_stash_per_rank", std::move(pk));
   j.set("device_bytes", Value::integer((long long)I.arena.bytes));
+  Value sb = Value::array();  // peak live activation bytes per local rank (slot bytes x peak)
+  for (int k = 0; k < I.nlocal; ++k) {
+    const int rank = I.first + k;
+    long long bytes = 0;
+    for (const auto& [key, cp] : I.copies)
+      if (key[0] == rank && !cp.slots.empty()) bytes = std::max(bytes, I.slot_bytes.at(key));
+    sb.push(Value::integer(bytes * (long long)I.peak_live[k]));
+  }
+  j.set("peak_stash_bytes_per_rank", std::move(sb));
   j.set("launches_per_step", Value::integer(I.launches_per_step));
   j.set("graph", Value::boolean(I.graph_exec != nullptr));
   j.set("steps", Value::integer(I.steps));
@@ -844,6 +927,10 @@ CK_API int ck_gpt_set_batch(ck_gpt* h, const int32_t* tokens, const int32_t* lab
 
 CK_API int ck_gpt_step(ck_gpt* h, float* loss) {
   return chimera::capi::guarded([&] { *loss = h->t->step(); });
+}
+
+CK_API int ck_gpt_profile_step(ck_gpt* h, char** out_json) {
+  return chimera::capi::guarded([&] { *out_json = chimera::capi::dup_string(h->t->profile_step()); });
 }
 
 CK_API int ck_gpt_launch(ck_gpt* h) {

@@ -16,6 +16,7 @@ class Trainer {
   ~Trainer();
   float step();          // one full iteration, returns the loss
   void launch_async();   // enqueue one iteration (graph replay) without host sync
+  std::string profile_step();  // one eager iteration with per-task GPU timestamps (JSON)
   void upload_batch(const int32_t* tokens, const int32_t* labels, bool from_host, void* stream);
   void set_params(int stage, const float* host);
   void get_params(int stage, float* host) const;

@@ -38,6 +38,7 @@ _lib.register("ck_gpt_get_params", C.c_int, [_vp, C.c_int, _lib._fp])
 _lib.register("ck_gpt_set_batch", C.c_int, [_vp, _vp, _vp, C.c_int])
 _lib.register("ck_gpt_step", C.c_int, [_vp, C.POINTER(C.c_float)])
 _lib.register("ck_gpt_launch", C.c_int, [_vp])
+_lib.register("ck_gpt_profile_step", C.c_int, [_vp, C.POINTER(_vp)])
 _lib.register("ck_gpt_set_graph", C.c_int, [_vp, C.c_int])
 _lib.register("ck_gpt_stream", _vp, [_vp])
 _lib.register("ck_gpt_ipc_handles", C.c_int, [_vp, C.c_char_p, C.c_int])
@@ -174,6 +175,10 @@ class Trainer:
         check(lib().ck_gpt_step(self._h, C.byref(loss)))
         return loss.value
 
+    def profile_step(self) -> dict:
+        """One eager iteration with per-task GPU timestamps (see measured_bubble)."""
+        return json.loads(call_str(lib().ck_gpt_profile_step, self._h))
+
     def launch(self):
         check(lib().ck_gpt_launch(self._h))
 
@@ -203,6 +208,39 @@ class Trainer:
         dist.broadcast_object_list(uid, src=0)
         allb = b"".join(blobs)
         check(lib().ck_gpt_connect(self._h, allb, len(allb), uid[0], len(uid[0])))
+
+
+def measured_bubble(profile: dict, ranks=None) -> dict:
+    """Per-rank idle fraction of a profiled iteration with the dessim definition
+    (proj/src/dessim.cpp:168-181): idle_w = (span_end - span_start) - busy_w
+    over the iteration span, busy_w = sum of the rank's task durations."""
+    tasks = profile["tasks"]
+    lo = min(t["start_ms"] for t in tasks)
+    hi = max(t["end_ms"] for t in tasks)
+    out = {}
+    for r in sorted({t["rank"] for t in tasks} if ranks is None else ranks):
+        busy = sum(t["end_ms"] - t["start_ms"] for t in tasks if t["rank"] == r)
+        out[r] = ((hi - lo) - busy) / (hi - lo)
+    return {"per_rank": out, "span_ms": hi - lo}
+
+
+def timeline_json(profile: dict, schedule_text: str) -> str:
+    """Measured timeline in the reference's Schedule JSON layout with `timing`
+    (proj/src/core.cpp:205-216), so reference tooling (bubble_ratio, gantt) can read it.
+    Times are milliseconds from the iteration start; replica 0's ranks only."""
+    sched = json.loads(schedule_text)
+    D = sched["config"]["D"]
+    spans = {(t["rank"] % D, t["kind"], t["pipeline"], t["micro"], t["stage"]): (t["start_ms"], t["end_ms"])
+             for t in profile["tasks"] if t["rank"] < D}
+    timing = []
+    for w, wl in enumerate(sched["per_worker"]):
+        row = []
+        for t in wl:
+            a, b = spans.get((w, t["kind"], t["pipeline_id"], t["micro_batch"], t["stage"]), (0.0, 0.0))
+            row.append({"start": a, "end": b})
+        timing.append(row)
+    sched["timing"] = timing
+    return json.dumps(sched)
 
 
 def smoke():
