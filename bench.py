@@ -203,6 +203,7 @@ def main():
     from paper_2107_06925_b200 import pipesim as P
     from paper_2107_06925_b200.gpt import Trainer, synthetic_batch
 
+    os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -274,7 +275,11 @@ def main():
         tasks = [t for x in allt for t in x]
 
     stats = tr.stats()
+    launches = int(stats["launches_per_step"] * args.steps)
     if world > 1:  # the loss is summed over the processes holding last stages
+        t = torch.tensor([launches], dtype=torch.float64)
+        dist.all_reduce(t)
+        launches = int(t)
         t = torch.tensor([loss])
         dist.all_reduce(t)
         loss = float(t)
@@ -331,7 +336,7 @@ def main():
             "peak_stash_bytes_per_rank": stats["peak_stash_bytes_per_rank"],
             "device_bytes": stats["device_bytes"],
             "loss": loss,
-            "gpu_launches": int(stats["launches_per_step"] * args.steps),
+            "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }

@@ -154,6 +154,10 @@ CK_API int ck_gpt_ipc_handles(ck_gpt* h, char* out, int cap);
 CK_API int ck_gpt_connect(ck_gpt* h, const char* all_handles, int n_bytes, const char* nccl_id,
                           int id_bytes);
 CK_API int ck_nccl_unique_id(char* out, int cap);
+/* Host-only: the cross-process message plan (producer/consumer ranks, every process's
+ * inbox/outbox layout, stage allreduce groups) for `ranks_per_proc` ranks per process. */
+CK_API int ck_link_plan(const char* schedule_json, int ranks_per_proc, long long msg_bytes,
+                        char** out_json);
 
 #ifdef __cplusplus
 }

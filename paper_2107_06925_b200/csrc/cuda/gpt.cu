@@ -37,6 +37,7 @@
 #include "gemm.cuh"
 #include "gpt_exec.hpp"
 #include "json_io.hpp"
+#include "link_plan.hpp"
 #include "links.hpp"
 #include "ops.cuh"
 #include "pipesim/analysis.hpp"
@@ -158,45 +159,8 @@ struct Trainer::Impl {
   long long msg_key(int r, int mb, int s, int dir) const {
     return (((long long)r * N + mb) * D + s) * 2 + dir;
   }
-  int proc_of(int rank) const { return rank / per; }
-  // producer / consumer rank of message (r, mb, s, dir): fwd s -> s+1, bwd s+1 -> s
-  int producer_of(int r, int mb, int s, int dir) const {
-    return r * D + worker_of.at({micro_pipeline[mb], dir == 0 ? s : s + 1});
-  }
-  int consumer_of(int r, int mb, int s, int dir) const {
-    return r * D + worker_of.at({micro_pipeline[mb], dir == 0 ? s + 1 : s});
-  }
-  // Deterministic inbox / outbox layouts of process q (identical on every process).
-  struct Slot {
-    size_t buf = 0, flag = 0;
-  };
-  size_t msg_bytes() const { return ((size_t)M * m.hidden * 2 + 255) / 256 * 256; }
-  std::map<long long, Slot> inbox_layout(int q, size_t* total) const {
-    std::map<long long, Slot> out;
-    std::vector<long long> keys;
-    for (int r = 0; r < W; ++r)
-      for (int mb = 0; mb < N; ++mb)
-        for (int s = 0; s + 1 < D; ++s)
-          for (int dir = 0; dir < 2; ++dir)
-            if (proc_of(consumer_of(r, mb, s, dir)) == q) keys.push_back(msg_key(r, mb, s, dir));
-    size_t off = 0;
-    for (long long k : keys) out[k].buf = off, off += msg_bytes();
-    for (long long k : keys) out[k].flag = off, off += 4;
-    *total = std::max<size_t>(off, 256);
-    return out;
-  }
-  std::map<long long, size_t> outbox_layout(int q, size_t* total) const {
-    std::map<long long, size_t> out;
-    size_t off = 0;
-    for (int r = 0; r < W; ++r)
-      for (int mb = 0; mb < N; ++mb)
-        for (int s = 0; s + 1 < D; ++s)
-          for (int dir = 0; dir < 2; ++dir)
-            if (proc_of(producer_of(r, mb, s, dir)) == q && proc_of(consumer_of(r, mb, s, dir)) != q)
-              out[msg_key(r, mb, s, dir)] = off, off += 4;
-    *total = std::max<size_t>(off, 256);
-    return out;
-  }
+  std::unique_ptr<plan::LinkPlan> lp;  // cross-process message plan (host/link_plan.hpp)
+  int proc_of(int rank) const { return lp->proc_of(rank); }
 };
 
 namespace {
@@ -238,17 +202,9 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
   I.per = n_ranks;
   I.procs = I.W * I.D / n_ranks;
   I.proc = first_rank / n_ranks;
-  I.micro_pipeline.assign(I.N, -1);
-  for (int w = 0; w < I.D; ++w)
-    for (const Task& t : sched.per_worker[w]) {
-      if (t.kind != TaskKind::Forward && t.kind != TaskKind::Backward) continue;
-      if (t.micro_batch < 0 || t.micro_batch >= I.N || t.stage < 0 || t.stage >= I.D)
-        throw pipesim::InvalidConfigError("task out of range");
-      I.micro_pipeline[t.micro_batch] = t.pipeline_id;
-      I.worker_of[{t.pipeline_id, t.stage}] = w;
-    }
-  for (int mb = 0; mb < I.N; ++mb)
-    if (I.micro_pipeline[mb] < 0) throw pipesim::InvalidConfigError("micro-batch without tasks");
+  I.lp = std::make_unique<plan::LinkPlan>(sched, n_ranks, ((size_t)I.M * shape.hidden * 2 + 255) / 256 * 256);
+  I.micro_pipeline = I.lp->micro_pipeline;
+  I.worker_of = I.lp->worker_of;
   cuda::require_sm100();
 
   const int h = shape.hidden, f = shape.ffn, Ls = shape.n_layer / I.D, M = I.M;
@@ -360,8 +316,8 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
   // ---- messages: fwd (r, m, s) feeds stage s+1; bwd (r, m, s) feeds stage s.
   //      Receive buffers + flags live in this process's inbox, acks in its outbox.
   size_t in_bytes = 0, out_bytes = 0;
-  const auto in_lay = I.inbox_layout(I.proc, &in_bytes);
-  const auto out_lay = I.outbox_layout(I.proc, &out_bytes);
+  const auto in_lay = I.lp->inbox_layout(I.proc, &in_bytes);
+  const auto out_lay = I.lp->outbox_layout(I.proc, &out_bytes);
   CK_CUDA(cudaMalloc(&I.inbox, in_bytes));
   CK_CUDA(cudaMalloc(&I.outbox, out_bytes));
   CK_CUDA(cudaMemset(I.inbox, 0, in_bytes));  // flags start at 0
@@ -374,8 +330,8 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
       for (int s = 0; s + 1 < I.D; ++s)
         for (int dir = 0; dir < 2; ++dir) {
           Msg g;
-          g.producer = I.producer_of(r, mb, s, dir);
-          g.consumer = I.consumer_of(r, mb, s, dir);
+          g.producer = I.lp->producer_of(r, mb, s, dir);
+          g.consumer = I.lp->consumer_of(r, mb, s, dir);
           g.prod_local = I.local(g.producer);
           g.cons_local = I.local(g.consumer);
           if (!g.prod_local && !g.cons_local) continue;
@@ -775,14 +731,14 @@ void Trainer::connect(const std::string& all_blobs, const std::string& nccl_id) 
   }
   // remote halves of the links: buffers/flags in the consumer's inbox, acks in the
   // producer's outbox
-  std::map<int, std::map<long long, Impl::Slot>> in_lay;
+  std::map<int, std::map<long long, plan::LinkPlan::Slot>> in_lay;
   std::map<int, std::map<long long, size_t>> out_lay;
   for (auto& [k, g] : I.msgs) {
     if (!g.cons_local) {
       const int q = I.proc_of(g.consumer);
       if (!in_lay.count(q)) {
         size_t t;
-        in_lay[q] = I.inbox_layout(q, &t);
+        in_lay[q] = I.lp->inbox_layout(q, &t);
       }
       const auto& sl = in_lay[q].at(k);
       g.buf = reinterpret_cast<bf16*>(static_cast<char*>(I.peer_inbox[q]) + sl.buf);
@@ -792,7 +748,7 @@ void Trainer::connect(const std::string& all_blobs, const std::string& nccl_id) 
       const int q = I.proc_of(g.producer);
       if (!out_lay.count(q)) {
         size_t t;
-        out_lay[q] = I.outbox_layout(q, &t);
+        out_lay[q] = I.lp->outbox_layout(q, &t);
       }
       g.ack = reinterpret_cast<uint32_t*>(static_cast<char*>(I.peer_outbox[q]) + out_lay[q].at(k));
     }
@@ -803,14 +759,7 @@ void Trainer::connect(const std::string& all_blobs, const std::string& nccl_id) 
   if (ncclCommInitRank(&I.world_comm, I.procs, id, I.proc) != ncclSuccess)
     throw capi::InternalError("ncclCommInitRank failed");
   for (int s = 0; s < I.D; ++s) {
-    std::vector<int> holders;  // processes holding stage s
-    for (int r = 0; r < I.W; ++r)
-      for (int p = 0; p < I.P; ++p) {
-        auto it = I.worker_of.find({p, s});
-        if (it == I.worker_of.end()) continue;
-        const int q = I.proc_of(r * I.D + it->second);
-        if (std::find(holders.begin(), holders.end(), q) == holders.end()) holders.push_back(q);
-      }
+    const std::vector<int> holders = I.lp->stage_holders(s);
     if (holders.size() < 2) continue;
     const bool mine = std::find(holders.begin(), holders.end(), I.proc) != holders.end();
     ncclComm_t c = nullptr;
