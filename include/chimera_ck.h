@@ -146,6 +146,11 @@ CK_API int ck_gpt_profile_step(ck_gpt* h, char** out_json);
 /* enqueue one iteration on the trainer stream without waiting (graph replay). */
 CK_API int ck_gpt_launch(ck_gpt* h);
 CK_API int ck_gpt_set_graph(ck_gpt* h, int on);
+/* dessim::SyncPolicy of the stage gradient allreduce (proj/src/dessim.cpp:101-135):
+ * 0 end-of-iteration, 1 eager-sync (default: each stage's allreduce + SGD launched on a
+ * comm stream as soon as its last local backward is issued), 2 eager-sync-opt (eager
+ * iff the reference's interior-slack rule marks every holder eager). */
+CK_API int ck_gpt_set_sync_policy(ck_gpt* h, int policy);
 CK_API void* ck_gpt_stream(ck_gpt* h);
 /* Multi-process (one process per GPU): export this process's 128 bytes of CUDA-IPC
  * handles, all-gather them (host side, e.g. torch.distributed), then connect with all

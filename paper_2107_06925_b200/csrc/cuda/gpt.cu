@@ -41,6 +41,8 @@
 #include "links.hpp"
 #include "ops.cuh"
 #include "pipesim/analysis.hpp"
+#include "pipesim/dessim.hpp"
+#include "sched_engine.hpp"
 #include "pipesim/core.hpp"
 
 namespace chimera::gpt {
@@ -134,6 +136,14 @@ struct Trainer::Impl {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   bool use_graph = true;
+  // gradient synchronisation policy (dessim::SyncPolicy): 0 end-of-iteration,
+  // 1 eager-sync, 2 eager-sync-opt (eager iff the reference's slack rule says so)
+  int sync_policy = 1;
+  cudaStream_t comm_stream = nullptr;
+  std::vector<int> coll_order;                   // stages in the global collective order
+  std::map<int, bool> stage_eager;               // stage -> launched at its completion
+  std::map<int, int> bwd_total;                  // stage -> local backward tasks per iteration
+  std::map<int, std::vector<cudaEvent_t>> stage_done_ev;  // per local copy, after its last bwd
   // profiled iteration: timing events around every task on its rank's stream
   bool profiling = false;
   struct TaskSpan {
@@ -373,6 +383,9 @@ Trainer::~Trainer() {
   cudaFree(I.outbox);
   for (auto e : I.rank_done) cudaEventDestroy(e);
   for (auto e : I.ev_pool) cudaEventDestroy(e);
+  for (auto& kv : I.stage_done_ev)
+    for (auto e : kv.second) cudaEventDestroy(e);
+  if (I.comm_stream) cudaStreamDestroy(I.comm_stream);
   cudaEventDestroy(I.start_ev);
   cudaEventDestroy(I.upd_ev);
   for (size_t k = 0; k < I.streams.size(); ++k)
@@ -528,8 +541,91 @@ void Trainer::backward_task(int rank, int p, int mb, int s) {
   cp.free_slots.push_back(slot);
 }
 
+namespace {
+
+// Global order of the per-stage gradient collectives, identical on every process:
+// eager stages by the unit-tick time at which their last backward (over all holders)
+// ends, then the end-of-iteration ones by stage id.
+void plan_sync(Trainer::Impl& I) {
+  const auto tl = pipesim::engine::tick_schedule(I.sched, pipesim::CostProfile{});
+  std::map<int, double> done_at;
+  for (int w = 0; w < I.D; ++w)
+    for (int i = 0; i < int(I.sched.per_worker[w].size()); ++i) {
+      const Task& t = I.sched.per_worker[w][i];
+      if (t.kind == TaskKind::Backward) done_at[t.stage] = std::max(done_at[t.stage], tl.spans[w][i].end);
+    }
+  std::map<std::pair<int, int>, bool> eager_ws;  // (worker, stage) -> eager (reference rule)
+  if (I.sync_policy == 2) {
+    pipesim::CostProfile prof;  // unit compute, small comm: alpha-beta only decides slack > 0
+    prof.alpha = 0.01, prof.beta = 0.001, prof.L_grad = 100.0;
+    pipesim::dessim::SimOptions o;
+    o.policy = pipesim::dessim::SyncPolicy::EagerSyncOpt;
+    for (const auto& ev : pipesim::dessim::simulate(I.sched, prof, o).allreduce_events)
+      eager_ws[{ev.worker, ev.stage}] = ev.eager;
+  }
+  I.stage_eager.clear();
+  for (int s = 0; s < I.D; ++s) {
+    bool e = I.sync_policy != 0;
+    if (I.sync_policy == 2)
+      for (const auto& [ws, eg] : eager_ws)
+        if (ws.second == s) e = e && eg;
+    I.stage_eager[s] = e;
+  }
+  std::vector<std::pair<double, int>> eager, late;
+  for (int s = 0; s < I.D; ++s) (I.stage_eager[s] ? eager : late).push_back({I.stage_eager[s] ? done_at[s] : s, s});
+  std::sort(eager.begin(), eager.end());
+  std::sort(late.begin(), late.end());
+  I.coll_order.clear();
+  for (auto& e : eager) I.coll_order.push_back(e.second);
+  for (auto& e : late) I.coll_order.push_back(e.second);
+  I.bwd_total.clear();
+  for (const auto& [w, i] : I.order) {
+    const Task& t = I.sched.per_worker[w][i];
+    if (t.kind != TaskKind::Backward) continue;
+    for (int r = 0; r < I.W; ++r)
+      if (I.local(r * I.D + w)) I.bwd_total[t.stage]++;
+  }
+  for (auto& [st, S] : I.stages) {
+    auto& evs = I.stage_done_ev[st];
+    while (evs.size() < S.grads.size()) {
+      cudaEvent_t e;
+      CK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      evs.push_back(e);
+    }
+  }
+  if (!I.comm_stream) CK_CUDA(cudaStreamCreateWithFlags(&I.comm_stream, cudaStreamNonBlocking));
+}
+
+// Sum the local copies, allreduce across the processes holding the stage (if any),
+// SGD -- on the comm stream, after every local copy's last backward.
+void sync_stage(Trainer::Impl& I, int s) {
+  StageState& S = I.stages.at(s);
+  cudaStream_t cs = I.comm_stream;
+  for (cudaEvent_t e : I.stage_done_ev.at(s)) CK_CUDA(cudaStreamWaitEvent(cs, e, 0));
+  auto it = I.stage_comm.find(s);
+  if (it == I.stage_comm.end()) {
+    ops::sgd_update(S.w32, S.w16, S.grads.data(), int(S.grads.size()), S.L.total, I.lr, cs);
+    I.launches_per_step += 1;
+    return;
+  }
+  float* g0 = S.grads[0];
+  if (S.grads.size() > 1) {
+    ops::reduce_copies(g0, S.grads.data(), int(S.grads.size()), S.L.total, cs);
+    for (size_t c = 1; c < S.grads.size(); ++c)
+      CK_CUDA(cudaMemsetAsync(S.grads[c], 0, S.L.total * sizeof(float), cs));
+    I.launches_per_step += 1;
+  }
+  if (ncclAllReduce(g0, g0, S.L.total, ncclFloat, ncclSum, it->second, cs) != ncclSuccess)
+    throw capi::InternalError("ncclAllReduce failed");
+  ops::sgd_update(S.w32, S.w16, &g0, 1, S.L.total, I.lr, cs);
+  I.launches_per_step += 1;
+}
+
+}  // namespace
+
 void Trainer::issue_iteration() {
   Impl& I = *d_;
+  if (I.coll_order.empty()) plan_sync(I);
   I.launches_per_step = 0;
   I.slot_of.clear();
   for (auto& kv : I.copies) {
@@ -540,6 +636,30 @@ void Trainer::issue_iteration() {
   CK_CUDA(cudaMemsetAsync(I.loss, 0, sizeof(float), I.main_stream));
   CK_CUDA(cudaEventRecord(I.start_ev, I.main_stream));
   for (auto s : I.streams) CK_CUDA(cudaStreamWaitEvent(s, I.start_ev, 0));
+  CK_CUDA(cudaStreamWaitEvent(I.comm_stream, I.start_ev, 0));
+  std::map<int, int> bwd_left = I.bwd_total;
+  std::map<int, int> copy_done;  // stage -> local copies whose last backward was issued
+  std::map<std::array<int, 2>, int> copy_bwd_left;  // (rank, pipeline) -> backwards left
+  for (const auto& [w, i] : I.order) {
+    const Task& t = I.sched.per_worker[w][i];
+    if (t.kind != TaskKind::Backward) continue;
+    for (int r = 0; r < I.W; ++r)
+      if (I.local(r * I.D + w)) copy_bwd_left[{r * I.D + w, t.pipeline_id}]++;
+  }
+  size_t next_coll = 0;
+  auto drain = [&](bool at_end) {
+    while (next_coll < I.coll_order.size()) {
+      const int s = I.coll_order[next_coll];
+      if (!I.stages.count(s) && !I.stage_comm.count(s)) {  // not held here
+        ++next_coll;
+        continue;
+      }
+      const bool ready = bwd_left[s] == 0;
+      if (!ready || (!I.stage_eager[s] && !at_end)) break;
+      sync_stage(I, s);
+      ++next_coll;
+    }
+  };
   for (const auto& [w, i] : I.order) {
     const Task& t = I.sched.per_worker[w][i];
     if (t.kind != TaskKind::Forward && t.kind != TaskKind::Backward) continue;
@@ -558,34 +678,38 @@ void Trainer::issue_iteration() {
         CK_CUDA(cudaEventRecord(sp.b, I.stream_of(rank)));
         I.spans.push_back(sp);
       }
+      if (t.kind == TaskKind::Backward) {
+        if (--copy_bwd_left[{rank, t.pipeline_id}] == 0) {
+          const int c = copy_done[t.stage]++;
+          CK_CUDA(cudaEventRecord(I.stage_done_ev.at(t.stage).at(c), I.stream_of(rank)));
+        }
+        if (--bwd_left[t.stage] == 0) drain(false);
+      }
     }
   }
+  drain(true);  // end-of-iteration collectives, still in the global order
+  if (next_coll != I.coll_order.size()) throw capi::InternalError("gradient sync incomplete");
   for (int k = 0; k < I.nlocal; ++k) {
     CK_CUDA(cudaEventRecord(I.rank_done[k], I.streams[k]));
     CK_CUDA(cudaStreamWaitEvent(I.main_stream, I.rank_done[k], 0));
   }
-  // gradient synchronisation + SGD, stage by stage in ascending stage order (the same
-  // order on every process, so collectives on overlapping groups cannot deadlock)
-  for (auto& [s, S] : I.stages) {
-    auto it = I.stage_comm.find(s);
-    if (it == I.stage_comm.end()) {
-      ops::sgd_update(S.w32, S.w16, S.grads.data(), int(S.grads.size()), S.L.total, I.lr, I.main_stream);
-      I.launches_per_step += 1;
-      continue;
-    }
-    float* g0 = S.grads[0];
-    if (S.grads.size() > 1) {
-      ops::reduce_copies(g0, S.grads.data(), int(S.grads.size()), S.L.total, I.main_stream);
-      for (size_t c = 1; c < S.grads.size(); ++c)
-        CK_CUDA(cudaMemsetAsync(S.grads[c], 0, S.L.total * sizeof(float), I.main_stream));
-      I.launches_per_step += 1;
-    }
-    if (ncclAllReduce(g0, g0, S.L.total, ncclFloat, ncclSum, it->second, I.main_stream) != ncclSuccess)
-      throw capi::InternalError("ncclAllReduce failed");
-    ops::sgd_update(S.w32, S.w16, &g0, 1, S.L.total, I.lr, I.main_stream);
-    I.launches_per_step += 1;
+  CK_CUDA(cudaEventRecord(I.upd_ev, I.comm_stream));
+  CK_CUDA(cudaStreamWaitEvent(I.main_stream, I.upd_ev, 0));
+}
+
+void Trainer::set_sync_policy(int policy) {
+  Impl& I = *d_;
+  if (policy < 0 || policy > 2) throw pipesim::InvalidConfigError("sync policy must be 0, 1 or 2");
+  I.sync_policy = policy;
+  I.coll_order.clear();
+  if (I.graph_exec) {
+    cudaGraphExecDestroy(I.graph_exec);
+    cudaGraphDestroy(I.graph);
+    I.graph_exec = nullptr, I.graph = nullptr;
   }
 }
+
+
 
 float Trainer::step() {
   Impl& I = *d_;
@@ -884,6 +1008,10 @@ CK_API int ck_gpt_profile_step(ck_gpt* h, char** out_json) {
 
 CK_API int ck_gpt_launch(ck_gpt* h) {
   return chimera::capi::guarded([&] { h->t->launch_async(); });
+}
+
+CK_API int ck_gpt_set_sync_policy(ck_gpt* h, int policy) {
+  return chimera::capi::guarded([&] { h->t->set_sync_policy(policy); });
 }
 
 CK_API int ck_gpt_set_graph(ck_gpt* h, int on) {

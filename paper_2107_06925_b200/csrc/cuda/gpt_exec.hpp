@@ -25,13 +25,16 @@ class Trainer {
   std::string stats_json() const;
   void* stream() const;
   void set_use_graph(bool on);
+  void set_sync_policy(int policy);  // 0 end-of-iteration, 1 eager-sync, 2 eager-sync-opt
   // multi-process: this process's IPC handles (inbox, outbox), then connect with the
   // handles of all processes (ordered by process index) and an NCCL unique id.
   std::string ipc_export() const;
   void connect(const std::string& all_handles, const std::string& nccl_id);
 
- private:
+ public:
   struct Impl;
+
+ private:
   void issue_iteration();
   void forward_task(int rank, int p, int mb, int s);
   void backward_task(int rank, int p, int mb, int s);

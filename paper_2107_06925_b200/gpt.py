@@ -40,6 +40,7 @@ _lib.register("ck_gpt_step", C.c_int, [_vp, C.POINTER(C.c_float)])
 _lib.register("ck_gpt_launch", C.c_int, [_vp])
 _lib.register("ck_gpt_profile_step", C.c_int, [_vp, C.POINTER(_vp)])
 _lib.register("ck_gpt_set_graph", C.c_int, [_vp, C.c_int])
+_lib.register("ck_gpt_set_sync_policy", C.c_int, [_vp, C.c_int])
 _lib.register("ck_gpt_stream", _vp, [_vp])
 _lib.register("ck_gpt_ipc_handles", C.c_int, [_vp, C.c_char_p, C.c_int])
 _lib.register("ck_gpt_connect", C.c_int, [_vp, C.c_char_p, C.c_int, C.c_char_p, C.c_int])
@@ -181,6 +182,11 @@ class Trainer:
 
     def launch(self):
         check(lib().ck_gpt_launch(self._h))
+
+    def set_sync_policy(self, policy: str):
+        """'end-of-iteration' | 'eager-sync' (default) | 'eager-sync-opt' (dessim.hpp:27)."""
+        check(lib().ck_gpt_set_sync_policy(self._h, {"end-of-iteration": 0, "eager-sync": 1,
+                                                      "eager-sync-opt": 2}[policy]))
 
     def use_graph(self, on: bool):
         check(lib().ck_gpt_set_graph(self._h, int(on)))

@@ -75,3 +75,26 @@ def test_baseline_schedules(scheme):
 def test_bidirectional_attention_and_tail_seq():
     shape = GPTShape(4, 256, 4, 1024, 72, 1000, 1024, False)
     _check_iteration(shape, P.PipelineConfig("chimera", 2, 1, 4, 2, 1, "backward-halving"))
+
+
+@pytest.mark.parametrize("policy", ["end-of-iteration", "eager-sync", "eager-sync-opt"])
+def test_sync_policies_same_math(policy):
+    shape = PRESETS["tiny"]
+    cfg = P.PipelineConfig("chimera", 4, 2, 4, 2, 1)
+    tr = Trainer(shape, cfg, lr=0.5)
+    tr.set_sync_policy(policy)
+    tr.init_params(0)
+    params = [tr.get_params(s).astype(np.float64) for s in range(cfg.D)]
+    tok, lab = synthetic_batch(shape, cfg.mini_batch(), 3)
+    tr.set_batch(tok, lab)
+    for _ in range(2):  # eager + graph replay
+        tr.step()
+    tr.set_batch(tok, lab)
+    sched = json.loads(tr.schedule_text)
+    p1, _, _, _ = O.run_iteration(sched, _oshape(shape), params, tok, lab, 0.5)
+    p2, _, _, _ = O.run_iteration(sched, _oshape(shape), p1, tok, lab, 0.5)
+    for s in range(cfg.D):
+        got = tr.get_params(s).astype(np.float64)
+        d, ref = got - params[s], p2[s] - params[s]
+        assert np.linalg.norm(d - ref) / np.linalg.norm(ref) <= 3e-2
+    tr.close()
