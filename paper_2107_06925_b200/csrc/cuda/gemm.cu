@@ -16,6 +16,9 @@
 // materialised in HBM.
 #include <cuda.h>
 
+#include <cstdlib>
+#include <string>
+
 #include "chimera_ck.h"
 #include "common.cuh"
 #include "gemm.cuh"
@@ -38,28 +41,55 @@ __device__ __forceinline__ float gelu_tanh_grad(float u) {
   return 0.5f * (1.f + t) + 0.5f * u * (1.f - t * t) * k0 * (1.f + 3.f * k1 * u * u);
 }
 
+// Epilogue of one 32-row x 32-column accumulator chunk by one warp.  Lane i owns row
+// row0+i in registers (the tcgen05.ld 32x32b layout); every global access goes through
+// a per-warp shared-memory tile so that 4 consecutive lanes cover one 64-byte (bf16) or
+// 128-byte (fp32) row segment -- fully coalesced, instead of 32 row-strided streams.
+constexpr int kEpiWarpBytes = 8192;  // per epilogue warp: staging tile (+ aux tile)
+constexpr int kStrideH = 80;         // bytes per staged bf16 row (64 + 16 pad: conflict-free)
+constexpr int kStrideF = 144;        // bytes per staged fp32 row (128 + 16 pad)
+
 template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(const EpiArgs& ep, int row, int col0, int N,
-                                               const uint32_t (&r)[32]) {
+__device__ __forceinline__ void epilogue_chunk(const EpiArgs& ep, int row0, int col0, int M, int N,
+                                               const uint32_t (&r)[32], uint8_t* stg, int lane,
+                                               bool atomic = false) {
   float v[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-  const bool full = col0 + 32 <= N;
+  const bool vec_ok = (N % 8) == 0;
   if constexpr (EPI == kAccF32 || EPI == kStoreF32) {
-    float* o = static_cast<float*>(ep.out) + (long long)row * ep.ldo + col0;
-    if (full) {
+    float* row_s = reinterpret_cast<float*>(stg + lane * kStrideF);
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        float4 x = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        if constexpr (EPI == kAccF32) {
-          const float4 y = *reinterpret_cast<const float4*>(o + j);
-          x.x += y.x, x.y += y.y, x.z += y.z, x.w += y.w;
+    for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(row_s + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    __syncwarp();
+    float* out = static_cast<float*>(ep.out);
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {  // 32 rows x 8 segments of 4 floats
+      const int idx = it * 32 + lane, rr = idx >> 3, sg = idx & 7;
+      const int row = row0 + rr, col = col0 + sg * 4;
+      if (row >= M || col >= N) continue;
+      const float4 x = *reinterpret_cast<const float4*>(stg + rr * kStrideF + sg * 16);
+      float* o = out + (long long)row * ep.ldo + col;
+      if (EPI == kAccF32 && atomic) {  // split-K partial sums
+        if (vec_ok && col + 4 <= N) {
+          atomicAdd(reinterpret_cast<float4*>(o), x);
+        } else {
+          const float xs[4] = {x.x, x.y, x.z, x.w};
+          for (int t = 0; t < 4 && col + t < N; ++t) atomicAdd(o + t, xs[t]);
         }
-        *reinterpret_cast<float4*>(o + j) = x;
+      } else if (vec_ok && col + 4 <= N) {
+        float4 y = x;
+        if constexpr (EPI == kAccF32) {
+          const float4 z = *reinterpret_cast<const float4*>(o);
+          y.x += z.x, y.y += z.y, y.z += z.z, y.w += z.w;
+        }
+        *reinterpret_cast<float4*>(o) = y;
+      } else {
+        const float xs[4] = {x.x, x.y, x.z, x.w};
+        for (int t = 0; t < 4 && col + t < N; ++t) o[t] = (EPI == kAccF32 ? o[t] : 0.f) + xs[t];
       }
-    } else {
-      for (int j = 0; j < 32 && col0 + j < N; ++j) o[j] = (EPI == kAccF32 ? o[j] : 0.f) + v[j];
     }
+    __syncwarp();
     return;
   } else {
     if (ep.bias && EPI != kGeluBwd) {
@@ -67,47 +97,64 @@ __device__ __forceinline__ void epilogue_chunk(const EpiArgs& ep, int row, int c
       for (int j = 0; j < 32; ++j) v[j] += (col0 + j < N) ? __bfloat162float(ep.bias[col0 + j]) : 0.f;
     }
     if constexpr (EPI == kBiasResid || EPI == kGeluBwd) {
-      const __nv_bfloat16* a = ep.aux + (long long)row * ep.ld_aux + col0;
-      if (full) {
+      uint8_t* aux_s = stg + 32 * kStrideH;  // second tile of the warp's staging area
 #pragma unroll
-        for (int j = 0; j < 32; j += 8) {
-          const uint4 q = *reinterpret_cast<const uint4*>(a + j);
-          const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q);
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const float x = __bfloat162float(h[t]);
-            v[j + t] = EPI == kBiasResid ? v[j + t] + x : v[j + t] * gelu_tanh_grad(x);
+      for (int it = 0; it < 4; ++it) {  // 32 rows x 4 segments of 8 bf16, coalesced loads
+        const int idx = it * 32 + lane, rr = idx >> 2, sg = idx & 3;
+        const int row = row0 + rr, col = col0 + sg * 8;
+        uint4 q = make_uint4(0, 0, 0, 0);
+        if (row < M && col < N) {
+          const __nv_bfloat16* a = ep.aux + (long long)row * ep.ld_aux + col;
+          if (vec_ok && col + 8 <= N) {
+            q = *reinterpret_cast<const uint4*>(a);
+          } else {
+            __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(&q);
+            for (int t = 0; t < 8 && col + t < N; ++t) h[t] = a[t];
           }
         }
-      } else {
-        for (int j = 0; j < 32 && col0 + j < N; ++j) {
-          const float x = __bfloat162float(a[j]);
-          v[j] = EPI == kBiasResid ? v[j] + x : v[j] * gelu_tanh_grad(x);
-        }
+        *reinterpret_cast<uint4*>(aux_s + rr * kStrideH + sg * 16) = q;
+      }
+      __syncwarp();
+      const __nv_bfloat16* mine = reinterpret_cast<const __nv_bfloat16*>(aux_s + lane * kStrideH);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float x = __bfloat162float(mine[j]);
+        v[j] = EPI == kBiasResid ? v[j] + x : v[j] * gelu_tanh_grad(x);
       }
     }
-    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + col0;
-    __nv_bfloat16* o2 = EPI == kBiasGelu ? ep.out2 + (long long)row * ep.ld_out2 + col0 : nullptr;
-    if (full) {
+    constexpr int kOuts = EPI == kBiasGelu ? 2 : 1;
+#pragma unroll
+    for (int o = 0; o < kOuts; ++o) {
+      __nv_bfloat16* row_s = reinterpret_cast<__nv_bfloat16*>(stg + lane * kStrideH);
 #pragma unroll
       for (int j = 0; j < 32; j += 8) {
-        uint4 q, q2;
+        uint4 q;
         __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(&q);
-        __nv_bfloat16* h2 = reinterpret_cast<__nv_bfloat16*>(&q2);
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
-          h[t] = __float2bfloat16_rn(v[j + t]);
-          if constexpr (EPI == kBiasGelu) h2[t] = __float2bfloat16_rn(gelu_tanh(__bfloat162float(h[t])));
+          const __nv_bfloat16 u = __float2bfloat16_rn(v[j + t]);
+          h[t] = (o == 0) ? u : __float2bfloat16_rn(gelu_tanh(__bfloat162float(u)));
         }
-        *reinterpret_cast<uint4*>(o + j) = q;
-        if constexpr (EPI == kBiasGelu) *reinterpret_cast<uint4*>(o2 + j) = q2;
+        *reinterpret_cast<uint4*>(row_s + j) = q;
       }
-    } else {
-      for (int j = 0; j < 32 && col0 + j < N; ++j) {
-        const __nv_bfloat16 b = __float2bfloat16_rn(v[j]);
-        o[j] = b;
-        if constexpr (EPI == kBiasGelu) o2[j] = __float2bfloat16_rn(gelu_tanh(__bfloat162float(b)));
+      __syncwarp();
+      __nv_bfloat16* out = o == 0 ? static_cast<__nv_bfloat16*>(ep.out) : ep.out2;
+      const long long ld = o == 0 ? ep.ldo : ep.ld_out2;
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const int idx = it * 32 + lane, rr = idx >> 2, sg = idx & 3;
+        const int row = row0 + rr, col = col0 + sg * 8;
+        if (row >= M || col >= N) continue;
+        const uint4 q = *reinterpret_cast<const uint4*>(stg + rr * kStrideH + sg * 16);
+        __nv_bfloat16* dst = out + (long long)row * ld + col;
+        if (vec_ok && col + 8 <= N) {
+          *reinterpret_cast<uint4*>(dst) = q;
+        } else {
+          const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q);
+          for (int t = 0; t < 8 && col + t < N; ++t) dst[t] = h[t];
+        }
       }
+      __syncwarp();
     }
   }
 }
@@ -119,13 +166,13 @@ struct Cfg {
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;
-  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256 + 4 * kEpiWarpBytes;
 };
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(256, 1)
     k_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-           const EpiArgs ep, int M, int N, int K) {
+           const EpiArgs ep, int M, int N, int K, int ksplit) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -137,7 +184,8 @@ __global__ void __launch_bounds__(256, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
-  const int tiles = num_m * num_n, num_kb = (K + BK - 1) / BK;
+  const int num_kb = (K + BK - 1) / BK, kb_per = (num_kb + ksplit - 1) / ksplit;
+  const int tiles = num_m * num_n * ksplit;
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&ta);
@@ -157,8 +205,9 @@ __global__ void __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int mb = tile % num_m, nb = tile / num_m;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int mb = tile % num_m, nb = (tile / num_m) % num_n, ks = tile / (num_m * num_n);
+        const int kb1 = min(num_kb, (ks + 1) * kb_per);
+        for (int kb = ks * kb_per; kb < kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::kStageBytes;
           uint8_t* sb = sa + C::kABytes;
@@ -192,7 +241,9 @@ __global__ void __launch_bounds__(256, 1)
         ptx::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int ks = tile / (num_m * num_n);
+        const int kb0 = ks * kb_per, kb1 = min(num_kb, (ks + 1) * kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           const uint32_t sa = ptx::smem_u32(smem + stage * C::kStageBytes);
@@ -203,7 +254,7 @@ __global__ void __launch_bounds__(256, 1)
                                      : ptx::smem_desc_sw128(sa + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? ptx::smem_desc_sw128(sb + k * 2048, BK * 128, 1024)
                                      : ptx::smem_desc_sw128(sb + k * 32, 16, 1024);
-            ptx::umma_f16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            ptx::umma_f16(d_tmem, ad, bd, idesc, (kb > kb0 || k) ? 1u : 0u);
           }
           ptx::umma_commit(&empty[stage]);
           if (++stage == C::kStages) stage = 0, phase ^= 1;
@@ -216,18 +267,19 @@ __global__ void __launch_bounds__(256, 1)
     int it = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
       const int acc = it & 1;
-      const int mb = tile % num_m, nb = tile / num_m;
+      const int mb = tile % num_m, nb = (tile / num_m) % num_n;
       ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
       ptx::tc_fence_after();
-      const int row = mb * BM + q * 32 + lane;
+      const int row0 = mb * BM + q * 32;
       const uint32_t t0 = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
+      uint8_t* stg = smem + C::kStages * C::kStageBytes + 256 + q * kEpiWarpBytes;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
         ptx::tmem_ld32(t0 + c * 32, r);
         ptx::tmem_ld_wait();
         const int col0 = nb * BN + c * 32;
-        if (row < M && col0 < N) epilogue_chunk<EPI>(ep, row, col0, N, r);
+        if (row0 < M && col0 < N) epilogue_chunk<EPI>(ep, row0, col0, M, N, r, stg, lane, ksplit > 1);
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -239,6 +291,173 @@ __global__ void __launch_bounds__(256, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem_base, C::kTmemCols);
   }
+}
+
+// Split-K for the fp32-accumulate (weight-gradient) epilogue: enough K slices to fill
+// the machine, each at least 8 K-blocks deep; slices combine with fp32 vector atomics.
+inline int split_k(int epi, int tiles, int slots, int K) {
+  if (epi != kAccF32 || tiles >= slots) return 1;
+  const int kb = (K + BK - 1) / BK;
+  int ks = (slots + tiles - 1) / tiles;
+  ks = ks < kb / 8 ? ks : kb / 8;
+  return ks < 1 ? 1 : ks;
+}
+
+// ---------------------------------------------------------- 2-SM variant ----
+// A CTA pair (cluster of 2 on one TPC) computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 (M = 256): each CTA stages its 128 rows of A and 128 of
+// the 256 rows of B per K-block, so per-SM operand traffic per MMA drops by 1/3 versus
+// the 128 x 256 single-CTA tile.  The leader (even) CTA issues the MMAs and owns the
+// smem-full and TMEM-empty barriers; commits are multicast to both CTAs.
+constexpr int kPairStages = 6;
+constexpr int kPairHalfBytes = 128 * BK * 2;            // one operand half per CTA
+constexpr int kPairStageBytes = 2 * kPairHalfBytes;     // A half + B half
+constexpr int kPairSmem = kPairStages * kPairStageBytes + 1024 + 256 + 4 * kEpiWarpBytes;
+
+template <bool A_MN, bool B_MN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    k_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const EpiArgs ep,
+            int M, int N, int K, int ksplit) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPairStages * kPairStageBytes);
+  uint64_t* empty = full + kPairStages;
+  uint64_t* tfull = empty + kPairStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t cta = ptx::cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int num_m = (M + 255) / 256, num_n = (N + 255) / 256;
+  const int num_kb = (K + BK - 1) / BK, kb_per = (num_kb + ksplit - 1) / ksplit;
+  const int tiles = num_m * num_n * ksplit;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&ta);
+    ptx::tma_prefetch(&tb);
+    for (int s = 0; s < kPairStages; ++s) ptx::mbar_init(&full[s], 1), ptx::mbar_init(&empty[s], 1);
+    for (int a = 0; a < 2; ++a) ptx::mbar_init(&tfull[a], 1), ptx::mbar_init(&tempty[a], 8);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc2(tmem_slot, 512);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = pair; tile < tiles; tile += npairs) {
+        const int mb = tile % num_m, nb = (tile / num_m) % num_n, ks = tile / (num_m * num_n);
+        const int m0 = mb * 256 + int(cta) * 128, n0 = nb * 256 + int(cta) * 128;
+        const int kb1 = min(num_kb, (ks + 1) * kb_per);
+        for (int kb = ks * kb_per; kb < kb1; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * kPairStageBytes;
+          uint8_t* sb = sa + kPairHalfBytes;
+          if (cta == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
+          if constexpr (!A_MN) {
+            ptx::tma_load_2d_pair(sa, &ta, &full[stage], kb * BK, m0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) ptx::tma_load_2d_pair(sa + c * (BK * 128), &ta, &full[stage], m0 + c * 64, kb * BK);
+          }
+          if constexpr (!B_MN) {
+            ptx::tma_load_2d_pair(sb, &tb, &full[stage], kb * BK, n0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) ptx::tma_load_2d_pair(sb + c * (BK * 128), &tb, &full[stage], n0 + c * 64, kb * BK);
+          }
+          if (++stage == kPairStages) stage = 0, phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (cta == 0 && lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16(256, 256, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = pair; tile < tiles; tile += npairs, ++it) {
+        const int acc = it & 1;
+        ptx::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * 256;
+        const int ks = tile / (num_m * num_n);
+        const int kb0 = ks * kb_per, kb1 = min(num_kb, (ks + 1) * kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(smem + stage * kPairStageBytes);
+          const uint32_t sb = sa + kPairHalfBytes;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? ptx::smem_desc_sw128(sa + k * 2048, BK * 128, 1024)
+                                     : ptx::smem_desc_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? ptx::smem_desc_sw128(sb + k * 2048, BK * 128, 1024)
+                                     : ptx::smem_desc_sw128(sb + k * 32, 16, 1024);
+            ptx::umma_f16_pair(d_tmem, ad, bd, idesc, (kb > kb0 || k) ? 1u : 0u);
+          }
+          ptx::umma_commit_pair(&empty[stage]);
+          if (++stage == kPairStages) stage = 0, phase ^= 1;
+        }
+        ptx::umma_commit_pair(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;
+    int it = 0;
+    for (int tile = pair; tile < tiles; tile += npairs, ++it) {
+      const int acc = it & 1;
+      const int mb = tile % num_m, nb = (tile / num_m) % num_n;
+      ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      ptx::tc_fence_after();
+      const int row0 = mb * 256 + int(cta) * 128 + q * 32;
+      const uint32_t t0 = tmem_base + (uint32_t(q * 32) << 16) + acc * 256;
+      uint8_t* stg = smem + kPairStages * kPairStageBytes + 256 + q * kEpiWarpBytes;
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        uint32_t r[32];
+        ptx::tmem_ld32(t0 + c * 32, r);
+        ptx::tmem_ld_wait();
+        const int col0 = nb * 256 + c * 32;
+        if (row0 < M && col0 < N) epilogue_chunk<EPI>(ep, row0, col0, M, N, r, stg, lane, ksplit > 1);
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_leader(&tempty[acc]);
+    }
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc2(tmem_base, 512);
+  }
+}
+
+template <bool A_MN, bool B_MN, int EPI>
+void launch_pair(int M, int N, int K, const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B,
+                 long long ldb, const EpiArgs& ep, cudaStream_t st) {
+  const CUtensorMap ta = A_MN ? cuda::make_map_2d_bf16(A, M, K, lda, 64, BK)
+                              : cuda::make_map_2d_bf16(A, K, M, lda, 64, 128);
+  const CUtensorMap tb = B_MN ? cuda::make_map_2d_bf16(B, N, K, ldb, 64, BK)
+                              : cuda::make_map_2d_bf16(B, K, N, ldb, 64, 128);
+  auto kern = k_gemm2<A_MN, B_MN, EPI>;
+  static bool attr = false;
+  if (!attr) {
+    CK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));
+    attr = true;
+  }
+  const int base = ((M + 255) / 256) * ((N + 255) / 256);
+  const int ks = split_k(EPI, base, cuda::kNumSMs / 2, K);
+  const int tiles = base * ks;
+  const int pairs = tiles < cuda::kNumSMs / 2 ? tiles : cuda::kNumSMs / 2;
+  kern<<<2 * pairs, 256, kPairSmem, st>>>(ta, tb, ep, M, N, K, ks);
+  CK_CUDA(cudaGetLastError());
 }
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
@@ -255,27 +474,36 @@ void launch(int M, int N, int K, const __nv_bfloat16* A, long long lda, const __
     CK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr = true;
   }
-  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int base = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int ks = split_k(EPI, base, cuda::kNumSMs, K);
+  const int tiles = base * ks;
   const int grid = tiles < cuda::kNumSMs ? tiles : cuda::kNumSMs;
-  kern<<<grid, 256, C::kSmem, st>>>(ta, tb, ep, M, N, K);
+  kern<<<grid, 256, C::kSmem, st>>>(ta, tb, ep, M, N, K, ks);
   CK_CUDA(cudaGetLastError());
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+void launch_any(int M, int N, int K, const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B,
+                long long ldb, const EpiArgs& ep, cudaStream_t st) {
+  if constexpr (BN == 0) launch_pair<A_MN, B_MN, EPI>(M, N, K, A, lda, B, ldb, ep, st);
+  else launch<BN, A_MN, B_MN, EPI>(M, N, K, A, lda, B, ldb, ep, st);
 }
 
 template <int BN, bool A_MN, bool B_MN>
 void by_epi(Epi epi, int M, int N, int K, const __nv_bfloat16* A, long long lda,
             const __nv_bfloat16* B, long long ldb, const EpiArgs& ep, cudaStream_t st) {
   switch (epi) {
-    case kStoreBF16: return launch<BN, A_MN, B_MN, kStoreBF16>(M, N, K, A, lda, B, ldb, ep, st);
-    case kStoreF32: return launch<BN, A_MN, B_MN, kStoreF32>(M, N, K, A, lda, B, ldb, ep, st);
-    case kAccF32: return launch<BN, A_MN, B_MN, kAccF32>(M, N, K, A, lda, B, ldb, ep, st);
+    case kStoreBF16: return launch_any<BN, A_MN, B_MN, kStoreBF16>(M, N, K, A, lda, B, ldb, ep, st);
+    case kStoreF32: return launch_any<BN, A_MN, B_MN, kStoreF32>(M, N, K, A, lda, B, ldb, ep, st);
+    case kAccF32: return launch_any<BN, A_MN, B_MN, kAccF32>(M, N, K, A, lda, B, ldb, ep, st);
     default: break;
   }
   if constexpr (!A_MN && !B_MN) {
-    if (epi == kBiasGelu) return launch<BN, false, false, kBiasGelu>(M, N, K, A, lda, B, ldb, ep, st);
-    if (epi == kBiasResid) return launch<BN, false, false, kBiasResid>(M, N, K, A, lda, B, ldb, ep, st);
+    if (epi == kBiasGelu) return launch_any<BN, false, false, kBiasGelu>(M, N, K, A, lda, B, ldb, ep, st);
+    if (epi == kBiasResid) return launch_any<BN, false, false, kBiasResid>(M, N, K, A, lda, B, ldb, ep, st);
   }
   if constexpr (!A_MN && B_MN) {
-    if (epi == kGeluBwd) return launch<BN, false, true, kGeluBwd>(M, N, K, A, lda, B, ldb, ep, st);
+    if (epi == kGeluBwd) return launch_any<BN, false, true, kGeluBwd>(M, N, K, A, lda, B, ldb, ep, st);
   }
   throw chimera::capi::InternalError("gemm: unsupported epilogue/layout combination");
 }
@@ -297,12 +525,20 @@ void gemm(Epi epi, bool a_mn, bool b_mn, int M, int N, int K, const __nv_bfloat1
   if (M <= 0 || N <= 0 || K <= 0) return;
   if ((lda % 8) || (ldb % 8) || (reinterpret_cast<uintptr_t>(A) % 16) || (reinterpret_cast<uintptr_t>(B) % 16))
     throw chimera::capi::InternalError("gemm: operands must be 16-byte aligned with ld % 8 == 0");
-  // 256-wide tiles when they still give at least one full wave of CTAs.
+  // CTA-pair 256 x 256 tiles for large problems, else single-CTA 128 x 256 / 128 x 128.
+  static const int force = [] {
+    const char* e = std::getenv("CK_GEMM_TILE");  // "pair" | "256" | "128" (benchmarks)
+    return !e ? -1 : std::string(e) == "pair" ? 0 : std::string(e) == "256" ? 256 : 128;
+  }();
+  const long long tiles_pair = (long long)((M + 255) / 256) * ((N + 255) / 256);
   const long long tiles256 = (long long)((M + BM - 1) / BM) * ((N + 255) / 256);
-  if (N >= 256 && tiles256 >= cuda::kNumSMs)
-    by_layout<256>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
-  else
-    by_layout<128>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
+  int choice = force;
+  (void)tiles256;
+  if (choice < 0) choice = (M >= 256 && N >= 256 && tiles_pair >= 48) ? 0 : (N > 128) ? 256 : 128;
+  if (choice == 0 && (M < 256 || N < 256)) choice = 128;
+  if (choice == 0) by_layout<0>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
+  else if (choice == 256) by_layout<256>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
+  else by_layout<128>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
 }
 
 }  // namespace chimera::gemm

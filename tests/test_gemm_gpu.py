@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 from paper_2107_06925_b200 import kernels as ck  # noqa: E402
 
 SHAPES = [(128, 128, 64), (256, 384, 192), (4096, 3072, 1024), (304, 200, 136), (632, 5120, 1280),
-          (1000, 1000, 72)]
+          (1000, 1000, 72), (1024, 1024, 4096), (768, 256, 4096)]
 
 
 def _rand(*shape):
