@@ -132,6 +132,11 @@ struct Trainer::Impl {
   std::vector<std::pair<int, int>> order;
   std::map<std::array<int, 4>, int> slot_of;  // (rank, p, m, s) -> slot index during issue
   std::vector<int> peak_live;                  // per local rank
+  // activation recomputation (config.recompute, forced by forward doubling): slots keep
+  // only the stage input; one full per-rank workspace is rebuilt by each backward
+  bool recompute = false;
+  std::vector<Stash> rscratch;  // per local rank
+  float* loss_dummy = nullptr;  // sink for the recomputed last-stage loss
   std::map<std::array<int, 2>, long long> slot_bytes;  // (rank, pipeline) -> bytes of one stash
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
@@ -203,7 +208,6 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
   if (shape.hidden % 256) throw pipesim::InvalidConfigError("hidden must be a multiple of 256");
   if (shape.vocab_padded % 8 || shape.vocab_padded < shape.vocab)
     throw pipesim::InvalidConfigError("vocab_padded must be >= vocab and a multiple of 8");
-  if (c.recompute) throw pipesim::InvalidConfigError("recompute is not supported by this executor yet");
   if (first_rank < 0 || n_ranks < 1 || first_rank + n_ranks > I.W * I.D)
     throw pipesim::InvalidConfigError("rank range outside W*D");
   if (int(sched.per_worker.size()) != I.D) throw pipesim::InvalidConfigError("schedule must have D workers");
@@ -264,13 +268,9 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
       I.peak_live[rank - first_rank] = std::max(I.peak_live[rank - first_rank], live_rank[rank - first_rank]);
     }
   }
-  for (auto& [key, cp] : I.copies) {
-    const StageLayout& L = I.stages[cp.stage].L;
-    const int nslots = peak[key];
-    const size_t before = I.arena.bytes;
-    for (int k = 0; k < nslots; ++k) {
-      Stash st;
-      if (L.has_embed) st.x0 = I.arena.alloc<bf16>((size_t)M * h);
+  I.recompute = c.recompute;
+  auto alloc_full = [&](Stash& st, bool embed, bool head) {
+      if (embed) st.x0 = I.arena.alloc<bf16>((size_t)M * h);
       for (int l = 0; l < Ls; ++l) {
         LayerStash ls;
         ls.h1 = I.arena.alloc<bf16>((size_t)M * h);
@@ -288,12 +288,33 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
         ls.lse = I.arena.alloc<float>((size_t)I.B * H * shape.seq);
         st.layers.push_back(ls);
       }
-      if (L.has_head) {
+      if (head) {
         st.xfinal = I.arena.alloc<bf16>((size_t)M * h);
         st.hf = I.arena.alloc<bf16>((size_t)M * h);
         st.meanf = I.arena.alloc<float>(M);
         st.rstdf = I.arena.alloc<float>(M);
         st.logits = I.arena.alloc<bf16>((size_t)M * shape.vocab_padded);
+      }
+  };
+  if (I.recompute) {  // one full workspace per rank; xo of the last layer is a sink
+    for (int k = 0; k < n_ranks; ++k) {
+      Stash st;
+      alloc_full(st, false, true);
+      st.layers.back().xo = I.arena.alloc<bf16>((size_t)M * h);
+      I.rscratch.push_back(std::move(st));
+    }
+    I.loss_dummy = I.arena.alloc<float>(1);
+  }
+  for (auto& [key, cp] : I.copies) {
+    const StageLayout& L = I.stages[cp.stage].L;
+    const int nslots = peak[key];
+    const size_t before = I.arena.bytes;
+    for (int k = 0; k < nslots; ++k) {
+      Stash st;
+      if (I.recompute) {
+        if (L.has_embed) st.x0 = I.arena.alloc<bf16>((size_t)M * h);  // the only stashed tensor
+      } else {
+        alloc_full(st, L.has_embed, L.has_head);
       }
       cp.slots.push_back(std::move(st));
     }
@@ -434,7 +455,23 @@ void Trainer::forward_task(int rank, int p, int mb, int s) {
   }
   const Msg* out_msg = (s + 1 < I.D) ? &I.msgs.at(I.msg_key(r, mb, s, 0)) : nullptr;
   if (out_msg) out_msg->before_produce(st);
-  bf16* out_final = out_msg ? out_msg->buf : X.xfinal;
+  Stash& Wk = I.recompute ? I.rscratch[rank - I.first] : X;  // activations land here
+  bf16* out_final = out_msg ? out_msg->buf : Wk.xfinal;
+  stage_forward(rank, s, Wk, x, out_final, tok0, I.loss);
+  if (!L.has_head) out_msg->after_produce(st);
+  if (s == 0) I.launches_per_step += 1;
+}
+
+// The layers (+ final LN, LM head, fused cross-entropy) of stage s for one
+// micro-batch: activations into X, stage output into out_final.
+void Trainer::stage_forward(int rank, int s, Stash& X, const bf16* x, bf16* out_final, size_t tok0,
+                            float* loss) {
+  Impl& I = *d_;
+  const ModelShape& m = I.m;
+  const int h = m.hidden, f = m.ffn, M = I.M, H = m.heads;
+  cudaStream_t st = I.stream_of(rank);
+  const StageLayout& L = I.stages.at(s).L;
+  const bf16* w = I.stages.at(s).w16;
   for (int l = 0; l < L.n_layers; ++l) {
     const LayerOffsets& o = L.layers[l];
     LayerStash& A = X.layers[l];
@@ -459,12 +496,9 @@ void Trainer::forward_task(int rank, int p, int mb, int s) {
                epi(X.logits, m.vocab_padded), st);
     const float scale = 1.f / float((double)I.W * I.N * I.B * m.seq);
     ops::xent_fwd_bwd(X.logits, m.vocab_padded, I.labels + tok0, M, m.vocab, m.vocab_padded, scale, scale,
-                      I.loss, st);
+                      loss, st);
     I.launches_per_step += 3;
-  } else {
-    out_msg->after_produce(st);
   }
-  if (s == 0) I.launches_per_step += 1;
 }
 
 void Trainer::backward_task(int rank, int p, int mb, int s) {
@@ -481,9 +515,15 @@ void Trainer::backward_task(int rank, int p, int mb, int s) {
   if (it == I.slot_of.end()) throw capi::InternalError("backward without stashed activation");
   const int slot = it->second;
   I.slot_of.erase(it);
-  Stash& X = cp.slots[slot];
+  Stash& Xslot = cp.slots[slot];
   Scratch& sc = I.scratch[rank - I.first];
   const size_t tok0 = (size_t)(r * I.N + mb) * I.B * m.seq;
+  const bf16* stage_in = s == 0 ? Xslot.x0 : I.msgs.at(I.msg_key(r, mb, s - 1, 0)).buf;
+  Stash& X = I.recompute ? I.rscratch[rank - I.first] : Xslot;
+  if (I.recompute) {  // rebuild the stage's activations from its stashed input
+    Stash& Wk = I.rscratch[rank - I.first];
+    stage_forward(rank, s, Wk, stage_in, L.has_head ? Wk.xfinal : Wk.layers.back().xo, tok0, I.loss_dummy);
+  }
 
   const bf16* dxo;
   if (L.has_head) {
@@ -506,8 +546,7 @@ void Trainer::backward_task(int rank, int p, int mb, int s) {
   for (int l = L.n_layers - 1; l >= 0; --l) {
     const LayerOffsets& o = L.layers[l];
     LayerStash& A = X.layers[l];
-    const bf16* xin = (l > 0) ? X.layers[l - 1].xo
-                              : (s == 0 ? X.x0 : I.msgs.at(I.msg_key(r, mb, s - 1, 0)).buf);
+    const bf16* xin = (l > 0) ? X.layers[l - 1].xo : stage_in;
     bf16* dxin = (l > 0) ? (dxo == sc.dxa ? sc.dxb : sc.dxa) : (dx_stage ? dx_stage : (dxo == sc.dxa ? sc.dxb : sc.dxa));
     // MLP
     ops::bias_grad(dxo, gw + o.b_fc2, M, h, st);

@@ -5,10 +5,14 @@
 #include <memory>
 #include <string>
 
+#include <cuda_bf16.h>
+
 #include "gpt_model.hpp"
 #include "pipesim/core.hpp"
 
 namespace chimera::gpt {
+
+struct Stash;
 
 class Trainer {
  public:
@@ -38,6 +42,8 @@ class Trainer {
   void issue_iteration();
   void forward_task(int rank, int p, int mb, int s);
   void backward_task(int rank, int p, int mb, int s);
+  void stage_forward(int rank, int s, Stash& X, const __nv_bfloat16* x, __nv_bfloat16* out_final,
+                     size_t tok0, float* loss);
   std::unique_ptr<Impl> d_;
 };
 

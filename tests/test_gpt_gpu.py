@@ -98,3 +98,17 @@ def test_sync_policies_same_math(policy):
         d, ref = got - params[s], p2[s] - params[s]
         assert np.linalg.norm(d - ref) / np.linalg.norm(ref) <= 3e-2
     tr.close()
+
+
+def test_forward_doubling_with_recompute():
+    # FD forces recompute (schedgen.cpp:183-184): forwards stash only the stage input and
+    # every backward re-runs its stage forward first.
+    cfg = P.PipelineConfig("chimera", 4, 1, 8, 1, 1, "forward-doubling")
+    st = _check_iteration(PRESETS["tiny"], cfg, iters=2)
+    assert json.loads(P.generate_json(cfg, None, -1))["config"]["recompute"] is True
+    assert st["graph"]
+
+
+def test_recompute_flag_on_direct_schedule():
+    cfg = P.PipelineConfig("chimera", 4, 2, 4, 2, 1, "direct", True)
+    _check_iteration(PRESETS["tiny"], cfg)
