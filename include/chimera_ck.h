@@ -111,6 +111,9 @@ CK_API int ck_sgd_update(float* w32, void* w16, float* const* grads, int copies,
 /* flash attention, head dim 64, over packed qkv [B*seq, 3*H*64]. */
 CK_API int ck_attn_fwd(const void* qkv, void* out, float* lse, int B, int seq, int H, int causal,
                        void* stream);
+/* tcgen05/TMEM flash attention forward (S and O accumulate in tensor memory). */
+CK_API int ck_attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int seq, int H,
+                          int causal, void* stream);
 CK_API int ck_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
                        void* dqkv, float* scratch, int B, int seq, int H, int causal, void* stream);
 CK_API long long ck_attn_bwd_scratch_floats(int B, int seq, int H);

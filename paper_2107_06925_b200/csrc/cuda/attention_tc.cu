@@ -1,0 +1,259 @@
+// Flash-attention forward on the 5th-generation tensor cores (sm_100a), head dim 64.
+//
+// CTA = (128-query tile, batch*head); 6 warps:
+//   warp 4  TMA producer: Q once, then 128-key K/V tiles into a 2-stage ring
+//   warp 5  TMEM allocator + single-thread MMA issuer:
+//             S  = Q K^T      tcgen05.mma kind::f16 M128 N128 K64  -> TMEM cols [0,128)
+//             O += P V        tcgen05.mma kind::f16 M128 N64  K128 -> TMEM cols [128,192)
+//   warps 0-3  softmax: thread t owns query row t (= TMEM lane t): two passes over the
+//             S row in TMEM (max, then exp2 + sum), P written as bf16 straight into the
+//             128-byte-swizzled K-major smem tile the next MMA reads, running O rescaled
+//             in TMEM (tcgen05.ld/st) when the row max moves; final O / l and the
+//             log-sum-exp go to HBM.
+// The Q/K/V tiles come straight out of the packed [tokens, 3*H*64] QKV GEMM output via
+// one 2-D TMA map (no head split), so the kernel reads exactly Q, K, V once per tile.
+// ~112 KB smem and 256 TMEM columns per CTA: two CTAs per SM overlap one CTA's softmax
+// with the other's MMAs.
+#include <cuda.h>
+
+#include "chimera_ck.h"
+#include "common.cuh"
+#include "ops.cuh"
+#include "ptx_sm100.cuh"
+#include "tma_host.hpp"
+
+namespace chimera::ops {
+
+namespace {
+
+constexpr int kQ = 128, kKV = 128, kD = 64;
+constexpr int kTileBytes = kQ * kD * 2;  // 16 KB: 128 rows x 128 B
+constexpr int kSmemQ = 0, kSmemK = kTileBytes, kSmemV = 3 * kTileBytes, kSmemP = 5 * kTileBytes;
+constexpr int kSmemBar = 7 * kTileBytes;  // after P (2 tiles)
+constexpr int kSmemTotal = kSmemBar + 256;
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+template <bool CAUSAL>
+__global__ void __launch_bounds__(192, 2)
+    k_attn_fwd_tc(const __grid_constant__ CUtensorMap tqkv, bf16* __restrict__ out, float* __restrict__ lse,
+                  int seq, int H) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((ptx::smem_u32(smem) & 1023) != 0) __trap();  // swizzle atoms need 1 KB alignment
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kSmemBar);
+  uint64_t *q_full = bar, *kv_full = bar + 1, *kv_empty = bar + 3, *s_full = bar + 5, *p_full = bar + 6,
+           *o_done = bar + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qb = blockIdx.x, bh = blockIdx.y, b = bh / H, hd = bh % H;
+  const int q0 = qb * kQ, row_base = b * seq;
+  const int nkv = (seq + kKV - 1) / kKV;
+  const int nkb = CAUSAL ? min(nkv, qb + 1) : nkv;
+
+  if (warp == 4 && lane == 0) {
+    ptx::tma_prefetch(&tqkv);
+    ptx::mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) ptx::mbar_init(&kv_full[s], 1), ptx::mbar_init(&kv_empty[s], 1);
+    ptx::mbar_init(s_full, 1);
+    ptx::mbar_init(p_full, 128);
+    ptx::mbar_init(o_done, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 5) ptx::tmem_alloc(tmem_slot, 256);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // S: cols [0,128), O: cols [128,192)
+
+  if (warp == 4) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(q_full, kTileBytes);
+      ptx::tma_load_2d(smem + kSmemQ, &tqkv, q_full, hd * kD, row_base + q0);
+      for (int j = 0; j < nkb; ++j) {
+        const int st = j & 1;
+        ptx::mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&kv_full[st], 2 * kTileBytes);
+        ptx::tma_load_2d(smem + kSmemK + st * kTileBytes, &tqkv, &kv_full[st], H * kD + hd * kD, row_base + j * kKV);
+        ptx::tma_load_2d(smem + kSmemV + st * kTileBytes, &tqkv, &kv_full[st], 2 * H * kD + hd * kD,
+                         row_base + j * kKV);
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      constexpr uint32_t id_s = ptx::idesc_bf16(kQ, kKV, false, false);
+      constexpr uint32_t id_o = ptx::idesc_bf16(kQ, kD, false, true);
+      const uint32_t sq = ptx::smem_u32(smem + kSmemQ), sp = ptx::smem_u32(smem + kSmemP);
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        ptx::mbar_wait(&kv_full[st], (j >> 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t sk = ptx::smem_u32(smem + kSmemK + st * kTileBytes);
+#pragma unroll
+        for (int k = 0; k < kD / 16; ++k)
+          ptx::umma_f16(tmem, ptx::smem_desc_sw128(sq + k * 32, 16, 1024), ptx::smem_desc_sw128(sk + k * 32, 16, 1024),
+                        id_s, k > 0);
+        ptx::umma_commit(s_full);
+      };
+      ptx::mbar_wait(q_full, 0);
+      issue_s(0);
+      for (int j = 0; j < nkb; ++j) {
+        ptx::mbar_wait(p_full, j & 1);  // P_j in smem, S free, O rescaled
+        ptx::tc_fence_after();
+        const uint32_t sv = ptx::smem_u32(smem + kSmemV + (j & 1) * kTileBytes);
+#pragma unroll
+        for (int k = 0; k < kKV / 16; ++k)
+          ptx::umma_f16(tmem + 128, ptx::smem_desc_sw128(sp + (k >> 2) * kTileBytes + (k & 3) * 32, 16, 1024),
+                        ptx::smem_desc_sw128(sv + k * 2048, kTileBytes, 1024), id_o, (j > 0 || k > 0) ? 1u : 0u);
+        ptx::umma_commit(&kv_empty[j & 1]);
+        ptx::umma_commit(o_done);
+        if (j + 1 < nkb) issue_s(j + 1);
+      }
+    }
+  } else {
+    // softmax warps: thread t <-> query row t <-> TMEM lane t
+    const int t = threadIdx.x;  // 0..127
+    const int q = q0 + t;
+    const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
+    const float sl2 = 0.125f * kLog2e;
+    float m = -INFINITY, l = 0.f;
+    uint8_t* sp = smem + kSmemP;
+    for (int j = 0; j < nkb; ++j) {
+      ptx::mbar_wait(s_full, j & 1);
+      ptx::tc_fence_after();
+      const int key0 = j * kKV;
+      // pass 1: row max over the scaled, masked scores
+      float mx = -INFINITY;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        ptx::tmem_ld32(trow + c * 32, r);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int key = key0 + c * 32 + i;
+          const bool ok = key < seq && (!CAUSAL || key <= q);
+          mx = fmaxf(mx, ok ? __uint_as_float(r[i]) * sl2 : -INFINITY);
+        }
+      }
+      const float mn = fmaxf(m, mx);
+      const float safe = mn == -INFINITY ? 0.f : mn;
+      const float alpha = exp2f(m - safe);
+      m = mn;
+      l *= alpha;
+      if (j > 0) {  // rescale the running output once the previous P V has landed
+        ptx::mbar_wait(o_done, (j - 1) & 1);
+        ptx::tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          uint32_t r[32];
+          ptx::tmem_ld32(trow + 128 + c * 32, r);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+          tmem_st32(trow + 128 + c * 32, r);
+        }
+        tmem_st_wait();
+      }
+      // pass 2: P = exp2(s - m) as bf16 into the swizzled K-major tile
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        ptx::tmem_ld32(trow + c * 32, r);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {  // 8 keys -> one 16-byte chunk
+          uint32_t pk[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float pv[2];
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int i = g * 8 + e * 2 + h2, key = key0 + c * 32 + i;
+              const bool ok = key < seq && (!CAUSAL || key <= q);
+              pv[h2] = ok ? exp2f(__uint_as_float(r[i]) * sl2 - safe) : 0.f;
+              l += pv[h2];
+            }
+            __nv_bfloat162 hb = __floats2bfloat162_rn(pv[0], pv[1]);
+            pk[e] = *reinterpret_cast<uint32_t*>(&hb);
+          }
+          const int k8 = c * 4 + g;  // chunk of 8 keys, 0..15
+          uint8_t* dst = sp + (k8 >> 3) * kTileBytes + t * 128 + (((k8 & 7) ^ (t & 7)) << 4);
+          *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+      }
+      ptx::fence_proxy_async();  // P (generic stores) -> visible to the tensor core
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(p_full);
+    }
+    // epilogue: O / l -> bf16, log-sum-exp
+    ptx::mbar_wait(o_done, (nkb - 1) & 1);
+    ptx::tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t r[32];
+      ptx::tmem_ld32(trow + 128 + c * 32, r);
+      ptx::tmem_ld_wait();
+      if (q < seq) {
+        bf16* orow = out + ((long long)row_base + q) * (H * kD) + hd * kD + c * 32;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          uint32_t pk[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            __nv_bfloat162 hb = __floats2bfloat162_rn(__uint_as_float(r[g * 8 + 2 * e]) * inv,
+                                                      __uint_as_float(r[g * 8 + 2 * e + 1]) * inv);
+            pk[e] = *reinterpret_cast<uint32_t*>(&hb);
+          }
+          *reinterpret_cast<uint4*>(orow + g * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+      }
+    }
+    if (q < seq) lse[(long long)bh * seq + q] = (m + __log2f(l)) / kLog2e;
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 256);
+  }
+}
+
+}  // namespace
+
+void attn_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int seq, int H, bool causal, cudaStream_t st) {
+  const long long ld = 3LL * H * kD;
+  const CUtensorMap m = cuda::make_map_2d_bf16(qkv, ld, (long long)B * seq, ld, 64, 128);
+  const dim3 grid((seq + kQ - 1) / kQ, B * H);
+  static bool attr = false;
+  if (!attr) {
+    CK_CUDA(cudaFuncSetAttribute(k_attn_fwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
+    CK_CUDA(cudaFuncSetAttribute(k_attn_fwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
+    attr = true;
+  }
+  if (causal) k_attn_fwd_tc<true><<<grid, 192, kSmemTotal, st>>>(m, out, lse, seq, H);
+  else k_attn_fwd_tc<false><<<grid, 192, kSmemTotal, st>>>(m, out, lse, seq, H);
+  CK_CUDA(cudaGetLastError());
+}
+
+}  // namespace chimera::ops
+
+extern "C" CK_API int ck_attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int seq, int H, int causal,
+                                     void* st) {
+  return chimera::capi::guarded([&] {
+    chimera::ops::attn_fwd_tc(static_cast<const chimera::ops::bf16*>(qkv), static_cast<chimera::ops::bf16*>(out), lse,
+                              B, seq, H, causal != 0, static_cast<cudaStream_t>(st));
+  });
+}

@@ -43,6 +43,9 @@ void cast_f32_bf16(const float* src, bf16* dst, long long n, cudaStream_t st);
 // 64-wide column blocks), head dim 64.  out [M, H*64]; lse [B*H*seq] (natural log).
 void attn_fwd(const bf16* qkv, bf16* out, float* lse, int B, int seq, int H, bool causal,
               cudaStream_t st);
+// tcgen05/TMEM version (cuda/attention_tc.cu): same contract as attn_fwd.
+void attn_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int seq, int H, bool causal,
+                 cudaStream_t st);
 // dqkv [M, 3*H*64] from dout, given qkv, out and lse of the forward.
 // `scratch` >= B*H*seq floats (row dot) + B*seq*H*64 floats (fp32 dq accumulator).
 void attn_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, bf16* dqkv,

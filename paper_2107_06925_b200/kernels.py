@@ -47,6 +47,7 @@ _lib.register("ck_xent_fwd_bwd", _i, [_vp, _ll, _vp, _i, _i, _i, C.c_float, C.c_
 _lib.register("ck_bias_grad", _i, [_vp, _vp, _i, _i, _vp])
 _lib.register("ck_sgd_update", _i, [_vp, _vp, _vp, _i, _ll, C.c_float, _vp])
 _lib.register("ck_attn_fwd", _i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp])
+_lib.register("ck_attn_fwd_tc", _i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp])
 _lib.register("ck_attn_bwd", _i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp])
 _lib.register("ck_attn_bwd_scratch_floats", _ll, [_i, _i, _i])
 
@@ -83,6 +84,10 @@ def bias_grad(dy, db, stream=None):
 
 def attn_fwd(qkv, out, lse, B, seq, H, causal=True, stream=None):
     check(lib().ck_attn_fwd(_p(qkv), _p(out), _p(lse), B, seq, H, int(causal), _stream(stream)))
+
+
+def attn_fwd_tc(qkv, out, lse, B, seq, H, causal=True, stream=None):
+    check(lib().ck_attn_fwd_tc(_p(qkv), _p(out), _p(lse), B, seq, H, int(causal), _stream(stream)))
 
 
 def attn_bwd(qkv, out, dout, lse, dqkv, B, seq, H, causal=True, stream=None):

@@ -85,14 +85,15 @@ def test_bias_grad():
     assert rel(db, dy.float().sum(0) + 1) < 1e-5
 
 
+@pytest.mark.parametrize("impl", ["mma_sync", "tcgen05"])
 @pytest.mark.parametrize("B,seq,H,causal", [(2, 256, 4, True), (1, 1024, 2, True), (2, 128, 16, False),
-                                             (1, 200, 2, True), (1, 632, 2, False)])
-def test_attention(B, seq, H, causal):
+                                             (1, 200, 2, True), (1, 632, 2, False), (3, 632, 2, True)])
+def test_attention(B, seq, H, causal, impl):
     d = 64
     qkv = (torch.randn(B * seq, 3 * H * d, device="cuda")).bfloat16()
     out = torch.empty(B * seq, H * d, device="cuda", dtype=torch.bfloat16)
     lse = torch.empty(B * H * seq, device="cuda")
-    ck.attn_fwd(qkv, out, lse, B, seq, H, causal)
+    (ck.attn_fwd if impl == "mma_sync" else ck.attn_fwd_tc)(qkv, out, lse, B, seq, H, causal)
     q, k, v = qkv.float().view(B, seq, 3, H, d).permute(2, 0, 3, 1, 4)
     q, k, v = (t.contiguous().requires_grad_() for t in (q, k, v))
     s = q @ k.transpose(-1, -2) / math.sqrt(d)
