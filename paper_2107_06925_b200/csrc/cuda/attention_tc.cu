@@ -26,6 +26,7 @@ namespace chimera::ops {
 
 namespace {
 
+using ptx::ex2_approx;
 constexpr int kQ = 128, kKV = 128, kD = 64;
 constexpr int kTileBytes = kQ * kD * 2;  // 16 KB: 128 rows x 128 B
 constexpr int kSmemQ = 0, kSmemK = kTileBytes, kSmemV = 3 * kTileBytes, kSmemP = 5 * kTileBytes;
@@ -83,7 +84,7 @@ __global__ void __launch_bounds__(192, 2)
       ptx::tma_load_2d(smem + kSmemQ, &tqkv, q_full, hd * kD, row_base + q0);
       for (int j = 0; j < nkb; ++j) {
         const int st = j & 1;
-        ptx::mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        ptx::mbar_wait_sleep(&kv_empty[st], ((j >> 1) & 1) ^ 1);
         ptx::mbar_arrive_expect_tx(&kv_full[st], 2 * kTileBytes);
         ptx::tma_load_2d(smem + kSmemK + st * kTileBytes, &tqkv, &kv_full[st], H * kD + hd * kD, row_base + j * kKV);
         ptx::tma_load_2d(smem + kSmemV + st * kTileBytes, &tqkv, &kv_full[st], 2 * H * kD + hd * kD,
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(192, 2)
       const uint32_t sq = ptx::smem_u32(smem + kSmemQ), sp = ptx::smem_u32(smem + kSmemP);
       auto issue_s = [&](int j) {
         const int st = j & 1;
-        ptx::mbar_wait(&kv_full[st], (j >> 1) & 1);
+        ptx::mbar_wait_sleep(&kv_full[st], (j >> 1) & 1);
         ptx::tc_fence_after();
         const uint32_t sk = ptx::smem_u32(smem + kSmemK + st * kTileBytes);
 #pragma unroll
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(192, 2)
       ptx::mbar_wait(q_full, 0);
       issue_s(0);
       for (int j = 0; j < nkb; ++j) {
-        ptx::mbar_wait(p_full, j & 1);  // P_j in smem, S free, O rescaled
+        ptx::mbar_wait_sleep(p_full, j & 1);  // P_j in smem, S free, O rescaled
         ptx::tc_fence_after();
         const uint32_t sv = ptx::smem_u32(smem + kSmemV + (j & 1) * kTileBytes);
 #pragma unroll
@@ -133,66 +134,66 @@ __global__ void __launch_bounds__(192, 2)
       ptx::mbar_wait(s_full, j & 1);
       ptx::tc_fence_after();
       const int key0 = j * kKV;
-      // pass 1: row max over the scaled, masked scores
+      // the whole 128-score row lives in registers (one TMEM pass)
+      uint32_t r[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) ptx::tmem_ld32(trow + c * 32, r[c]);
+      ptx::tmem_ld_wait();
+      // masking only on the diagonal (causal) / sequence-tail tile: warp-uniform branch
+      const bool edge = (CAUSAL && key0 + kKV - 1 > q0) || key0 + kKV > seq;
       float mx = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        ptx::tmem_ld32(trow + c * 32, r);
-        ptx::tmem_ld_wait();
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const int key = key0 + c * 32 + i;
-          const bool ok = key < seq && (!CAUSAL || key <= q);
-          mx = fmaxf(mx, ok ? __uint_as_float(r[i]) * sl2 : -INFINITY);
+          float v = __uint_as_float(r[c][i]) * sl2;
+          if (edge) {
+            const int key = key0 + c * 32 + i;
+            if (key >= seq || (CAUSAL && key > q)) v = -INFINITY;
+          }
+          r[c][i] = __float_as_uint(v);
+          mx = fmaxf(mx, v);
         }
-      }
       const float mn = fmaxf(m, mx);
       const float safe = mn == -INFINITY ? 0.f : mn;
-      const float alpha = exp2f(m - safe);
+      const float alpha = ex2_approx(m - safe);
       m = mn;
       l *= alpha;
-      if (j > 0) {  // rescale the running output once the previous P V has landed
+      if (j > 0) {  // the previous P V must have landed before O is touched / P rewritten
         ptx::mbar_wait(o_done, (j - 1) & 1);
         ptx::tc_fence_after();
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {  // rescale only when a row max moved
 #pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
-          uint32_t r[32];
-          ptx::tmem_ld32(trow + 128 + c * 32, r);
-          ptx::tmem_ld_wait();
+          for (int c = 0; c < 2; ++c) {
+            uint32_t o[32];
+            ptx::tmem_ld32(trow + 128 + c * 32, o);
+            ptx::tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-          tmem_st32(trow + 128 + c * 32, r);
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(trow + 128 + c * 32, o);
+          }
+          tmem_st_wait();
         }
-        tmem_st_wait();
       }
-      // pass 2: P = exp2(s - m) as bf16 into the swizzled K-major tile
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        ptx::tmem_ld32(trow + c * 32, r);
-        ptx::tmem_ld_wait();
+      // P = exp2(s - m) as bf16 into the swizzled K-major tile
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
 #pragma unroll
         for (int g = 0; g < 4; ++g) {  // 8 keys -> one 16-byte chunk
           uint32_t pk[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            float pv[2];
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-              const int i = g * 8 + e * 2 + h2, key = key0 + c * 32 + i;
-              const bool ok = key < seq && (!CAUSAL || key <= q);
-              pv[h2] = ok ? exp2f(__uint_as_float(r[i]) * sl2 - safe) : 0.f;
-              l += pv[h2];
-            }
-            __nv_bfloat162 hb = __floats2bfloat162_rn(pv[0], pv[1]);
+            const int i = g * 8 + e * 2;
+            const float p0 = ex2_approx(__uint_as_float(r[c][i]) - safe);
+            const float p1 = ex2_approx(__uint_as_float(r[c][i + 1]) - safe);
+            l += p0 + p1;
+            __nv_bfloat162 hb = __floats2bfloat162_rn(p0, p1);
             pk[e] = *reinterpret_cast<uint32_t*>(&hb);
           }
           const int k8 = c * 4 + g;  // chunk of 8 keys, 0..15
           uint8_t* dst = sp + (k8 >> 3) * kTileBytes + t * 128 + (((k8 & 7) ^ (t & 7)) << 4);
           *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
-      }
       ptx::fence_proxy_async();  // P (generic stores) -> visible to the tensor core
       ptx::tc_fence_before();
       ptx::mbar_arrive(p_full);
