@@ -117,6 +117,9 @@ CK_API int ck_attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int seq
 CK_API int ck_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
                        void* dqkv, float* scratch, int B, int seq, int H, int causal, void* stream);
 CK_API long long ck_attn_bwd_scratch_floats(int B, int seq, int H);
+/* tcgen05/TMEM flash attention backward (same contract / scratch as ck_attn_bwd). */
+CK_API int ck_attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float* lse,
+                          void* dqkv, float* scratch, int B, int seq, int H, int causal, void* stream);
 
 /* ------------------------------------------------------- GPT-2 stage executor */
 /* Transformer shape (head dim 64; vocab padded to a multiple of 8, e.g. 50304). */

@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(128) k_attn_bwd(const bf16* __restrict__ qkv, 
   __shared__ alignas(128) bf16 sdO[kTile * kLd];
   __shared__ alignas(128) bf16 sdS[kTile * kLd];
   __shared__ float sL[kTile], sD[kTile];
-  const int kb = blockIdx.x, bh = blockIdx.y, b = bh / H, hd = bh % H;
+  const int kb = blockIdx.x, bh = blockIdx.y, b = bh / H, hd = bh % H;  // causal: kb 0 has most work
   const long long ld = 3LL * H * kHd, ldo = (long long)H * kHd;
   const bf16* base = qkv + (long long)b * seq * ld;
   const bf16* gq = base + hd * kHd;
@@ -303,10 +303,8 @@ __global__ void __launch_bounds__(128) k_attn_bwd(const bf16* __restrict__ qkv, 
         if (q >= seq) continue;
         float* acc = dq_acc + ((long long)b * seq + q) * (H * kHd) + hd * kHd;
 #pragma unroll
-        for (int dn = 0; dn < 8; ++dn) {
-          atomicAdd(acc + dn * 8 + 2 * t, dq[dn][2 * r]);
-          atomicAdd(acc + dn * 8 + 2 * t + 1, dq[dn][2 * r + 1]);
-        }
+        for (int dn = 0; dn < 8; ++dn)  // vector fp32 atomic (sm_90+): 2 columns per op
+          atomicAdd(reinterpret_cast<float2*>(acc + dn * 8 + 2 * t), make_float2(dq[dn][2 * r], dq[dn][2 * r + 1]));
       }
     }
     __syncthreads();
@@ -350,6 +348,17 @@ void attn_fwd(const bf16* qkv, bf16* out, float* lse, int B, int seq, int H, boo
 
 size_t attn_bwd_scratch_floats(int B, int seq, int H) {
   return size_t(B) * H * seq + size_t(B) * seq * H * kHd;
+}
+
+void attn_bwd_dot(const bf16* out, const bf16* dout, float* D, int M, int seq, int H, cudaStream_t st) {
+  k_attn_bwd_dot<<<cuda::ceil_div((long long)M * H * 32, 256), 256, 0, st>>>(out, dout, D, M, seq, H);
+  CK_CUDA(cudaGetLastError());
+}
+
+void attn_dq_out(const float* dq, bf16* dqkv, int M, int H, cudaStream_t st) {
+  const long long n = (long long)M * H * kHd;
+  k_dq_out<<<std::min<long long>((n / 2 + 255) / 256, 148LL * 16), 256, 0, st>>>(dq, dqkv, M, H);
+  CK_CUDA(cudaGetLastError());
 }
 
 void attn_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, bf16* dqkv,

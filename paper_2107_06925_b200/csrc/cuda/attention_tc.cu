@@ -58,7 +58,8 @@ __global__ void __launch_bounds__(192, 2)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qb = blockIdx.x, bh = blockIdx.y, b = bh / H, hd = bh % H;
+  // causal: the longest query tiles (most key tiles) are scheduled first
+  const int qb = CAUSAL ? gridDim.x - 1 - blockIdx.x : blockIdx.x, bh = blockIdx.y, b = bh / H, hd = bh % H;
   const int q0 = qb * kQ, row_base = b * seq;
   const int nkv = (seq + kKV - 1) / kKV;
   const int nkb = CAUSAL ? min(nkv, qb + 1) : nkv;
@@ -232,6 +233,232 @@ __global__ void __launch_bounds__(192, 2)
   }
 }
 
+// ----------------------------------------------------------------- backward --
+// CTA = (128-key tile, batch*head), same 6-warp split.  Per 128-query tile:
+//   S^T  = K Q^T     (M128 keys, N128 q, K64)   TMEM [0,128)
+//   dP^T = V dO^T    (M128, N128, K64)          TMEM [128,256)
+//   compute warps (thread = key row): P^T = exp2(S^T*c - lse2), dS^T = P^T (dP^T - D)
+//     -> bf16, 128-byte-swizzled K-major smem tiles
+//   dV  += P^T dO    (M128 keys, N64, K128 q)   TMEM [256,320)
+//   dK  += dS^T Q    (M128 keys, N64, K128 q)   TMEM [320,384)
+//   dQ   = dS K      (M128 q, N64, K128 keys)   TMEM [384,448)  -- the dS^T tile read
+//     as an MN-major A operand; compute warps (thread = query row) add it to the fp32
+//     dQ accumulator with 16-byte vector atomics.
+constexpr int kB_K = 0, kB_V = kTileBytes, kB_Q = 2 * kTileBytes, kB_DO = 4 * kTileBytes,
+              kB_P = 6 * kTileBytes, kB_DS = 8 * kTileBytes, kB_LD = 10 * kTileBytes;  // lse/D [2][2][128]
+constexpr int kB_BAR = kB_LD + 4 * 128 * 4;
+constexpr int kBwdSmem = kB_BAR + 256;
+
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <bool CAUSAL>
+__global__ void __launch_bounds__(192, 1)
+    k_attn_bwd_tc(const __grid_constant__ CUtensorMap tqkv, const __grid_constant__ CUtensorMap tdo,
+                  const float* __restrict__ lse, const float* __restrict__ Dv, float* __restrict__ dq_acc,
+                  bf16* __restrict__ dqkv, int seq, int H) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((ptx::smem_u32(smem) & 1023) != 0) __trap();
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kB_BAR);
+  uint64_t *kv_full = bar, *qd_full = bar + 1, *qd_empty = bar + 3, *s_full = bar + 5, *ds_full = bar + 6,
+           *mm_done = bar + 7, *dq_free = bar + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
+  float* sLD = reinterpret_cast<float*>(smem + kB_LD);  // [buf][0=lse2,1=D][128]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.x, bh = blockIdx.y, b = bh / H, hd = bh % H;
+  const int k0 = kb * kKV, row_base = b * seq;
+  const int nq = (seq + kQ - 1) / kQ;
+  const int j0 = CAUSAL ? kb : 0;  // first query tile that can see these keys
+  const int niter = nq - j0;
+
+  if (warp == 4 && lane == 0) {
+    ptx::tma_prefetch(&tqkv);
+    ptx::tma_prefetch(&tdo);
+    ptx::mbar_init(kv_full, 1);
+    for (int s2 = 0; s2 < 2; ++s2) ptx::mbar_init(&qd_full[s2], 1), ptx::mbar_init(&qd_empty[s2], 1);
+    ptx::mbar_init(s_full, 1);
+    ptx::mbar_init(ds_full, 128);
+    ptx::mbar_init(mm_done, 1);
+    ptx::mbar_init(dq_free, 128);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 5) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t kSt = 0, kDPt = 128, kDV = 256, kDK = 320, kDQ = 384;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(kv_full, 2 * kTileBytes);
+      ptx::tma_load_2d(smem + kB_K, &tqkv, kv_full, H * kD + hd * kD, row_base + k0);
+      ptx::tma_load_2d(smem + kB_V, &tqkv, kv_full, 2 * H * kD + hd * kD, row_base + k0);
+      for (int it = 0; it < niter; ++it) {
+        const int st = it & 1, q0 = (j0 + it) * kQ;
+        ptx::mbar_wait_sleep(&qd_empty[st], ((it >> 1) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&qd_full[st], 2 * kTileBytes);
+        ptx::tma_load_2d(smem + kB_Q + st * kTileBytes, &tqkv, &qd_full[st], hd * kD, row_base + q0);
+        ptx::tma_load_2d(smem + kB_DO + st * kTileBytes, &tdo, &qd_full[st], hd * kD, row_base + q0);
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      constexpr uint32_t id_s = ptx::idesc_bf16(128, 128, false, false);
+      constexpr uint32_t id_kv = ptx::idesc_bf16(128, 64, false, true);  // A K-major, B MN-major
+      constexpr uint32_t id_q = ptx::idesc_bf16(128, 64, true, true);    // A MN-major (dS^T^T), B MN-major
+      const uint32_t sk = ptx::smem_u32(smem + kB_K), sv = ptx::smem_u32(smem + kB_V);
+      const uint32_t sp = ptx::smem_u32(smem + kB_P), sds = ptx::smem_u32(smem + kB_DS);
+      ptx::mbar_wait(kv_full, 0);
+      for (int it = 0; it < niter; ++it) {
+        const int st = it & 1;
+        const uint32_t sq = ptx::smem_u32(smem + kB_Q + st * kTileBytes);
+        const uint32_t sdo = ptx::smem_u32(smem + kB_DO + st * kTileBytes);
+        ptx::mbar_wait_sleep(&qd_full[st], (it >> 1) & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < kD / 16; ++k) {
+          ptx::umma_f16(tmem + kSt, ptx::smem_desc_sw128(sk + k * 32, 16, 1024), ptx::smem_desc_sw128(sq + k * 32, 16, 1024),
+                        id_s, k > 0);
+          ptx::umma_f16(tmem + kDPt, ptx::smem_desc_sw128(sv + k * 32, 16, 1024),
+                        ptx::smem_desc_sw128(sdo + k * 32, 16, 1024), id_s, k > 0);
+        }
+        ptx::umma_commit(s_full);
+        ptx::mbar_wait_sleep(ds_full, it & 1);  // P^T, dS^T in smem; S^T / dP^T consumed
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < kQ / 16; ++k) {
+          const uint64_t a_p = ptx::smem_desc_sw128(sp + (k >> 2) * kTileBytes + (k & 3) * 32, 16, 1024);
+          const uint64_t a_ds = ptx::smem_desc_sw128(sds + (k >> 2) * kTileBytes + (k & 3) * 32, 16, 1024);
+          ptx::umma_f16(tmem + kDV, a_p, ptx::smem_desc_sw128(sdo + k * 2048, kTileBytes, 1024), id_kv,
+                        (it > 0 || k > 0) ? 1u : 0u);
+          ptx::umma_f16(tmem + kDK, a_ds, ptx::smem_desc_sw128(sq + k * 2048, kTileBytes, 1024), id_kv,
+                        (it > 0 || k > 0) ? 1u : 0u);
+        }
+        if (it > 0) ptx::mbar_wait_sleep(dq_free, (it - 1) & 1);  // previous dQ read out
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < kKV / 16; ++k)  // dQ = dS K: reduce over 16 keys per step
+          ptx::umma_f16(tmem + kDQ, ptx::smem_desc_sw128(sds + k * 2048, kTileBytes, 1024),
+                        ptx::smem_desc_sw128(sk + k * 2048, kTileBytes, 1024), id_q, k > 0);
+        ptx::umma_commit(&qd_empty[st]);
+        ptx::umma_commit(mm_done);
+      }
+    }
+  } else {
+    const int t = threadIdx.x;  // key row for S^T / dP^T / dK / dV; query row for dQ
+    const int key = k0 + t;
+    const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
+    const float sl2 = 0.125f * kLog2e;
+    uint8_t* sp = smem + kB_P;
+    uint8_t* sds = smem + kB_DS;
+    for (int it = 0; it < niter; ++it) {
+      const int q0 = (j0 + it) * kQ;
+      float* L2 = sLD + (it & 1) * 256;
+      {
+        const int q = q0 + t;
+        L2[t] = q < seq ? lse[(long long)bh * seq + q] * kLog2e : 0.f;
+        L2[128 + t] = q < seq ? Dv[(long long)bh * seq + q] : 0.f;
+      }
+      named_bar_sync(1, 128);
+      ptx::mbar_wait(s_full, it & 1);
+      ptx::tc_fence_after();
+      const bool edge = (CAUSAL && q0 < k0 + kKV - 1) || q0 + kQ > seq || k0 + kKV > seq;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t rs[32], rd[32];
+        ptx::tmem_ld32(trow + kSt + c * 32, rs);
+        ptx::tmem_ld32(trow + kDPt + c * 32, rd);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          uint32_t pk[4], dk[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float pv[2], dsv[2];
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int i = g * 8 + e * 2 + h2, ql = c * 32 + i, q = q0 + ql;
+              float p = ex2_approx(__uint_as_float(rs[i]) * sl2 - L2[ql]);
+              if (edge && (q >= seq || key >= seq || (CAUSAL && key > q))) p = 0.f;
+              pv[h2] = p;
+              dsv[h2] = p * (__uint_as_float(rd[i]) - L2[128 + ql]);
+            }
+            __nv_bfloat162 hp = __floats2bfloat162_rn(pv[0], pv[1]);
+            __nv_bfloat162 hd2 = __floats2bfloat162_rn(dsv[0], dsv[1]);
+            pk[e] = *reinterpret_cast<uint32_t*>(&hp);
+            dk[e] = *reinterpret_cast<uint32_t*>(&hd2);
+          }
+          const int k8 = c * 4 + g;
+          const int off = (k8 >> 3) * kTileBytes + t * 128 + (((k8 & 7) ^ (t & 7)) << 4);
+          *reinterpret_cast<uint4*>(sp + off) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4*>(sds + off) = make_uint4(dk[0], dk[1], dk[2], dk[3]);
+        }
+      }
+      ptx::fence_proxy_async();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(ds_full);
+      // dQ of this query tile: thread t <-> query row q0 + t
+      ptx::mbar_wait(mm_done, it & 1);
+      ptx::tc_fence_after();
+      const int q = q0 + t;
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        uint32_t r[32];
+        ptx::tmem_ld32(trow + kDQ + c * 32, r);
+        ptx::tmem_ld_wait();
+        if (q < seq) {
+          float* acc = dq_acc + ((long long)row_base + q) * (H * kD) + hd * kD + c * 32;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            atomicAdd(reinterpret_cast<float4*>(acc + i),
+                      make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]), __uint_as_float(r[i + 2]),
+                                  __uint_as_float(r[i + 3])));
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(dq_free);
+    }
+    // dK (scaled by 1/sqrt(d)) and dV for this key tile: thread t <-> key row k0 + t
+    if (niter > 0) {
+#pragma unroll 1
+      for (int part = 0; part < 2; ++part) {
+        const uint32_t base = part == 0 ? kDK : kDV;
+        const float sc = part == 0 ? 0.125f : 1.f;
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          uint32_t r[32];
+          ptx::tmem_ld32(trow + base + c * 32, r);
+          ptx::tmem_ld_wait();
+          if (key < seq) {
+            bf16* dst = dqkv + ((long long)row_base + key) * (3LL * H * kD) + (part == 0 ? 1 : 2) * (long long)H * kD +
+                        hd * kD + c * 32;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              uint32_t pk[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                __nv_bfloat162 hb = __floats2bfloat162_rn(__uint_as_float(r[g * 8 + 2 * e]) * sc,
+                                                          __uint_as_float(r[g * 8 + 2 * e + 1]) * sc);
+                pk[e] = *reinterpret_cast<uint32_t*>(&hb);
+              }
+              *reinterpret_cast<uint4*>(dst + g * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
+          }
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
 }  // namespace
 
 void attn_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int seq, int H, bool causal, cudaStream_t st) {
@@ -249,7 +476,40 @@ void attn_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int seq, int H, 
   CK_CUDA(cudaGetLastError());
 }
 
+// dqkv from dout on the tensor cores; `scratch` as attn_bwd (row dots D, fp32 dQ).
+void attn_bwd_tc(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, bf16* dqkv, float* scratch,
+                 int B, int seq, int H, bool causal, cudaStream_t st) {
+  float* D = scratch;
+  float* dq = scratch + size_t(B) * H * seq;
+  const int M = B * seq;
+  CK_CUDA(cudaMemsetAsync(dq, 0, size_t(M) * H * kD * sizeof(float), st));
+  attn_bwd_dot(out, dout, D, M, seq, H, st);
+  const long long ld = 3LL * H * kD;
+  const CUtensorMap mq = cuda::make_map_2d_bf16(qkv, ld, (long long)M, ld, 64, 128);
+  const CUtensorMap mo = cuda::make_map_2d_bf16(dout, (long long)H * kD, (long long)M, (long long)H * kD, 64, 128);
+  static bool attr = false;
+  if (!attr) {
+    CK_CUDA(cudaFuncSetAttribute(k_attn_bwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem));
+    CK_CUDA(cudaFuncSetAttribute(k_attn_bwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem));
+    attr = true;
+  }
+  const dim3 grid((seq + kKV - 1) / kKV, B * H);
+  if (causal) k_attn_bwd_tc<true><<<grid, 192, kBwdSmem, st>>>(mq, mo, lse, D, dq, dqkv, seq, H);
+  else k_attn_bwd_tc<false><<<grid, 192, kBwdSmem, st>>>(mq, mo, lse, D, dq, dqkv, seq, H);
+  CK_CUDA(cudaGetLastError());
+  attn_dq_out(dq, dqkv, M, H, st);
+}
+
 }  // namespace chimera::ops
+
+extern "C" CK_API int ck_attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv,
+                                     float* scratch, int B, int seq, int H, int causal, void* st) {
+  using chimera::ops::bf16;
+  return chimera::capi::guarded([&] {
+    chimera::ops::attn_bwd_tc((const bf16*)qkv, (const bf16*)out, (const bf16*)dout, lse, (bf16*)dqkv, scratch, B, seq,
+                              H, causal != 0, (cudaStream_t)st);
+  });
+}
 
 extern "C" CK_API int ck_attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int seq, int H, int causal,
                                      void* st) {

@@ -479,7 +479,7 @@ void Trainer::stage_forward(int rank, int s, Stash& X, const bf16* x, bf16* out_
     ops::layernorm_fwd(x, w + o.ln1_g, w + o.ln1_b, A.h1, A.mean1, A.rstd1, M, h, st);
     gemm::gemm(gemm::kStoreBF16, false, false, M, 3 * h, h, A.h1, h, w + o.w_qkv, h,
                epi(A.qkv, 3 * h, w + o.b_qkv), st);
-    ops::attn_fwd(A.qkv, A.a, A.lse, I.B, m.seq, H, m.causal, st);
+    ops::attn_fwd_tc(A.qkv, A.a, A.lse, I.B, m.seq, H, m.causal, st);
     gemm::gemm(gemm::kBiasResid, false, false, M, h, h, A.a, h, w + o.w_o, h,
                epi(A.x2, h, w + o.b_o, x, h), st);
     ops::layernorm_fwd(A.x2, w + o.ln2_g, w + o.ln2_b, A.h2, A.mean2, A.rstd2, M, h, st);

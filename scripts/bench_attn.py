@@ -10,7 +10,8 @@ for (B, s, H, causal) in [(4, 1024, 16, True), (8, 128, 16, False), (1, 632, 20,
     fl = 4 * s * s * 64 * B * H * (0.5 if causal else 1.0)
     for name, fn in [("fwd_mma", lambda: ck.attn_fwd(qkv, out, lse, B, s, H, causal)),
                      ("fwd_tc", lambda: ck.attn_fwd_tc(qkv, out, lse, B, s, H, causal)),
-                     ("bwd_mma", lambda: ck.attn_bwd(qkv, out, dout, lse, dqkv, B, s, H, causal))]:
+                     ("bwd_mma", lambda: ck.attn_bwd(qkv, out, dout, lse, dqkv, B, s, H, causal)),
+                     ("bwd_tc", lambda: ck.attn_bwd(qkv, out, dout, lse, dqkv, B, s, H, causal, impl="tcgen05"))]:
         for _ in range(3): fn()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record()

@@ -106,7 +106,7 @@ def test_attention(B, seq, H, causal, impl):
     assert rel(lse, ref_lse.reshape(-1)) < 1e-4
     dout = torch.randn_like(out)
     dqkv = torch.empty_like(qkv)
-    ck.attn_bwd(qkv, out, dout, lse, dqkv, B, seq, H, causal)
+    ck.attn_bwd(qkv, out, dout, lse, dqkv, B, seq, H, causal, impl=impl)
     dq, dk, dv = torch.autograd.grad(ref, (q, k, v), dout.float())
     got = dqkv.float().view(B, seq, 3, H, d).permute(2, 0, 3, 1, 4)
     assert rel(got[0], dq) < 2e-2
