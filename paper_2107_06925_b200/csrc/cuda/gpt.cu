@@ -560,7 +560,7 @@ void Trainer::backward_task(int rank, int p, int mb, int s) {
     ops::bias_grad(sc.dx2, gw + o.b_o, M, h, st);
     gemm::gemm(gemm::kAccF32, true, true, h, h, M, sc.dx2, h, A.a, h, epi(gw + o.w_o, h), st);
     gemm::gemm(gemm::kStoreBF16, false, true, M, h, h, sc.dx2, h, w + o.w_o, h, epi(sc.da, h), st);
-    ops::attn_bwd(A.qkv, A.a, sc.da, A.lse, sc.dqkv, sc.attn, I.B, m.seq, H, m.causal, st);
+    ops::attn_bwd_tc(A.qkv, A.a, sc.da, A.lse, sc.dqkv, sc.attn, I.B, m.seq, H, m.causal, st);
     ops::bias_grad(sc.dqkv, gw + o.b_qkv, M, 3 * h, st);
     gemm::gemm(gemm::kAccF32, true, true, 3 * h, h, M, sc.dqkv, 3 * h, A.h1, h, epi(gw + o.w_qkv, h), st);
     gemm::gemm(gemm::kStoreBF16, false, true, M, h, 3 * h, sc.dqkv, 3 * h, w + o.w_qkv, h, epi(sc.dh, h), st);
