@@ -31,13 +31,19 @@ namespace {
 
 constexpr int BM = 128, BK = 64;
 
+// Hardware tanh (one MUFU op, ~2^-11 relative error: below the bf16 output rounding).
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float gelu_tanh(float u) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  return 0.5f * u * (1.f + tanhf(k0 * (u + k1 * u * u * u)));
+  return 0.5f * u * (1.f + tanh_fast(k0 * (u + k1 * u * u * u)));
 }
 __device__ __forceinline__ float gelu_tanh_grad(float u) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  const float t = tanhf(k0 * (u + k1 * u * u * u));
+  const float t = tanh_fast(k0 * (u + k1 * u * u * u));
   return 0.5f * (1.f + t) + 0.5f * u * (1.f - t * t) * k0 * (1.f + 3.f * k1 * u * u);
 }
 
@@ -45,7 +51,7 @@ __device__ __forceinline__ float gelu_tanh_grad(float u) {
 // row0+i in registers (the tcgen05.ld 32x32b layout); every global access goes through
 // a per-warp shared-memory tile so that 4 consecutive lanes cover one 64-byte (bf16) or
 // 128-byte (fp32) row segment -- fully coalesced, instead of 32 row-strided streams.
-constexpr int kEpiWarpBytes = 8192;  // per epilogue warp: staging tile (+ aux tile)
+constexpr int kEpiWarpBytes = 5120;  // per epilogue warp: staging tile (+ aux tile)
 constexpr int kStrideH = 80;         // bytes per staged bf16 row (64 + 16 pad: conflict-free)
 constexpr int kStrideF = 144;        // bytes per staged fp32 row (128 + 16 pad)
 
@@ -309,13 +315,14 @@ inline int split_k(int epi, int tiles, int slots, int K) {
 // the 256 rows of B per K-block, so per-SM operand traffic per MMA drops by 1/3 versus
 // the 128 x 256 single-CTA tile.  The leader (even) CTA issues the MMAs and owns the
 // smem-full and TMEM-empty barriers; commits are multicast to both CTAs.
-constexpr int kPairStages = 6;
+constexpr int kPairStages = 5;
+constexpr int kPairEpiWarps = 8;  // two per TMEM lane quarter, each owning 128 of the 256 columns
 constexpr int kPairHalfBytes = 128 * BK * 2;            // one operand half per CTA
 constexpr int kPairStageBytes = 2 * kPairHalfBytes;     // A half + B half
-constexpr int kPairSmem = kPairStages * kPairStageBytes + 1024 + 256 + 4 * kEpiWarpBytes;
+constexpr int kPairSmem = kPairStages * kPairStageBytes + 1024 + 256 + kPairEpiWarps * kEpiWarpBytes;
 
 template <bool A_MN, bool B_MN, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiWarps, 1)
     k_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const EpiArgs ep,
             int M, int N, int K, int ksplit) {
   extern __shared__ uint8_t smem_raw[];
@@ -337,7 +344,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     ptx::tma_prefetch(&ta);
     ptx::tma_prefetch(&tb);
     for (int s = 0; s < kPairStages; ++s) ptx::mbar_init(&full[s], 1), ptx::mbar_init(&empty[s], 1);
-    for (int a = 0; a < 2; ++a) ptx::mbar_init(&tfull[a], 1), ptx::mbar_init(&tempty[a], 8);
+    for (int a = 0; a < 2; ++a) ptx::mbar_init(&tfull[a], 1), ptx::mbar_init(&tempty[a], 2 * kPairEpiWarps);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc2(tmem_slot, 512);
@@ -408,7 +415,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
-    const int q = warp - 4;
+    const int q = warp & 3, half = (warp - 4) >> 2;  // lane quarter, column half
     int it = 0;
     for (int tile = pair; tile < tiles; tile += npairs, ++it) {
       const int acc = it & 1;
@@ -417,9 +424,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       ptx::tc_fence_after();
       const int row0 = mb * 256 + int(cta) * 128 + q * 32;
       const uint32_t t0 = tmem_base + (uint32_t(q * 32) << 16) + acc * 256;
-      uint8_t* stg = smem + kPairStages * kPairStageBytes + 256 + q * kEpiWarpBytes;
+      uint8_t* stg = smem + kPairStages * kPairStageBytes + 256 + (warp - 4) * kEpiWarpBytes;
 #pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
+      for (int c = half * 4; c < half * 4 + 4; ++c) {
         uint32_t r[32];
         ptx::tmem_ld32(t0 + c * 32, r);
         ptx::tmem_ld_wait();
@@ -456,7 +463,7 @@ void launch_pair(int M, int N, int K, const __nv_bfloat16* A, long long lda, con
   const int ks = split_k(EPI, base, cuda::kNumSMs / 2, K);
   const int tiles = base * ks;
   const int pairs = tiles < cuda::kNumSMs / 2 ? tiles : cuda::kNumSMs / 2;
-  kern<<<2 * pairs, 256, kPairSmem, st>>>(ta, tb, ep, M, N, K, ks);
+  kern<<<2 * pairs, 128 + 32 * kPairEpiWarps, kPairSmem, st>>>(ta, tb, ep, M, N, K, ks);
   CK_CUDA(cudaGetLastError());
 }
 
