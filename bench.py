@@ -28,8 +28,22 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "GPT-2 seqs/sec at D=8 on 8×B200; bubble ratio vs (D-2)/(2N+D-2)"
-SHAPE_NAME = "gpt2-medium"
-CFG = dict(scheme="chimera", D=4, W=2, N=4, B=4, f=1, scaling="direct")
+# BASELINE.json configs (the default, configs[1], is the one the driver measures).
+CONFIGS = {
+    "gpt2-medium": ("gpt2-medium", dict(scheme="chimera", D=4, W=2, N=4, B=4, f=1, scaling="direct"),
+                    "GPT-2 medium Chimera D=4 N=4 W=2 B=4 (BASELINE configs[1])"),
+    "bert48": ("bert48", dict(scheme="chimera", D=8, W=1, N=8, B=8, f=1, scaling="direct"),
+               "Bert-48 shape (bidirectional, dense MLM head) Chimera D=8 N=8 B=8 (BASELINE configs[2])"),
+    "gpt2-1.3b": ("gpt2-1.3b", dict(scheme="chimera", D=8, W=1, N=32, B=1, f=1, scaling="forward-doubling"),
+                  "GPT-2 1.3B s=632 Chimera D=8 N=32 forward-doubling + recompute (BASELINE configs[3])"),
+    "q4": ("gpt2-32l", dict(scheme="chimera", D=8, W=1, N=16, B=1, f=2, scaling="direct"),
+           "GPT-2 32-layer s=632 Chimera f=2 (4 pipelines) D=8 N=16 (BASELINE configs[4])"),
+    "q4-gpipe": ("gpt2-32l", dict(scheme="gpipe", D=8, W=1, N=16, B=1, f=1, scaling="direct"),
+                 "GPT-2 32-layer s=632 GPipe D=8 N=16 (configs[4] baseline)"),
+    "q4-dapple": ("gpt2-32l", dict(scheme="dapple", D=8, W=1, N=16, B=1, f=1, scaling="direct"),
+                  "GPT-2 32-layer s=632 1F1B/DAPPLE D=8 N=16 (configs[4] baseline)"),
+}
+SHAPE_NAME, CFG, WORKLOAD = CONFIGS["gpt2-medium"]
 
 
 def peaks():
@@ -175,8 +189,8 @@ def run_reference(args, shape):
     line = {"metric": METRIC, "value": v, "unit": "seqs/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "GPT-2 medium Chimera D=4 N=4 W=2 B=4 (BASELINE configs[1])",
-                       "model": SHAPE_NAME, "global_batch": 32, "seq_len": shape.seq},
+            "config": {"workload": WORKLOAD, "model": SHAPE_NAME, "global_batch": CFG["B"] * CFG["N"] * CFG["W"],
+                       "seq_len": shape.seq},
             "cpu_baseline": {"value": v, "unit": "seqs/s", "cores": os.cpu_count(), "kind": "port",
                              "sample": s["sample"]},
             "e2e": {"value": v, "unit": "seqs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -190,8 +204,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="chimera")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default="gpt2-medium", choices=sorted(CONFIGS))
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    global SHAPE_NAME, CFG, WORKLOAD
+    SHAPE_NAME, CFG, WORKLOAD = CONFIGS[args.config]
 
     from paper_2107_06925_b200.gpt import PRESETS
     shape = PRESETS[SHAPE_NAME]
@@ -313,9 +330,11 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic tokens (uniform, next-token labels), random-init weights N(0,0.02)",
-            "config": {"workload": "GPT-2 medium Chimera D=4 N=4 W=2 B=4 (BASELINE configs[1])",
+            "config": {"workload": WORKLOAD,
                        "model": SHAPE_NAME, "global_batch": n_seq, "seq_len": shape.seq,
-                       "parallelism": f"chimera D={cfg.D} W={cfg.W} f=1: {n_logical} logical ranks on {world} GPU(s)",
+                       "parallelism": f"{cfg.scheme} D={cfg.D} W={cfg.W} f={cfg.f} {cfg.scaling}"
+                                      f"{' +recompute' if cfg.scaling == 'forward-doubling' else ''}: "
+                                      f"{n_logical} logical ranks on {world} GPU(s)",
                        "l2": "working set per step >> L2 (weights, grads, stashes ~40 GB)"},
             "e2e": {"value": round(n_seq / (e2e_ms * 1e-3), 2), "unit": "seqs/s",
                     "h2d_bytes_per_step": int(tok.nbytes + lab.nbytes), "d2h_bytes_per_step": 4},
