@@ -205,6 +205,8 @@ def main():
     ap.add_argument("--impl", default="chimera")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--config", default="gpt2-medium", choices=sorted(CONFIGS))
+    ap.add_argument("--partition", default="balanced", choices=["balanced", "even"],
+                    help="layers per stage: balanced per pipeline worker (LM-head stage shorter) or even")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     global SHAPE_NAME, CFG, WORKLOAD
@@ -212,6 +214,11 @@ def main():
 
     from paper_2107_06925_b200.gpt import PRESETS
     shape = PRESETS[SHAPE_NAME]
+    if args.impl != "reference" and args.partition == "balanced":
+        import dataclasses
+        from paper_2107_06925_b200 import pipesim as P
+        from paper_2107_06925_b200.gpt import balanced_partition
+        shape = dataclasses.replace(shape, stage_layers=balanced_partition(shape, P.PipelineConfig(**CFG)))
     if args.impl == "reference":
         return run_reference(args, shape)
 
@@ -332,6 +339,7 @@ def main():
             "data": "synthetic tokens (uniform, next-token labels), random-init weights N(0,0.02)",
             "config": {"workload": WORKLOAD,
                        "model": SHAPE_NAME, "global_batch": n_seq, "seq_len": shape.seq,
+                       "stage_layers": list(shape.stage_layers) or None,
                        "parallelism": f"{cfg.scheme} D={cfg.D} W={cfg.W} f={cfg.f} {cfg.scaling}"
                                       f"{' +recompute' if cfg.scaling == 'forward-doubling' else ''}: "
                                       f"{n_logical} logical ranks on {world} GPU(s)",

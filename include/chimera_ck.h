@@ -125,6 +125,8 @@ CK_API int ck_attn_bwd_tc(const void* qkv, const void* out, const void* dout, co
 /* Transformer shape (head dim 64; vocab padded to a multiple of 8, e.g. 50304). */
 typedef struct ck_gpt_model {
   int n_layer, hidden, heads, ffn, seq, vocab, vocab_padded, causal;
+  const int* stage_layers;  /* optional layers per stage (D entries summing to n_layer) */
+  int n_stage_layers;       /* 0 = even split */
 } ck_gpt_model;
 typedef struct ck_gpt ck_gpt;
 /* A trainer for logical ranks [first_rank, first_rank + n_ranks) of the schedule

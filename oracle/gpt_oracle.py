@@ -39,6 +39,7 @@ class Shape:
     vocab: int = 1024
     vocab_padded: int = 1024
     causal: bool = True
+    stage_layers: tuple = ()
 
 
 def stage_layout(m: Shape, D: int, s: int):
@@ -51,12 +52,13 @@ def stage_layout(m: Shape, D: int, s: int):
         out.append((name, total, rows, cols, init))
         total += (rows * cols + 63) // 64 * 64
 
-    per = m.n_layer // D
+    parts = list(m.stage_layers) or [m.n_layer // D] * D
+    per, first = parts[s], sum(parts[:s])
     if s == 0:
         add("wte", m.vocab_padded, h, "normal")
         add("wpe", m.seq, h, "normal")
     for l in range(per):
-        p = f"h{s * per + l}."
+        p = f"h{first + l}."
         add(p + "ln1.g", 1, h, "one"); add(p + "ln1.b", 1, h, "zero")
         add(p + "attn.w_qkv", 3 * h, h, "normal"); add(p + "attn.b_qkv", 1, 3 * h, "zero")
         add(p + "attn.w_o", h, h, "normal"); add(p + "attn.b_o", 1, h, "zero")
@@ -139,8 +141,8 @@ class StageModel:
     def __init__(self, m: Shape, D: int, s: int):
         self.m, self.D, self.s = m, D, s
         self.layout, self.total = stage_layout(m, D, s)
-        self.per = m.n_layer // D
-        self.first = s * self.per
+        parts = list(m.stage_layers) or [m.n_layer // D] * D
+        self.per, self.first = parts[s], sum(parts[:s])
 
     def forward(self, P, x_or_tok, labels, B, loss_scale):
         m = self.m

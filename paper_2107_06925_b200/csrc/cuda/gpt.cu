@@ -203,7 +203,14 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
   I.first = first_rank;
   I.nlocal = n_ranks;
   I.M = I.B * shape.seq;
-  if (shape.n_layer % I.D) throw pipesim::InvalidConfigError("n_layer must be divisible by D");
+  if (shape.stage_layers.empty()) {
+    if (shape.n_layer % I.D) throw pipesim::InvalidConfigError("n_layer must be divisible by D");
+  } else {
+    int sum = 0;
+    for (int v : shape.stage_layers) sum += v, v < 1 ? throw pipesim::InvalidConfigError("empty stage") : 0;
+    if (int(shape.stage_layers.size()) != I.D || sum != shape.n_layer)
+      throw pipesim::InvalidConfigError("stage_layers must have D entries summing to n_layer");
+  }
   if (shape.hidden != shape.heads * 64) throw pipesim::InvalidConfigError("head dim must be 64");
   if (shape.hidden % 256) throw pipesim::InvalidConfigError("hidden must be a multiple of 256");
   if (shape.vocab_padded % 8 || shape.vocab_padded < shape.vocab)
@@ -221,7 +228,9 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
   I.worker_of = I.lp->worker_of;
   cuda::require_sm100();
 
-  const int h = shape.hidden, f = shape.ffn, Ls = shape.n_layer / I.D, M = I.M;
+  const int h = shape.hidden, f = shape.ffn, M = I.M;
+  int Lmax = 0;
+  for (int st = 0; st < I.D; ++st) Lmax = std::max(Lmax, shape.layers_of(I.D, st));
   const int H = shape.heads;
   // ---- stage weights and per-copy state
   for (int rank = first_rank; rank < first_rank + n_ranks; ++rank) {
@@ -269,7 +278,7 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
     }
   }
   I.recompute = c.recompute;
-  auto alloc_full = [&](Stash& st, bool embed, bool head) {
+  auto alloc_full = [&](Stash& st, bool embed, bool head, int Ls) {
       if (embed) st.x0 = I.arena.alloc<bf16>((size_t)M * h);
       for (int l = 0; l < Ls; ++l) {
         LayerStash ls;
@@ -299,7 +308,7 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
   if (I.recompute) {  // one full workspace per rank; xo of the last layer is a sink
     for (int k = 0; k < n_ranks; ++k) {
       Stash st;
-      alloc_full(st, false, true);
+      alloc_full(st, false, true, Lmax);
       st.layers.back().xo = I.arena.alloc<bf16>((size_t)M * h);
       I.rscratch.push_back(std::move(st));
     }
@@ -314,7 +323,7 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
       if (I.recompute) {
         if (L.has_embed) st.x0 = I.arena.alloc<bf16>((size_t)M * h);  // the only stashed tensor
       } else {
-        alloc_full(st, L.has_embed, L.has_head);
+        alloc_full(st, L.has_embed, L.has_head, L.n_layers);
       }
       cp.slots.push_back(std::move(st));
     }
@@ -995,6 +1004,7 @@ CK_API int ck_gpt_create(const ck_gpt_model* mdl, const char* schedule_json, flo
     chimera::gpt::ModelShape m;
     m.n_layer = mdl->n_layer, m.hidden = mdl->hidden, m.heads = mdl->heads, m.ffn = mdl->ffn;
     m.seq = mdl->seq, m.vocab = mdl->vocab, m.vocab_padded = mdl->vocab_padded, m.causal = mdl->causal != 0;
+    if (mdl->n_stage_layers > 0) m.stage_layers.assign(mdl->stage_layers, mdl->stage_layers + mdl->n_stage_layers);
     const auto s = pipesim::schedule_from_json(schedule_json);
     const auto v = pipesim::validate_config_shape(s.config);
     if (!v.empty()) throw pipesim::InvalidConfigError(v.front());

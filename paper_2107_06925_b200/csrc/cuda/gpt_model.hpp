@@ -16,6 +16,14 @@ namespace chimera::gpt {
 struct ModelShape {
   int n_layer = 8, hidden = 256, heads = 4, ffn = 1024, seq = 128, vocab = 1024, vocab_padded = 1024;
   bool causal = true;
+  std::vector<int> stage_layers;  // layers per stage (empty = n_layer / D each)
+
+  int layers_of(int D, int s) const { return stage_layers.empty() ? n_layer / D : stage_layers[s]; }
+  int first_layer_of(int D, int s) const {
+    int f = 0;
+    for (int k = 0; k < s; ++k) f += layers_of(D, k);
+    return f;
+  }
 };
 
 enum class Init { Zero, One, Normal };
@@ -44,8 +52,8 @@ struct StageLayout {
 inline StageLayout make_stage_layout(const ModelShape& m, int D, int s) {
   StageLayout L;
   L.stage = s;
-  const int per = m.n_layer / D;
-  L.first_layer = s * per;
+  const int per = m.layers_of(D, s);
+  L.first_layer = m.first_layer_of(D, s);
   L.n_layers = per;
   L.has_embed = s == 0;
   L.has_head = s == D - 1;

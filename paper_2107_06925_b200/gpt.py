@@ -23,7 +23,7 @@ from .pipesim import PipelineConfig, Schedule, generate_json
 
 class ck_gpt_model(C.Structure):
     _fields_ = [(n, C.c_int) for n in ("n_layer", "hidden", "heads", "ffn", "seq", "vocab", "vocab_padded",
-                                        "causal")]
+                                        "causal")] + [("stage_layers", C.POINTER(C.c_int)), ("n_stage_layers", C.c_int)]
 
 
 _vp = C.c_void_p
@@ -63,6 +63,7 @@ class GPTShape:
     vocab: int
     vocab_padded: int
     causal: bool = True
+    stage_layers: tuple = ()  # layers per pipeline stage; () = even split
 
     def flops_per_seq(self) -> float:
         """Algorithmic fwd+bwd FLOPs per sequence:
@@ -83,6 +84,32 @@ PRESETS = {
     "gpt2-1.3b": GPTShape(64, 1280, 20, 5120, 632, 50257, 50304, True),
     "gpt2-32l": GPTShape(32, 1280, 20, 5120, 632, 50257, 50304, True),
 }
+
+
+def balanced_partition(shape: GPTShape, config) -> tuple:
+    """Layers per stage minimising the busiest pipeline worker's load (then the busiest
+    stage), counting a layer as 1 and the LM head as its FLOP ratio
+    V / (12 h + 2 s*causal_fraction) to a layer.  Chimera worker w holds stage w of the
+    down pipelines and the mirrored stage of the up ones, so the stage carrying the
+    head should be shorter than the middle ones (e.g. GPT-2 medium D=4 -> (5, 7, 7, 5))."""
+    import itertools
+    D, L = config.D, shape.n_layer
+    attn = shape.seq * (0.5 if shape.causal else 1.0)
+    head = shape.vocab / (12.0 * shape.hidden + 2.0 * attn)
+    sched = json.loads(generate_json(config, None, -1))
+    holds = [sorted({t["stage"] for t in wl}) for wl in sched["per_worker"]]
+    best, best_key = None, None
+    lo, hi = max(1, L // D - 3), L // D + 3
+    for parts in itertools.product(range(lo, hi + 1), repeat=D - 1):
+        last = L - sum(parts)
+        if last < 1:
+            continue
+        p = tuple(parts) + (last,)
+        cost = [p[s] + (head if s == D - 1 else 0.0) for s in range(D)]
+        key = (round(max(sum(cost[s] for s in h) for h in holds), 6), round(max(cost), 6), p)
+        if best_key is None or key < best_key:
+            best, best_key = p, key
+    return best
 
 
 def init_stage(layout_stage: dict, seed: int) -> np.ndarray:
@@ -124,8 +151,9 @@ class Trainer:
         self.shape = shape
         if n_ranks is None:
             n_ranks = cfg["W"] * cfg["D"] - first_rank
+        self._parts = (C.c_int * max(1, len(shape.stage_layers)))(*shape.stage_layers)
         mdl = ck_gpt_model(shape.n_layer, shape.hidden, shape.heads, shape.ffn, shape.seq, shape.vocab,
-                           shape.vocab_padded, int(shape.causal))
+                           shape.vocab_padded, int(shape.causal), self._parts, len(shape.stage_layers))
         h = C.c_void_p()
         check(lib().ck_gpt_create(C.byref(mdl), text.encode(), lr, first_rank, n_ranks, C.byref(h)))
         self._h = h

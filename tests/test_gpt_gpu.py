@@ -112,3 +112,11 @@ def test_forward_doubling_with_recompute():
 def test_recompute_flag_on_direct_schedule():
     cfg = P.PipelineConfig("chimera", 4, 2, 4, 2, 1, "direct", True)
     _check_iteration(PRESETS["tiny"], cfg)
+
+
+def test_uneven_stage_partition():
+    import dataclasses
+    shape = dataclasses.replace(PRESETS["tiny"], stage_layers=(3, 2, 2, 1))
+    _check_iteration(shape, P.PipelineConfig("chimera", 4, 1, 4, 2, 1))
+    rc = dataclasses.replace(PRESETS["tiny"], stage_layers=(1, 3, 3, 1))
+    _check_iteration(rc, P.PipelineConfig("chimera", 4, 1, 8, 1, 1, "forward-doubling"))

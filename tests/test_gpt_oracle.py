@@ -71,3 +71,12 @@ def test_finite_differences():
                 fd = (lp - lm) / (2 * eps)
                 worst = max(worst, abs(fd - g[s][idx]) / max(1.0, abs(fd), abs(g[s][idx])))
     assert worst <= 1e-5
+
+
+def test_balanced_partition_prefers_short_head_stage():
+    from paper_2107_06925_b200.gpt import PRESETS, balanced_partition
+    part = balanced_partition(PRESETS["gpt2-medium"], P.PipelineConfig("chimera", 4, 2, 4, 4, 1))
+    assert sum(part) == 24 and part[-1] < part[1]
+    m = O.Shape(n_layer=4, hidden=128, heads=2, ffn=256, seq=16, vocab=50, vocab_padded=64, causal=True,
+                stage_layers=(2, 1, 1, 0 + 0) if False else (1, 1, 1, 1))
+    assert O.stage_layout(m, 4, 3)[0][-1][0] == "lm_head"
