@@ -30,7 +30,7 @@
 #include <string>
 #include <vector>
 
-#include <nccl.h>
+#include "nccl_rt.hpp"
 
 #include "chimera_ck.h"
 #include "common.cuh"
@@ -403,8 +403,8 @@ Trainer::~Trainer() {
   if (I.graph) cudaGraphDestroy(I.graph);
   for (auto& kv : I.msgs)
     if (kv.second.ev) cudaEventDestroy(kv.second.ev);
-  for (auto& kv : I.stage_comm) ncclCommDestroy(kv.second);
-  if (I.world_comm) ncclCommDestroy(I.world_comm);
+  for (auto& kv : I.stage_comm) Nccl::get().CommDestroy(kv.second);
+  if (I.world_comm) Nccl::get().CommDestroy(I.world_comm);
   for (void* p : I.peer_inbox)
     if (p) cudaIpcCloseMemHandle(p);
   for (void* p : I.peer_outbox)
@@ -663,7 +663,7 @@ void sync_stage(Trainer::Impl& I, int s) {
       CK_CUDA(cudaMemsetAsync(S.grads[c], 0, S.L.total * sizeof(float), cs));
     I.launches_per_step += 1;
   }
-  if (ncclAllReduce(g0, g0, S.L.total, ncclFloat, ncclSum, it->second, cs) != ncclSuccess)
+  if (Nccl::get().AllReduce(g0, g0, S.L.total, ncclFloat, ncclSum, it->second, cs) != ncclSuccess)
     throw capi::InternalError("ncclAllReduce failed");
   ops::sgd_update(S.w32, S.w16, &g0, 1, S.L.total, I.lr, cs);
   I.launches_per_step += 1;
@@ -928,14 +928,14 @@ void Trainer::connect(const std::string& all_blobs, const std::string& nccl_id) 
   // NCCL: world communicator, then one split per stage whose holders span >1 process
   ncclUniqueId id;
   std::memcpy(&id, nccl_id.data(), sizeof id);
-  if (ncclCommInitRank(&I.world_comm, I.procs, id, I.proc) != ncclSuccess)
+  if (Nccl::get().CommInitRank(&I.world_comm, I.procs, id, I.proc) != ncclSuccess)
     throw capi::InternalError("ncclCommInitRank failed");
   for (int s = 0; s < I.D; ++s) {
     const std::vector<int> holders = I.lp->stage_holders(s);
     if (holders.size() < 2) continue;
     const bool mine = std::find(holders.begin(), holders.end(), I.proc) != holders.end();
     ncclComm_t c = nullptr;
-    if (ncclCommSplit(I.world_comm, mine ? s : NCCL_SPLIT_NOCOLOR, I.proc, &c, nullptr) != ncclSuccess)
+    if (Nccl::get().CommSplit(I.world_comm, mine ? s : NCCL_SPLIT_NOCOLOR, I.proc, &c, nullptr) != ncclSuccess)
       throw capi::InternalError("ncclCommSplit failed");
     if (mine) I.stage_comm[s] = c;
   }
@@ -1087,7 +1087,7 @@ CK_API int ck_nccl_unique_id(char* out, int cap) {
   return chimera::capi::guarded([&] {
     ncclUniqueId id;
     if (cap < int(sizeof id)) throw pipesim::InvalidConfigError("buffer too small");
-    if (ncclGetUniqueId(&id) != ncclSuccess) throw chimera::capi::InternalError("ncclGetUniqueId failed");
+    if (chimera::gpt::Nccl::get().GetUniqueId(&id) != ncclSuccess) throw chimera::capi::InternalError("ncclGetUniqueId failed");
     std::memcpy(out, &id, sizeof id);
   });
 }

@@ -41,3 +41,15 @@ def test_status_codes_and_last_error():
         assert e.status == 2 and "even number of stages" in str(e)
     else:
         raise AssertionError("expected InvalidConfigError")
+
+
+def test_library_does_not_pin_nccl_before_torch():
+    # libchimera.so must not drag a second libnccl.so.2 into the process (torch bundles
+    # its own): load the library first, then torch, in a fresh interpreter.
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, '.'); from paper_2107_06925_b200 import _lib; _lib.lib(); "
+            "import torch; print('ok')")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
