@@ -5,11 +5,12 @@
 //   warp 5  TMEM allocator + single-thread MMA issuer:
 //             S  = Q K^T      tcgen05.mma kind::f16 M128 N128 K64  -> TMEM cols [0,128)
 //             O += P V        tcgen05.mma kind::f16 M128 N64  K128 -> TMEM cols [128,192)
-//   warps 0-3  softmax: thread t owns query row t (= TMEM lane t): two passes over the
-//             S row in TMEM (max, then exp2 + sum), P written as bf16 straight into the
-//             128-byte-swizzled K-major smem tile the next MMA reads, running O rescaled
-//             in TMEM (tcgen05.ld/st) when the row max moves; final O / l and the
-//             log-sum-exp go to HBM.
+//   warps 0-3  softmax: thread t owns query row t (= TMEM lane t): the S row is pulled
+//             into registers in one pass, which frees the S columns at once (s_free) so
+//             the MMA warp computes S_{j+1} underneath this tile's exp2s; P is written as
+//             bf16 straight into the 128-byte-swizzled K-major smem tile the PV MMA reads,
+//             running O rescaled in TMEM (tcgen05.ld/st) only when a row max moves; final
+//             O / l and the log-sum-exp go to HBM.
 // The Q/K/V tiles come straight out of the packed [tokens, 3*H*64] QKV GEMM output via
 // one 2-D TMA map (no head split), so the kernel reads exactly Q, K, V once per tile.
 // ~112 KB smem and 256 TMEM columns per CTA: two CTAs per SM overlap one CTA's softmax
@@ -54,12 +55,15 @@ __global__ void __launch_bounds__(192, 2)
   if ((ptx::smem_u32(smem) & 1023) != 0) __trap();  // swizzle atoms need 1 KB alignment
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kSmemBar);
   uint64_t *q_full = bar, *kv_full = bar + 1, *kv_empty = bar + 3, *s_full = bar + 5, *p_full = bar + 6,
-           *o_done = bar + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
+           *o_done = bar + 7, *s_free = bar + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // causal: the longest query tiles (most key tiles) are scheduled first
-  const int qb = CAUSAL ? gridDim.x - 1 - blockIdx.x : blockIdx.x, bh = blockIdx.y, b = bh / H, hd = bh % H;
+  // 1-D grid, tile-major: with causal masking the longest query tiles (most key tiles) of
+  // every head are dispatched first, so the short ones fill the tail of the last wave
+  const int BH = gridDim.x / ((seq + kQ - 1) / kQ);
+  const int tile = blockIdx.x / BH, bh = blockIdx.x % BH, b = bh / H, hd = bh % H;
+  const int qb = CAUSAL ? (seq + kQ - 1) / kQ - 1 - tile : tile;
   const int q0 = qb * kQ, row_base = b * seq;
   const int nkv = (seq + kKV - 1) / kKV;
   const int nkb = CAUSAL ? min(nkv, qb + 1) : nkv;
@@ -71,6 +75,7 @@ __global__ void __launch_bounds__(192, 2)
     ptx::mbar_init(s_full, 1);
     ptx::mbar_init(p_full, 128);
     ptx::mbar_init(o_done, 1);
+    ptx::mbar_init(s_free, 128);
     ptx::fence_barrier_init();
   }
   if (warp == 5) ptx::tmem_alloc(tmem_slot, 256);
@@ -111,7 +116,12 @@ __global__ void __launch_bounds__(192, 2)
       ptx::mbar_wait(q_full, 0);
       issue_s(0);
       for (int j = 0; j < nkb; ++j) {
-        ptx::mbar_wait_sleep(p_full, j & 1);  // P_j in smem, S free, O rescaled
+        if (j + 1 < nkb) {  // S_j is in the softmax registers: compute S_{j+1} under its exp2s
+          ptx::mbar_wait_sleep(s_free, j & 1);
+          ptx::tc_fence_after();
+          issue_s(j + 1);
+        }
+        ptx::mbar_wait_sleep(p_full, j & 1);  // P_j in smem, O rescaled
         ptx::tc_fence_after();
         const uint32_t sv = ptx::smem_u32(smem + kSmemV + (j & 1) * kTileBytes);
 #pragma unroll
@@ -120,7 +130,6 @@ __global__ void __launch_bounds__(192, 2)
                         ptx::smem_desc_sw128(sv + k * 2048, kTileBytes, 1024), id_o, (j > 0 || k > 0) ? 1u : 0u);
         ptx::umma_commit(&kv_empty[j & 1]);
         ptx::umma_commit(o_done);
-        if (j + 1 < nkb) issue_s(j + 1);
       }
     }
   } else {
@@ -140,9 +149,13 @@ __global__ void __launch_bounds__(192, 2)
 #pragma unroll
       for (int c = 0; c < 4; ++c) ptx::tmem_ld32(trow + c * 32, r[c]);
       ptx::tmem_ld_wait();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(s_free);
       // masking only on the diagonal (causal) / sequence-tail tile: warp-uniform branch
       const bool edge = (CAUSAL && key0 + kKV - 1 > q0) || key0 + kKV > seq;
-      float mx = -INFINITY;
+      float mxp[8];  // 8 independent max chains
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mxp[u] = -INFINITY;
 #pragma unroll
       for (int c = 0; c < 4; ++c)
 #pragma unroll
@@ -153,8 +166,10 @@ __global__ void __launch_bounds__(192, 2)
             if (key >= seq || (CAUSAL && key > q)) v = -INFINITY;
           }
           r[c][i] = __float_as_uint(v);
-          mx = fmaxf(mx, v);
+          mxp[i & 7] = fmaxf(mxp[i & 7], v);
         }
+      const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                             fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
       const float mn = fmaxf(m, mx);
       const float safe = mn == -INFINITY ? 0.f : mn;
       const float alpha = ex2_approx(m - safe);
@@ -177,6 +192,7 @@ __global__ void __launch_bounds__(192, 2)
         }
       }
       // P = exp2(s - m) as bf16 into the swizzled K-major tile
+      float ls[4] = {0.f, 0.f, 0.f, 0.f};  // independent sum chains
 #pragma unroll
       for (int c = 0; c < 4; ++c)
 #pragma unroll
@@ -187,7 +203,7 @@ __global__ void __launch_bounds__(192, 2)
             const int i = g * 8 + e * 2;
             const float p0 = ex2_approx(__uint_as_float(r[c][i]) - safe);
             const float p1 = ex2_approx(__uint_as_float(r[c][i + 1]) - safe);
-            l += p0 + p1;
+            ls[e] += p0 + p1;
             __nv_bfloat162 hb = __floats2bfloat162_rn(p0, p1);
             pk[e] = *reinterpret_cast<uint32_t*>(&hb);
           }
@@ -195,6 +211,7 @@ __global__ void __launch_bounds__(192, 2)
           uint8_t* dst = sp + (k8 >> 3) * kTileBytes + t * 128 + (((k8 & 7) ^ (t & 7)) << 4);
           *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
+      l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
       ptx::fence_proxy_async();  // P (generic stores) -> visible to the tensor core
       ptx::tc_fence_before();
       ptx::mbar_arrive(p_full);
@@ -267,7 +284,10 @@ __global__ void __launch_bounds__(192, 1)
   float* sLD = reinterpret_cast<float*>(smem + kB_LD);  // [buf][0=lse2,1=D][128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kb = blockIdx.x, bh = blockIdx.y, b = bh / H, hd = bh % H;
+  // 1-D grid, tile-major: key tile 0 sees every query tile under causal masking, so the
+  // heavy CTAs of all heads go first
+  const int BH = gridDim.x / ((seq + kKV - 1) / kKV);
+  const int kb = blockIdx.x / BH, bh = blockIdx.x % BH, b = bh / H, hd = bh % H;
   const int k0 = kb * kKV, row_base = b * seq;
   const int nq = (seq + kQ - 1) / kQ;
   const int j0 = CAUSAL ? kb : 0;  // first query tile that can see these keys
@@ -464,7 +484,7 @@ __global__ void __launch_bounds__(192, 1)
 void attn_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int seq, int H, bool causal, cudaStream_t st) {
   const long long ld = 3LL * H * kD;
   const CUtensorMap m = cuda::make_map_2d_bf16(qkv, ld, (long long)B * seq, ld, 64, 128);
-  const dim3 grid((seq + kQ - 1) / kQ, B * H);
+  const dim3 grid((seq + kQ - 1) / kQ * B * H);
   static bool attr = false;
   if (!attr) {
     CK_CUDA(cudaFuncSetAttribute(k_attn_fwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
@@ -493,7 +513,7 @@ void attn_bwd_tc(const bf16* qkv, const bf16* out, const bf16* dout, const float
     CK_CUDA(cudaFuncSetAttribute(k_attn_bwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem));
     attr = true;
   }
-  const dim3 grid((seq + kKV - 1) / kKV, B * H);
+  const dim3 grid((seq + kKV - 1) / kKV * B * H);
   if (causal) k_attn_bwd_tc<true><<<grid, 192, kBwdSmem, st>>>(mq, mo, lse, D, dq, dqkv, seq, H);
   else k_attn_bwd_tc<false><<<grid, 192, kBwdSmem, st>>>(mq, mo, lse, D, dq, dqkv, seq, H);
   CK_CUDA(cudaGetLastError());
