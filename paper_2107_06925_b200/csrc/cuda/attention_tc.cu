@@ -25,6 +25,33 @@
 
 namespace chimera::ops {
 
+// Per-phase clock64() stamps of CTA 0 (scripts/attn_trace.cu builds with CK_ATTN_TRACE).
+#ifdef CK_ATTN_TRACE
+__device__ long long g_attn_trace[32][16];
+__device__ long long g_attn_cta[4096][3];  // smid, globaltimer at entry / exit
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int smid() {
+  int v;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(v));
+  return v;
+}
+#define ATTN_CTA(slot) \
+  if (threadIdx.x == 0 && blockIdx.x < 4096) g_attn_cta[blockIdx.x][slot] = slot == 0 ? smid() : gtimer()
+#define ATTN_TRACE(cond, j, ev)                                                  \
+  do {                                                                           \
+    if ((cond) && blockIdx.x == 0 && (j) < 32) g_attn_trace[j][ev] = clock64(); \
+  } while (0)
+#else
+#define ATTN_TRACE(cond, j, ev) \
+  do {                          \
+  } while (0)
+#define ATTN_CTA(slot)
+#endif
+
 namespace {
 
 using ptx::ex2_approx;
@@ -34,6 +61,12 @@ constexpr int kSmemQ = 0, kSmemK = kTileBytes, kSmemV = 3 * kTileBytes, kSmemP =
 constexpr int kSmemBar = 7 * kTileBytes;  // after P (2 tiles)
 constexpr int kSmemTotal = kSmemBar + 256;
 constexpr float kLog2e = 1.4426950408889634f;
+// Share of the softmax exp2s computed by ptx::ex2_poly2 on the FMA pipes: every
+// kPolyEvery-th pair (0 = all on MUFU; measured neutral at 2-8 for head dim 64).
+#ifndef CK_ATTN_POLY_EVERY
+#define CK_ATTN_POLY_EVERY 0
+#endif
+constexpr int kPolyEvery = CK_ATTN_POLY_EVERY;
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
@@ -53,6 +86,8 @@ __global__ void __launch_bounds__(192, 2)
                   int seq, int H) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((ptx::smem_u32(smem) & 1023) != 0) __trap();  // swizzle atoms need 1 KB alignment
+  ATTN_CTA(0);
+  ATTN_CTA(1);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kSmemBar);
   uint64_t *q_full = bar, *kv_full = bar + 1, *kv_empty = bar + 3, *s_full = bar + 5, *p_full = bar + 6,
            *o_done = bar + 7, *s_free = bar + 8;
@@ -91,6 +126,7 @@ __global__ void __launch_bounds__(192, 2)
       for (int j = 0; j < nkb; ++j) {
         const int st = j & 1;
         ptx::mbar_wait_sleep(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        ATTN_TRACE(true, j, 0);
         ptx::mbar_arrive_expect_tx(&kv_full[st], 2 * kTileBytes);
         ptx::tma_load_2d(smem + kSmemK + st * kTileBytes, &tqkv, &kv_full[st], H * kD + hd * kD, row_base + j * kKV);
         ptx::tma_load_2d(smem + kSmemV + st * kTileBytes, &tqkv, &kv_full[st], 2 * H * kD + hd * kD,
@@ -105,6 +141,7 @@ __global__ void __launch_bounds__(192, 2)
       auto issue_s = [&](int j) {
         const int st = j & 1;
         ptx::mbar_wait_sleep(&kv_full[st], (j >> 1) & 1);
+        ATTN_TRACE(true, j, 1);
         ptx::tc_fence_after();
         const uint32_t sk = ptx::smem_u32(smem + kSmemK + st * kTileBytes);
 #pragma unroll
@@ -118,10 +155,12 @@ __global__ void __launch_bounds__(192, 2)
       for (int j = 0; j < nkb; ++j) {
         if (j + 1 < nkb) {  // S_j is in the softmax registers: compute S_{j+1} under its exp2s
           ptx::mbar_wait_sleep(s_free, j & 1);
+          ATTN_TRACE(true, j, 2);
           ptx::tc_fence_after();
           issue_s(j + 1);
         }
         ptx::mbar_wait_sleep(p_full, j & 1);  // P_j in smem, O rescaled
+        ATTN_TRACE(true, j, 3);
         ptx::tc_fence_after();
         const uint32_t sv = ptx::smem_u32(smem + kSmemV + (j & 1) * kTileBytes);
 #pragma unroll
@@ -141,7 +180,9 @@ __global__ void __launch_bounds__(192, 2)
     float m = -INFINITY, l = 0.f;
     uint8_t* sp = smem + kSmemP;
     for (int j = 0; j < nkb; ++j) {
+      ATTN_TRACE(t == 0, j, 4);
       ptx::mbar_wait(s_full, j & 1);
+      ATTN_TRACE(t == 0, j, 5);
       ptx::tc_fence_after();
       const int key0 = j * kKV;
       // the whole 128-score row lives in registers (one TMEM pass)
@@ -149,34 +190,63 @@ __global__ void __launch_bounds__(192, 2)
 #pragma unroll
       for (int c = 0; c < 4; ++c) ptx::tmem_ld32(trow + c * 32, r[c]);
       ptx::tmem_ld_wait();
+      ATTN_TRACE(t == 0, j, 6);
       ptx::tc_fence_before();
       ptx::mbar_arrive(s_free);
-      // masking only on the diagonal (causal) / sequence-tail tile: warp-uniform branch
-      const bool edge = (CAUSAL && key0 + kKV - 1 > q0) || key0 + kKV > seq;
-      float mxp[8];  // 8 independent max chains
+      // masking only on the diagonal (causal) / sequence-tail tile (warp-uniform branch):
+      // keys past `lim` (tile-relative) drop out as raw -inf scores
+      if ((CAUSAL && key0 + kKV - 1 > q0) || key0 + kKV > seq) {
+        const int lim = CAUSAL ? min(q - key0, seq - 1 - key0) : seq - 1 - key0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c * 32 + i > lim) r[c][i] = 0xff800000u;
+      }
+      // row max on the raw scores (the 1/sqrt(d)*log2(e) scale is applied inside the
+      // exp2 FMA below); 8 independent chains
+      float mxp[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) mxp[u] = -INFINITY;
 #pragma unroll
       for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float v = __uint_as_float(r[c][i]) * sl2;
-          if (edge) {
-            const int key = key0 + c * 32 + i;
-            if (key >= seq || (CAUSAL && key > q)) v = -INFINITY;
-          }
-          r[c][i] = __float_as_uint(v);
-          mxp[i & 7] = fmaxf(mxp[i & 7], v);
-        }
+        for (int i = 0; i < 32; ++i) mxp[i & 7] = fmaxf(mxp[i & 7], __uint_as_float(r[c][i]));
       const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
-                             fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
-      const float mn = fmaxf(m, mx);
+                             fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7]))) * sl2;
+      // the running max only moves when the new one exceeds it by more than 2^8 (P <= 256
+      // is exact enough in fp32 / bf16), so the O rescale below almost never runs
+      const float mn = mx > m + 8.f ? mx : m;
       const float safe = mn == -INFINITY ? 0.f : mn;
       const float alpha = ex2_approx(m - safe);
       m = mn;
       l *= alpha;
+      ATTN_TRACE(t == 0, j, 7);
+      // P = exp2(s * scale - m) -> bf16 pairs in registers first, so that the previous
+      // P V (which still reads the P tile and writes O) completes underneath
+      const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-safe, -safe);
+      float2 ls[4] = {};  // independent packed sum chains
+      uint32_t pk[64];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float2 x = ptx::fma2(make_float2(__uint_as_float(r[c][i]), __uint_as_float(r[c][i + 1])), sc2, nm2);
+          // every kPolyEvery-th pair on the FMA pipes, the rest on MUFU
+          const float2 p = (kPolyEvery > 0 && (i >> 1) % (kPolyEvery > 0 ? kPolyEvery : 1) == kPolyEvery - 1)
+                               ? ptx::ex2_poly2(x)
+                                                                      : make_float2(ex2_approx(x.x), ex2_approx(x.y));
+          ls[(i >> 1) & 3] = ptx::add2(ls[(i >> 1) & 3], p);
+          __nv_bfloat162 hb = __floats2bfloat162_rn(p.x, p.y);
+          pk[c * 16 + (i >> 1)] = *reinterpret_cast<uint32_t*>(&hb);
+        }
+      {
+        const float2 s01 = ptx::add2(ptx::add2(ls[0], ls[1]), ptx::add2(ls[2], ls[3]));
+        l += s01.x + s01.y;
+      }
       if (j > 0) {  // the previous P V must have landed before O is touched / P rewritten
         ptx::mbar_wait(o_done, (j - 1) & 1);
+        ATTN_TRACE(t == 0, j, 8);
         ptx::tc_fence_after();
         if (__any_sync(0xffffffffu, alpha != 1.f)) {  // rescale only when a row max moved
 #pragma unroll 1
@@ -185,33 +255,24 @@ __global__ void __launch_bounds__(192, 2)
             ptx::tmem_ld32(trow + 128 + c * 32, o);
             ptx::tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            for (int i = 0; i < 32; i += 2) {
+              const float2 v = ptx::mul2(make_float2(__uint_as_float(o[i]), __uint_as_float(o[i + 1])),
+                                         make_float2(alpha, alpha));
+              o[i] = __float_as_uint(v.x);
+              o[i + 1] = __float_as_uint(v.y);
+            }
             tmem_st32(trow + 128 + c * 32, o);
           }
           tmem_st_wait();
         }
       }
-      // P = exp2(s - m) as bf16 into the swizzled K-major tile
-      float ls[4] = {0.f, 0.f, 0.f, 0.f};  // independent sum chains
+      // P into the 128-byte-swizzled K-major tile: 8 keys -> one 16-byte chunk
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {  // 8 keys -> one 16-byte chunk
-          uint32_t pk[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int i = g * 8 + e * 2;
-            const float p0 = ex2_approx(__uint_as_float(r[c][i]) - safe);
-            const float p1 = ex2_approx(__uint_as_float(r[c][i + 1]) - safe);
-            ls[e] += p0 + p1;
-            __nv_bfloat162 hb = __floats2bfloat162_rn(p0, p1);
-            pk[e] = *reinterpret_cast<uint32_t*>(&hb);
-          }
-          const int k8 = c * 4 + g;  // chunk of 8 keys, 0..15
-          uint8_t* dst = sp + (k8 >> 3) * kTileBytes + t * 128 + (((k8 & 7) ^ (t & 7)) << 4);
-          *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        }
-      l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      for (int k8 = 0; k8 < 16; ++k8) {
+        uint8_t* dst = sp + (k8 >> 3) * kTileBytes + t * 128 + (((k8 & 7) ^ (t & 7)) << 4);
+        *reinterpret_cast<uint4*>(dst) = make_uint4(pk[4 * k8], pk[4 * k8 + 1], pk[4 * k8 + 2], pk[4 * k8 + 3]);
+      }
+      ATTN_TRACE(t == 0, j, 9);
       ptx::fence_proxy_async();  // P (generic stores) -> visible to the tensor core
       ptx::tc_fence_before();
       ptx::mbar_arrive(p_full);
@@ -248,6 +309,7 @@ __global__ void __launch_bounds__(192, 2)
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 256);
   }
+  ATTN_CTA(2);
 }
 
 // ----------------------------------------------------------------- backward --

@@ -66,6 +66,53 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+// Packed fp32x2 FMA / add (FFMA2 / FADD2 on sm_100): half the issue slots of two scalars.
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n"
+      "mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n mov.b64 rc, {%6,%7};\n"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n"
+      "mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n"
+      "add.rn.f32x2 rd, ra, rb;\n mov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n"
+      "mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n"
+      "mul.rn.f32x2 rd, ra, rb;\n mov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
+// 2^x for a pair on the FMA pipes (x <= 126): x = n + f with n = rint(x) from the
+// 1.5*2^23 shifter, f in [-0.5, 0.5], 2^f by a degree-3 relative-minimax polynomial
+// (max rel. error 1.0e-4, far below bf16's 2^-8), 2^n added into the exponent field.
+// Inputs below -127 (incl. -inf) give exactly 0.  Used to take a share of the softmax
+// exponentials off the MUFU unit.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 t = add2(x, make_float2(12582912.f, 12582912.f));
+  const float2 n = add2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = fma2(n, make_float2(-1.f, -1.f), x);
+  float2 p = fma2(f, make_float2(0.05500794f, 0.05500794f), make_float2(0.24220875f, 0.24220875f));
+  p = fma2(p, f, make_float2(0.69328278f, 0.69328278f));
+  p = fma2(p, f, make_float2(1.f, 1.f));  // p(0) = 1 exactly: 2^-127 -> +0, never a wrapped exponent
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 // --------------------------------------------------------------------- TMA --
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");

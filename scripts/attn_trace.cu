@@ -1,0 +1,74 @@
+// Phase timeline of the tcgen05 attention forward for CTA 0 plus per-CTA SM/start/end
+// stamps.  Build + run (on a B200):
+//   nvcc -std=c++20 -O3 -gencode arch=compute_100a,code=sm_100a --expt-relaxed-constexpr \
+//     -Iinclude -Ipaper_2107_06925_b200/csrc/cuda -Ipaper_2107_06925_b200/csrc/host \
+//     scripts/attn_trace.cu $(ls build/csrc/*.o | grep -v attention_tc) -lcuda -o scripts/_bin/attn_trace
+#define CK_ATTN_TRACE 1
+#include "../paper_2107_06925_b200/csrc/cuda/attention_tc.cu"
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+int main(int argc, char** argv) {
+  const int B = argc > 1 ? atoi(argv[1]) : 4, seq = argc > 2 ? atoi(argv[2]) : 1024, H = argc > 3 ? atoi(argv[3]) : 16;
+  const size_t M = size_t(B) * seq;
+  std::vector<__nv_bfloat16> h(M * 3 * H * 64);
+  uint32_t x = 12345;
+  for (auto& v : h) {
+    x = x * 1664525u + 1013904223u;
+    v = __float2bfloat16(((x >> 8) / 16777216.f - 0.5f) * 2.f);
+  }
+  __nv_bfloat16 *qkv, *out;
+  float* lse;
+  cudaMalloc(&qkv, h.size() * 2);
+  cudaMalloc(&out, M * H * 64 * 2);
+  cudaMalloc(&lse, M * H * 4);
+  cudaMemcpy(qkv, h.data(), h.size() * 2, cudaMemcpyHostToDevice);
+  for (int i = 0; i < 5; ++i) chimera::ops::attn_fwd_tc(qkv, out, lse, B, seq, H, true, 0);
+  cudaDeviceSynchronize();
+  static long long tr[32][16], cta[4096][3];
+  cudaMemcpyFromSymbol(tr, chimera::ops::g_attn_trace, sizeof(tr));
+  cudaMemcpyFromSymbol(cta, chimera::ops::g_attn_cta, sizeof(cta));
+  const int ncta = (seq + 127) / 128 * B * H;
+  long long t0 = cta[0][1], tend = 0, tmin = cta[0][1];
+  for (int i = 0; i < ncta; ++i) tmin = std::min(tmin, cta[i][1]), tend = std::max(tend, cta[i][2]);
+  printf("kernel span %.1f us, %d CTAs\n", (tend - tmin) / 1e3, ncta);
+  printf("CTA0 sm %lld start +%.2f us dur %.2f us\n", cta[0][0], (t0 - tmin) / 1e3, (cta[0][2] - cta[0][1]) / 1e3);
+  // per-tile stamps relative to kv_full of tile 0 (cycles)
+  const long long c0 = tr[0][1];
+  const char* names[] = {"tma:kv_empty", "mma:kv_full", "mma:s_free", "mma:p_full", "sm:wait_s",
+                         "sm:s_full",    "sm:ld_done",  "sm:max_done", "sm:o_done", "sm:p_done"};
+  printf("%-4s", "j");
+  for (int e = 0; e < 10; ++e) printf(" %12s", names[e]);
+  printf("\n");
+  for (int j = 0; j < 8; ++j) {
+    printf("%-4d", j);
+    for (int e = 0; e < 10; ++e) printf(" %12lld", tr[j][e] ? tr[j][e] - c0 : -1);
+    printf("\n");
+  }
+  // tail: histogram of CTA end times
+  int sm_busy[256] = {0};
+  long long last_end[256] = {0};
+  for (int i = 0; i < ncta; ++i) {
+    sm_busy[cta[i][0]]++;
+    last_end[cta[i][0]] = std::max(last_end[cta[i][0]], cta[i][2]);
+  }
+  long long e_min = tend, e_max = 0;
+  for (int s = 0; s < 148; ++s) if (sm_busy[s]) e_min = std::min(e_min, last_end[s]), e_max = std::max(e_max, last_end[s]);
+  printf("SM finish spread: first idle SM at %.1f us, last at %.1f us\n", (e_min - tmin) / 1e3, (e_max - tmin) / 1e3);
+  double dur_sum = 0;
+  for (int i = 0; i < ncta; ++i) dur_sum += cta[i][2] - cta[i][1];
+  printf("sum CTA durations / (148 SMs * 2) = %.1f us\n", dur_sum / 1e3 / 296);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int i = 0; i < 50; ++i) chimera::ops::attn_fwd_tc(qkv, out, lse, B, seq, H, true, 0);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("avg launch %.2f us (traced build)\n", ms * 1000 / 50);
+  return 0;
+}
