@@ -197,19 +197,63 @@ __global__ void __launch_bounds__(128) k_attn_fwd(const bf16* __restrict__ qkv, 
   }
 }
 
-// D[bh][q] = sum_d dO[q][d] * O[q][d]   (one warp per (token, head))
-__global__ void k_attn_bwd_dot(const bf16* __restrict__ out, const bf16* __restrict__ dout,
-                               float* __restrict__ D, int M, int seq, int H) {
-  const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= (long long)M * H) return;
-  const int tok = int(w / H), hd = int(w % H);
-  const long long off = (long long)tok * H * kHd + hd * kHd + lane * 2;
-  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(out + off));
-  const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dout + off));
-  const float s = cuda::warp_sum(a.x * c.x + a.y * c.y);
-  const int b = tok / seq, q = tok % seq;
-  if (lane == 0) D[((long long)b * H + hd) * seq + q] = s;
+// D[bh][q] = sum_d dO[q][d] * O[q][d]: 8 threads per (token, head) row, 16-byte loads,
+// two rows per thread in flight (pure HBM stream: 2 x M*H*128 bytes).  With `dq` set, the
+// same threads also zero the fp32 dQ accumulator (M*H*64 floats, 32 bytes per row part).
+__global__ void __launch_bounds__(256) k_attn_bwd_dot(const bf16* __restrict__ out, const bf16* __restrict__ dout,
+                                                      float* __restrict__ D, float* __restrict__ dq, int M, int seq,
+                                                      int H) {
+  const long long rows = (long long)M * H;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int part = threadIdx.x & 7;
+  const long long stride = (long long)gridDim.x * blockDim.x / 8;
+  for (long long r0 = t >> 3; r0 < rows; r0 += 2 * stride) {
+    if (dq) {  // row r of [tok][H*64] is the contiguous 64 floats at r*64
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      float4* p0 = reinterpret_cast<float4*>(dq + r0 * kHd + part * 8);
+      p0[0] = z;
+      p0[1] = z;
+      if (r0 + stride < rows) {
+        float4* p1 = reinterpret_cast<float4*>(dq + (r0 + stride) * kHd + part * 8);
+        p1[0] = z;
+        p1[1] = z;
+      }
+    }
+    const long long r1 = r0 + stride;
+    uint4 a0 = __ldcs(reinterpret_cast<const uint4*>(out + r0 * kHd + part * 8));
+    uint4 c0 = __ldcs(reinterpret_cast<const uint4*>(dout + r0 * kHd + part * 8));
+    uint4 a1 = make_uint4(0, 0, 0, 0), c1 = a1;
+    if (r1 < rows) {
+      a1 = __ldcs(reinterpret_cast<const uint4*>(out + r1 * kHd + part * 8));
+      c1 = __ldcs(reinterpret_cast<const uint4*>(dout + r1 * kHd + part * 8));
+    }
+    auto dot8 = [](uint4 a, uint4 c) {
+      const __nv_bfloat162* x = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* y = reinterpret_cast<const __nv_bfloat162*>(&c);
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 u = __bfloat1622float2(x[i]), v = __bfloat1622float2(y[i]);
+        s = fmaf(u.x, v.x, fmaf(u.y, v.y, s));
+      }
+      return s;
+    };
+    float s0 = dot8(a0, c0), s1 = dot8(a1, c1);
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if (part == 0) {
+      // row r = tok * H + hd  ->  D[(b * H + hd) * seq + q]
+      const int tok0 = int(r0 / H), hd0 = int(r0 % H);
+      D[((long long)(tok0 / seq) * H + hd0) * seq + tok0 % seq] = s0;
+      if (r1 < rows) {
+        const int tok1 = int(r1 / H), hd1 = int(r1 % H);
+        D[((long long)(tok1 / seq) * H + hd1) * seq + tok1 % seq] = s1;
+      }
+    }
+  }
 }
 
 template <bool CAUSAL>
@@ -326,13 +370,18 @@ __global__ void __launch_bounds__(128) k_attn_bwd(const bf16* __restrict__ qkv, 
 }
 
 // dqkv[:, q-part] = bf16(dq_acc * scale)
-__global__ void k_dq_out(const float* __restrict__ acc, bf16* __restrict__ dqkv, long long n_rows, int H) {
-  const int w = H * kHd;
-  const long long n = n_rows * w;
-  for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 2; i < n;
-       i += (long long)gridDim.x * blockDim.x * 2) {
-    const long long r = i / w, c = i % w;
-    *reinterpret_cast<uint32_t*>(dqkv + r * 3 * w + c) = pack(acc[i] * 0.125f, acc[i + 1] * 0.125f);
+// dQ (fp32 accumulator, scaled by 1/sqrt(d)) -> bf16 Q-part of dqkv (L2-resident stream)
+__global__ void __launch_bounds__(256) k_dq_out(const float* __restrict__ acc, bf16* __restrict__ dqkv, int n_rows,
+                                                int H) {
+  const int w = H * kHd;  // multiple of 64
+  const int n8 = n_rows * w / 8;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
+    const float4* p = reinterpret_cast<const float4*>(acc) + 2 * i;
+    const float4 a = __ldcs(p), b = __ldcs(p + 1);
+    const int e = i * 8, r = e / w, c = e - r * w;
+    *reinterpret_cast<uint4*>(dqkv + (long long)r * 3 * w + c) =
+        make_uint4(pack(a.x * 0.125f, a.y * 0.125f), pack(a.z * 0.125f, a.w * 0.125f), pack(b.x * 0.125f, b.y * 0.125f),
+                   pack(b.z * 0.125f, b.w * 0.125f));
   }
 }
 
@@ -350,14 +399,15 @@ size_t attn_bwd_scratch_floats(int B, int seq, int H) {
   return size_t(B) * H * seq + size_t(B) * seq * H * kHd;
 }
 
-void attn_bwd_dot(const bf16* out, const bf16* dout, float* D, int M, int seq, int H, cudaStream_t st) {
-  k_attn_bwd_dot<<<cuda::ceil_div((long long)M * H * 32, 256), 256, 0, st>>>(out, dout, D, M, seq, H);
+void attn_bwd_dot(const bf16* out, const bf16* dout, float* D, int M, int seq, int H, cudaStream_t st, float* dq_zero) {
+  k_attn_bwd_dot<<<std::min<long long>(cuda::ceil_div((long long)M * H * 8, 512), 148LL * 8), 256, 0, st>>>(
+      out, dout, D, dq_zero, M, seq, H);
   CK_CUDA(cudaGetLastError());
 }
 
 void attn_dq_out(const float* dq, bf16* dqkv, int M, int H, cudaStream_t st) {
   const long long n = (long long)M * H * kHd;
-  k_dq_out<<<std::min<long long>((n / 2 + 255) / 256, 148LL * 16), 256, 0, st>>>(dq, dqkv, M, H);
+  k_dq_out<<<std::min<long long>((n / 8 + 255) / 256, 148LL * 8), 256, 0, st>>>(dq, dqkv, M, H);
   CK_CUDA(cudaGetLastError());
 }
 
@@ -366,13 +416,11 @@ void attn_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* l
   float* D = scratch;
   float* dq = scratch + size_t(B) * H * seq;
   const int M = B * seq;
-  CK_CUDA(cudaMemsetAsync(dq, 0, size_t(M) * H * kHd * sizeof(float), st));
-  k_attn_bwd_dot<<<cuda::ceil_div((long long)M * H * 32, 256), 256, 0, st>>>(out, dout, D, M, seq, H);
+  attn_bwd_dot(out, dout, D, M, seq, H, st, dq);
   const dim3 grid((seq + kTile - 1) / kTile, B * H);
   if (causal) k_attn_bwd<true><<<grid, 128, 0, st>>>(qkv, dout, lse, D, dq, dqkv, seq, H);
   else k_attn_bwd<false><<<grid, 128, 0, st>>>(qkv, dout, lse, D, dq, dqkv, seq, H);
-  const long long n = (long long)M * H * kHd;
-  k_dq_out<<<std::min<long long>((n / 2 + 255) / 256, 148LL * 16), 256, 0, st>>>(dq, dqkv, M, H);
+  attn_dq_out(dq, dqkv, M, H, st);
   CK_CUDA(cudaGetLastError());
 }
 

@@ -68,6 +68,16 @@ constexpr float kLog2e = 1.4426950408889634f;
 #endif
 constexpr int kPolyEvery = CK_ATTN_POLY_EVERY;
 
+// The MMA issuer sits on the critical path of every hand-off (P ready -> PV, dS ready
+// -> dV/dK/dQ): it polls (try_wait) instead of sleeping, whose wake-up costs ~400 cycles.
+#ifndef CK_ATTN_MMA_SPIN
+#define CK_ATTN_MMA_SPIN 1
+#endif
+__device__ __forceinline__ void mma_wait(uint64_t* bar, uint32_t parity) {
+  if (CK_ATTN_MMA_SPIN) ptx::mbar_wait(bar, parity);
+  else ptx::mbar_wait_sleep(bar, parity);
+}
+
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -140,7 +150,7 @@ __global__ void __launch_bounds__(192, 2)
       const uint32_t sq = ptx::smem_u32(smem + kSmemQ), sp = ptx::smem_u32(smem + kSmemP);
       auto issue_s = [&](int j) {
         const int st = j & 1;
-        ptx::mbar_wait_sleep(&kv_full[st], (j >> 1) & 1);
+        mma_wait(&kv_full[st], (j >> 1) & 1);
         ATTN_TRACE(true, j, 1);
         ptx::tc_fence_after();
         const uint32_t sk = ptx::smem_u32(smem + kSmemK + st * kTileBytes);
@@ -154,12 +164,12 @@ __global__ void __launch_bounds__(192, 2)
       issue_s(0);
       for (int j = 0; j < nkb; ++j) {
         if (j + 1 < nkb) {  // S_j is in the softmax registers: compute S_{j+1} under its exp2s
-          ptx::mbar_wait_sleep(s_free, j & 1);
+          mma_wait(s_free, j & 1);
           ATTN_TRACE(true, j, 2);
           ptx::tc_fence_after();
           issue_s(j + 1);
         }
-        ptx::mbar_wait_sleep(p_full, j & 1);  // P_j in smem, O rescaled
+        mma_wait(p_full, j & 1);  // P_j in smem, O rescaled
         ATTN_TRACE(true, j, 3);
         ptx::tc_fence_after();
         const uint32_t sv = ptx::smem_u32(smem + kSmemV + (j & 1) * kTileBytes);
@@ -313,37 +323,53 @@ __global__ void __launch_bounds__(192, 2)
 }
 
 // ----------------------------------------------------------------- backward --
-// CTA = (128-key tile, batch*head), same 6-warp split.  Per 128-query tile:
-//   S^T  = K Q^T     (M128 keys, N128 q, K64)   TMEM [0,128)
-//   dP^T = V dO^T    (M128, N128, K64)          TMEM [128,256)
-//   compute warps (thread = key row): P^T = exp2(S^T*c - lse2), dS^T = P^T (dP^T - D)
-//     -> bf16, 128-byte-swizzled K-major smem tiles
-//   dV  += P^T dO    (M128 keys, N64, K128 q)   TMEM [256,320)
-//   dK  += dS^T Q    (M128 keys, N64, K128 q)   TMEM [320,384)
-//   dQ   = dS K      (M128 q, N64, K128 keys)   TMEM [384,448)  -- the dS^T tile read
-//     as an MN-major A operand; compute warps (thread = query row) add it to the fp32
-//     dQ accumulator with 16-byte vector atomics.
+// CTA = (128-key tile, batch*head); 10 warps, one CTA per SM (512 TMEM columns):
+//   warp 8   TMA producer: K, V once; per 128-query tile Q and dO into a 2-stage ring,
+//            and (all lanes) the tile's -lse*log2(e) and -D rows into smem
+//   warp 9   TMEM allocator + single-thread MMA issuer
+//   warps 0-7  two compute warpgroups; WG g owns query columns [64g, 64g+64) of every
+//            tile; warp w reads TMEM lanes 32*(w%4).. (thread <-> key row)
+// Per query tile j:
+//   S^T  = K Q^T, dP^T = V dO^T     (M128 keys, N128 q, K64)  TMEM [0,128), [128,256);
+//     issued as soon as tile j-1's S^T / dP^T sit in registers (st_free)
+//   P^T = exp2(S^T c - lse2), dS^T = P^T (dP^T - D) -> bf16, 128-byte-swizzled K-major
+//     smem tiles (each WG writes its own 64-query block)
+//   dV += P^T dO, dK += dS^T Q       (M128 keys, N64, K128 q)  TMEM [256,320), [320,384)
+//   dQ_j = dS K                      (M128 q, N64, K128 keys)  TMEM [384 + 64 (j&1), ..)
+//     -- the dS^T tile read as an MN-major A operand; double-buffered so the MMA never
+//     waits for the drain
+//   dQ_j is drained one tile later (underneath tile j+1's math) by the compute WGs, 32
+//   columns each, through a swizzled smem stage and one TMA bulk tensor reduce-add into
+//   the fp32 dQ accumulator -- no per-thread atomics.
 constexpr int kB_K = 0, kB_V = kTileBytes, kB_Q = 2 * kTileBytes, kB_DO = 4 * kTileBytes,
-              kB_P = 6 * kTileBytes, kB_DS = 8 * kTileBytes, kB_LD = 10 * kTileBytes;  // lse/D [2][2][128]
+              kB_P = 6 * kTileBytes, kB_DS = 8 * kTileBytes, kB_DQ = 10 * kTileBytes,  // dQ stage [WG][128][128 B]
+    kB_LD = 12 * kTileBytes;                                                           // [stage][-lse2 | -D][128]
 constexpr int kB_BAR = kB_LD + 4 * 128 * 4;
 constexpr int kBwdSmem = kB_BAR + 256;
+constexpr int kBwdThreads = 320;
+#ifndef CK_ATTN_BWD_POLY_EVERY
+#define CK_ATTN_BWD_POLY_EVERY 0
+#endif
+constexpr int kBwdPolyEvery = CK_ATTN_BWD_POLY_EVERY;
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 template <bool CAUSAL>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kBwdThreads, 1)
     k_attn_bwd_tc(const __grid_constant__ CUtensorMap tqkv, const __grid_constant__ CUtensorMap tdo,
-                  const float* __restrict__ lse, const float* __restrict__ Dv, float* __restrict__ dq_acc,
-                  bf16* __restrict__ dqkv, int seq, int H) {
+                  const __grid_constant__ CUtensorMap tdq, const float* __restrict__ lse,
+                  const float* __restrict__ Dv, bf16* __restrict__ dqkv, int seq, int H) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((ptx::smem_u32(smem) & 1023) != 0) __trap();
+  ATTN_CTA(0);
+  ATTN_CTA(1);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kB_BAR);
-  uint64_t *kv_full = bar, *qd_full = bar + 1, *qd_empty = bar + 3, *s_full = bar + 5, *ds_full = bar + 6,
-           *mm_done = bar + 7, *dq_free = bar + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
-  float* sLD = reinterpret_cast<float*>(smem + kB_LD);  // [buf][0=lse2,1=D][128]
+  uint64_t *kv_full = bar, *qd_full = bar + 1, *qd_empty = bar + 3, *s_full = bar + 5, *st_free = bar + 6,
+           *ds_full = bar + 7, *mm_done = bar + 8, *dq_free = bar + 9;  // dq_free[2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
+  float* sLD = reinterpret_cast<float*>(smem + kB_LD);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // 1-D grid, tile-major: key tile 0 sees every query tile under causal masking, so the
@@ -355,50 +381,77 @@ __global__ void __launch_bounds__(192, 1)
   const int j0 = CAUSAL ? kb : 0;  // first query tile that can see these keys
   const int niter = nq - j0;
 
-  if (warp == 4 && lane == 0) {
+  if (warp == 8 && lane == 0) {
     ptx::tma_prefetch(&tqkv);
     ptx::tma_prefetch(&tdo);
+    ptx::tma_prefetch(&tdq);
     ptx::mbar_init(kv_full, 1);
-    for (int s2 = 0; s2 < 2; ++s2) ptx::mbar_init(&qd_full[s2], 1), ptx::mbar_init(&qd_empty[s2], 1);
+    for (int s2 = 0; s2 < 2; ++s2) ptx::mbar_init(&qd_full[s2], 32), ptx::mbar_init(&qd_empty[s2], 1);
     ptx::mbar_init(s_full, 1);
-    ptx::mbar_init(ds_full, 128);
+    ptx::mbar_init(st_free, 256);
+    ptx::mbar_init(ds_full, 256);
     ptx::mbar_init(mm_done, 1);
-    ptx::mbar_init(dq_free, 128);
+    for (int s2 = 0; s2 < 2; ++s2) ptx::mbar_init(&dq_free[s2], 256);
     ptx::fence_barrier_init();
   }
-  if (warp == 5) ptx::tmem_alloc(tmem_slot, 512);
+  if (warp == 9) ptx::tmem_alloc(tmem_slot, 512);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   constexpr uint32_t kSt = 0, kDPt = 128, kDV = 256, kDK = 320, kDQ = 384;
 
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0) {
       ptx::mbar_arrive_expect_tx(kv_full, 2 * kTileBytes);
       ptx::tma_load_2d(smem + kB_K, &tqkv, kv_full, H * kD + hd * kD, row_base + k0);
       ptx::tma_load_2d(smem + kB_V, &tqkv, kv_full, 2 * H * kD + hd * kD, row_base + k0);
-      for (int it = 0; it < niter; ++it) {
-        const int st = it & 1, q0 = (j0 + it) * kQ;
-        ptx::mbar_wait_sleep(&qd_empty[st], ((it >> 1) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&qd_full[st], 2 * kTileBytes);
+    }
+    // the tile's lse / D rows are fetched into registers one tile ahead, so their global
+    // load latency hides under the wait for the ring slot
+    float lv[4], dv[4];
+    auto fetch = [&](int it) {
+      const int q0 = (j0 + it) * kQ;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int q = q0 + lane + 32 * k;
+        lv[k] = q < seq ? lse[(long long)bh * seq + q] : 0.f;
+        dv[k] = q < seq ? Dv[(long long)bh * seq + q] : 0.f;
+      }
+    };
+    fetch(0);
+    for (int it = 0; it < niter; ++it) {
+      const int st = it & 1, q0 = (j0 + it) * kQ;
+      if (lane == 0) ptx::mbar_wait_sleep(&qd_empty[st], ((it >> 1) & 1) ^ 1);
+      __syncwarp();
+      ATTN_TRACE(lane == 0, it, 9);
+      if (lane == 0) {
+        ptx::mbar_expect_tx(&qd_full[st], 2 * kTileBytes);
         ptx::tma_load_2d(smem + kB_Q + st * kTileBytes, &tqkv, &qd_full[st], hd * kD, row_base + q0);
         ptx::tma_load_2d(smem + kB_DO + st * kTileBytes, &tdo, &qd_full[st], hd * kD, row_base + q0);
       }
+      float* L = sLD + st * 256;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        L[lane + 32 * k] = -lv[k] * kLog2e;
+        L[128 + lane + 32 * k] = -dv[k];
+      }
+      ptx::mbar_arrive(&qd_full[st]);
+      if (it + 1 < niter) fetch(it + 1);
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     if (lane == 0) {
       constexpr uint32_t id_s = ptx::idesc_bf16(128, 128, false, false);
       constexpr uint32_t id_kv = ptx::idesc_bf16(128, 64, false, true);  // A K-major, B MN-major
       constexpr uint32_t id_q = ptx::idesc_bf16(128, 64, true, true);    // A MN-major (dS^T^T), B MN-major
       const uint32_t sk = ptx::smem_u32(smem + kB_K), sv = ptx::smem_u32(smem + kB_V);
       const uint32_t sp = ptx::smem_u32(smem + kB_P), sds = ptx::smem_u32(smem + kB_DS);
-      ptx::mbar_wait(kv_full, 0);
-      for (int it = 0; it < niter; ++it) {
+      auto issue_s = [&](int it) {
         const int st = it & 1;
         const uint32_t sq = ptx::smem_u32(smem + kB_Q + st * kTileBytes);
         const uint32_t sdo = ptx::smem_u32(smem + kB_DO + st * kTileBytes);
-        ptx::mbar_wait_sleep(&qd_full[st], (it >> 1) & 1);
+        mma_wait(&qd_full[st], (it >> 1) & 1);
+        ATTN_TRACE(true, it, 0);
         ptx::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kD / 16; ++k) {
@@ -408,7 +461,20 @@ __global__ void __launch_bounds__(192, 1)
                         ptx::smem_desc_sw128(sdo + k * 32, 16, 1024), id_s, k > 0);
         }
         ptx::umma_commit(s_full);
-        ptx::mbar_wait_sleep(ds_full, it & 1);  // P^T, dS^T in smem; S^T / dP^T consumed
+      };
+      ptx::mbar_wait(kv_full, 0);
+      issue_s(0);
+      for (int it = 0; it < niter; ++it) {
+        const int st = it & 1;
+        if (it + 1 < niter) {  // tile it's S^T / dP^T are in registers: next tile's scores now
+          mma_wait(st_free, it & 1);
+          ptx::tc_fence_after();
+          issue_s(it + 1);
+        }
+        const uint32_t sq = ptx::smem_u32(smem + kB_Q + st * kTileBytes);
+        const uint32_t sdo = ptx::smem_u32(smem + kB_DO + st * kTileBytes);
+        mma_wait(ds_full, it & 1);  // P^T, dS^T of tile it in smem
+        ATTN_TRACE(true, it, 1);
         ptx::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kQ / 16; ++k) {
@@ -419,126 +485,157 @@ __global__ void __launch_bounds__(192, 1)
           ptx::umma_f16(tmem + kDK, a_ds, ptx::smem_desc_sw128(sq + k * 2048, kTileBytes, 1024), id_kv,
                         (it > 0 || k > 0) ? 1u : 0u);
         }
-        if (it > 0) ptx::mbar_wait_sleep(dq_free, (it - 1) & 1);  // previous dQ read out
+        ptx::umma_commit(&qd_empty[st]);  // Q / dO of tile it: last read by dK / dV
+        if (it >= 2) mma_wait(&dq_free[st], ((it >> 1) & 1) ^ 1);  // dQ_{it-2} drained
+        ATTN_TRACE(true, it, 2);
         ptx::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kKV / 16; ++k)  // dQ = dS K: reduce over 16 keys per step
-          ptx::umma_f16(tmem + kDQ, ptx::smem_desc_sw128(sds + k * 2048, kTileBytes, 1024),
+          ptx::umma_f16(tmem + kDQ + 64 * st, ptx::smem_desc_sw128(sds + k * 2048, kTileBytes, 1024),
                         ptx::smem_desc_sw128(sk + k * 2048, kTileBytes, 1024), id_q, k > 0);
-        ptx::umma_commit(&qd_empty[st]);
         ptx::umma_commit(mm_done);
       }
     }
   } else {
-    const int t = threadIdx.x;  // key row for S^T / dP^T / dK / dV; query row for dQ
-    const int key = k0 + t;
-    const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
+    const int g = warp >> 2;                 // compute warpgroup: query columns [64g, 64g+64)
+    const int r = (warp & 3) * 32 + lane;    // TMEM lane: key row (S^T, dP^T, dK, dV) / query row (dQ)
+    const int ct = threadIdx.x & 127;        // thread within the WG
+    const int key = k0 + r;
+    const uint32_t trow = tmem + (uint32_t((warp & 3) * 32) << 16);
     const float sl2 = 0.125f * kLog2e;
-    uint8_t* sp = smem + kB_P;
-    uint8_t* sds = smem + kB_DS;
+    uint8_t* sp = smem + kB_P + g * kTileBytes;
+    uint8_t* sds = smem + kB_DS + g * kTileBytes;
+    uint8_t* stage = smem + kB_DQ + g * kTileBytes;
+    // dQ_j (TMEM buffer j&1) -> swizzled smem stage -> TMA reduce-add; this WG's 32 columns
+    auto drain_dq = [&](int j) {
+      const int qj0 = (j0 + j) * kQ;
+      if (ct == 0) ptx::bulk_wait_read0();  // previous reduce has read the stage
+      named_bar_sync(2 + g, 128);
+      uint32_t v[32];
+      ptx::tmem_ld32(trow + kDQ + 64 * (j & 1) + 32 * g, v);
+      ptx::tmem_ld_wait();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&dq_free[j & 1]);
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<uint4*>(stage + r * 128 + ((c ^ (r & 7)) << 4)) =
+            make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+      ptx::fence_proxy_async();
+      named_bar_sync(2 + g, 128);
+      if (ct == 0) {
+        ptx::tma_reduce_add_2d(&tdq, stage, hd * kD + 32 * g, row_base + qj0);
+        ptx::bulk_commit();
+      }
+    };
+    const float2 sc2 = make_float2(sl2, sl2);
     for (int it = 0; it < niter; ++it) {
-      const int q0 = (j0 + it) * kQ;
-      float* L2 = sLD + (it & 1) * 256;
-      {
-        const int q = q0 + t;
-        L2[t] = q < seq ? lse[(long long)bh * seq + q] * kLog2e : 0.f;
-        L2[128 + t] = q < seq ? Dv[(long long)bh * seq + q] : 0.f;
-      }
-      named_bar_sync(1, 128);
+      const int st = it & 1, q0 = (j0 + it) * kQ;
+      ATTN_TRACE(threadIdx.x == 0, it, 3);
+      ptx::mbar_wait(&qd_full[st], (it >> 1) & 1);  // -lse2 / -D rows of this tile
+      ATTN_TRACE(threadIdx.x == 0, it, 4);
       ptx::mbar_wait(s_full, it & 1);
+      ATTN_TRACE(threadIdx.x == 0, it, 5);
       ptx::tc_fence_after();
-      const bool edge = (CAUSAL && q0 < k0 + kKV - 1) || q0 + kQ > seq || k0 + kKV > seq;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t rs[32], rd[32];
-        ptx::tmem_ld32(trow + kSt + c * 32, rs);
-        ptx::tmem_ld32(trow + kDPt + c * 32, rd);
-        ptx::tmem_ld_wait();
+      uint32_t rs[2][32], rd[2][32];
+      ptx::tmem_ld32(trow + kSt + 64 * g, rs[0]);
+      ptx::tmem_ld32(trow + kSt + 64 * g + 32, rs[1]);
+      ptx::tmem_ld32(trow + kDPt + 64 * g, rd[0]);
+      ptx::tmem_ld32(trow + kDPt + 64 * g + 32, rd[1]);
+      ptx::tmem_ld_wait();
+      ATTN_TRACE(threadIdx.x == 0, it, 10);
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(st_free);
+      // masking only on diagonal / tail tiles (warp-uniform branch): the score of a
+      // query column outside [lo, hi) drops to -inf, so P = dS = 0 there
+      if ((CAUSAL && q0 < k0 + kKV - 1) || q0 + kQ > seq || k0 + kKV > seq) {
+        const int lo = key >= seq ? kQ : (CAUSAL ? key - q0 - 64 * g : -1), hi = seq - q0 - 64 * g;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          uint32_t pk[4], dk[4];
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            float pv[2], dsv[2];
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-              const int i = g * 8 + e * 2 + h2, ql = c * 32 + i, q = q0 + ql;
-              float p = ex2_approx(__uint_as_float(rs[i]) * sl2 - L2[ql]);
-              if (edge && (q >= seq || key >= seq || (CAUSAL && key > q))) p = 0.f;
-              pv[h2] = p;
-              dsv[h2] = p * (__uint_as_float(rd[i]) - L2[128 + ql]);
-            }
-            __nv_bfloat162 hp = __floats2bfloat162_rn(pv[0], pv[1]);
-            __nv_bfloat162 hd2 = __floats2bfloat162_rn(dsv[0], dsv[1]);
-            pk[e] = *reinterpret_cast<uint32_t*>(&hp);
-            dk[e] = *reinterpret_cast<uint32_t*>(&hd2);
-          }
-          const int k8 = c * 4 + g;
-          const int off = (k8 >> 3) * kTileBytes + t * 128 + (((k8 & 7) ^ (t & 7)) << 4);
-          *reinterpret_cast<uint4*>(sp + off) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          *reinterpret_cast<uint4*>(sds + off) = make_uint4(dk[0], dk[1], dk[2], dk[3]);
-        }
+          for (int i = 0; i < 32; ++i)
+            if (32 * h + i < lo || 32 * h + i >= hi) rs[h][i] = 0xff800000u;
       }
+      const float* L = sLD + st * 256 + 64 * g;
+      uint32_t pk[32], dk[32];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const int c = 32 * h + i;
+#ifdef CK_ATTN_EXPT_NOLDS
+          const float2 nl = make_float2(-3.f, -3.f), nd = make_float2(0.1f, 0.1f);
+#else
+          const float2 nl = *reinterpret_cast<const float2*>(L + c);
+          const float2 nd = *reinterpret_cast<const float2*>(L + 128 + c);
+#endif
+          const float2 x = ptx::fma2(make_float2(__uint_as_float(rs[h][i]), __uint_as_float(rs[h][i + 1])), sc2, nl);
+          const float2 p = (kBwdPolyEvery > 0 && (c >> 1) % (kBwdPolyEvery > 0 ? kBwdPolyEvery : 1) == kBwdPolyEvery - 1)
+                               ? ptx::ex2_poly2(x)
+                               : make_float2(ex2_approx(x.x), ex2_approx(x.y));
+          const float2 ds =
+              ptx::mul2(p, ptx::add2(make_float2(__uint_as_float(rd[h][i]), __uint_as_float(rd[h][i + 1])), nd));
+          __nv_bfloat162 hp = __floats2bfloat162_rn(p.x, p.y);
+          __nv_bfloat162 hs = __floats2bfloat162_rn(ds.x, ds.y);
+          pk[c >> 1] = *reinterpret_cast<uint32_t*>(&hp);
+          dk[c >> 1] = *reinterpret_cast<uint32_t*>(&hs);
+        }
+      ATTN_TRACE(threadIdx.x == 0, it, 11);
+      if (it > 0) {  // tile it-1's dV / dK / dQ MMAs have read the P^T / dS^T tiles
+        ptx::mbar_wait(mm_done, (it - 1) & 1);
+        ptx::tc_fence_after();
+      }
+      ATTN_TRACE(threadIdx.x == 0, it, 12);
+#pragma unroll
+      for (int k8 = 0; k8 < 8; ++k8) {  // 8 queries -> one 16-byte chunk of this WG's block
+        const int off = r * 128 + ((k8 ^ (r & 7)) << 4);
+        *reinterpret_cast<uint4*>(sp + off) = make_uint4(pk[4 * k8], pk[4 * k8 + 1], pk[4 * k8 + 2], pk[4 * k8 + 3]);
+        *reinterpret_cast<uint4*>(sds + off) = make_uint4(dk[4 * k8], dk[4 * k8 + 1], dk[4 * k8 + 2], dk[4 * k8 + 3]);
+      }
+      ATTN_TRACE(threadIdx.x == 0, it, 6);
       ptx::fence_proxy_async();
       ptx::tc_fence_before();
       ptx::mbar_arrive(ds_full);
-      // dQ of this query tile: thread t <-> query row q0 + t
-      ptx::mbar_wait(mm_done, it & 1);
-      ptx::tc_fence_after();
-      const int q = q0 + t;
+      if (it > 0) drain_dq(it - 1);
+      ATTN_TRACE(threadIdx.x == 0, it, 8);
+    }
+    ptx::mbar_wait(mm_done, (niter - 1) & 1);
+    ATTN_TRACE(threadIdx.x == 0, niter - 1, 7);
+    ptx::tc_fence_after();
+    drain_dq(niter - 1);
+    // dK (WG 0, scaled by 1/sqrt(d)) or dV (WG 1) for this key tile: thread <-> key row
+    {
+      const uint32_t base = g == 0 ? kDK : kDV;
+      const float sc = g == 0 ? 0.125f : 1.f;
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
-        uint32_t r[32];
-        ptx::tmem_ld32(trow + kDQ + c * 32, r);
+        uint32_t v[32];
+        ptx::tmem_ld32(trow + base + c * 32, v);
         ptx::tmem_ld_wait();
-        if (q < seq) {
-          float* acc = dq_acc + ((long long)row_base + q) * (H * kD) + hd * kD + c * 32;
+        if (key < seq) {
+          bf16* dst = dqkv + ((long long)row_base + key) * (3LL * H * kD) + (1 + g) * (long long)H * kD + hd * kD + c * 32;
 #pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            atomicAdd(reinterpret_cast<float4*>(acc + i),
-                      make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]), __uint_as_float(r[i + 2]),
-                                  __uint_as_float(r[i + 3])));
-        }
-      }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(dq_free);
-    }
-    // dK (scaled by 1/sqrt(d)) and dV for this key tile: thread t <-> key row k0 + t
-    if (niter > 0) {
-#pragma unroll 1
-      for (int part = 0; part < 2; ++part) {
-        const uint32_t base = part == 0 ? kDK : kDV;
-        const float sc = part == 0 ? 0.125f : 1.f;
-#pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
-          uint32_t r[32];
-          ptx::tmem_ld32(trow + base + c * 32, r);
-          ptx::tmem_ld_wait();
-          if (key < seq) {
-            bf16* dst = dqkv + ((long long)row_base + key) * (3LL * H * kD) + (part == 0 ? 1 : 2) * (long long)H * kD +
-                        hd * kD + c * 32;
+          for (int q8 = 0; q8 < 4; ++q8) {
+            uint32_t pk[4];
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              uint32_t pk[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                __nv_bfloat162 hb = __floats2bfloat162_rn(__uint_as_float(r[g * 8 + 2 * e]) * sc,
-                                                          __uint_as_float(r[g * 8 + 2 * e + 1]) * sc);
-                pk[e] = *reinterpret_cast<uint32_t*>(&hb);
-              }
-              *reinterpret_cast<uint4*>(dst + g * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 hb = __floats2bfloat162_rn(__uint_as_float(v[q8 * 8 + 2 * e]) * sc,
+                                                        __uint_as_float(v[q8 * 8 + 2 * e + 1]) * sc);
+              pk[e] = *reinterpret_cast<uint32_t*>(&hb);
             }
+            *reinterpret_cast<uint4*>(dst + q8 * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           }
         }
       }
     }
+    if (ct == 0) ptx::bulk_wait0();
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 9) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 512);
   }
+  ATTN_CTA(2);
 }
 
 }  // namespace
@@ -564,11 +661,11 @@ void attn_bwd_tc(const bf16* qkv, const bf16* out, const bf16* dout, const float
   float* D = scratch;
   float* dq = scratch + size_t(B) * H * seq;
   const int M = B * seq;
-  CK_CUDA(cudaMemsetAsync(dq, 0, size_t(M) * H * kD * sizeof(float), st));
-  attn_bwd_dot(out, dout, D, M, seq, H, st);
+  attn_bwd_dot(out, dout, D, M, seq, H, st, dq);  // + zeroes the dQ accumulator
   const long long ld = 3LL * H * kD;
   const CUtensorMap mq = cuda::make_map_2d_bf16(qkv, ld, (long long)M, ld, 64, 128);
   const CUtensorMap mo = cuda::make_map_2d_bf16(dout, (long long)H * kD, (long long)M, (long long)H * kD, 64, 128);
+  const CUtensorMap mdq = cuda::make_map_2d_f32(dq, (long long)H * kD, (long long)M, (long long)H * kD, 32, 128);
   static bool attr = false;
   if (!attr) {
     CK_CUDA(cudaFuncSetAttribute(k_attn_bwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem));
@@ -576,8 +673,8 @@ void attn_bwd_tc(const bf16* qkv, const bf16* out, const bf16* dout, const float
     attr = true;
   }
   const dim3 grid((seq + kKV - 1) / kKV * B * H);
-  if (causal) k_attn_bwd_tc<true><<<grid, 192, kBwdSmem, st>>>(mq, mo, lse, D, dq, dqkv, seq, H);
-  else k_attn_bwd_tc<false><<<grid, 192, kBwdSmem, st>>>(mq, mo, lse, D, dq, dqkv, seq, H);
+  if (causal) k_attn_bwd_tc<true><<<grid, kBwdThreads, kBwdSmem, st>>>(mq, mo, mdq, lse, D, dqkv, seq, H);
+  else k_attn_bwd_tc<false><<<grid, kBwdThreads, kBwdSmem, st>>>(mq, mo, mdq, lse, D, dqkv, seq, H);
   CK_CUDA(cudaGetLastError());
   attn_dq_out(dq, dqkv, M, H, st);
 }

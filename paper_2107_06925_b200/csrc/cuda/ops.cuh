@@ -54,7 +54,10 @@ size_t attn_bwd_scratch_floats(int B, int seq, int H);
 void attn_bwd_tc(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, bf16* dqkv,
                  float* scratch, int B, int seq, int H, bool causal, cudaStream_t st);
 // pieces shared by both backward implementations
-void attn_bwd_dot(const bf16* out, const bf16* dout, float* D, int M, int seq, int H, cudaStream_t st);
+// D = rowsum(dO * O) per (token, head); zeroes the fp32 dQ accumulator `dq_zero` if given
+void attn_bwd_dot(const bf16* out, const bf16* dout, float* D, int M, int seq, int H, cudaStream_t st,
+                  float* dq_zero = nullptr);
+// dq (scaled by 1/8) -> Q columns of dqkv
 void attn_dq_out(const float* dq, bf16* dqkv, int M, int H, cudaStream_t st);
 
 }  // namespace chimera::ops

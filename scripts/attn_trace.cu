@@ -12,6 +12,7 @@
 
 int main(int argc, char** argv) {
   const int B = argc > 1 ? atoi(argv[1]) : 4, seq = argc > 2 ? atoi(argv[2]) : 1024, H = argc > 3 ? atoi(argv[3]) : 16;
+  const bool bwd = argc > 4 && argv[4][0] == 'b';
   const size_t M = size_t(B) * seq;
   std::vector<__nv_bfloat16> h(M * 3 * H * 64);
   uint32_t x = 12345;
@@ -25,7 +26,18 @@ int main(int argc, char** argv) {
   cudaMalloc(&out, M * H * 64 * 2);
   cudaMalloc(&lse, M * H * 4);
   cudaMemcpy(qkv, h.data(), h.size() * 2, cudaMemcpyHostToDevice);
-  for (int i = 0; i < 5; ++i) chimera::ops::attn_fwd_tc(qkv, out, lse, B, seq, H, true, 0);
+  __nv_bfloat16 *dout, *dqkv;
+  float* scratch;
+  cudaMalloc(&dout, M * H * 64 * 2);
+  cudaMalloc(&dqkv, h.size() * 2);
+  cudaMalloc(&scratch, (M * H + M * H * 64) * 4);
+  cudaMemcpy(dout, h.data(), M * H * 64 * 2, cudaMemcpyHostToDevice);
+  auto run = [&] {
+    if (bwd) chimera::ops::attn_bwd_tc(qkv, out, dout, lse, dqkv, scratch, B, seq, H, true, 0);
+    else chimera::ops::attn_fwd_tc(qkv, out, lse, B, seq, H, true, 0);
+  };
+  chimera::ops::attn_fwd_tc(qkv, out, lse, B, seq, H, true, 0);
+  for (int i = 0; i < 5; ++i) run();
   cudaDeviceSynchronize();
   static long long tr[32][16], cta[4096][3];
   cudaMemcpyFromSymbol(tr, chimera::ops::g_attn_trace, sizeof(tr));
@@ -36,15 +48,20 @@ int main(int argc, char** argv) {
   printf("kernel span %.1f us, %d CTAs\n", (tend - tmin) / 1e3, ncta);
   printf("CTA0 sm %lld start +%.2f us dur %.2f us\n", cta[0][0], (t0 - tmin) / 1e3, (cta[0][2] - cta[0][1]) / 1e3);
   // per-tile stamps relative to kv_full of tile 0 (cycles)
-  const long long c0 = tr[0][1];
-  const char* names[] = {"tma:kv_empty", "mma:kv_full", "mma:s_free", "mma:p_full", "sm:wait_s",
-                         "sm:s_full",    "sm:ld_done",  "sm:max_done", "sm:o_done", "sm:p_done"};
+  const long long c0 = bwd ? tr[0][3] : tr[0][1];
+  const char* fnames[] = {"tma:kv_empty", "mma:kv_full", "mma:s_free", "mma:p_full", "sm:wait_s",
+                          "sm:s_full",    "sm:ld_done",  "sm:max_done", "sm:o_done", "sm:p_done"};
+  const char* bnames[] = {"mma:qd_full", "mma:ds_full", "mma:dq_free", "c:start", "c:lse_bar",
+                          "c:s_full",    "c:ds_done",   "c:mm_done",   "c:dq_done", "tma:qd_empty",
+                          "c:ld_done",   "c:math_done", "c:mm_wait"};
+  const char** names = bwd ? bnames : fnames;
   printf("%-4s", "j");
-  for (int e = 0; e < 10; ++e) printf(" %12s", names[e]);
+  const int nev = bwd ? 13 : 10;
+  for (int e = 0; e < nev; ++e) printf(" %12s", names[e]);
   printf("\n");
   for (int j = 0; j < 8; ++j) {
     printf("%-4d", j);
-    for (int e = 0; e < 10; ++e) printf(" %12lld", tr[j][e] ? tr[j][e] - c0 : -1);
+    for (int e = 0; e < nev; ++e) printf(" %12lld", tr[j][e] ? tr[j][e] - c0 : -1);
     printf("\n");
   }
   // tail: histogram of CTA end times
@@ -59,12 +76,12 @@ int main(int argc, char** argv) {
   printf("SM finish spread: first idle SM at %.1f us, last at %.1f us\n", (e_min - tmin) / 1e3, (e_max - tmin) / 1e3);
   double dur_sum = 0;
   for (int i = 0; i < ncta; ++i) dur_sum += cta[i][2] - cta[i][1];
-  printf("sum CTA durations / (148 SMs * 2) = %.1f us\n", dur_sum / 1e3 / 296);
+  printf("sum CTA durations / (148 SMs * %d) = %.1f us\n", bwd ? 1 : 2, dur_sum / 1e3 / (bwd ? 148 : 296));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  for (int i = 0; i < 50; ++i) chimera::ops::attn_fwd_tc(qkv, out, lse, B, seq, H, true, 0);
+  for (int i = 0; i < 50; ++i) run();
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0;
