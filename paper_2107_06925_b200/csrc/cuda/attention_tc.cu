@@ -324,27 +324,26 @@ __global__ void __launch_bounds__(192, 2)
 
 // ----------------------------------------------------------------- backward --
 // CTA = (128-key tile, batch*head); 10 warps, one CTA per SM (512 TMEM columns):
-//   warp 8   TMA producer: K, V once; per 128-query tile Q and dO into a 2-stage ring,
-//            and (all lanes) the tile's -lse*log2(e) and -D rows into smem
+//   warp 8   TMA producer: K, V once; per 128-query tile Q and dO into a 2-stage ring
 //   warp 9   TMEM allocator + single-thread MMA issuer
-//   warps 0-7  two compute warpgroups; WG g owns query columns [64g, 64g+64) of every
-//            tile; warp w reads TMEM lanes 32*(w%4).. (thread <-> key row)
+//   warps 0-7  two compute warpgroups; warp w reads TMEM lanes 32*(w%4).. (thread <->
+//            query row), WG g owns key columns [64g, 64g+64) of every tile, so the
+//            row's log-sum-exp and D are two per-thread scalars
 // Per query tile j:
-//   S^T  = K Q^T, dP^T = V dO^T     (M128 keys, N128 q, K64)  TMEM [0,128), [128,256);
-//     issued as soon as tile j-1's S^T / dP^T sit in registers (st_free)
-//   P^T = exp2(S^T c - lse2), dS^T = P^T (dP^T - D) -> bf16, 128-byte-swizzled K-major
-//     smem tiles (each WG writes its own 64-query block)
+//   S  = Q K^T, dP = dO V^T          (M128 q, N128 keys, K64)  TMEM [0,128), [128,256);
+//     issued as soon as tile j-1's S / dP sit in registers (st_free)
+//   P = exp2(S c - lse2), dS = P (dP - D) -> bf16, 128-byte-swizzled [q][key] smem tiles
+//     (each WG writes its own 64-key block)
 //   dV += P^T dO, dK += dS^T Q       (M128 keys, N64, K128 q)  TMEM [256,320), [320,384)
+//     -- P / dS read as MN-major A operands
 //   dQ_j = dS K                      (M128 q, N64, K128 keys)  TMEM [384 + 64 (j&1), ..)
-//     -- the dS^T tile read as an MN-major A operand; double-buffered so the MMA never
-//     waits for the drain
+//     double-buffered so the MMA never waits for the drain
 //   dQ_j is drained one tile later (underneath tile j+1's math) by the compute WGs, 32
 //   columns each, through a swizzled smem stage and one TMA bulk tensor reduce-add into
 //   the fp32 dQ accumulator -- no per-thread atomics.
 constexpr int kB_K = 0, kB_V = kTileBytes, kB_Q = 2 * kTileBytes, kB_DO = 4 * kTileBytes,
-              kB_P = 6 * kTileBytes, kB_DS = 8 * kTileBytes, kB_DQ = 10 * kTileBytes,  // dQ stage [WG][128][128 B]
-    kB_LD = 12 * kTileBytes;                                                           // [stage][-lse2 | -D][128]
-constexpr int kB_BAR = kB_LD + 4 * 128 * 4;
+              kB_P = 6 * kTileBytes, kB_DS = 8 * kTileBytes, kB_DQ = 10 * kTileBytes;  // dQ stage [WG][128][128 B]
+constexpr int kB_BAR = 12 * kTileBytes;
 constexpr int kBwdSmem = kB_BAR + 256;
 constexpr int kBwdThreads = 320;
 #ifndef CK_ATTN_BWD_POLY_EVERY
@@ -369,7 +368,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t *kv_full = bar, *qd_full = bar + 1, *qd_empty = bar + 3, *s_full = bar + 5, *st_free = bar + 6,
            *ds_full = bar + 7, *mm_done = bar + 8, *dq_free = bar + 9;  // dq_free[2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
-  float* sLD = reinterpret_cast<float*>(smem + kB_LD);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // 1-D grid, tile-major: key tile 0 sees every query tile under causal masking, so the
@@ -386,7 +384,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     ptx::tma_prefetch(&tdo);
     ptx::tma_prefetch(&tdq);
     ptx::mbar_init(kv_full, 1);
-    for (int s2 = 0; s2 < 2; ++s2) ptx::mbar_init(&qd_full[s2], 32), ptx::mbar_init(&qd_empty[s2], 1);
+    for (int s2 = 0; s2 < 2; ++s2) ptx::mbar_init(&qd_full[s2], 1), ptx::mbar_init(&qd_empty[s2], 1);
     ptx::mbar_init(s_full, 1);
     ptx::mbar_init(st_free, 256);
     ptx::mbar_init(ds_full, 256);
@@ -399,7 +397,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  constexpr uint32_t kSt = 0, kDPt = 128, kDV = 256, kDK = 320, kDQ = 384;
+  constexpr uint32_t kS = 0, kDP = 128, kDV = 256, kDK = 320, kDQ = 384;
 
   if (warp == 8) {
     if (lane == 0) {
@@ -407,43 +405,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       ptx::tma_load_2d(smem + kB_K, &tqkv, kv_full, H * kD + hd * kD, row_base + k0);
       ptx::tma_load_2d(smem + kB_V, &tqkv, kv_full, 2 * H * kD + hd * kD, row_base + k0);
     }
-    // the tile's lse / D rows are fetched into registers one tile ahead, so their global
-    // load latency hides under the wait for the ring slot
-    float lv[4], dv[4];
-    auto fetch = [&](int it) {
-      const int q0 = (j0 + it) * kQ;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int q = q0 + lane + 32 * k;
-        lv[k] = q < seq ? lse[(long long)bh * seq + q] : 0.f;
-        dv[k] = q < seq ? Dv[(long long)bh * seq + q] : 0.f;
-      }
-    };
-    fetch(0);
-    for (int it = 0; it < niter; ++it) {
-      const int st = it & 1, q0 = (j0 + it) * kQ;
-      if (lane == 0) ptx::mbar_wait_sleep(&qd_empty[st], ((it >> 1) & 1) ^ 1);
-      __syncwarp();
-      ATTN_TRACE(lane == 0, it, 9);
-      if (lane == 0) {
-        ptx::mbar_expect_tx(&qd_full[st], 2 * kTileBytes);
+    if (lane == 0) {
+      for (int it = 0; it < niter; ++it) {
+        const int st = it & 1, q0 = (j0 + it) * kQ;
+        ptx::mbar_wait_sleep(&qd_empty[st], ((it >> 1) & 1) ^ 1);
+        ATTN_TRACE(true, it, 9);
+        ptx::mbar_arrive_expect_tx(&qd_full[st], 2 * kTileBytes);
         ptx::tma_load_2d(smem + kB_Q + st * kTileBytes, &tqkv, &qd_full[st], hd * kD, row_base + q0);
         ptx::tma_load_2d(smem + kB_DO + st * kTileBytes, &tdo, &qd_full[st], hd * kD, row_base + q0);
       }
-      float* L = sLD + st * 256;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        L[lane + 32 * k] = -lv[k] * kLog2e;
-        L[128 + lane + 32 * k] = -dv[k];
-      }
-      ptx::mbar_arrive(&qd_full[st]);
-      if (it + 1 < niter) fetch(it + 1);
     }
   } else if (warp == 9) {
     if (lane == 0) {
       constexpr uint32_t id_s = ptx::idesc_bf16(128, 128, false, false);
-      constexpr uint32_t id_kv = ptx::idesc_bf16(128, 64, false, true);  // A K-major, B MN-major
-      constexpr uint32_t id_q = ptx::idesc_bf16(128, 64, true, true);    // A MN-major (dS^T^T), B MN-major
+      constexpr uint32_t id_kv = ptx::idesc_bf16(128, 64, true, true);  // A = P^T / dS^T (MN-major), B MN-major
+      constexpr uint32_t id_q = ptx::idesc_bf16(128, 64, false, true);  // A = dS (K-major), B = K (MN-major)
       const uint32_t sk = ptx::smem_u32(smem + kB_K), sv = ptx::smem_u32(smem + kB_V);
       const uint32_t sp = ptx::smem_u32(smem + kB_P), sds = ptx::smem_u32(smem + kB_DS);
       auto issue_s = [&](int it) {
@@ -455,10 +431,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ptx::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kD / 16; ++k) {
-          ptx::umma_f16(tmem + kSt, ptx::smem_desc_sw128(sk + k * 32, 16, 1024), ptx::smem_desc_sw128(sq + k * 32, 16, 1024),
+          ptx::umma_f16(tmem + kS, ptx::smem_desc_sw128(sq + k * 32, 16, 1024), ptx::smem_desc_sw128(sk + k * 32, 16, 1024),
                         id_s, k > 0);
-          ptx::umma_f16(tmem + kDPt, ptx::smem_desc_sw128(sv + k * 32, 16, 1024),
-                        ptx::smem_desc_sw128(sdo + k * 32, 16, 1024), id_s, k > 0);
+          ptx::umma_f16(tmem + kDP, ptx::smem_desc_sw128(sdo + k * 32, 16, 1024),
+                        ptx::smem_desc_sw128(sv + k * 32, 16, 1024), id_s, k > 0);
         }
         ptx::umma_commit(s_full);
       };
@@ -477,9 +453,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ATTN_TRACE(true, it, 1);
         ptx::tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < kQ / 16; ++k) {
-          const uint64_t a_p = ptx::smem_desc_sw128(sp + (k >> 2) * kTileBytes + (k & 3) * 32, 16, 1024);
-          const uint64_t a_ds = ptx::smem_desc_sw128(sds + (k >> 2) * kTileBytes + (k & 3) * 32, 16, 1024);
+        for (int k = 0; k < kQ / 16; ++k) {  // reduce over 16 queries per step
+          const uint64_t a_p = ptx::smem_desc_sw128(sp + k * 2048, kTileBytes, 1024);
+          const uint64_t a_ds = ptx::smem_desc_sw128(sds + k * 2048, kTileBytes, 1024);
           ptx::umma_f16(tmem + kDV, a_p, ptx::smem_desc_sw128(sdo + k * 2048, kTileBytes, 1024), id_kv,
                         (it > 0 || k > 0) ? 1u : 0u);
           ptx::umma_f16(tmem + kDK, a_ds, ptx::smem_desc_sw128(sq + k * 2048, kTileBytes, 1024), id_kv,
@@ -491,16 +467,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ptx::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kKV / 16; ++k)  // dQ = dS K: reduce over 16 keys per step
-          ptx::umma_f16(tmem + kDQ + 64 * st, ptx::smem_desc_sw128(sds + k * 2048, kTileBytes, 1024),
+          ptx::umma_f16(tmem + kDQ + 64 * st, ptx::smem_desc_sw128(sds + (k >> 2) * kTileBytes + (k & 3) * 32, 16, 1024),
                         ptx::smem_desc_sw128(sk + k * 2048, kTileBytes, 1024), id_q, k > 0);
         ptx::umma_commit(mm_done);
       }
     }
   } else {
-    const int g = warp >> 2;                 // compute warpgroup: query columns [64g, 64g+64)
-    const int r = (warp & 3) * 32 + lane;    // TMEM lane: key row (S^T, dP^T, dK, dV) / query row (dQ)
+    const int g = warp >> 2;                 // compute warpgroup: key columns [64g, 64g+64)
+    const int r = (warp & 3) * 32 + lane;    // TMEM lane: query row (S, dP, dQ) / key row (dK, dV)
     const int ct = threadIdx.x & 127;        // thread within the WG
-    const int key = k0 + r;
     const uint32_t trow = tmem + (uint32_t((warp & 3) * 32) << 16);
     const float sl2 = 0.125f * kLog2e;
     uint8_t* sp = smem + kB_P + g * kTileBytes;
@@ -527,66 +502,68 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ptx::bulk_commit();
       }
     };
+    // this row's -lse*log2(e) and -D, fetched one tile ahead
+    auto fetch = [&](int it, float& nl, float& nd) {
+      const int q = (j0 + it) * kQ + r;
+      nl = q < seq ? -lse[(long long)bh * seq + q] * kLog2e : 0.f;
+      nd = q < seq ? -Dv[(long long)bh * seq + q] : 0.f;
+    };
+    float nl, nd;
+    fetch(0, nl, nd);
     const float2 sc2 = make_float2(sl2, sl2);
     for (int it = 0; it < niter; ++it) {
-      const int st = it & 1, q0 = (j0 + it) * kQ;
+      const int q0 = (j0 + it) * kQ, q = q0 + r;
       ATTN_TRACE(threadIdx.x == 0, it, 3);
-      ptx::mbar_wait(&qd_full[st], (it >> 1) & 1);  // -lse2 / -D rows of this tile
-      ATTN_TRACE(threadIdx.x == 0, it, 4);
       ptx::mbar_wait(s_full, it & 1);
       ATTN_TRACE(threadIdx.x == 0, it, 5);
       ptx::tc_fence_after();
       uint32_t rs[2][32], rd[2][32];
-      ptx::tmem_ld32(trow + kSt + 64 * g, rs[0]);
-      ptx::tmem_ld32(trow + kSt + 64 * g + 32, rs[1]);
-      ptx::tmem_ld32(trow + kDPt + 64 * g, rd[0]);
-      ptx::tmem_ld32(trow + kDPt + 64 * g + 32, rd[1]);
+      ptx::tmem_ld32(trow + kS + 64 * g, rs[0]);
+      ptx::tmem_ld32(trow + kS + 64 * g + 32, rs[1]);
+      ptx::tmem_ld32(trow + kDP + 64 * g, rd[0]);
+      ptx::tmem_ld32(trow + kDP + 64 * g + 32, rd[1]);
       ptx::tmem_ld_wait();
       ATTN_TRACE(threadIdx.x == 0, it, 10);
       ptx::tc_fence_before();
       ptx::mbar_arrive(st_free);
-      // masking only on diagonal / tail tiles (warp-uniform branch): the score of a
-      // query column outside [lo, hi) drops to -inf, so P = dS = 0 there
-      if ((CAUSAL && q0 < k0 + kKV - 1) || q0 + kQ > seq || k0 + kKV > seq) {
-        const int lo = key >= seq ? kQ : (CAUSAL ? key - q0 - 64 * g : -1), hi = seq - q0 - 64 * g;
+      // masking only on diagonal / tail tiles (warp-uniform branch): keys of this WG's
+      // block at index >= hi drop to a -inf score (P = dS = 0); rows past seq drop out
+      if ((CAUSAL && k0 + kKV - 1 > q0) || q0 + kQ > seq || k0 + kKV > seq) {
+        const int kg = k0 + 64 * g;
+        const int hi = q >= seq ? 0 : min(CAUSAL ? q - kg + 1 : 64, seq - kg);
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
           for (int i = 0; i < 32; ++i)
-            if (32 * h + i < lo || 32 * h + i >= hi) rs[h][i] = 0xff800000u;
+            if (32 * h + i >= hi) rs[h][i] = 0xff800000u;
       }
-      const float* L = sLD + st * 256 + 64 * g;
+      const float2 nl2 = make_float2(nl, nl), nd2 = make_float2(nd, nd);
       uint32_t pk[32], dk[32];
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
           const int c = 32 * h + i;
-#ifdef CK_ATTN_EXPT_NOLDS
-          const float2 nl = make_float2(-3.f, -3.f), nd = make_float2(0.1f, 0.1f);
-#else
-          const float2 nl = *reinterpret_cast<const float2*>(L + c);
-          const float2 nd = *reinterpret_cast<const float2*>(L + 128 + c);
-#endif
-          const float2 x = ptx::fma2(make_float2(__uint_as_float(rs[h][i]), __uint_as_float(rs[h][i + 1])), sc2, nl);
+          const float2 x = ptx::fma2(make_float2(__uint_as_float(rs[h][i]), __uint_as_float(rs[h][i + 1])), sc2, nl2);
           const float2 p = (kBwdPolyEvery > 0 && (c >> 1) % (kBwdPolyEvery > 0 ? kBwdPolyEvery : 1) == kBwdPolyEvery - 1)
                                ? ptx::ex2_poly2(x)
                                : make_float2(ex2_approx(x.x), ex2_approx(x.y));
           const float2 ds =
-              ptx::mul2(p, ptx::add2(make_float2(__uint_as_float(rd[h][i]), __uint_as_float(rd[h][i + 1])), nd));
+              ptx::mul2(p, ptx::add2(make_float2(__uint_as_float(rd[h][i]), __uint_as_float(rd[h][i + 1])), nd2));
           __nv_bfloat162 hp = __floats2bfloat162_rn(p.x, p.y);
           __nv_bfloat162 hs = __floats2bfloat162_rn(ds.x, ds.y);
           pk[c >> 1] = *reinterpret_cast<uint32_t*>(&hp);
           dk[c >> 1] = *reinterpret_cast<uint32_t*>(&hs);
         }
+      if (it + 1 < niter) fetch(it + 1, nl, nd);
       ATTN_TRACE(threadIdx.x == 0, it, 11);
-      if (it > 0) {  // tile it-1's dV / dK / dQ MMAs have read the P^T / dS^T tiles
+      if (it > 0) {  // tile it-1's dV / dK / dQ MMAs have read the P / dS tiles
         ptx::mbar_wait(mm_done, (it - 1) & 1);
         ptx::tc_fence_after();
       }
       ATTN_TRACE(threadIdx.x == 0, it, 12);
 #pragma unroll
-      for (int k8 = 0; k8 < 8; ++k8) {  // 8 queries -> one 16-byte chunk of this WG's block
+      for (int k8 = 0; k8 < 8; ++k8) {  // 8 keys -> one 16-byte chunk of this WG's block
         const int off = r * 128 + ((k8 ^ (r & 7)) << 4);
         *reinterpret_cast<uint4*>(sp + off) = make_uint4(pk[4 * k8], pk[4 * k8 + 1], pk[4 * k8 + 2], pk[4 * k8 + 3]);
         *reinterpret_cast<uint4*>(sds + off) = make_uint4(dk[4 * k8], dk[4 * k8 + 1], dk[4 * k8 + 2], dk[4 * k8 + 3]);
@@ -602,7 +579,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     ATTN_TRACE(threadIdx.x == 0, niter - 1, 7);
     ptx::tc_fence_after();
     drain_dq(niter - 1);
-    // dK (WG 0, scaled by 1/sqrt(d)) or dV (WG 1) for this key tile: thread <-> key row
+    // dK (WG 0, scaled by 1/sqrt(d)) or dV (WG 1) for this key tile: TMEM lane <-> key row
     {
       const uint32_t base = g == 0 ? kDK : kDV;
       const float sc = g == 0 ? 0.125f : 1.f;
@@ -611,8 +588,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         uint32_t v[32];
         ptx::tmem_ld32(trow + base + c * 32, v);
         ptx::tmem_ld_wait();
-        if (key < seq) {
-          bf16* dst = dqkv + ((long long)row_base + key) * (3LL * H * kD) + (1 + g) * (long long)H * kD + hd * kD + c * 32;
+        if (k0 + r < seq) {
+          bf16* dst = dqkv + ((long long)row_base + k0 + r) * (3LL * H * kD) + (1 + g) * (long long)H * kD + hd * kD + c * 32;
 #pragma unroll
           for (int q8 = 0; q8 < 4; ++q8) {
             uint32_t pk[4];
