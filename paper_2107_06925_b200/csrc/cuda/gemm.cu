@@ -27,6 +27,19 @@
 
 namespace chimera::gemm {
 
+// clock64() stamps per tile of CTA 0 (scripts/gemm_trace.cu builds with CK_GEMM_TRACE)
+#ifdef CK_GEMM_TRACE
+__device__ long long g_gemm_trace[16][8];
+#define GEMM_TRACE(cond, t, ev)                                                  \
+  do {                                                                           \
+    if ((cond) && blockIdx.x == 0 && (t) < 16) g_gemm_trace[t][ev] = clock64(); \
+  } while (0)
+#else
+#define GEMM_TRACE(cond, t, ev) \
+  do {                          \
+  } while (0)
+#endif
+
 namespace {
 
 constexpr int BM = 128, BK = 64;
@@ -37,132 +50,179 @@ __device__ __forceinline__ float tanh_fast(float x) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ float gelu_tanh(float u) {
-  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  return 0.5f * u * (1.f + tanh_fast(k0 * (u + k1 * u * u * u)));
-}
-__device__ __forceinline__ float gelu_tanh_grad(float u) {
-  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  const float t = tanh_fast(k0 * (u + k1 * u * u * u));
-  return 0.5f * (1.f + t) + 0.5f * u * (1.f - t * t) * k0 * (1.f + 3.f * k1 * u * u);
-}
+// Epilogue of one 32-row x 32-column accumulator chunk by one warp.  The tcgen05.ld
+// 32x32b layout gives lane i row row0+i; the fp32 row is staged once through a padded
+// per-warp smem tile and read back in "store layout" (lane <-> 8 consecutive bf16 or 4
+// fp32 columns of one row), where bias / aux / accumulator operands -- prefetched into
+// registers before the accumulator is even ready (EpiPre) -- are combined and written
+// with fully coalesced 16-byte stores.
+constexpr int kStgStride = 36;                         // floats per staged row (32 + 4 pad: conflict-free)
+constexpr int kEpiWarpBytes = 32 * kStgStride * 4;     // 4608 B per epilogue warp
 
-// Epilogue of one 32-row x 32-column accumulator chunk by one warp.  Lane i owns row
-// row0+i in registers (the tcgen05.ld 32x32b layout); every global access goes through
-// a per-warp shared-memory tile so that 4 consecutive lanes cover one 64-byte (bf16) or
-// 128-byte (fp32) row segment -- fully coalesced, instead of 32 row-strided streams.
-constexpr int kEpiWarpBytes = 5120;  // per epilogue warp: staging tile (+ aux tile)
-constexpr int kStrideH = 80;         // bytes per staged bf16 row (64 + 16 pad: conflict-free)
-constexpr int kStrideF = 144;        // bytes per staged fp32 row (128 + 16 pad)
+struct EpiPre {
+  uint4 aux[4];   // bf16 aux rows (kBiasResid / kGeluBwd), store layout
+  float4 acc[8];  // fp32 output rows (kAccF32), store layout
+  uint4 bias;     // 8 bias values of this lane's columns
+};
+
+__device__ __forceinline__ float2 bf2f(uint32_t u) {
+  return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
+}
+__device__ __forceinline__ uint32_t f2bf(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
 
 template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(const EpiArgs& ep, int row0, int col0, int M, int N,
-                                               const uint32_t (&r)[32], uint8_t* stg, int lane,
-                                               bool atomic = false) {
-  float v[32];
+__device__ __forceinline__ void epilogue_prefetch(const EpiArgs& ep, int row0, int col0, int M, int N, int lane,
+                                                  bool atomic, EpiPre& pre) {
+  if constexpr (EPI == kAccF32) {
+    if (atomic) return;
+    const int col = col0 + (lane & 7) * 4;
+    const float* out = static_cast<const float*>(ep.out);
+    const bool vec = (N % 4) == 0 && (ep.ldo % 4) == 0 && col + 4 <= N;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-  const bool vec_ok = (N % 8) == 0;
-  if constexpr (EPI == kAccF32 || EPI == kStoreF32) {
-    float* row_s = reinterpret_cast<float*>(stg + lane * kStrideF);
-#pragma unroll
-    for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(row_s + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-    __syncwarp();
-    float* out = static_cast<float*>(ep.out);
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {  // 32 rows x 8 segments of 4 floats
-      const int idx = it * 32 + lane, rr = idx >> 3, sg = idx & 7;
-      const int row = row0 + rr, col = col0 + sg * 4;
-      if (row >= M || col >= N) continue;
-      const float4 x = *reinterpret_cast<const float4*>(stg + rr * kStrideF + sg * 16);
-      float* o = out + (long long)row * ep.ldo + col;
-      if (EPI == kAccF32 && atomic) {  // split-K partial sums
-        if (vec_ok && col + 4 <= N) {
-          atomicAdd(reinterpret_cast<float4*>(o), x);
-        } else {
-          const float xs[4] = {x.x, x.y, x.z, x.w};
-          for (int t = 0; t < 4 && col + t < N; ++t) atomicAdd(o + t, xs[t]);
-        }
-      } else if (vec_ok && col + 4 <= N) {
-        float4 y = x;
-        if constexpr (EPI == kAccF32) {
-          const float4 z = *reinterpret_cast<const float4*>(o);
-          y.x += z.x, y.y += z.y, y.z += z.z, y.w += z.w;
-        }
-        *reinterpret_cast<float4*>(o) = y;
+    for (int it = 0; it < 8; ++it) {
+      const int row = row0 + it * 4 + (lane >> 3);
+      pre.acc[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (row < M && vec) pre.acc[it] = *reinterpret_cast<const float4*>(out + (long long)row * ep.ldo + col);
+    }
+  } else if constexpr (EPI != kStoreF32) {
+    const int col = col0 + (lane & 3) * 8;
+    pre.bias = make_uint4(0, 0, 0, 0);
+    if (ep.bias && EPI != kGeluBwd) {
+      if ((N % 8) == 0 && col + 8 <= N) {
+        pre.bias = *reinterpret_cast<const uint4*>(ep.bias + col);
       } else {
-        const float xs[4] = {x.x, x.y, x.z, x.w};
-        for (int t = 0; t < 4 && col + t < N; ++t) o[t] = (EPI == kAccF32 ? o[t] : 0.f) + xs[t];
+        __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(&pre.bias);
+        for (int t = 0; t < 8 && col + t < N; ++t) h[t] = ep.bias[col + t];
       }
     }
-    __syncwarp();
-    return;
-  } else {
-    if (ep.bias && EPI != kGeluBwd) {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] += (col0 + j < N) ? __bfloat162float(ep.bias[col0 + j]) : 0.f;
-    }
     if constexpr (EPI == kBiasResid || EPI == kGeluBwd) {
-      uint8_t* aux_s = stg + 32 * kStrideH;  // second tile of the warp's staging area
+      const bool vec = (N % 8) == 0 && (ep.ld_aux % 8) == 0 && col + 8 <= N;
 #pragma unroll
-      for (int it = 0; it < 4; ++it) {  // 32 rows x 4 segments of 8 bf16, coalesced loads
-        const int idx = it * 32 + lane, rr = idx >> 2, sg = idx & 3;
-        const int row = row0 + rr, col = col0 + sg * 8;
+      for (int it = 0; it < 4; ++it) {
+        const int row = row0 + it * 8 + (lane >> 2);
         uint4 q = make_uint4(0, 0, 0, 0);
         if (row < M && col < N) {
           const __nv_bfloat16* a = ep.aux + (long long)row * ep.ld_aux + col;
-          if (vec_ok && col + 8 <= N) {
+          if (vec) {
             q = *reinterpret_cast<const uint4*>(a);
           } else {
             __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(&q);
             for (int t = 0; t < 8 && col + t < N; ++t) h[t] = a[t];
           }
         }
-        *reinterpret_cast<uint4*>(aux_s + rr * kStrideH + sg * 16) = q;
+        pre.aux[it] = q;
       }
-      __syncwarp();
-      const __nv_bfloat16* mine = reinterpret_cast<const __nv_bfloat16*>(aux_s + lane * kStrideH);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float x = __bfloat162float(mine[j]);
-        v[j] = EPI == kBiasResid ? v[j] + x : v[j] * gelu_tanh_grad(x);
-      }
-    }
-    constexpr int kOuts = EPI == kBiasGelu ? 2 : 1;
-#pragma unroll
-    for (int o = 0; o < kOuts; ++o) {
-      __nv_bfloat16* row_s = reinterpret_cast<__nv_bfloat16*>(stg + lane * kStrideH);
-#pragma unroll
-      for (int j = 0; j < 32; j += 8) {
-        uint4 q;
-        __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(&q);
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const __nv_bfloat16 u = __float2bfloat16_rn(v[j + t]);
-          h[t] = (o == 0) ? u : __float2bfloat16_rn(gelu_tanh(__bfloat162float(u)));
-        }
-        *reinterpret_cast<uint4*>(row_s + j) = q;
-      }
-      __syncwarp();
-      __nv_bfloat16* out = o == 0 ? static_cast<__nv_bfloat16*>(ep.out) : ep.out2;
-      const long long ld = o == 0 ? ep.ldo : ep.ld_out2;
-#pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        const int idx = it * 32 + lane, rr = idx >> 2, sg = idx & 3;
-        const int row = row0 + rr, col = col0 + sg * 8;
-        if (row >= M || col >= N) continue;
-        const uint4 q = *reinterpret_cast<const uint4*>(stg + rr * kStrideH + sg * 16);
-        __nv_bfloat16* dst = out + (long long)row * ld + col;
-        if (vec_ok && col + 8 <= N) {
-          *reinterpret_cast<uint4*>(dst) = q;
-        } else {
-          const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q);
-          for (int t = 0; t < 8 && col + t < N; ++t) dst[t] = h[t];
-        }
-      }
-      __syncwarp();
     }
   }
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(const EpiArgs& ep, int row0, int col0, int M, int N,
+                                               const uint32_t (&r)[32], uint8_t* stg_bytes, int lane, bool atomic,
+                                               const EpiPre& pre) {
+  float* stg = reinterpret_cast<float*>(stg_bytes);
+#pragma unroll
+  for (int j = 0; j < 32; j += 4)
+    *reinterpret_cast<uint4*>(stg + lane * kStgStride + j) = make_uint4(r[j], r[j + 1], r[j + 2], r[j + 3]);
+  __syncwarp();
+  if constexpr (EPI == kAccF32 || EPI == kStoreF32) {
+    float* out = static_cast<float*>(ep.out);
+    const int sg = lane & 7, col = col0 + sg * 4;
+    const bool vec = (N % 4) == 0 && (ep.ldo % 4) == 0 && col + 4 <= N;
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {  // 32 rows x 8 segments of 4 floats
+      const int rr = it * 4 + (lane >> 3), row = row0 + rr;
+      if (row >= M || col >= N) continue;
+      float4 x = *reinterpret_cast<const float4*>(stg + rr * kStgStride + sg * 4);
+      float* o = out + (long long)row * ep.ldo + col;
+      if (EPI == kAccF32 && atomic) {  // split-K partial sums
+        if (vec) {
+          atomicAdd(reinterpret_cast<float4*>(o), x);
+        } else {
+          const float xs[4] = {x.x, x.y, x.z, x.w};
+          for (int t = 0; t < 4 && col + t < N; ++t) atomicAdd(o + t, xs[t]);
+        }
+      } else if (vec) {
+        if constexpr (EPI == kAccF32) x.x += pre.acc[it].x, x.y += pre.acc[it].y, x.z += pre.acc[it].z, x.w += pre.acc[it].w;
+        *reinterpret_cast<float4*>(o) = x;
+      } else {
+        const float xs[4] = {x.x, x.y, x.z, x.w};
+        for (int t = 0; t < 4 && col + t < N; ++t) o[t] = (EPI == kAccF32 ? o[t] : 0.f) + xs[t];
+      }
+    }
+  } else {
+    const int sg = lane & 3, col = col0 + sg * 8;
+    const bool vec_o = (N % 8) == 0 && (ep.ldo % 8) == 0 && col + 8 <= N;
+    const bool vec_o2 = (N % 8) == 0 && (ep.ld_out2 % 8) == 0 && col + 8 <= N;
+    float2 bias[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) bias[e] = bf2f((&pre.bias.x)[e]);
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {  // 32 rows x 4 segments of 8 columns
+      const int rr = it * 8 + (lane >> 2), row = row0 + rr;
+      if (row >= M || col >= N) continue;
+      const float4 x0 = *reinterpret_cast<const float4*>(stg + rr * kStgStride + sg * 8);
+      const float4 x1 = *reinterpret_cast<const float4*>(stg + rr * kStgStride + sg * 8 + 4);
+      float2 v[4] = {make_float2(x0.x, x0.y), make_float2(x0.z, x0.w), make_float2(x1.x, x1.y), make_float2(x1.z, x1.w)};
+      if (EPI != kGeluBwd) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = ptx::add2(v[e], bias[e]);
+      }
+      if constexpr (EPI == kBiasResid) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = ptx::add2(v[e], bf2f((&pre.aux[it].x)[e]));
+      }
+      if constexpr (EPI == kGeluBwd) {  // v *= gelu_tanh'(u), u = aux
+        const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 u = bf2f((&pre.aux[it].x)[e]);
+          const float2 u2 = ptx::mul2(u, u);
+          const float2 z = ptx::mul2(u, ptx::fma2(u2, make_float2(k0 * k1, k0 * k1), make_float2(k0, k0)));
+          const float2 t = make_float2(tanh_fast(z.x), tanh_fast(z.y));
+          const float2 a = ptx::fma2(t, make_float2(0.5f, 0.5f), make_float2(0.5f, 0.5f));
+          const float2 om = ptx::fma2(make_float2(-t.x, -t.y), t, make_float2(1.f, 1.f));
+          const float2 c = ptx::fma2(u2, make_float2(3.f * k0 * k1, 3.f * k0 * k1), make_float2(k0, k0));
+          const float2 hb = ptx::mul2(ptx::mul2(u, make_float2(0.5f, 0.5f)), om);
+          v[e] = ptx::mul2(v[e], ptx::fma2(hb, c, a));
+        }
+      }
+      uint4 q;
+      q.x = f2bf(v[0].x, v[0].y), q.y = f2bf(v[1].x, v[1].y), q.z = f2bf(v[2].x, v[2].y), q.w = f2bf(v[3].x, v[3].y);
+      __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + col;
+      if (vec_o) {
+        *reinterpret_cast<uint4*>(dst) = q;
+      } else {
+        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q);
+        for (int t = 0; t < 8 && col + t < N; ++t) dst[t] = h[t];
+      }
+      if constexpr (EPI == kBiasGelu) {  // G = gelu_tanh(U) of the bf16-rounded U
+        const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+        uint4 g;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 u = bf2f((&q.x)[e]);
+          const float2 u2 = ptx::mul2(u, u);
+          const float2 z = ptx::mul2(u, ptx::fma2(u2, make_float2(k0 * k1, k0 * k1), make_float2(k0, k0)));
+          const float2 t = make_float2(tanh_fast(z.x), tanh_fast(z.y));
+          const float2 hu = ptx::mul2(u, make_float2(0.5f, 0.5f));
+          const float2 y = ptx::fma2(hu, t, hu);
+          (&g.x)[e] = f2bf(y.x, y.y);
+        }
+        __nv_bfloat16* dst2 = ep.out2 + (long long)row * ep.ld_out2 + col;
+        if (vec_o2) {
+          *reinterpret_cast<uint4*>(dst2) = g;
+        } else {
+          const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&g);
+          for (int t = 0; t < 8 && col + t < N; ++t) dst2[t] = h[t];
+        }
+      }
+    }
+  }
+  __syncwarp();
 }
 
 template <int BN>
@@ -279,13 +339,17 @@ __global__ void __launch_bounds__(256, 1)
       const int row0 = mb * BM + q * 32;
       const uint32_t t0 = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
       uint8_t* stg = smem + C::kStages * C::kStageBytes + 256 + q * kEpiWarpBytes;
+      EpiPre pre;
+      epilogue_prefetch<EPI>(ep, row0, nb * BN, M, N, lane, ksplit > 1, pre);
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
         ptx::tmem_ld32(t0 + c * 32, r);
-        ptx::tmem_ld_wait();
         const int col0 = nb * BN + c * 32;
-        if (row0 < M && col0 < N) epilogue_chunk<EPI>(ep, row0, col0, M, N, r, stg, lane, ksplit > 1);
+        EpiPre cur = pre;
+        if (c + 1 < BN / 32) epilogue_prefetch<EPI>(ep, row0, col0 + 32, M, N, lane, ksplit > 1, pre);
+        ptx::tmem_ld_wait();
+        if (row0 < M && col0 < N) epilogue_chunk<EPI>(ep, row0, col0, M, N, r, stg, lane, ksplit > 1, cur);
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -299,14 +363,24 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
-// Split-K for the fp32-accumulate (weight-gradient) epilogue: enough K slices to fill
-// the machine, each at least 8 K-blocks deep; slices combine with fp32 vector atomics.
+// Split-K for the fp32-accumulate (weight-gradient) epilogue when the output tiles alone
+// cannot fill the machine: the smallest slice count (each >= 8 K-blocks deep) whose
+// last wave is (nearly) as full as the best achievable; slices combine with fp32 vector
+// atomics.
 inline int split_k(int epi, int tiles, int slots, int K) {
   if (epi != kAccF32 || tiles >= slots) return 1;
   const int kb = (K + BK - 1) / BK;
-  int ks = (slots + tiles - 1) / tiles;
-  ks = ks < kb / 8 ? ks : kb / 8;
-  return ks < 1 ? 1 : ks;
+  // (more than 4 slices: the extra fp32 atomic traffic costs more than the wave it fills)
+  const int kmax = kb / 8 < 1 ? 1 : (kb / 8 > 4 ? 4 : kb / 8);
+  auto eff = [&](int ks) {
+    const long long u = (long long)tiles * ks, waves = (u + slots - 1) / slots;
+    return double(u) / double(waves * slots);
+  };
+  double best = 0.0;
+  for (int ks = 1; ks <= kmax; ++ks) best = eff(ks) > best ? eff(ks) : best;
+  for (int ks = 1; ks <= kmax; ++ks)
+    if (eff(ks) >= best - 0.03) return ks;
+  return 1;
 }
 
 // ---------------------------------------------------------- 2-SM variant ----
@@ -391,6 +465,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
       for (int tile = pair; tile < tiles; tile += npairs, ++it) {
         const int acc = it & 1;
         ptx::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        GEMM_TRACE(true, it, 0);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * 256;
         const int ks = tile / (num_m * num_n);
@@ -411,6 +486,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
           ptx::umma_commit_pair(&empty[stage]);
           if (++stage == kPairStages) stage = 0, phase ^= 1;
         }
+        GEMM_TRACE(true, it, 1);
         ptx::umma_commit_pair(&tfull[acc]);
       }
     }
@@ -420,7 +496,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
     for (int tile = pair; tile < tiles; tile += npairs, ++it) {
       const int acc = it & 1;
       const int mb = tile % num_m, nb = (tile / num_m) % num_n;
+      EpiPre pre;  // this tile's first-chunk operands are fetched while the MMAs run
+      epilogue_prefetch<EPI>(ep, mb * 256 + int(cta) * 128 + q * 32, nb * 256 + half * 128, M, N, lane, ksplit > 1,
+                             pre);
       ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      GEMM_TRACE(warp == 4 && lane == 0, it, 2);
+      GEMM_TRACE(warp == 11 && lane == 0, it, 4);
       ptx::tc_fence_after();
       const int row0 = mb * 256 + int(cta) * 128 + q * 32;
       const uint32_t t0 = tmem_base + (uint32_t(q * 32) << 16) + acc * 256;
@@ -429,12 +510,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
       for (int c = half * 4; c < half * 4 + 4; ++c) {
         uint32_t r[32];
         ptx::tmem_ld32(t0 + c * 32, r);
-        ptx::tmem_ld_wait();
         const int col0 = nb * 256 + c * 32;
-        if (row0 < M && col0 < N) epilogue_chunk<EPI>(ep, row0, col0, M, N, r, stg, lane, ksplit > 1);
+        EpiPre cur = pre;
+        if (c + 1 < half * 4 + 4) epilogue_prefetch<EPI>(ep, row0, col0 + 32, M, N, lane, ksplit > 1, pre);
+        ptx::tmem_ld_wait();
+        if (row0 < M && col0 < N) epilogue_chunk<EPI>(ep, row0, col0, M, N, r, stg, lane, ksplit > 1, cur);
       }
       ptx::tc_fence_before();
       __syncwarp();
+      GEMM_TRACE(warp == 4 && lane == 0, it, 3);
+      GEMM_TRACE(warp == 11 && lane == 0, it, 5);
       if (lane == 0) ptx::mbar_arrive_leader(&tempty[acc]);
     }
   }
