@@ -73,6 +73,21 @@ __device__ __forceinline__ uint32_t f2bf(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// Output-tile order of the persistent loop: the tile index runs fastest over the
+// dimension with fewer tiles, so one wave covers few blocks of the long operand, each
+// shared by concurrently running tiles (read from HBM once) while the short operand
+// stays L2-resident -- e.g. the LM-head weight gradient (50304 x 1024, K = tokens)
+// would otherwise stream its 400 MB dlogits operand once per 256-column block.
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
+  if (num_n <= num_m) {
+    nb = tile % num_n;
+    mb = (tile / num_n) % num_m;
+  } else {
+    mb = tile % num_m;
+    nb = (tile / num_m) % num_n;
+  }
+}
+
 template <int EPI>
 __device__ __forceinline__ void epilogue_prefetch(const EpiArgs& ep, int row0, int col0, int M, int N, int lane,
                                                   bool atomic, EpiPre& pre) {
@@ -271,7 +286,9 @@ __global__ void __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int mb = tile % num_m, nb = (tile / num_m) % num_n, ks = tile / (num_m * num_n);
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, mb, nb);
+        const int ks = tile / (num_m * num_n);
         const int kb1 = min(num_kb, (ks + 1) * kb_per);
         for (int kb = ks * kb_per; kb < kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
@@ -333,7 +350,8 @@ __global__ void __launch_bounds__(256, 1)
     int it = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
       const int acc = it & 1;
-      const int mb = tile % num_m, nb = (tile / num_m) % num_n;
+      int mb, nb;
+      tile_coords(tile, num_m, num_n, mb, nb);
       ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
       ptx::tc_fence_after();
       const int row0 = mb * BM + q * 32;
@@ -432,7 +450,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = pair; tile < tiles; tile += npairs) {
-        const int mb = tile % num_m, nb = (tile / num_m) % num_n, ks = tile / (num_m * num_n);
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, mb, nb);
+        const int ks = tile / (num_m * num_n);
         const int m0 = mb * 256 + int(cta) * 128, n0 = nb * 256 + int(cta) * 128;
         const int kb1 = min(num_kb, (ks + 1) * kb_per);
         for (int kb = ks * kb_per; kb < kb1; ++kb) {
@@ -495,7 +515,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
     int it = 0;
     for (int tile = pair; tile < tiles; tile += npairs, ++it) {
       const int acc = it & 1;
-      const int mb = tile % num_m, nb = (tile / num_m) % num_n;
+      int mb, nb;
+      tile_coords(tile, num_m, num_n, mb, nb);
       EpiPre pre;  // this tile's first-chunk operands are fetched while the MMAs run
       epilogue_prefetch<EPI>(ep, mb * 256 + int(cta) * 128 + q * 32, nb * 256 + half * 128, M, N, lane, ksplit > 1,
                              pre);
