@@ -16,8 +16,7 @@ using cuda::ceil_div;
 
 struct Vec8 {  // 8 bf16 <-> 8 fp32
   float f[8];
-  __device__ __forceinline__ void load(const bf16* p) {
-    const uint4 q = *reinterpret_cast<const uint4*>(p);
+  __device__ __forceinline__ void set(const uint4& q) {
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
@@ -25,6 +24,7 @@ struct Vec8 {  // 8 bf16 <-> 8 fp32
       f[2 * t] = v.x, f[2 * t + 1] = v.y;
     }
   }
+  __device__ __forceinline__ void load(const bf16* p) { set(*reinterpret_cast<const uint4*>(p)); }
   __device__ __forceinline__ void store(bf16* p) const {
     uint4 q;
     __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
@@ -92,24 +92,44 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const bf16* __restrict__ dy, con
 #pragma unroll
     for (int t = 0; t < 8; ++t) acc_g[c][t] = acc_b[c][t] = 0.f;
   }
-  for (int row = blockIdx.x * 8 + warp; row < M; row += gridDim.x * 8) {
-    const float mu = mean[row], rs = rstd[row];
-    Vec8 dv[VPL], xv[VPL];
+  // rows are software-pipelined: the next row's dy / x / dres / statistics are in flight
+  // (raw 16-byte vectors) while the current one is reduced and written
+  const int stride = gridDim.x * 8;
+  uint4 nd[VPL], nx[VPL], nr[VPL];
+  float nmu = 0.f, nrs = 0.f;
+  auto fetch = [&](int r) {
+#pragma unroll
+    for (int c = 0; c < VPL; ++c) {
+      const long long off = (long long)r * h + (c * 32 + lane) * 8;
+      nd[c] = *reinterpret_cast<const uint4*>(dy + off);
+      nx[c] = *reinterpret_cast<const uint4*>(x + off);
+      nr[c] = dres ? *reinterpret_cast<const uint4*>(dres + off) : make_uint4(0, 0, 0, 0);
+    }
+    nmu = mean[r];
+    nrs = rstd[r];
+  };
+  int row = blockIdx.x * 8 + warp;
+  if (row < M) fetch(row);
+  for (; row < M; row += stride) {
+    const float mu = nmu, rs = nrs;
+    uint4 cd[VPL], cx[VPL], cr[VPL];  // current row, raw (converted per chunk, twice)
+#pragma unroll
+    for (int c = 0; c < VPL; ++c) cd[c] = nd[c], cx[c] = nx[c], cr[c] = nr[c];
+    if (row + stride < M) fetch(row + stride);
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int c = 0; c < VPL; ++c) {
-      const int col = (c * 32 + lane) * 8;
-      dv[c].load(dy + (long long)row * h + col);
-      xv[c].load(x + (long long)row * h + col);
+      Vec8 dv, xv;
+      dv.set(cd[c]);
+      xv.set(cx[c]);
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
-        const float xh = (xv[c].f[t] - mu) * rs;
-        const float gg = dv[c].f[t] * gam[c].f[t];
+        const float xh = (xv.f[t] - mu) * rs;
+        const float gg = dv.f[t] * gam[c].f[t];
         s1 += gg;
         s2 += gg * xh;
-        acc_g[c][t] += dv[c].f[t] * xh;
-        acc_b[c][t] += dv[c].f[t];
-        xv[c].f[t] = xh;
+        acc_g[c][t] += dv.f[t] * xh;
+        acc_b[c][t] += dv.f[t];
       }
     }
     s1 = cuda::warp_sum(s1) * (1.f / h);
@@ -117,11 +137,13 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const bf16* __restrict__ dy, con
 #pragma unroll
     for (int c = 0; c < VPL; ++c) {
       const int col = (c * 32 + lane) * 8;
-      Vec8 r, o;
-      if (dres) r.load(dres + (long long)row * h + col);
+      Vec8 dv, xv, rv, o;
+      dv.set(cd[c]);
+      xv.set(cx[c]);
+      rv.set(cr[c]);
 #pragma unroll
       for (int t = 0; t < 8; ++t)
-        o.f[t] = rs * (dv[c].f[t] * gam[c].f[t] - s1 - xv[c].f[t] * s2) + (dres ? r.f[t] : 0.f);
+        o.f[t] = rs * (dv.f[t] * gam[c].f[t] - s1 - (xv.f[t] - mu) * rs * s2) + rv.f[t];
       o.store(dx + (long long)row * h + col);
     }
   }
@@ -309,7 +331,7 @@ void layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* 
 void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* g,
                    const bf16* dres, bf16* dx, float* dgamma, float* dbeta, int M, int h,
                    cudaStream_t st) {
-  const int grid = std::min(ceil_div(M, 8), 2 * cuda::kNumSMs);
+  const int grid = std::min(ceil_div(M, 8), cuda::kNumSMs);  // one 8-warp CTA per SM (255 registers)
   const size_t smem = size_t(16) * h * sizeof(float);
   switch (h) {
 #define CK_LN(V)                                                                                   \
