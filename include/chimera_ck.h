@@ -151,6 +151,16 @@ CK_API int ck_gpt_step(ck_gpt* h, float* loss);
  * stream: JSON {iteration_ms, tasks:[{rank, kind, pipeline, micro, stage, start_ms,
  * end_ms}]} relative to the iteration start on this process. */
 CK_API int ck_gpt_profile_step(ck_gpt* h, char** out_json);
+/* Engine-style driving of one iteration (replaces oracle::Engine's loop,
+ * proj/src/oracle.cpp:304-356): begin, then one call per task of the schedule in a
+ * dependency-respecting order -- task = int32[6] {kind, pipeline_id, micro_batch, stage,
+ * worker, replica_group} (pipesim::Task field order, core.hpp:57-64), run for every
+ * local replica -- then end (gradient sync + SGD, *loss = mean token loss).  A task
+ * whose input activation / gradient was not produced yet returns 3 (the reference's
+ * MissingActivationError) with nothing enqueued; foreign or repeated tasks return 2. */
+CK_API int ck_gpt_begin_iteration(ck_gpt* h);
+CK_API int ck_gpt_run_task(ck_gpt* h, const int32_t* task);
+CK_API int ck_gpt_end_iteration(ck_gpt* h, float* loss);
 /* enqueue one iteration on the trainer stream without waiting (graph replay). */
 CK_API int ck_gpt_launch(ck_gpt* h);
 CK_API int ck_gpt_set_graph(ck_gpt* h, int on);

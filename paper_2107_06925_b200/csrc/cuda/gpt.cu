@@ -27,6 +27,7 @@
 #include <map>
 #include <memory>
 #include <numeric>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -168,6 +169,15 @@ struct Trainer::Impl {
   }
   int steps = 0;
   long long launches_per_step = 0;
+  // issue state of the open iteration (begin_iteration .. end_iteration)
+  struct IterState {
+    bool open = false;
+    std::map<int, int> bwd_left;                       // stage -> local backwards not yet issued
+    std::map<int, int> copy_done;                      // stage -> local copies fully issued
+    std::map<std::array<int, 2>, int> copy_bwd_left;   // (rank, pipeline) -> backwards left
+    std::set<std::array<int, 4>> issued;               // (kind, pipeline, micro, stage)
+    size_t next_coll = 0;
+  } it;
 
   bool local(int rank) const { return rank >= first && rank < first + nlocal; }
   cudaStream_t stream_of(int rank) const { return streams[rank - first]; }
@@ -671,8 +681,13 @@ void sync_stage(Trainer::Impl& I, int s) {
 
 }  // namespace
 
-void Trainer::issue_iteration() {
+// Iteration issue, split Engine-style (oracle.cpp:304-356): begin, one call per task in
+// replay order (every local replica of it, like the reference's loop over r), end.
+// issue_iteration() drives it from the schedule's replay order; the C-ABI exposes the
+// same three calls so a host scheduler can drive the GPU task by task.
+void Trainer::begin_iteration() {
   Impl& I = *d_;
+  if (I.it.open) throw pipesim::InvalidConfigError("iteration already open");
   if (I.coll_order.empty()) plan_sync(I);
   I.launches_per_step = 0;
   I.slot_of.clear();
@@ -685,64 +700,114 @@ void Trainer::issue_iteration() {
   CK_CUDA(cudaEventRecord(I.start_ev, I.main_stream));
   for (auto s : I.streams) CK_CUDA(cudaStreamWaitEvent(s, I.start_ev, 0));
   CK_CUDA(cudaStreamWaitEvent(I.comm_stream, I.start_ev, 0));
-  std::map<int, int> bwd_left = I.bwd_total;
-  std::map<int, int> copy_done;  // stage -> local copies whose last backward was issued
-  std::map<std::array<int, 2>, int> copy_bwd_left;  // (rank, pipeline) -> backwards left
+  Impl::IterState& S = I.it;
+  S = Impl::IterState{};
+  S.open = true;
+  S.bwd_left = I.bwd_total;
   for (const auto& [w, i] : I.order) {
     const Task& t = I.sched.per_worker[w][i];
     if (t.kind != TaskKind::Backward) continue;
     for (int r = 0; r < I.W; ++r)
-      if (I.local(r * I.D + w)) copy_bwd_left[{r * I.D + w, t.pipeline_id}]++;
+      if (I.local(r * I.D + w)) S.copy_bwd_left[{r * I.D + w, t.pipeline_id}]++;
   }
-  size_t next_coll = 0;
-  auto drain = [&](bool at_end) {
-    while (next_coll < I.coll_order.size()) {
-      const int s = I.coll_order[next_coll];
-      if (!I.stages.count(s) && !I.stage_comm.count(s)) {  // not held here
-        ++next_coll;
-        continue;
-      }
-      const bool ready = bwd_left[s] == 0;
-      if (!ready || (!I.stage_eager[s] && !at_end)) break;
-      sync_stage(I, s);
-      ++next_coll;
+}
+
+// Launch the stage collectives that became ready, in the global order (drain).
+static void drain_collectives(Trainer::Impl& I, bool at_end) {
+  Trainer::Impl::IterState& S = I.it;
+  while (S.next_coll < I.coll_order.size()) {
+    const int s = I.coll_order[S.next_coll];
+    if (!I.stages.count(s) && !I.stage_comm.count(s)) {  // not held here
+      ++S.next_coll;
+      continue;
     }
-  };
-  for (const auto& [w, i] : I.order) {
-    const Task& t = I.sched.per_worker[w][i];
-    if (t.kind != TaskKind::Forward && t.kind != TaskKind::Backward) continue;
-    for (int r = 0; r < I.W; ++r) {
-      const int rank = r * I.D + w;
-      if (!I.local(rank)) continue;
-      Impl::TaskSpan sp{rank, int(t.kind), t.pipeline_id, t.micro_batch, t.stage, nullptr, nullptr};
-      if (I.profiling) {
-        sp.a = I.timed_event();
-        CK_CUDA(cudaEventRecord(sp.a, I.stream_of(rank)));
+    const bool ready = S.bwd_left[s] == 0;
+    if (!ready || (!I.stage_eager[s] && !at_end)) break;
+    sync_stage(I, s);
+    ++S.next_coll;
+  }
+}
+
+void Trainer::run_task(const pipesim::Task& t) {
+  Impl& I = *d_;
+  Impl::IterState& S = I.it;
+  if (!S.open) throw pipesim::InvalidConfigError("run_task outside begin_iteration / end_iteration");
+  if (t.kind != TaskKind::Forward && t.kind != TaskKind::Backward) return;
+  if (t.worker < 0 || t.worker >= I.D || t.stage < 0 || t.stage >= I.D || t.pipeline_id < 0 ||
+      t.micro_batch < 0 || t.micro_batch >= I.N || I.worker_of.count({t.pipeline_id, t.stage}) == 0 ||
+      I.worker_of.at({t.pipeline_id, t.stage}) != t.worker)
+    throw pipesim::InvalidConfigError("task does not belong to this schedule");
+  // the reference Engine's stash discipline (oracle.cpp:202-280): a forward needs the
+  // previous stage's output, a backward its own forward's stash and the next stage's
+  // gradient -- otherwise MissingActivationError, here before anything is enqueued
+  const bool fwd = t.kind == TaskKind::Forward;
+  const std::array<int, 4> self{fwd ? 0 : 1, t.pipeline_id, t.micro_batch, t.stage};
+  if (S.issued.count(self)) throw pipesim::InvalidConfigError("task issued twice in one iteration");
+  const bool ok = fwd ? (t.stage == 0 || S.issued.count({0, t.pipeline_id, t.micro_batch, t.stage - 1}))
+                      : (S.issued.count({0, t.pipeline_id, t.micro_batch, t.stage}) &&
+                         (t.stage == I.D - 1 || S.issued.count({1, t.pipeline_id, t.micro_batch, t.stage + 1})));
+  if (!ok) throw MissingActivation("no stashed activation for (pipeline " + std::to_string(t.pipeline_id) +
+                                   ", micro " + std::to_string(t.micro_batch) + ", stage " +
+                                   std::to_string(t.stage) + ")");
+  S.issued.insert(self);
+  for (int r = 0; r < I.W; ++r) {
+    const int rank = r * I.D + t.worker;
+    if (!I.local(rank)) continue;
+    Impl::TaskSpan sp{rank, int(t.kind), t.pipeline_id, t.micro_batch, t.stage, nullptr, nullptr};
+    if (I.profiling) {
+      sp.a = I.timed_event();
+      CK_CUDA(cudaEventRecord(sp.a, I.stream_of(rank)));
+    }
+    if (fwd) forward_task(rank, t.pipeline_id, t.micro_batch, t.stage);
+    else backward_task(rank, t.pipeline_id, t.micro_batch, t.stage);
+    if (I.profiling) {
+      sp.b = I.timed_event();
+      CK_CUDA(cudaEventRecord(sp.b, I.stream_of(rank)));
+      I.spans.push_back(sp);
+    }
+    if (!fwd) {
+      if (--S.copy_bwd_left[{rank, t.pipeline_id}] == 0) {
+        const int c = S.copy_done[t.stage]++;
+        CK_CUDA(cudaEventRecord(I.stage_done_ev.at(t.stage).at(c), I.stream_of(rank)));
       }
-      if (t.kind == TaskKind::Forward) forward_task(rank, t.pipeline_id, t.micro_batch, t.stage);
-      else backward_task(rank, t.pipeline_id, t.micro_batch, t.stage);
-      if (I.profiling) {
-        sp.b = I.timed_event();
-        CK_CUDA(cudaEventRecord(sp.b, I.stream_of(rank)));
-        I.spans.push_back(sp);
-      }
-      if (t.kind == TaskKind::Backward) {
-        if (--copy_bwd_left[{rank, t.pipeline_id}] == 0) {
-          const int c = copy_done[t.stage]++;
-          CK_CUDA(cudaEventRecord(I.stage_done_ev.at(t.stage).at(c), I.stream_of(rank)));
-        }
-        if (--bwd_left[t.stage] == 0) drain(false);
-      }
+      if (--S.bwd_left[t.stage] == 0) drain_collectives(I, false);
     }
   }
-  drain(true);  // end-of-iteration collectives, still in the global order
-  if (next_coll != I.coll_order.size()) throw capi::InternalError("gradient sync incomplete");
+}
+
+void Trainer::end_iteration() {
+  Impl& I = *d_;
+  Impl::IterState& S = I.it;
+  if (!S.open) throw pipesim::InvalidConfigError("end_iteration without begin_iteration");
+  S.open = false;
+  for (const auto& kv : S.bwd_left)
+    if (kv.second != 0)
+      throw pipesim::InvalidConfigError("iteration ended with backward tasks of stage " + std::to_string(kv.first) +
+                                        " not issued");
+  drain_collectives(I, true);  // end-of-iteration collectives, still in the global order
+  if (S.next_coll != I.coll_order.size()) throw capi::InternalError("gradient sync incomplete");
   for (int k = 0; k < I.nlocal; ++k) {
     CK_CUDA(cudaEventRecord(I.rank_done[k], I.streams[k]));
     CK_CUDA(cudaStreamWaitEvent(I.main_stream, I.rank_done[k], 0));
   }
   CK_CUDA(cudaEventRecord(I.upd_ev, I.comm_stream));
   CK_CUDA(cudaStreamWaitEvent(I.main_stream, I.upd_ev, 0));
+}
+
+void Trainer::issue_iteration() {
+  Impl& I = *d_;
+  begin_iteration();
+  for (const auto& [w, i] : I.order) run_task(I.sched.per_worker[w][i]);
+  end_iteration();
+}
+
+float Trainer::finish_step() {
+  Impl& I = *d_;
+  ++I.steps;
+  float loss = 0;
+  CK_CUDA(cudaMemcpyAsync(&loss, I.loss, sizeof(float), cudaMemcpyDeviceToHost, I.main_stream));
+  CK_CUDA(cudaStreamSynchronize(I.main_stream));
+  return loss;
 }
 
 void Trainer::set_sync_policy(int policy) {
@@ -773,11 +838,7 @@ float Trainer::step() {
     }
     CK_CUDA(cudaGraphLaunch(I.graph_exec, I.main_stream));
   }
-  ++I.steps;
-  float loss = 0;
-  CK_CUDA(cudaMemcpyAsync(&loss, I.loss, sizeof(float), cudaMemcpyDeviceToHost, I.main_stream));
-  CK_CUDA(cudaStreamSynchronize(I.main_stream));
-  return loss;
+  return finish_step();
 }
 
 std::string Trainer::profile_step() {
@@ -835,6 +896,7 @@ void Trainer::launch_async() {
 }
 
 void* Trainer::stream() const { return d_->main_stream; }
+bool Trainer::connected() const { return d_->connected; }
 void Trainer::set_use_graph(bool on) { d_->use_graph = on; }
 
 void Trainer::upload_batch(const int32_t* tokens, const int32_t* labels, bool from_host, void* stream) {
@@ -1053,6 +1115,34 @@ CK_API int ck_gpt_step(ck_gpt* h, float* loss) {
 
 CK_API int ck_gpt_profile_step(ck_gpt* h, char** out_json) {
   return chimera::capi::guarded([&] { *out_json = chimera::capi::dup_string(h->t->profile_step()); });
+}
+
+CK_API int ck_gpt_begin_iteration(ck_gpt* h) {
+  return chimera::capi::guarded([&] {
+    if (!h->t->connected()) throw chimera::capi::InternalError("multi-process trainer: call connect() first");
+    h->t->begin_iteration();
+  });
+}
+
+CK_API int ck_gpt_run_task(ck_gpt* h, const int32_t* task) {
+  return chimera::capi::guarded([&] {
+    if (!task) throw pipesim::InvalidConfigError("null task");
+    if (task[0] < 0 || task[0] > int(pipesim::TaskKind::AllReduceStart))
+      throw pipesim::InvalidConfigError("bad task kind");
+    pipesim::Task t;
+    t.kind = static_cast<pipesim::TaskKind>(task[0]);
+    t.pipeline_id = task[1], t.micro_batch = task[2], t.stage = task[3], t.worker = task[4];
+    t.replica_group = task[5];
+    h->t->run_task(t);
+  });
+}
+
+CK_API int ck_gpt_end_iteration(ck_gpt* h, float* loss) {
+  return chimera::capi::guarded([&] {
+    h->t->end_iteration();
+    const float l = h->t->finish_step();
+    if (loss) *loss = l;
+  });
 }
 
 CK_API int ck_gpt_launch(ck_gpt* h) {

@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <stdexcept>
 #include <string>
 
 #include <cuda_bf16.h>
@@ -13,6 +14,11 @@
 namespace chimera::gpt {
 
 struct Stash;
+
+// oracle::MissingActivationError analogue (status 3 at the C-ABI)
+struct MissingActivation : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 
 class Trainer {
  public:
@@ -34,6 +40,14 @@ class Trainer {
   // handles of all processes (ordered by process index) and an NCCL unique id.
   std::string ipc_export() const;
   void connect(const std::string& all_handles, const std::string& nccl_id);
+  // Engine-style driving (oracle.cpp:304-356): begin, run_task for every task in a
+  // dependency-respecting order (each covers all local replicas), end -> loss.
+  // Out-of-order tasks throw MissingActivation before anything is enqueued.
+  void begin_iteration();
+  void run_task(const pipesim::Task& t);
+  void end_iteration();
+  float finish_step();  // wait for the iteration, ++steps, return the loss
+  bool connected() const;
 
  public:
   struct Impl;

@@ -38,6 +38,9 @@ _lib.register("ck_gpt_get_params", C.c_int, [_vp, C.c_int, _lib._fp])
 _lib.register("ck_gpt_set_batch", C.c_int, [_vp, _vp, _vp, C.c_int])
 _lib.register("ck_gpt_step", C.c_int, [_vp, C.POINTER(C.c_float)])
 _lib.register("ck_gpt_launch", C.c_int, [_vp])
+_lib.register("ck_gpt_begin_iteration", C.c_int, [_vp])
+_lib.register("ck_gpt_run_task", C.c_int, [_vp, C.POINTER(C.c_int32)])
+_lib.register("ck_gpt_end_iteration", C.c_int, [_vp, C.POINTER(C.c_float)])
 _lib.register("ck_gpt_profile_step", C.c_int, [_vp, C.POINTER(_vp)])
 _lib.register("ck_gpt_set_graph", C.c_int, [_vp, C.c_int])
 _lib.register("ck_gpt_set_sync_policy", C.c_int, [_vp, C.c_int])
@@ -203,6 +206,29 @@ class Trainer:
         loss = C.c_float()
         check(lib().ck_gpt_step(self._h, C.byref(loss)))
         return loss.value
+
+    # Engine-style driving (reference oracle.cpp:304-356): the host walks the schedule.
+    def begin_iteration(self):
+        check(lib().ck_gpt_begin_iteration(self._h))
+
+    def run_task(self, task):
+        """task = (kind, pipeline_id, micro_batch, stage, worker, replica_group) as in
+        pipesim::Task (kind 0 Forward, 1 Backward); runs every local replica of it.
+        Raises CKError (status 3) if its input activation / gradient is missing."""
+        arr = (C.c_int32 * 6)(*[int(x) for x in task])
+        check(lib().ck_gpt_run_task(self._h, arr))
+
+    def end_iteration(self) -> float:
+        loss = C.c_float()
+        check(lib().ck_gpt_end_iteration(self._h, C.byref(loss)))
+        return loss.value
+
+    def run_iteration(self, tasks) -> float:
+        """One iteration from an explicit task sequence (e.g. pipesim replay order)."""
+        self.begin_iteration()
+        for t in tasks:
+            self.run_task(t)
+        return self.end_iteration()
 
     def profile_step(self) -> dict:
         """One eager iteration with per-task GPU timestamps (see measured_bubble)."""

@@ -120,3 +120,72 @@ def test_uneven_stage_partition():
     _check_iteration(shape, P.PipelineConfig("chimera", 4, 1, 4, 2, 1))
     rc = dataclasses.replace(PRESETS["tiny"], stage_layers=(1, 3, 3, 1))
     _check_iteration(rc, P.PipelineConfig("chimera", 4, 1, 8, 1, 1, "forward-doubling"))
+
+
+def _replay_tasks(schedule_text):
+    s = json.loads(schedule_text)
+    kinds = {"Forward": 0, "Backward": 1}
+    out = []
+    for w, i in P.replay_order(schedule_text):
+        t = s["per_worker"][w][i]
+        out.append((kinds[t["kind"]], t["pipeline_id"], t["micro_batch"], t["stage"], t["worker"],
+                    t["replica_group"]))
+    return out
+
+
+def test_engine_style_task_driving_matches_oracle():
+    # The host walks the schedule task by task (reference Engine::run_iteration loop,
+    # oracle.cpp:304-356) through ck_gpt_begin_iteration / run_task / end_iteration.
+    shape, cfg = PRESETS["tiny"], P.PipelineConfig("chimera", 4, 2, 4, 2, 1)
+    tr = Trainer(shape, cfg, lr=0.5)
+    tr.init_params(0)
+    params = [tr.get_params(s).astype(np.float64) for s in range(cfg.D)]
+    tok, lab = synthetic_batch(shape, cfg.mini_batch(), 11)
+    tr.set_batch(tok, lab)
+    loss = tr.run_iteration(_replay_tasks(tr.schedule_text))
+    new_ref, ref_loss, g_ref, _ = O.run_iteration(json.loads(tr.schedule_text), _oshape(shape), params, tok, lab,
+                                                  0.5)
+    assert abs(loss - ref_loss) <= 2e-2 * abs(ref_loss)
+    for s in range(cfg.D):
+        g = (params[s] - tr.get_params(s).astype(np.float64)) / 0.5
+        assert g @ g_ref[s] / (np.linalg.norm(g) * np.linalg.norm(g_ref[s])) >= 0.999
+    # the graph-replayed step() continues from the task-driven weights
+    tr.set_batch(tok, lab)
+    assert np.isfinite(tr.step())
+    tr.close()
+
+
+def test_engine_style_missing_activation_and_misuse():
+    from paper_2107_06925_b200._lib import CKError, InvalidConfigError
+    shape, cfg = PRESETS["tiny"], P.PipelineConfig("chimera", 4, 1, 4, 2, 1)
+    tr = Trainer(shape, cfg, lr=0.1)
+    tr.init_params(0)
+    tok, lab = synthetic_batch(shape, cfg.mini_batch(), 1)
+    tr.set_batch(tok, lab)
+    tasks = _replay_tasks(tr.schedule_text)
+    with pytest.raises(CKError):  # run_task outside an iteration
+        tr.run_task(tasks[0])
+    tr.begin_iteration()
+    bwd = next(t for t in tasks if t[0] == 1)
+    with pytest.raises(CKError) as e:  # backward before its forward: MissingActivationError
+        tr.run_task(bwd)
+    assert e.value.status == 3 and "no stashed activation" in str(e.value)
+    late_fwd = next(t for t in tasks if t[0] == 0 and t[3] > 0)
+    with pytest.raises(CKError) as e:  # forward before the previous stage's forward
+        tr.run_task(late_fwd)
+    assert e.value.status == 3
+    with pytest.raises(InvalidConfigError):  # not a task of this schedule (wrong worker)
+        tr.run_task((0, tasks[0][1], tasks[0][2], tasks[0][3], (tasks[0][4] + 1) % cfg.D, 0))
+    tr.run_task(tasks[0])
+    with pytest.raises(InvalidConfigError):  # issued twice
+        tr.run_task(tasks[0])
+    for t in tasks[1:]:
+        tr.run_task(t)
+    assert np.isfinite(tr.end_iteration())
+    with pytest.raises(InvalidConfigError):  # incomplete iteration
+        tr.begin_iteration()
+        tr.run_task(tasks[0])
+        tr.end_iteration()
+    tr.set_batch(tok, lab)
+    assert np.isfinite(tr.step())
+    tr.close()
