@@ -56,6 +56,16 @@ CK_API int pipesim_memory_profile(const char* schedule_json, const char* profile
  * 1 eager-sync, 2 eager-sync-opt. */
 CK_API int pipesim_simulate(const char* schedule_json, const char* profile_json, int policy,
                      int zero_comm, double eager_overhead, char** out_json);
+/* The `pipesim simulate -o <prefix>` outputs (proj/tools/main.cpp:134-170,367-370):
+ * the timeline JSON document (indent 2 + newline) and the Gantt chart of the same
+ * simulation (gantt::render_svg / render_ascii, proj/src/gantt.cpp:35-125). */
+CK_API int pipesim_simulate_timeline(const char* schedule_json, const char* profile_json, int policy,
+                                     double eager_overhead, char** out_json);
+CK_API int pipesim_gantt(const char* schedule_json, const char* profile_json, int policy,
+                         double eager_overhead, int svg, char** out);
+/* Gantt chart of a timeline document in that schema -- e.g. a measured GPU iteration
+ * (gpt.measured_timeline); time unit = the profile's F_t for the ASCII columns. */
+CK_API int pipesim_gantt_timeline(const char* timeline_json, const char* profile_json, int svg, char** out);
 /* perfmodel::replicas_per_stage / critical_path / predict_T (perfmodel.hpp:61-75). */
 CK_API int pipesim_replicas_per_stage(const char* config_json);
 CK_API int pipesim_critical_path(const char* schedule_json, const char* profile_json, int* C_f,

@@ -68,6 +68,8 @@ class RefLib:
         L.ref_simulate.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_double,
                                    C.POINTER(C.c_void_p)]
         L.ref_replicas_per_stage.argtypes = [C.c_char_p]
+        L.ref_gantt.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_double, C.c_int, C.POINTER(C.c_void_p)]
+        L.ref_simulate_timeline.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_double, C.POINTER(C.c_void_p)]
         L.ref_critical_path.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.ref_predict_T.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_double)]
         L.ref_toy_make_model.argtypes = [_ip, C.c_int, C.c_uint64, _dp]
@@ -122,6 +124,15 @@ class RefLib:
                  eager_overhead: float = -1.0) -> dict:
         return json.loads(self._str(self.L.ref_simulate, sched_json.encode(), prof_json.encode(),
                                     policy, int(zero_comm), eager_overhead))
+
+    def gantt(self, sched_json: str, prof_json: str, policy: int = 0, eps: float = -1.0,
+              svg: bool = False) -> str:
+        return self._str(self.L.ref_gantt, sched_json.encode(), prof_json.encode(), policy, C.c_double(eps),
+                         int(svg))
+
+    def simulate_timeline(self, sched_json: str, prof_json: str, policy: int = 0, eps: float = -1.0) -> str:
+        return self._str(self.L.ref_simulate_timeline, sched_json.encode(), prof_json.encode(), policy,
+                         C.c_double(eps))
 
     def replicas_per_stage(self, cfg_json: str) -> int:
         return self.L.ref_replicas_per_stage(cfg_json.encode())

@@ -13,10 +13,13 @@
 #include <string>
 #include <vector>
 
+#include <json.hpp>
+
 #include "listsched.hpp"
 #include "pipesim/analysis.hpp"
 #include "pipesim/core.hpp"
 #include "pipesim/dessim.hpp"
+#include "pipesim/gantt.hpp"
 #include "pipesim/oracle.hpp"
 #include "pipesim/perfmodel.hpp"
 #include "pipesim/schedgen.hpp"
@@ -254,6 +257,65 @@ int ref_toy_check_gradients(const int* dims, int n_dims, const double* params,
   return guard([&] {
     *err = oracle::check_gradients(unflatten(dims, n_dims, params),
                                    make_b(dims, n_dims, batch, inputs, targets));
+  });
+}
+
+// gantt::render_svg / render_ascii (proj/src/gantt.cpp:35,98) of dessim::simulate
+int ref_gantt(const char* sched, const char* prof, int policy, double eps, int svg, char** out) {
+  return guard([&] {
+    dessim::SimOptions o;
+    o.policy = static_cast<dessim::SyncPolicy>(policy);
+    o.eager_overhead = eps;
+    const CostProfile p = profile_from_json(prof);
+    const auto r = dessim::simulate(schedule_from_json(sched), p, o);
+    *out = dup(svg ? gantt::render_svg(r, p) : gantt::render_ascii(r, p));
+  });
+}
+
+// The `simulate -o <prefix>.json` document.  Its writer lives in the reference CLI
+// (proj/tools/main.cpp:134-170, not part of the library): restated here over the
+// reference's dessim result with the same nlohmann ordered_json, dump(2) + newline.
+int ref_simulate_timeline(const char* sched, const char* prof, int policy, double eps, char** out) {
+  return guard([&] {
+    dessim::SimOptions o;
+    o.policy = static_cast<dessim::SyncPolicy>(policy);
+    o.eager_overhead = eps;
+    const auto r = dessim::simulate(schedule_from_json(sched), profile_from_json(prof), o);
+    using oj = nlohmann::ordered_json;
+    oj j;
+    j["policy"] = dessim::to_string(o.policy);
+    j["makespan"] = r.makespan;
+    j["compute_makespan"] = r.compute_makespan;
+    j["allreduce_exposed"] = r.allreduce_exposed;
+    j["per_worker_idle"] = r.per_worker_idle;
+    oj ev = oj::array();
+    for (std::size_t w = 0; w < r.timed.per_worker.size(); ++w)
+      for (std::size_t i = 0; i < r.timed.per_worker[w].size(); ++i) {
+        const Task& t = r.timed.per_worker[w][i];
+        const TimeSpan& ts = (*r.timed.timing)[w][i];
+        oj e;
+        e["worker"] = t.worker;
+        e["kind"] = to_string(t.kind);
+        e["pipeline_id"] = t.pipeline_id;
+        e["micro_batch"] = t.micro_batch;
+        e["stage"] = t.stage;
+        e["start"] = ts.start;
+        e["end"] = ts.end;
+        ev.push_back(std::move(e));
+      }
+    j["events"] = std::move(ev);
+    oj ar = oj::array();
+    for (const auto& a : r.allreduce_events) {
+      oj e;
+      e["worker"] = a.worker;
+      e["stage"] = a.stage;
+      e["eager"] = a.eager;
+      e["start"] = a.start;
+      e["end"] = a.end;
+      ar.push_back(std::move(e));
+    }
+    j["allreduce"] = std::move(ar);
+    *out = dup(j.dump(2) + "\n");
   });
 }
 

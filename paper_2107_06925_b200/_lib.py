@@ -31,6 +31,11 @@ SIGNATURES = {
                                          C.POINTER(C.c_int), C.POINTER(C.c_double), C.c_int]),
     "pipesim_simulate": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_double,
                                    C.POINTER(C.c_void_p)]),
+    "pipesim_simulate_timeline": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.c_double,
+                                            C.POINTER(C.c_void_p)]),
+    "pipesim_gantt": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.c_double, C.c_int,
+                                C.POINTER(C.c_void_p)]),
+    "pipesim_gantt_timeline": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]),
     "pipesim_replicas_per_stage": (C.c_int, [C.c_char_p]),
     "pipesim_critical_path": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(C.c_int),
                                         C.POINTER(C.c_int)]),

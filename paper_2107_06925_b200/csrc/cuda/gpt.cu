@@ -157,6 +157,12 @@ struct Trainer::Impl {
     cudaEvent_t a, b;
   };
   std::vector<TaskSpan> spans;
+  struct CollSpan {  // one stage's allreduce + SGD on the comm stream
+    int stage;
+    bool eager;
+    cudaEvent_t a, b;
+  };
+  std::vector<CollSpan> coll_spans;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_next = 0;
   cudaEvent_t timed_event() {
@@ -656,7 +662,20 @@ void plan_sync(Trainer::Impl& I) {
 
 // Sum the local copies, allreduce across the processes holding the stage (if any),
 // SGD -- on the comm stream, after every local copy's last backward.
+void sync_stage_body(Trainer::Impl& I, int s);
+
+// Stage s's gradient sync + SGD on the comm stream; timed when profiling.
 void sync_stage(Trainer::Impl& I, int s) {
+  if (!I.profiling) return sync_stage_body(I, s);
+  Trainer::Impl::CollSpan c{s, I.stage_eager.count(s) && I.stage_eager.at(s), I.timed_event(), nullptr};
+  CK_CUDA(cudaEventRecord(c.a, I.comm_stream));
+  sync_stage_body(I, s);
+  c.b = I.timed_event();
+  CK_CUDA(cudaEventRecord(c.b, I.comm_stream));
+  I.coll_spans.push_back(c);
+}
+
+void sync_stage_body(Trainer::Impl& I, int s) {
   StageState& S = I.stages.at(s);
   cudaStream_t cs = I.comm_stream;
   for (cudaEvent_t e : I.stage_done_ev.at(s)) CK_CUDA(cudaStreamWaitEvent(cs, e, 0));
@@ -845,6 +864,7 @@ std::string Trainer::profile_step() {
   Impl& I = *d_;
   if (!I.connected) throw capi::InternalError("multi-process trainer: call connect() first");
   I.spans.clear();
+  I.coll_spans.clear();
   I.ev_next = 0;
   cudaEvent_t t0 = I.timed_event();
   CK_CUDA(cudaEventRecord(t0, I.main_stream));
@@ -876,11 +896,32 @@ std::string Trainer::profile_step() {
     x.set("end_ms", Value::number(b));
     arr.push(std::move(x));
   }
+  Value colls = Value::array();
+  for (const auto& c : I.coll_spans) {
+    float a = 0, b = 0;
+    CK_CUDA(cudaEventElapsedTime(&a, t0, c.a));
+    CK_CUDA(cudaEventElapsedTime(&b, t0, c.b));
+    Value x = Value::object();
+    x.set("stage", Value::integer(c.stage));
+    x.set("eager", Value::boolean(c.eager));
+    Value holders = Value::array();  // local ranks holding a copy of the stage
+    for (int k = 0; k < I.nlocal; ++k)
+      for (int p = 0; p < 2 * I.sched.config.f; ++p)
+        if (stage_of(I.sched, (I.first + k) % I.D, p) == c.stage) {
+          holders.push(Value::integer(I.first + k));
+          break;
+        }
+    x.set("ranks", std::move(holders));
+    x.set("start_ms", Value::number(a));
+    x.set("end_ms", Value::number(b));
+    colls.push(std::move(x));
+  }
   float tot = 0;
   CK_CUDA(cudaEventElapsedTime(&tot, t0, t1));
   Value j = Value::object();
   j.set("iteration_ms", Value::number(tot));
   j.set("tasks", std::move(arr));
+  j.set("allreduce", std::move(colls));
   return json::dump(j, -1);
 }
 

@@ -12,9 +12,11 @@
 #include "json_io.hpp"
 #include "pipesim/analysis.hpp"
 #include "pipesim/dessim.hpp"
+#include "pipesim/gantt.hpp"
 #include "pipesim/perfmodel.hpp"
 #include "pipesim/schedgen.hpp"
 #include "sched_engine.hpp"
+#include "timeline.hpp"
 
 using namespace pipesim;
 using chimera::capi::dup_string;
@@ -80,6 +82,40 @@ int pipesim_memory_profile(const char* schedule_json, const char* profile_json, 
     }
     *peak_worker = mp.peak_worker;
     *peak_bytes = mp.peak_bytes;
+  });
+}
+
+// dessim::simulate -> the `pipesim simulate -o <prefix>` JSON file (indent 2 + newline)
+int pipesim_simulate_timeline(const char* schedule_json, const char* profile_json, int policy,
+                              double eager_overhead, char** out_json) {
+  return guarded([&] {
+    if (policy < 0 || policy > 2) throw InvalidConfigError("unknown sync policy");
+    dessim::SimOptions o;
+    o.policy = static_cast<dessim::SyncPolicy>(policy);
+    o.eager_overhead = eager_overhead;
+    const auto r = dessim::simulate(schedule_from_json(schedule_json), profile_from_json(profile_json), o);
+    *out_json = dup_string(chimera::timeline::to_json(r, o.policy, 2) + "\n");
+  });
+}
+
+int pipesim_gantt(const char* schedule_json, const char* profile_json, int policy, double eager_overhead,
+                  int svg, char** out) {
+  return guarded([&] {
+    if (policy < 0 || policy > 2) throw InvalidConfigError("unknown sync policy");
+    dessim::SimOptions o;
+    o.policy = static_cast<dessim::SyncPolicy>(policy);
+    o.eager_overhead = eager_overhead;
+    const CostProfile p = profile_from_json(profile_json);
+    const auto r = dessim::simulate(schedule_from_json(schedule_json), p, o);
+    *out = dup_string(svg ? gantt::render_svg(r, p) : gantt::render_ascii(r, p));
+  });
+}
+
+int pipesim_gantt_timeline(const char* timeline_json, const char* profile_json, int svg, char** out) {
+  return guarded([&] {
+    const CostProfile p = profile_from_json(profile_json);
+    const auto r = chimera::timeline::from_json(timeline_json);
+    *out = dup_string(svg ? gantt::render_svg(r, p) : gantt::render_ascii(r, p));
   });
 }
 

@@ -303,6 +303,34 @@ def timeline_json(profile: dict, schedule_text: str) -> str:
     return json.dumps(sched)
 
 
+def measured_timeline(profile: dict, schedule_text: str, policy: str = "eager-sync") -> str:
+    """A profiled GPU iteration (Trainer.profile_step) as the reference's
+    ``pipesim simulate -o`` timeline document (tools/main.cpp:134-170): replica 0's
+    ranks, milliseconds from the first task start, dessim's idle definition, one
+    allreduce event per holder worker of each stage sync.  Render it with
+    ``pipesim.gantt_timeline`` (the same code path as the simulated charts)."""
+    sched = json.loads(schedule_text)
+    D = sched["config"]["D"]
+    spans = {(t["rank"], t["kind"], t["pipeline"], t["micro"], t["stage"]): (t["start_ms"], t["end_ms"])
+             for t in profile["tasks"] if t["rank"] < D}
+    t0 = min(a for a, _ in spans.values())
+    events, busy = [], [0.0] * D
+    for w, wl in enumerate(sched["per_worker"]):
+        for t in wl:
+            a, b = spans[(w, t["kind"], t["pipeline_id"], t["micro_batch"], t["stage"])]
+            events.append({"worker": w, "kind": t["kind"], "pipeline_id": t["pipeline_id"],
+                           "micro_batch": t["micro_batch"], "stage": t["stage"], "start": a - t0, "end": b - t0})
+            busy[w] += b - a
+    compute = max(e["end"] for e in events)
+    ar = [{"worker": r, "stage": c["stage"], "eager": c["eager"], "start": c["start_ms"] - t0,
+           "end": c["end_ms"] - t0} for c in profile.get("allreduce", []) for r in c["ranks"] if r < D]
+    makespan = max([compute] + [e["end"] for e in ar])
+    doc = {"policy": policy, "makespan": makespan, "compute_makespan": compute,
+           "allreduce_exposed": makespan - compute, "per_worker_idle": [compute - b for b in busy],
+           "events": events, "allreduce": ar}
+    return json.dumps(doc, indent=2) + "\n"
+
+
 def smoke():
     """One Chimera iteration of the tiny GPT on cuda:0 vs the numpy oracle."""
     import sys

@@ -175,6 +175,27 @@ def simulate(schedule, profile=None, policy: str = "end-of-iteration", zero_comm
                                POLICIES[policy], int(zero_comm), eager_overhead))
 
 
+def simulate_timeline(schedule, profile=None, policy: str = "end-of-iteration",
+                      eager_overhead: float = -1.0) -> str:
+    """The ``pipesim simulate -o <prefix>.json`` document (tools/main.cpp:134-170,367)."""
+    return call_str(lib().pipesim_simulate_timeline, _sched(schedule), _prof(profile), POLICIES[policy],
+                    eager_overhead)
+
+
+def gantt(schedule, profile=None, policy: str = "end-of-iteration", svg: bool = False,
+          eager_overhead: float = -1.0) -> str:
+    """``gantt::render_svg`` / ``render_ascii`` (gantt.hpp:28-31) of dessim::simulate."""
+    return call_str(lib().pipesim_gantt, _sched(schedule), _prof(profile), POLICIES[policy], eager_overhead,
+                    int(svg))
+
+
+def gantt_timeline(timeline, profile=None, svg: bool = False) -> str:
+    """Gantt chart of a timeline document in the simulate -o schema (e.g. a measured GPU
+    iteration from ``gpt.measured_timeline``); ASCII columns are F_t of ``profile``."""
+    text = timeline if isinstance(timeline, str) else json.dumps(timeline)
+    return call_str(lib().pipesim_gantt_timeline, text.encode(), _prof(profile), int(svg))
+
+
 def replicas_per_stage(config) -> int:
     return lib().pipesim_replicas_per_stage(_cfg(config))
 

@@ -189,3 +189,29 @@ def test_engine_style_missing_activation_and_misuse():
     tr.set_batch(tok, lab)
     assert np.isfinite(tr.step())
     tr.close()
+
+
+def test_measured_timeline_renders_with_reference_gantt():
+    # profiled GPU iteration -> `simulate -o` timeline document -> pipesim::gantt
+    shape, cfg = PRESETS["tiny"], P.PipelineConfig("chimera", 4, 1, 4, 2, 1)
+    tr = Trainer(shape, cfg, lr=0.1)
+    tr.init_params(0)
+    tok, lab = synthetic_batch(shape, cfg.mini_batch(), 2)
+    tr.set_batch(tok, lab)
+    tr.step()
+    prof = tr.profile_step()
+    assert {c["stage"] for c in prof["allreduce"]} == set(range(cfg.D))
+    from paper_2107_06925_b200.gpt import measured_timeline
+    tl = measured_timeline(prof, tr.schedule_text)
+    doc = json.loads(tl)
+    sched = json.loads(tr.schedule_text)
+    assert len(doc["events"]) == sum(len(w) for w in sched["per_worker"])
+    assert len(doc["allreduce"]) == cfg.D * 2  # f=1: every stage held by 2 workers
+    assert all(e["end"] >= e["start"] >= 0 for e in doc["events"])
+    assert doc["makespan"] >= doc["compute_makespan"] > 0
+    f_mean = np.mean([e["end"] - e["start"] for e in doc["events"] if e["kind"] == "Forward"])
+    ascii_chart = P.gantt_timeline(tl, P.CostProfile(F_t=float(f_mean)))
+    assert ascii_chart.count("\n") == cfg.D and ascii_chart.startswith("P0 |")
+    svg = P.gantt_timeline(tl, P.CostProfile(F_t=float(f_mean)), svg=True)
+    assert svg.startswith("<svg") and svg.count("<rect") >= len(doc["events"])
+    tr.close()
