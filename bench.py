@@ -174,6 +174,37 @@ def gemm_roofline(stream_handle, peak_tflops):
             "flops_per_launch_avg": tot_flops / len(shapes), "avg_launch_ms": tot_ms / len(shapes)}
 
 
+def measure_alpha_beta(world):
+    """alpha (ms) and beta (ms/byte) of perfmodel's Rabenseifner allreduce cost
+    2 log2(r) alpha + 2 (r-1)/r beta L (perfmodel.cpp:24-28), fitted from NCCL
+    allreduce times at two sizes over all ranks (max over ranks)."""
+    import math
+    import torch
+    import torch.distributed as dist
+    g = dist.new_group(list(range(world)), backend="nccl")
+    times = []
+    for n in (1 << 10, 1 << 24):  # 4 KiB and 64 MiB of fp32
+        x = torch.ones(n, device="cuda")
+        for _ in range(3):
+            dist.all_reduce(x, group=g)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            dist.all_reduce(x, group=g)
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / 10])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        times.append((4.0 * n, float(t)))
+    dist.destroy_process_group(g)
+    (s0, t0), (s1, t1) = times
+    slope = max(0.0, (t1 - t0) / (s1 - s0))
+    icpt = max(0.0, t0 - slope * s0)
+    r = float(world)
+    return icpt / (2.0 * math.log2(r)), slope * r / (2.0 * (r - 1.0))
+
+
 def run_reference(args, shape):
     """--impl reference: the reference path's CPU implementation (the numpy port of the
     reference Engine; the reference itself has no transformer), all host threads."""
@@ -292,11 +323,15 @@ def main():
     if world > 1:
         dist.barrier()
     prof = tr.profile_step()
-    tasks = prof["tasks"]
-    if world > 1:
+    tasks, colls = prof["tasks"], prof.get("allreduce", [])
+    if world > 1:  # per-process clocks, each relative to its own iteration start
         allt = [None] * world
-        dist.all_gather_object(allt, tasks)
-        tasks = [t for x in allt for t in x]
+        dist.all_gather_object(allt, (tasks, colls))
+        tasks = [t for x in allt for t in x[0]]
+        colls = [c for x in allt for c in x[1]]
+
+    # ---- alpha / beta of the collective fabric (Eq. 1's allreduce term), NCCL over all ranks
+    ab = measure_alpha_beta(world) if world > 1 else (0.0, 0.0)
 
     stats = tr.stats()
     launches = int(stats["launches_per_step"] * args.steps)
@@ -325,10 +360,22 @@ def main():
         bub_at_ratio = P.bubble_ratio(P.generate_json(cfg, prof_m, -1), prof_m)
         one_rank_per_gpu = per == 1
         mb = measured_bubble({"tasks": tasks}) if one_rank_per_gpu else None
-        if os.environ.get("CK_TIMELINE"):
-            with open(os.environ["CK_TIMELINE"], "w") as fh:
-                fh.write(timeline_json({"tasks": tasks}, sched))
+        if os.environ.get("CK_TIMELINE"):  # prefix: measured timeline + Gantt charts
+            from paper_2107_06925_b200.gpt import measured_timeline
+            pre = os.environ["CK_TIMELINE"]
+            tl = measured_timeline({"tasks": tasks, "allreduce": colls}, sched)
+            ft = P.CostProfile(F_t=max(1e-6, sum(fwd) / len(fwd)))
+            for ext, text in ((".json", tl), (".svg", P.gantt_timeline(tl, ft, svg=True)),
+                              (".txt", P.gantt_timeline(tl, ft)), (".sched.json", timeline_json({"tasks": tasks}, sched))):
+                with open(pre + ext, "w") as fh:
+                    fh.write(text)
         mp = P.memory_profile(sched)
+        # Eq. 1 (perfmodel::predict_T, perfmodel.cpp:157) on the measured B200 CostProfile
+        l_grad = 4.0 * max(st["numel"] for st in tr.layout)  # fp32 gradient of the largest held stage
+        prof_b200 = P.CostProfile(F_t=sum(fwd) / len(fwd), backward_ratio=float(Fraction(ratio).limit_denominator(16)),
+                                  alpha=ab[0], beta=ab[1], L_grad=l_grad,
+                                  L_act=2.0 * CFG["B"] * shape.seq * shape.hidden)
+        pred = P.predict_T(cfg, prof_b200)
         rl = gemm_roofline(tr.stream_handle(), peak)
         flops_seq = shape.flops_per_seq()
         cpu = None if args.no_cpu_baseline else cpu_port_sample(shape)
@@ -358,6 +405,15 @@ def main():
                        "reference_schedule_at_measured_B/F": str(bub_at_ratio),
                        "note": (None if one_rank_per_gpu else
                                 f"{per} logical ranks share each GPU: per-rank bubble not observable")},
+            "perfmodel": {"predicted_ms": round(pred, 3), "measured_ms": round(ms, 3),
+                          "rel_err": round((ms - pred) / ms, 4),
+                          "valid": one_rank_per_gpu,
+                          "profile": {"F_t_ms": round(prof_b200.F_t, 4), "backward_ratio": prof_b200.backward_ratio,
+                                      "alpha_ms": ab[0], "beta_ms_per_byte": ab[1], "L_grad": l_grad,
+                                      "L_act": prof_b200.L_act},
+                          "note": ("Eq. 1 assumes one worker per GPU" if not one_rank_per_gpu else
+                                   "p2p term: alpha + beta * L_act with the allreduce fit (upper bound; "
+                                   "stage outputs are stored into the peer slot by the producing kernel)")},
             "act_counts_per_worker": mp["act_counts"],
             "peak_stash_per_rank": stats["peak_stash_per_rank"],
             "peak_stash_bytes_per_rank": stats["peak_stash_bytes_per_rank"],
