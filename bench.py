@@ -262,7 +262,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # CK_PROCS_PER_GPU=k (validation only): k consecutive processes share one GPU, e.g. the
+    # 8-GPU one-rank-per-process layout exercised on 4 GPUs
+    torch.cuda.set_device(local // int(os.environ.get("CK_PROCS_PER_GPU", "1")))
     cfg = P.PipelineConfig(**CFG)
     n_logical = cfg.W * cfg.D
     if n_logical % world:

@@ -182,7 +182,10 @@ CK_API int ck_gpt_set_sync_policy(ck_gpt* h, int policy);
 CK_API void* ck_gpt_stream(ck_gpt* h);
 /* Multi-process (one process per GPU): export this process's 128 bytes of CUDA-IPC
  * handles, all-gather them (host side, e.g. torch.distributed), then connect with all
- * processes' handles in process order and one ncclUniqueId (ck_nccl_unique_id). */
+ * processes' handles in process order and the NCCL ids (ck_nccl_unique_id): either one
+ * (a world communicator split per stage) or D, one per stage (each stage communicator
+ * initialised on its own: no world communicator, so several processes may share a GPU
+ * as long as every stage's holders are on distinct GPUs). */
 CK_API int ck_gpt_ipc_handles(ck_gpt* h, char* out, int cap);
 CK_API int ck_gpt_connect(ck_gpt* h, const char* all_handles, int n_bytes, const char* nccl_id,
                           int id_bytes);

@@ -418,6 +418,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
     k_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const EpiArgs ep,
             int M, int N, int K, int ksplit) {
   extern __shared__ uint8_t smem_raw[];
+  GEMM_TRACE(threadIdx.x == 32, 0, 6);
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPairStages * kPairStageBytes);
   uint64_t* empty = full + kPairStages;

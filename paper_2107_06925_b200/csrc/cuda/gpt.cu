@@ -993,7 +993,9 @@ void Trainer::connect(const std::string& all_blobs, const std::string& nccl_id) 
   Impl& I = *d_;
   const size_t hb = sizeof(cudaIpcMemHandle_t);
   if (all_blobs.size() != size_t(I.procs) * 2 * hb) throw pipesim::InvalidConfigError("bad IPC blob size");
-  if (nccl_id.size() != sizeof(ncclUniqueId)) throw pipesim::InvalidConfigError("bad NCCL id size");
+  const size_t n_ids = nccl_id.size() / sizeof(ncclUniqueId);
+  if (nccl_id.size() % sizeof(ncclUniqueId) || (n_ids != 1 && n_ids != size_t(I.D)))
+    throw pipesim::InvalidConfigError("NCCL ids: expected 1 (world + split) or D (one per stage) ids");
   I.peer_inbox.assign(I.procs, nullptr);
   I.peer_outbox.assign(I.procs, nullptr);
   for (int q = 0; q < I.procs; ++q) {
@@ -1028,18 +1030,31 @@ void Trainer::connect(const std::string& all_blobs, const std::string& nccl_id) 
       g.ack = reinterpret_cast<uint32_t*>(static_cast<char*>(I.peer_outbox[q]) + out_lay[q].at(k));
     }
   }
-  // NCCL: world communicator, then one split per stage whose holders span >1 process
-  ncclUniqueId id;
-  std::memcpy(&id, nccl_id.data(), sizeof id);
-  if (Nccl::get().CommInitRank(&I.world_comm, I.procs, id, I.proc) != ncclSuccess)
+  // NCCL: one communicator per stage whose holders span >1 process -- either split
+  // from a world communicator (one id), or initialised directly from its own id (D
+  // ids: no world communicator, so processes may share a GPU as long as each stage's
+  // holders sit on distinct GPUs).  Stages are visited in the same order everywhere.
+  auto id_at = [&](size_t k) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id.data() + k * sizeof id, sizeof id);
+    return id;
+  };
+  if (n_ids == 1 && Nccl::get().CommInitRank(&I.world_comm, I.procs, id_at(0), I.proc) != ncclSuccess)
     throw capi::InternalError("ncclCommInitRank failed");
   for (int s = 0; s < I.D; ++s) {
     const std::vector<int> holders = I.lp->stage_holders(s);
     if (holders.size() < 2) continue;
-    const bool mine = std::find(holders.begin(), holders.end(), I.proc) != holders.end();
+    const auto pos = std::find(holders.begin(), holders.end(), I.proc);
+    const bool mine = pos != holders.end();
     ncclComm_t c = nullptr;
-    if (Nccl::get().CommSplit(I.world_comm, mine ? s : NCCL_SPLIT_NOCOLOR, I.proc, &c, nullptr) != ncclSuccess)
-      throw capi::InternalError("ncclCommSplit failed");
+    if (n_ids == 1) {
+      if (Nccl::get().CommSplit(I.world_comm, mine ? s : NCCL_SPLIT_NOCOLOR, I.proc, &c, nullptr) != ncclSuccess)
+        throw capi::InternalError("ncclCommSplit failed");
+    } else if (mine) {
+      if (Nccl::get().CommInitRank(&c, int(holders.size()), id_at(size_t(s)), int(pos - holders.begin())) !=
+          ncclSuccess)
+        throw capi::InternalError("ncclCommInitRank (stage " + std::to_string(s) + ") failed");
+    }
     if (mine) I.stage_comm[s] = c;
   }
   CK_CUDA(cudaDeviceSynchronize());

@@ -264,7 +264,9 @@ class Trainer:
         world, rank = dist.get_world_size(), dist.get_rank()
         blobs = [None] * world
         dist.all_gather_object(blobs, self.ipc_handles())
-        uid = [nccl_unique_id() if rank == 0 else None]
+        # one NCCL id per stage: each stage communicator is initialised on its own (no
+        # world communicator), see ck_gpt_connect
+        uid = [b"".join(nccl_unique_id() for _ in range(self.config.D)) if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         allb = b"".join(blobs)
         check(lib().ck_gpt_connect(self._h, allb, len(allb), uid[0], len(uid[0])))

@@ -40,6 +40,7 @@ int main(int argc, char** argv) {
   cudaMemcpyFromSymbol(tr, chimera::gemm::g_gemm_trace, sizeof(tr));
   const long long c0 = tr[0][0];
   printf("tile  mma_start  mma_issued  epi4_start  epi4_end  epi11_start epi11_end   (cycles from tile 0 start)\n");
+  printf("kernel entry -> tile0 mma start: %lld cycles\n", tr[0][0] - tr[0][6]);
   for (int t = 0; t < 16 && tr[t][0]; ++t)
     printf("%4d %10lld %11lld %11lld %9lld %11lld %9lld\n", t, tr[t][0] - c0, tr[t][1] - c0, tr[t][2] - c0,
            tr[t][3] - c0, tr[t][4] - c0, tr[t][5] - c0);

@@ -10,7 +10,7 @@ from paper_2107_06925_b200.gpt import PRESETS, Trainer, synthetic_batch
 
 dist.init_process_group("gloo")
 world, rank = dist.get_world_size(), dist.get_rank()
-torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) // int(os.environ.get("CK_PROCS_PER_GPU", "1")))
 shape = PRESETS["tiny"]
 cfg = P.PipelineConfig("chimera", 4, 2, 4, 2, 1)
 per = cfg.W * cfg.D // world
