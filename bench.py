@@ -177,32 +177,38 @@ def gemm_roofline(stream_handle, peak_tflops):
 def measure_alpha_beta(world):
     """alpha (ms) and beta (ms/byte) of perfmodel's Rabenseifner allreduce cost
     2 log2(r) alpha + 2 (r-1)/r beta L (perfmodel.cpp:24-28), fitted from NCCL
-    allreduce times at two sizes over all ranks (max over ranks)."""
+    allreduce times at two sizes over one process per GPU (max over ranks)."""
     import math
     import torch
     import torch.distributed as dist
-    g = dist.new_group(list(range(world)), backend="nccl")
-    times = []
-    for n in (1 << 10, 1 << 24):  # 4 KiB and 64 MiB of fp32
-        x = torch.ones(n, device="cuda")
-        for _ in range(3):
-            dist.all_reduce(x, group=g)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(10):
-            dist.all_reduce(x, group=g)
-        e1.record()
-        torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1) / 10])
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        times.append((4.0 * n, float(t)))
+    ppg = int(os.environ.get("CK_PROCS_PER_GPU", "1"))
+    members = list(range(0, world, ppg))
+    g = dist.new_group(members, backend="nccl")
+    out = torch.zeros(2, dtype=torch.float64)
+    if len(members) > 1 and dist.get_rank() in members:
+        times = []
+        for n in (1 << 10, 1 << 24):  # 4 KiB and 64 MiB of fp32
+            x = torch.ones(n, device="cuda")
+            for _ in range(3):
+                dist.all_reduce(x, group=g)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(10):
+                dist.all_reduce(x, group=g)
+            e1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1) / 10], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=g)
+            times.append((4.0 * n, float(t)))
+        (s0, t0), (s1, t1) = times
+        slope = max(0.0, (t1 - t0) / (s1 - s0))
+        icpt = max(0.0, t0 - slope * s0)
+        r = float(len(members))
+        out = torch.tensor([icpt / (2.0 * math.log2(r)), slope * r / (2.0 * (r - 1.0))], dtype=torch.float64)
+    dist.broadcast(out, src=0)  # default (gloo) group
     dist.destroy_process_group(g)
-    (s0, t0), (s1, t1) = times
-    slope = max(0.0, (t1 - t0) / (s1 - s0))
-    icpt = max(0.0, t0 - slope * s0)
-    r = float(world)
-    return icpt / (2.0 * math.log2(r)), slope * r / (2.0 * (r - 1.0))
+    return float(out[0]), float(out[1])
 
 
 def run_reference(args, shape):
