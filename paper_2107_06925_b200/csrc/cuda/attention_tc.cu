@@ -323,27 +323,34 @@ __global__ void __launch_bounds__(192, 2)
 }
 
 // ----------------------------------------------------------------- backward --
-// CTA = (128-key tile, batch*head); 10 warps, one CTA per SM (512 TMEM columns):
-//   warp 8   TMA producer: K, V once; per 128-query tile Q and dO into a 2-stage ring
+// Persistent: one CTA per SM walks its share of the (128-key tile, batch*head) work
+// items -- heaviest first (key tile 0 sees every query tile under causal masking),
+// dealt boustrophedon-wise over the CTAs (the order balances like dynamic LPT) --
+// and pipelines across items: the next item's K/V land in the second K/V buffer and
+// its first S/dP MMAs run while the current item's dK/dV are written out.  10 warps:
+//   warp 8   TMA producer: per item K, V (2 buffers); per 128-query tile Q and dO
+//            (2-stage ring)
 //   warp 9   TMEM allocator + single-thread MMA issuer
 //   warps 0-7  two compute warpgroups; warp w reads TMEM lanes 32*(w%4).. (thread <->
 //            query row), WG g owns key columns [64g, 64g+64) of every tile, so the
 //            row's log-sum-exp and D are two per-thread scalars
-// Per query tile j:
+// Per query tile (global iteration counter g runs across items):
 //   S  = Q K^T, dP = dO V^T          (M128 q, N128 keys, K64)  TMEM [0,128), [128,256);
-//     issued as soon as tile j-1's S / dP sit in registers (st_free)
+//     issued as soon as the previous tile's S / dP sit in registers (st_free)
 //   P = exp2(S c - lse2), dS = P (dP - D) -> bf16, 128-byte-swizzled [q][key] smem tiles
 //     (each WG writes its own 64-key block)
 //   dV += P^T dO, dK += dS^T Q       (M128 keys, N64, K128 q)  TMEM [256,320), [320,384)
 //     -- P / dS read as MN-major A operands
-//   dQ_j = dS K                      (M128 q, N64, K128 keys)  TMEM [384 + 64 (j&1), ..)
+//   dQ_g = dS K                      (M128 q, N64, K128 keys)  TMEM [384 + 64 (g&1), ..)
 //     double-buffered so the MMA never waits for the drain
-//   dQ_j is drained one tile later (underneath tile j+1's math) by the compute WGs, 32
-//   columns each, through a swizzled smem stage and one TMA bulk tensor reduce-add into
-//   the fp32 dQ accumulator -- no per-thread atomics.
-constexpr int kB_K = 0, kB_V = kTileBytes, kB_Q = 2 * kTileBytes, kB_DO = 4 * kTileBytes,
-              kB_P = 6 * kTileBytes, kB_DS = 8 * kTileBytes, kB_DQ = 10 * kTileBytes;  // dQ stage [WG][128][128 B]
-constexpr int kB_BAR = 12 * kTileBytes;
+//   dQ_g is drained one tile later (underneath the next tile's math) by the compute
+//   WGs, 32 columns each, through a swizzled smem stage and one TMA bulk tensor
+//   reduce-add into the fp32 dQ accumulator -- no per-thread atomics.
+// Item epilogue: dK (x 1/sqrt(d)) / dV leave TMEM (acc_free lets the next item's MMAs
+// accumulate), are staged bf16 in the same swizzled stage and written by TMA stores.
+constexpr int kB_K = 0, kB_V = 2 * kTileBytes, kB_Q = 4 * kTileBytes, kB_DO = 6 * kTileBytes,
+              kB_P = 8 * kTileBytes, kB_DS = 10 * kTileBytes, kB_DQ = 12 * kTileBytes;  // stage [WG][128][128 B]
+constexpr int kB_BAR = 14 * kTileBytes;
 constexpr int kBwdSmem = kB_BAR + 256;
 constexpr int kBwdThreads = 320;
 #ifndef CK_ATTN_BWD_POLY_EVERY
@@ -355,41 +362,68 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// The CTA's sequence of (item, query tile) iterations.
+struct BwdSeq {
+  int G, c, n_items, BH, nk, nq;
+  bool causal;
+  int r = 0, n = 0;          // round, item ordinal within this CTA
+  int item = -1, kb = 0, bh = 0, j0 = 0, niter = 0, it = 0;
+  __device__ int item_of(int rr) const {
+    const int i = rr * G + ((rr & 1) ? G - 1 - c : c);
+    return i < n_items ? i : -1;
+  }
+  __device__ void load() {
+    item = item_of(r);
+    if (item < 0) return;
+    kb = item / BH, bh = item % BH, j0 = causal ? kb : 0, niter = nq - j0, it = 0;
+  }
+  __device__ bool valid() const { return item >= 0; }
+  __device__ void advance() {  // next query tile (possibly of the next item)
+    if (++it == niter) {
+      ++r, ++n;
+      load();
+    }
+  }
+};
+
 template <bool CAUSAL>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     k_attn_bwd_tc(const __grid_constant__ CUtensorMap tqkv, const __grid_constant__ CUtensorMap tdo,
-                  const __grid_constant__ CUtensorMap tdq, const float* __restrict__ lse,
-                  const float* __restrict__ Dv, bf16* __restrict__ dqkv, int seq, int H) {
+                  const __grid_constant__ CUtensorMap tdq, const __grid_constant__ CUtensorMap tdqkv,
+                  const float* __restrict__ lse, const float* __restrict__ Dv, bf16* __restrict__ dqkv, int seq, int H,
+                  int BH) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((ptx::smem_u32(smem) & 1023) != 0) __trap();
   ATTN_CTA(0);
   ATTN_CTA(1);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kB_BAR);
-  uint64_t *kv_full = bar, *qd_full = bar + 1, *qd_empty = bar + 3, *s_full = bar + 5, *st_free = bar + 6,
-           *ds_full = bar + 7, *mm_done = bar + 8, *dq_free = bar + 9;  // dq_free[2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
+  uint64_t *kv_full = bar, *kv_empty = bar + 2, *qd_full = bar + 4, *qd_empty = bar + 6, *s_full = bar + 8,
+           *st_free = bar + 9, *ds_full = bar + 10, *mm_done = bar + 11, *dq_free = bar + 12,  // [2]
+      *acc_free = bar + 14;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 15);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // 1-D grid, tile-major: key tile 0 sees every query tile under causal masking, so the
-  // heavy CTAs of all heads go first
-  const int BH = gridDim.x / ((seq + kKV - 1) / kKV);
-  const int kb = blockIdx.x / BH, bh = blockIdx.x % BH, b = bh / H, hd = bh % H;
-  const int k0 = kb * kKV, row_base = b * seq;
-  const int nq = (seq + kQ - 1) / kQ;
-  const int j0 = CAUSAL ? kb : 0;  // first query tile that can see these keys
-  const int niter = nq - j0;
+  const int nk = (seq + kKV - 1) / kKV, nq = (seq + kQ - 1) / kQ;
+  BwdSeq seq0;
+  seq0.G = gridDim.x, seq0.c = blockIdx.x, seq0.n_items = nk * BH, seq0.BH = BH, seq0.nk = nk, seq0.nq = nq;
+  seq0.causal = CAUSAL;
+  seq0.load();
 
   if (warp == 8 && lane == 0) {
     ptx::tma_prefetch(&tqkv);
     ptx::tma_prefetch(&tdo);
     ptx::tma_prefetch(&tdq);
-    ptx::mbar_init(kv_full, 1);
-    for (int s2 = 0; s2 < 2; ++s2) ptx::mbar_init(&qd_full[s2], 1), ptx::mbar_init(&qd_empty[s2], 1);
+    ptx::tma_prefetch(&tdqkv);
+    for (int b2 = 0; b2 < 2; ++b2) {
+      ptx::mbar_init(&kv_full[b2], 1), ptx::mbar_init(&kv_empty[b2], 1);
+      ptx::mbar_init(&qd_full[b2], 1), ptx::mbar_init(&qd_empty[b2], 1);
+      ptx::mbar_init(&dq_free[b2], 256);
+    }
     ptx::mbar_init(s_full, 1);
     ptx::mbar_init(st_free, 256);
     ptx::mbar_init(ds_full, 256);
     ptx::mbar_init(mm_done, 1);
-    for (int s2 = 0; s2 < 2; ++s2) ptx::mbar_init(&dq_free[s2], 256);
+    ptx::mbar_init(acc_free, 256);
     ptx::fence_barrier_init();
   }
   if (warp == 9) ptx::tmem_alloc(tmem_slot, 512);
@@ -401,34 +435,43 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp == 8) {
     if (lane == 0) {
-      ptx::mbar_arrive_expect_tx(kv_full, 2 * kTileBytes);
-      ptx::tma_load_2d(smem + kB_K, &tqkv, kv_full, H * kD + hd * kD, row_base + k0);
-      ptx::tma_load_2d(smem + kB_V, &tqkv, kv_full, 2 * H * kD + hd * kD, row_base + k0);
-    }
-    if (lane == 0) {
-      for (int it = 0; it < niter; ++it) {
-        const int st = it & 1, q0 = (j0 + it) * kQ;
-        ptx::mbar_wait_sleep(&qd_empty[st], ((it >> 1) & 1) ^ 1);
-        ATTN_TRACE(true, it, 9);
-        ptx::mbar_arrive_expect_tx(&qd_full[st], 2 * kTileBytes);
-        ptx::tma_load_2d(smem + kB_Q + st * kTileBytes, &tqkv, &qd_full[st], hd * kD, row_base + q0);
-        ptx::tma_load_2d(smem + kB_DO + st * kTileBytes, &tdo, &qd_full[st], hd * kD, row_base + q0);
+      int g = 0;
+      for (BwdSeq q = seq0; q.valid();) {
+        const int b = q.bh / H, hd = q.bh % H, row_base = b * seq;
+        const int kvb = q.n & 1, u = q.n >> 1;
+        ptx::mbar_wait_sleep(&kv_empty[kvb], (u & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&kv_full[kvb], 2 * kTileBytes);
+        ptx::tma_load_2d(smem + kB_K + kvb * kTileBytes, &tqkv, &kv_full[kvb], H * kD + hd * kD, row_base + q.kb * kKV);
+        ptx::tma_load_2d(smem + kB_V + kvb * kTileBytes, &tqkv, &kv_full[kvb], 2 * H * kD + hd * kD,
+                         row_base + q.kb * kKV);
+        const int n0 = q.n;
+        while (q.valid() && q.n == n0) {
+          const int st = g & 1, q0 = (q.j0 + q.it) * kQ;
+          ptx::mbar_wait_sleep(&qd_empty[st], ((g >> 1) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&qd_full[st], 2 * kTileBytes);
+          ptx::tma_load_2d(smem + kB_Q + st * kTileBytes, &tqkv, &qd_full[st], hd * kD, row_base + q0);
+          ptx::tma_load_2d(smem + kB_DO + st * kTileBytes, &tdo, &qd_full[st], hd * kD, row_base + q0);
+          ++g;
+          q.advance();
+        }
       }
     }
   } else if (warp == 9) {
-    if (lane == 0) {
+    if (lane == 0 && seq0.valid()) {
       constexpr uint32_t id_s = ptx::idesc_bf16(128, 128, false, false);
       constexpr uint32_t id_kv = ptx::idesc_bf16(128, 64, true, true);  // A = P^T / dS^T (MN-major), B MN-major
       constexpr uint32_t id_q = ptx::idesc_bf16(128, 64, false, true);  // A = dS (K-major), B = K (MN-major)
-      const uint32_t sk = ptx::smem_u32(smem + kB_K), sv = ptx::smem_u32(smem + kB_V);
       const uint32_t sp = ptx::smem_u32(smem + kB_P), sds = ptx::smem_u32(smem + kB_DS);
-      auto issue_s = [&](int it) {
-        const int st = it & 1;
+      // S / dP of iteration (g, item ordinal n) -- waits for that item's K/V the first time
+      auto issue_s = [&](int g, int n, bool first_of_item) {
+        const int st = g & 1, kvb = n & 1;
+        if (first_of_item) mma_wait(&kv_full[kvb], (n >> 1) & 1);
+        mma_wait(&qd_full[st], (g >> 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t sk = ptx::smem_u32(smem + kB_K + kvb * kTileBytes);
+        const uint32_t sv = ptx::smem_u32(smem + kB_V + kvb * kTileBytes);
         const uint32_t sq = ptx::smem_u32(smem + kB_Q + st * kTileBytes);
         const uint32_t sdo = ptx::smem_u32(smem + kB_DO + st * kTileBytes);
-        mma_wait(&qd_full[st], (it >> 1) & 1);
-        ATTN_TRACE(true, it, 0);
-        ptx::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kD / 16; ++k) {
           ptx::umma_f16(tmem + kS, ptx::smem_desc_sw128(sq + k * 32, 16, 1024), ptx::smem_desc_sw128(sk + k * 32, 16, 1024),
@@ -438,19 +481,24 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         ptx::umma_commit(s_full);
       };
-      ptx::mbar_wait(kv_full, 0);
-      issue_s(0);
-      for (int it = 0; it < niter; ++it) {
-        const int st = it & 1;
-        if (it + 1 < niter) {  // tile it's S^T / dP^T are in registers: next tile's scores now
-          mma_wait(st_free, it & 1);
+      issue_s(0, 0, true);
+      int g = 0;
+      for (BwdSeq q = seq0; q.valid(); ++g) {
+        const int st = g & 1, n = q.n, kvb = n & 1, it = q.it;
+        const bool last = it + 1 == q.niter;
+        BwdSeq nx = q;
+        nx.advance();
+        if (nx.valid()) {  // this tile's S / dP are in registers: next tile's scores now
+          mma_wait(st_free, g & 1);
           ptx::tc_fence_after();
-          issue_s(it + 1);
+          issue_s(g + 1, nx.n, nx.n != n);
         }
+        const uint32_t sk = ptx::smem_u32(smem + kB_K + kvb * kTileBytes);
         const uint32_t sq = ptx::smem_u32(smem + kB_Q + st * kTileBytes);
         const uint32_t sdo = ptx::smem_u32(smem + kB_DO + st * kTileBytes);
-        mma_wait(ds_full, it & 1);  // P^T, dS^T of tile it in smem
-        ATTN_TRACE(true, it, 1);
+        mma_wait(ds_full, g & 1);  // P, dS of this tile in smem
+        ATTN_TRACE(true, g, 1);
+        if (it == 0 && n > 0) mma_wait(acc_free, (n - 1) & 1);  // previous item's dK / dV read out
         ptx::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kQ / 16; ++k) {  // reduce over 16 queries per step
@@ -461,76 +509,86 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           ptx::umma_f16(tmem + kDK, a_ds, ptx::smem_desc_sw128(sq + k * 2048, kTileBytes, 1024), id_kv,
                         (it > 0 || k > 0) ? 1u : 0u);
         }
-        ptx::umma_commit(&qd_empty[st]);  // Q / dO of tile it: last read by dK / dV
-        if (it >= 2) mma_wait(&dq_free[st], ((it >> 1) & 1) ^ 1);  // dQ_{it-2} drained
-        ATTN_TRACE(true, it, 2);
+        ptx::umma_commit(&qd_empty[st]);  // Q / dO of this tile: last read by dK / dV
+        if (g >= 2) mma_wait(&dq_free[st], ((g >> 1) & 1) ^ 1);  // dQ_{g-2} drained
+        ATTN_TRACE(true, g, 2);
         ptx::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kKV / 16; ++k)  // dQ = dS K: reduce over 16 keys per step
           ptx::umma_f16(tmem + kDQ + 64 * st, ptx::smem_desc_sw128(sds + (k >> 2) * kTileBytes + (k & 3) * 32, 16, 1024),
                         ptx::smem_desc_sw128(sk + k * 2048, kTileBytes, 1024), id_q, k > 0);
         ptx::umma_commit(mm_done);
+        if (last) ptx::umma_commit(&kv_empty[kvb]);  // this item's K / V no longer read
+        q = nx;
       }
     }
   } else {
-    const int g = warp >> 2;                 // compute warpgroup: key columns [64g, 64g+64)
-    const int r = (warp & 3) * 32 + lane;    // TMEM lane: query row (S, dP, dQ) / key row (dK, dV)
-    const int ct = threadIdx.x & 127;        // thread within the WG
+    const int g2 = warp >> 2;               // compute warpgroup: key columns [64 g2, 64 g2 + 64)
+    const int r = (warp & 3) * 32 + lane;   // TMEM lane: query row (S, dP, dQ) / key row (dK, dV)
+    const int ct = threadIdx.x & 127;       // thread within the WG
     const uint32_t trow = tmem + (uint32_t((warp & 3) * 32) << 16);
     const float sl2 = 0.125f * kLog2e;
-    uint8_t* sp = smem + kB_P + g * kTileBytes;
-    uint8_t* sds = smem + kB_DS + g * kTileBytes;
-    uint8_t* stage = smem + kB_DQ + g * kTileBytes;
-    // dQ_j (TMEM buffer j&1) -> swizzled smem stage -> TMA reduce-add; this WG's 32 columns
-    auto drain_dq = [&](int j) {
-      const int qj0 = (j0 + j) * kQ;
-      if (ct == 0) ptx::bulk_wait_read0();  // previous reduce has read the stage
-      named_bar_sync(2 + g, 128);
+    uint8_t* sp = smem + kB_P + g2 * kTileBytes;
+    uint8_t* sds = smem + kB_DS + g2 * kTileBytes;
+    uint8_t* stage = smem + kB_DQ + g2 * kTileBytes;
+    // the WG's stage is free once its previous bulk op has read it
+    auto stage_acquire = [&] {
+      if (ct == 0) ptx::bulk_wait_read0();
+      named_bar_sync(2 + g2, 128);
+    };
+    auto stage_release = [&] {
+      ptx::fence_proxy_async();
+      named_bar_sync(2 + g2, 128);
+    };
+    // dQ of global iteration g (query tile q0, head (b, hd)) -> TMA reduce-add; 32 columns
+    auto drain_dq = [&](int g, int q0, int row_base, int hd) {
+      stage_acquire();
       uint32_t v[32];
-      ptx::tmem_ld32(trow + kDQ + 64 * (j & 1) + 32 * g, v);
+      ptx::tmem_ld32(trow + kDQ + 64 * (g & 1) + 32 * g2, v);
       ptx::tmem_ld_wait();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&dq_free[j & 1]);
+      ptx::mbar_arrive(&dq_free[g & 1]);
 #pragma unroll
       for (int c = 0; c < 8; ++c)
         *reinterpret_cast<uint4*>(stage + r * 128 + ((c ^ (r & 7)) << 4)) =
             make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-      ptx::fence_proxy_async();
-      named_bar_sync(2 + g, 128);
+      stage_release();
       if (ct == 0) {
-        ptx::tma_reduce_add_2d(&tdq, stage, hd * kD + 32 * g, row_base + qj0);
+        ptx::tma_reduce_add_2d(&tdq, stage, hd * kD + 32 * g2, row_base + q0);
         ptx::bulk_commit();
       }
     };
-    // this row's -lse*log2(e) and -D, fetched one tile ahead
-    auto fetch = [&](int it, float& nl, float& nd) {
-      const int q = (j0 + it) * kQ + r;
-      nl = q < seq ? -lse[(long long)bh * seq + q] * kLog2e : 0.f;
-      nd = q < seq ? -Dv[(long long)bh * seq + q] : 0.f;
+    auto fetch = [&](const BwdSeq& q, float& nl, float& nd) {  // -lse*log2(e), -D of this row
+      nl = 0.f, nd = 0.f;
+      if (!q.valid()) return;
+      const int qi = (q.j0 + q.it) * kQ + r;
+      if (qi < seq) nl = -lse[(long long)q.bh * seq + qi] * kLog2e, nd = -Dv[(long long)q.bh * seq + qi];
     };
-    float nl, nd;
-    fetch(0, nl, nd);
     const float2 sc2 = make_float2(sl2, sl2);
-    for (int it = 0; it < niter; ++it) {
-      const int q0 = (j0 + it) * kQ, q = q0 + r;
-      ATTN_TRACE(threadIdx.x == 0, it, 3);
-      ptx::mbar_wait(s_full, it & 1);
-      ATTN_TRACE(threadIdx.x == 0, it, 5);
+    float nl, nd;
+    fetch(seq0, nl, nd);
+    int g = 0;
+    for (BwdSeq q = seq0; q.valid(); ++g) {
+      const int b = q.bh / H, hd = q.bh % H, row_base = b * seq;
+      const int k0 = q.kb * kKV, q0 = (q.j0 + q.it) * kQ, qr = q0 + r, it = q.it;
+      const bool last = it + 1 == q.niter;
+      ATTN_TRACE(threadIdx.x == 0, g, 3);
+      ptx::mbar_wait(s_full, g & 1);
+      ATTN_TRACE(threadIdx.x == 0, g, 5);
       ptx::tc_fence_after();
       uint32_t rs[2][32], rd[2][32];
-      ptx::tmem_ld32(trow + kS + 64 * g, rs[0]);
-      ptx::tmem_ld32(trow + kS + 64 * g + 32, rs[1]);
-      ptx::tmem_ld32(trow + kDP + 64 * g, rd[0]);
-      ptx::tmem_ld32(trow + kDP + 64 * g + 32, rd[1]);
+      ptx::tmem_ld32(trow + kS + 64 * g2, rs[0]);
+      ptx::tmem_ld32(trow + kS + 64 * g2 + 32, rs[1]);
+      ptx::tmem_ld32(trow + kDP + 64 * g2, rd[0]);
+      ptx::tmem_ld32(trow + kDP + 64 * g2 + 32, rd[1]);
       ptx::tmem_ld_wait();
-      ATTN_TRACE(threadIdx.x == 0, it, 10);
       ptx::tc_fence_before();
       ptx::mbar_arrive(st_free);
       // masking only on diagonal / tail tiles (warp-uniform branch): keys of this WG's
       // block at index >= hi drop to a -inf score (P = dS = 0); rows past seq drop out
       if ((CAUSAL && k0 + kKV - 1 > q0) || q0 + kQ > seq || k0 + kKV > seq) {
-        const int kg = k0 + 64 * g;
-        const int hi = q >= seq ? 0 : min(CAUSAL ? q - kg + 1 : 64, seq - kg);
+        const int kg = k0 + 64 * g2;
+        const int hi = qr >= seq ? 0 : min(CAUSAL ? qr - kg + 1 : 64, seq - kg);
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -555,54 +613,64 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           pk[c >> 1] = *reinterpret_cast<uint32_t*>(&hp);
           dk[c >> 1] = *reinterpret_cast<uint32_t*>(&hs);
         }
-      if (it + 1 < niter) fetch(it + 1, nl, nd);
-      ATTN_TRACE(threadIdx.x == 0, it, 11);
-      if (it > 0) {  // tile it-1's dV / dK / dQ MMAs have read the P / dS tiles
-        ptx::mbar_wait(mm_done, (it - 1) & 1);
+      BwdSeq nx = q;
+      nx.advance();
+      fetch(nx, nl, nd);
+      if (g > 0) {  // the previous tile's dV / dK / dQ MMAs have read the P / dS tiles
+        ptx::mbar_wait(mm_done, (g - 1) & 1);
         ptx::tc_fence_after();
       }
-      ATTN_TRACE(threadIdx.x == 0, it, 12);
 #pragma unroll
       for (int k8 = 0; k8 < 8; ++k8) {  // 8 keys -> one 16-byte chunk of this WG's block
         const int off = r * 128 + ((k8 ^ (r & 7)) << 4);
         *reinterpret_cast<uint4*>(sp + off) = make_uint4(pk[4 * k8], pk[4 * k8 + 1], pk[4 * k8 + 2], pk[4 * k8 + 3]);
         *reinterpret_cast<uint4*>(sds + off) = make_uint4(dk[4 * k8], dk[4 * k8 + 1], dk[4 * k8 + 2], dk[4 * k8 + 3]);
       }
-      ATTN_TRACE(threadIdx.x == 0, it, 6);
+      ATTN_TRACE(threadIdx.x == 0, g, 6);
       ptx::fence_proxy_async();
       ptx::tc_fence_before();
       ptx::mbar_arrive(ds_full);
-      if (it > 0) drain_dq(it - 1);
-      ATTN_TRACE(threadIdx.x == 0, it, 8);
-    }
-    ptx::mbar_wait(mm_done, (niter - 1) & 1);
-    ATTN_TRACE(threadIdx.x == 0, niter - 1, 7);
-    ptx::tc_fence_after();
-    drain_dq(niter - 1);
-    // dK (WG 0, scaled by 1/sqrt(d)) or dV (WG 1) for this key tile: TMEM lane <-> key row
-    {
-      const uint32_t base = g == 0 ? kDK : kDV;
-      const float sc = g == 0 ? 0.125f : 1.f;
-#pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
-        uint32_t v[32];
-        ptx::tmem_ld32(trow + base + c * 32, v);
+      if (it > 0) drain_dq(g - 1, q0 - kQ, row_base, hd);
+      if (last) {  // item epilogue: last dQ, then dK (WG 0, x 1/sqrt(d)) or dV (WG 1)
+        ptx::mbar_wait(mm_done, g & 1);
+        ptx::tc_fence_after();
+        drain_dq(g, q0, row_base, hd);
+        uint32_t v[2][32];
+        ptx::tmem_ld32(trow + (g2 == 0 ? kDK : kDV), v[0]);
+        ptx::tmem_ld32(trow + (g2 == 0 ? kDK : kDV) + 32, v[1]);
         ptx::tmem_ld_wait();
-        if (k0 + r < seq) {
-          bf16* dst = dqkv + ((long long)row_base + k0 + r) * (3LL * H * kD) + (1 + g) * (long long)H * kD + hd * kD + c * 32;
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(acc_free);
+        const float sc = g2 == 0 ? 0.125f : 1.f;
+        uint4 w[8];  // key row r: 64 bf16 = 8 chunks of 16 bytes
 #pragma unroll
-          for (int q8 = 0; q8 < 4; ++q8) {
-            uint32_t pk[4];
+        for (int c = 0; c < 8; ++c) {
+          uint32_t w4[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              __nv_bfloat162 hb = __floats2bfloat162_rn(__uint_as_float(v[q8 * 8 + 2 * e]) * sc,
-                                                        __uint_as_float(v[q8 * 8 + 2 * e + 1]) * sc);
-              pk[e] = *reinterpret_cast<uint32_t*>(&hb);
-            }
-            *reinterpret_cast<uint4*>(dst + q8 * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          for (int e = 0; e < 4; ++e) {
+            const int j = c * 8 + 2 * e;
+            __nv_bfloat162 hb = __floats2bfloat162_rn(__uint_as_float(v[j >> 5][j & 31]) * sc,
+                                                      __uint_as_float(v[j >> 5][(j & 31) + 1]) * sc);
+            w4[e] = *reinterpret_cast<uint32_t*>(&hb);
           }
+          w[c] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+        }
+        if (k0 + kKV <= seq) {  // whole tile inside the sequence: swizzled stage + TMA store
+          stage_acquire();
+#pragma unroll
+          for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(stage + r * 128 + ((c ^ (r & 7)) << 4)) = w[c];
+          stage_release();
+          if (ct == 0) {
+            ptx::tma_store_2d(&tdqkv, stage, (1 + g2) * H * kD + hd * kD, row_base + k0);
+            ptx::bulk_commit();
+          }
+        } else if (k0 + r < seq) {  // sequence tail: rows past seq belong to the next sequence
+          bf16* dst = dqkv + ((long long)row_base + k0 + r) * (3LL * H * kD) + (1 + g2) * (long long)H * kD + hd * kD;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(dst + c * 8) = w[c];
         }
       }
+      q = nx;
     }
     if (ct == 0) ptx::bulk_wait0();
   }
@@ -643,15 +711,17 @@ void attn_bwd_tc(const bf16* qkv, const bf16* out, const bf16* dout, const float
   const CUtensorMap mq = cuda::make_map_2d_bf16(qkv, ld, (long long)M, ld, 64, 128);
   const CUtensorMap mo = cuda::make_map_2d_bf16(dout, (long long)H * kD, (long long)M, (long long)H * kD, 64, 128);
   const CUtensorMap mdq = cuda::make_map_2d_f32(dq, (long long)H * kD, (long long)M, (long long)H * kD, 32, 128);
+  const CUtensorMap mdqkv = cuda::make_map_2d_bf16(dqkv, ld, (long long)M, ld, 64, 128);
   static bool attr = false;
   if (!attr) {
     CK_CUDA(cudaFuncSetAttribute(k_attn_bwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem));
     CK_CUDA(cudaFuncSetAttribute(k_attn_bwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem));
     attr = true;
   }
-  const dim3 grid((seq + kKV - 1) / kKV * B * H);
-  if (causal) k_attn_bwd_tc<true><<<grid, kBwdThreads, kBwdSmem, st>>>(mq, mo, mdq, lse, D, dqkv, seq, H);
-  else k_attn_bwd_tc<false><<<grid, kBwdThreads, kBwdSmem, st>>>(mq, mo, mdq, lse, D, dqkv, seq, H);
+  const int items = (seq + kKV - 1) / kKV * B * H;
+  const dim3 grid(std::min(items, cuda::kNumSMs));  // persistent: one CTA per SM
+  if (causal) k_attn_bwd_tc<true><<<grid, kBwdThreads, kBwdSmem, st>>>(mq, mo, mdq, mdqkv, lse, D, dqkv, seq, H, B * H);
+  else k_attn_bwd_tc<false><<<grid, kBwdThreads, kBwdSmem, st>>>(mq, mo, mdq, mdqkv, lse, D, dqkv, seq, H, B * H);
   CK_CUDA(cudaGetLastError());
   attn_dq_out(dq, dqkv, M, H, st);
 }
