@@ -4,16 +4,17 @@
 //   warp 4  TMA producer: Q once, then 128-key K/V tiles into a 2-stage ring
 //   warp 5  TMEM allocator + single-thread MMA issuer:
 //             S  = Q K^T      tcgen05.mma kind::f16 M128 N128 K64  -> TMEM cols [0,128)
-//             O += P V        tcgen05.mma kind::f16 M128 N64  K128 -> TMEM cols [128,192)
+//             O += P V        tcgen05.mma kind::f16 M128 N64  K128 -> TMEM cols [128,192),
+//                             A = P straight from TMEM cols [192,256) (bf16 pairs)
 //   warps 0-3  softmax: thread t owns query row t (= TMEM lane t): the S row is pulled
 //             into registers in one pass, which frees the S columns at once (s_free) so
-//             the MMA warp computes S_{j+1} underneath this tile's exp2s; P is written as
-//             bf16 straight into the 128-byte-swizzled K-major smem tile the PV MMA reads,
-//             running O rescaled in TMEM (tcgen05.ld/st) only when a row max moves; final
-//             O / l and the log-sum-exp go to HBM.
+//             the MMA warp computes S_{j+1} underneath this tile's exp2s; P goes back to
+//             TMEM as bf16 pairs (tcgen05.st) for the PV MMA, running O is rescaled in
+//             TMEM only when a row max moves by more than 2^8; final O / l and the
+//             log-sum-exp go to HBM.
 // The Q/K/V tiles come straight out of the packed [tokens, 3*H*64] QKV GEMM output via
 // one 2-D TMA map (no head split), so the kernel reads exactly Q, K, V once per tile.
-// ~112 KB smem and 256 TMEM columns per CTA: two CTAs per SM overlap one CTA's softmax
+// ~80 KB smem and 256 TMEM columns per CTA: two CTAs per SM overlap one CTA's softmax
 // with the other's MMAs.
 #include <cuda.h>
 
@@ -57,8 +58,8 @@ namespace {
 using ptx::ex2_approx;
 constexpr int kQ = 128, kKV = 128, kD = 64;
 constexpr int kTileBytes = kQ * kD * 2;  // 16 KB: 128 rows x 128 B
-constexpr int kSmemQ = 0, kSmemK = kTileBytes, kSmemV = 3 * kTileBytes, kSmemP = 5 * kTileBytes;
-constexpr int kSmemBar = 7 * kTileBytes;  // after P (2 tiles)
+constexpr int kSmemQ = 0, kSmemK = 2 * kTileBytes, kSmemV = 4 * kTileBytes;  // Q[2], K[2], V[2]
+constexpr int kSmemBar = 6 * kTileBytes;
 constexpr int kSmemTotal = kSmemBar + 256;
 constexpr float kLog2e = 1.4426950408889634f;
 // Share of the softmax exp2s computed by ptx::ex2_poly2 on the FMA pipes: every
@@ -90,69 +91,107 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// The CTA's sequence of (query tile item, key tile) iterations: items (qb, batch*head)
+// heaviest first (under causal masking the last query tiles see the most key tiles),
+// dealt boustrophedon-wise over the persistent CTAs.
+struct FwdSeq {
+  int G, c, n_items, BH, nq;
+  bool causal;
+  int r = 0, n = 0;  // round, item ordinal within this CTA
+  int item = -1, qb = 0, bh = 0, nkb = 0, j = 0;
+  __device__ int item_of(int rr) const {
+    const int i = rr * G + ((rr & 1) ? G - 1 - c : c);
+    return i < n_items ? i : -1;
+  }
+  __device__ void load() {
+    item = item_of(r);
+    if (item < 0) return;
+    const int tile = item / BH;
+    bh = item % BH, qb = causal ? nq - 1 - tile : tile, nkb = causal ? qb + 1 : nq, j = 0;
+  }
+  __device__ bool valid() const { return item >= 0; }
+  __device__ void advance() {
+    if (++j == nkb) {
+      ++r, ++n;
+      load();
+    }
+  }
+};
+
+// Persistent: two CTAs per SM, each walking its items; the next item's Q lands in the
+// second Q buffer and its first S MMA runs while the current item's O is written out.
 template <bool CAUSAL>
 __global__ void __launch_bounds__(192, 2)
     k_attn_fwd_tc(const __grid_constant__ CUtensorMap tqkv, bf16* __restrict__ out, float* __restrict__ lse,
-                  int seq, int H) {
+                  int seq, int H, int BH) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((ptx::smem_u32(smem) & 1023) != 0) __trap();  // swizzle atoms need 1 KB alignment
   ATTN_CTA(0);
   ATTN_CTA(1);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kSmemBar);
-  uint64_t *q_full = bar, *kv_full = bar + 1, *kv_empty = bar + 3, *s_full = bar + 5, *p_full = bar + 6,
-           *o_done = bar + 7, *s_free = bar + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
+  uint64_t *q_full = bar, *q_empty = bar + 2, *kv_full = bar + 4, *kv_empty = bar + 6, *s_full = bar + 8,
+           *p_full = bar + 9, *o_done = bar + 10, *s_free = bar + 11, *o_free = bar + 12;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // 1-D grid, tile-major: with causal masking the longest query tiles (most key tiles) of
-  // every head are dispatched first, so the short ones fill the tail of the last wave
-  const int BH = gridDim.x / ((seq + kQ - 1) / kQ);
-  const int tile = blockIdx.x / BH, bh = blockIdx.x % BH, b = bh / H, hd = bh % H;
-  const int qb = CAUSAL ? (seq + kQ - 1) / kQ - 1 - tile : tile;
-  const int q0 = qb * kQ, row_base = b * seq;
-  const int nkv = (seq + kKV - 1) / kKV;
-  const int nkb = CAUSAL ? min(nkv, qb + 1) : nkv;
+  const int nq = (seq + kQ - 1) / kQ;
+  FwdSeq seq0;
+  seq0.G = gridDim.x, seq0.c = blockIdx.x, seq0.n_items = nq * BH, seq0.BH = BH, seq0.nq = nq, seq0.causal = CAUSAL;
+  seq0.load();
 
   if (warp == 4 && lane == 0) {
     ptx::tma_prefetch(&tqkv);
-    ptx::mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) ptx::mbar_init(&kv_full[s], 1), ptx::mbar_init(&kv_empty[s], 1);
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&q_full[s], 1), ptx::mbar_init(&q_empty[s], 1);
+      ptx::mbar_init(&kv_full[s], 1), ptx::mbar_init(&kv_empty[s], 1);
+    }
     ptx::mbar_init(s_full, 1);
     ptx::mbar_init(p_full, 128);
     ptx::mbar_init(o_done, 1);
     ptx::mbar_init(s_free, 128);
+    ptx::mbar_init(o_free, 128);
     ptx::fence_barrier_init();
   }
   if (warp == 5) ptx::tmem_alloc(tmem_slot, 256);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;  // S: cols [0,128), O: cols [128,192)
+  const uint32_t tmem = *tmem_slot;  // S: cols [0,128), O: [128,192), P (bf16 pairs): [192,256)
 
   if (warp == 4) {
     if (lane == 0) {
-      ptx::mbar_arrive_expect_tx(q_full, kTileBytes);
-      ptx::tma_load_2d(smem + kSmemQ, &tqkv, q_full, hd * kD, row_base + q0);
-      for (int j = 0; j < nkb; ++j) {
-        const int st = j & 1;
-        ptx::mbar_wait_sleep(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        ATTN_TRACE(true, j, 0);
-        ptx::mbar_arrive_expect_tx(&kv_full[st], 2 * kTileBytes);
-        ptx::tma_load_2d(smem + kSmemK + st * kTileBytes, &tqkv, &kv_full[st], H * kD + hd * kD, row_base + j * kKV);
-        ptx::tma_load_2d(smem + kSmemV + st * kTileBytes, &tqkv, &kv_full[st], 2 * H * kD + hd * kD,
-                         row_base + j * kKV);
+      int g = 0;
+      for (FwdSeq q = seq0; q.valid();) {
+        const int b = q.bh / H, hd = q.bh % H, row_base = b * seq, qbuf = q.n & 1;
+        ptx::mbar_wait_sleep(&q_empty[qbuf], ((q.n >> 1) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&q_full[qbuf], kTileBytes);
+        ptx::tma_load_2d(smem + kSmemQ + qbuf * kTileBytes, &tqkv, &q_full[qbuf], hd * kD, row_base + q.qb * kQ);
+        const int n0 = q.n;
+        while (q.valid() && q.n == n0) {
+          const int st = g & 1;
+          ptx::mbar_wait_sleep(&kv_empty[st], ((g >> 1) & 1) ^ 1);
+          ATTN_TRACE(true, g, 0);
+          ptx::mbar_arrive_expect_tx(&kv_full[st], 2 * kTileBytes);
+          ptx::tma_load_2d(smem + kSmemK + st * kTileBytes, &tqkv, &kv_full[st], H * kD + hd * kD,
+                           row_base + q.j * kKV);
+          ptx::tma_load_2d(smem + kSmemV + st * kTileBytes, &tqkv, &kv_full[st], 2 * H * kD + hd * kD,
+                           row_base + q.j * kKV);
+          ++g;
+          q.advance();
+        }
       }
     }
   } else if (warp == 5) {
-    if (lane == 0) {
+    if (lane == 0 && seq0.valid()) {
       constexpr uint32_t id_s = ptx::idesc_bf16(kQ, kKV, false, false);
       constexpr uint32_t id_o = ptx::idesc_bf16(kQ, kD, false, true);
-      const uint32_t sq = ptx::smem_u32(smem + kSmemQ), sp = ptx::smem_u32(smem + kSmemP);
-      auto issue_s = [&](int j) {
-        const int st = j & 1;
-        mma_wait(&kv_full[st], (j >> 1) & 1);
-        ATTN_TRACE(true, j, 1);
+      auto issue_s = [&](int g, int n, bool first_of_item) {
+        const int st = g & 1, qbuf = n & 1;
+        if (first_of_item) mma_wait(&q_full[qbuf], (n >> 1) & 1);
+        mma_wait(&kv_full[st], (g >> 1) & 1);
+        ATTN_TRACE(true, g, 1);
         ptx::tc_fence_after();
+        const uint32_t sq = ptx::smem_u32(smem + kSmemQ + qbuf * kTileBytes);
         const uint32_t sk = ptx::smem_u32(smem + kSmemK + st * kTileBytes);
 #pragma unroll
         for (int k = 0; k < kD / 16; ++k)
@@ -160,39 +199,49 @@ __global__ void __launch_bounds__(192, 2)
                         id_s, k > 0);
         ptx::umma_commit(s_full);
       };
-      ptx::mbar_wait(q_full, 0);
-      issue_s(0);
-      for (int j = 0; j < nkb; ++j) {
-        if (j + 1 < nkb) {  // S_j is in the softmax registers: compute S_{j+1} under its exp2s
-          mma_wait(s_free, j & 1);
-          ATTN_TRACE(true, j, 2);
+      issue_s(0, 0, true);
+      int g = 0;
+      for (FwdSeq q = seq0; q.valid(); ++g) {
+        const int n = q.n, j = q.j;
+        const bool last = j + 1 == q.nkb;
+        FwdSeq nx = q;
+        nx.advance();
+        if (nx.valid()) {  // S_g is in the softmax registers: compute the next scores now
+          mma_wait(s_free, g & 1);
+          ATTN_TRACE(true, g, 2);
           ptx::tc_fence_after();
-          issue_s(j + 1);
+          issue_s(g + 1, nx.n, nx.n != n);
         }
-        mma_wait(p_full, j & 1);  // P_j in smem, O rescaled
-        ATTN_TRACE(true, j, 3);
+        mma_wait(p_full, g & 1);  // P_g in TMEM, O rescaled
+        ATTN_TRACE(true, g, 3);
+        if (j == 0 && n > 0) mma_wait(o_free, (n - 1) & 1);  // previous item's O read out
         ptx::tc_fence_after();
-        const uint32_t sv = ptx::smem_u32(smem + kSmemV + (j & 1) * kTileBytes);
+        const uint32_t sv = ptx::smem_u32(smem + kSmemV + (g & 1) * kTileBytes);
 #pragma unroll
-        for (int k = 0; k < kKV / 16; ++k)
-          ptx::umma_f16(tmem + 128, ptx::smem_desc_sw128(sp + (k >> 2) * kTileBytes + (k & 3) * 32, 16, 1024),
-                        ptx::smem_desc_sw128(sv + k * 2048, kTileBytes, 1024), id_o, (j > 0 || k > 0) ? 1u : 0u);
-        ptx::umma_commit(&kv_empty[j & 1]);
+        for (int k = 0; k < kKV / 16; ++k)  // A = P from TMEM cols [192, 256): 16 keys = 8 columns
+          ptx::umma_f16_ts(tmem + 128, tmem + 192 + k * 8, ptx::smem_desc_sw128(sv + k * 2048, kTileBytes, 1024), id_o,
+                           (j > 0 || k > 0) ? 1u : 0u);
+        ptx::umma_commit(&kv_empty[g & 1]);
         ptx::umma_commit(o_done);
+        if (last) ptx::umma_commit(&q_empty[n & 1]);
+        q = nx;
       }
     }
   } else {
-    // softmax warps: thread t <-> query row t <-> TMEM lane t
+    // softmax warps: thread t owns query row t (= TMEM lane t)
     const int t = threadIdx.x;  // 0..127
-    const int q = q0 + t;
     const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
     const float sl2 = 0.125f * kLog2e;
     float m = -INFINITY, l = 0.f;
-    uint8_t* sp = smem + kSmemP;
-    for (int j = 0; j < nkb; ++j) {
-      ATTN_TRACE(t == 0, j, 4);
-      ptx::mbar_wait(s_full, j & 1);
-      ATTN_TRACE(t == 0, j, 5);
+    int g = 0;
+    for (FwdSeq q = seq0; q.valid(); ++g) {
+      const int b = q.bh / H, hd = q.bh % H, row_base = b * seq;
+      const int q0 = q.qb * kQ, qr = q0 + t, j = q.j;
+      const bool last = j + 1 == q.nkb;
+      if (j == 0) m = -INFINITY, l = 0.f;
+      ATTN_TRACE(t == 0, g, 4);
+      ptx::mbar_wait(s_full, g & 1);
+      ATTN_TRACE(t == 0, g, 5);
       ptx::tc_fence_after();
       const int key0 = j * kKV;
       // the whole 128-score row lives in registers (one TMEM pass)
@@ -200,13 +249,13 @@ __global__ void __launch_bounds__(192, 2)
 #pragma unroll
       for (int c = 0; c < 4; ++c) ptx::tmem_ld32(trow + c * 32, r[c]);
       ptx::tmem_ld_wait();
-      ATTN_TRACE(t == 0, j, 6);
+      ATTN_TRACE(t == 0, g, 6);
       ptx::tc_fence_before();
       ptx::mbar_arrive(s_free);
       // masking only on the diagonal (causal) / sequence-tail tile (warp-uniform branch):
       // keys past `lim` (tile-relative) drop out as raw -inf scores
       if ((CAUSAL && key0 + kKV - 1 > q0) || key0 + kKV > seq) {
-        const int lim = CAUSAL ? min(q - key0, seq - 1 - key0) : seq - 1 - key0;
+        const int lim = CAUSAL ? min(qr - key0, seq - 1 - key0) : seq - 1 - key0;
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
@@ -231,9 +280,9 @@ __global__ void __launch_bounds__(192, 2)
       const float alpha = ex2_approx(m - safe);
       m = mn;
       l *= alpha;
-      ATTN_TRACE(t == 0, j, 7);
+      ATTN_TRACE(t == 0, g, 7);
       // P = exp2(s * scale - m) -> bf16 pairs in registers first, so that the previous
-      // P V (which still reads the P tile and writes O) completes underneath
+      // P V (which still reads the P columns and writes O) completes underneath
       const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-safe, -safe);
       float2 ls[4] = {};  // independent packed sum chains
       uint32_t pk[64];
@@ -245,7 +294,7 @@ __global__ void __launch_bounds__(192, 2)
           // every kPolyEvery-th pair on the FMA pipes, the rest on MUFU
           const float2 p = (kPolyEvery > 0 && (i >> 1) % (kPolyEvery > 0 ? kPolyEvery : 1) == kPolyEvery - 1)
                                ? ptx::ex2_poly2(x)
-                                                                      : make_float2(ex2_approx(x.x), ex2_approx(x.y));
+                               : make_float2(ex2_approx(x.x), ex2_approx(x.y));
           ls[(i >> 1) & 3] = ptx::add2(ls[(i >> 1) & 3], p);
           __nv_bfloat162 hb = __floats2bfloat162_rn(p.x, p.y);
           pk[c * 16 + (i >> 1)] = *reinterpret_cast<uint32_t*>(&hb);
@@ -254,11 +303,11 @@ __global__ void __launch_bounds__(192, 2)
         const float2 s01 = ptx::add2(ptx::add2(ls[0], ls[1]), ptx::add2(ls[2], ls[3]));
         l += s01.x + s01.y;
       }
-      if (j > 0) {  // the previous P V must have landed before O is touched / P rewritten
-        ptx::mbar_wait(o_done, (j - 1) & 1);
-        ATTN_TRACE(t == 0, j, 8);
+      if (g > 0) {  // the previous P V must have read P (and, within the item, written O)
+        ptx::mbar_wait(o_done, (g - 1) & 1);
+        ATTN_TRACE(t == 0, g, 8);
         ptx::tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {  // rescale only when a row max moved
+        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {  // rescale only when a row max moved
 #pragma unroll 1
           for (int c = 0; c < 2; ++c) {
             uint32_t o[32];
@@ -276,42 +325,42 @@ __global__ void __launch_bounds__(192, 2)
           tmem_st_wait();
         }
       }
-      // P into the 128-byte-swizzled K-major tile: 8 keys -> one 16-byte chunk
-#pragma unroll
-      for (int k8 = 0; k8 < 16; ++k8) {
-        uint8_t* dst = sp + (k8 >> 3) * kTileBytes + t * 128 + (((k8 & 7) ^ (t & 7)) << 4);
-        *reinterpret_cast<uint4*>(dst) = make_uint4(pk[4 * k8], pk[4 * k8 + 1], pk[4 * k8 + 2], pk[4 * k8 + 3]);
-      }
-      ATTN_TRACE(t == 0, j, 9);
-      ptx::fence_proxy_async();  // P (generic stores) -> visible to the tensor core
+      // P (bf16 pairs) into TMEM cols [192, 256) of this row: the PV MMA's A operand
+      tmem_st32(trow + 192, *reinterpret_cast<const uint32_t(*)[32]>(pk));
+      tmem_st32(trow + 224, *reinterpret_cast<const uint32_t(*)[32]>(pk + 32));
+      tmem_st_wait();
+      ATTN_TRACE(t == 0, g, 9);
       ptx::tc_fence_before();
       ptx::mbar_arrive(p_full);
-    }
-    // epilogue: O / l -> bf16, log-sum-exp
-    ptx::mbar_wait(o_done, (nkb - 1) & 1);
-    ptx::tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-#pragma unroll 1
-    for (int c = 0; c < 2; ++c) {
-      uint32_t r[32];
-      ptx::tmem_ld32(trow + 128 + c * 32, r);
-      ptx::tmem_ld_wait();
-      if (q < seq) {
-        bf16* orow = out + ((long long)row_base + q) * (H * kD) + hd * kD + c * 32;
+      if (last) {  // item epilogue: O / l -> bf16, log-sum-exp
+        ptx::mbar_wait(o_done, g & 1);
+        ptx::tc_fence_after();
+        uint32_t o[2][32];
+        ptx::tmem_ld32(trow + 128, o[0]);
+        ptx::tmem_ld32(trow + 160, o[1]);
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(o_free);
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        if (qr < seq) {
+          bf16* orow = out + ((long long)row_base + qr) * (H * kD) + hd * kD;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          uint32_t pk[4];
+          for (int g8 = 0; g8 < 8; ++g8) {
+            uint32_t pk4[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            __nv_bfloat162 hb = __floats2bfloat162_rn(__uint_as_float(r[g * 8 + 2 * e]) * inv,
-                                                      __uint_as_float(r[g * 8 + 2 * e + 1]) * inv);
-            pk[e] = *reinterpret_cast<uint32_t*>(&hb);
+            for (int e = 0; e < 4; ++e) {
+              const int jj = g8 * 8 + 2 * e;
+              __nv_bfloat162 hb = __floats2bfloat162_rn(__uint_as_float(o[jj >> 5][jj & 31]) * inv,
+                                                        __uint_as_float(o[jj >> 5][(jj & 31) + 1]) * inv);
+              pk4[e] = *reinterpret_cast<uint32_t*>(&hb);
+            }
+            *reinterpret_cast<uint4*>(orow + g8 * 8) = make_uint4(pk4[0], pk4[1], pk4[2], pk4[3]);
           }
-          *reinterpret_cast<uint4*>(orow + g * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          lse[(long long)q.bh * seq + qr] = (m + __log2f(l)) / kLog2e;
         }
       }
+      q.advance();
     }
-    if (q < seq) lse[(long long)bh * seq + q] = (m + __log2f(l)) / kLog2e;
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -688,15 +737,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 void attn_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int seq, int H, bool causal, cudaStream_t st) {
   const long long ld = 3LL * H * kD;
   const CUtensorMap m = cuda::make_map_2d_bf16(qkv, ld, (long long)B * seq, ld, 64, 128);
-  const dim3 grid((seq + kQ - 1) / kQ * B * H);
+  const int items = (seq + kQ - 1) / kQ * B * H;
+  const dim3 grid(std::min(items, 2 * cuda::kNumSMs));  // persistent: two CTAs per SM
   static bool attr = false;
   if (!attr) {
     CK_CUDA(cudaFuncSetAttribute(k_attn_fwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
     CK_CUDA(cudaFuncSetAttribute(k_attn_fwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
     attr = true;
   }
-  if (causal) k_attn_fwd_tc<true><<<grid, 192, kSmemTotal, st>>>(m, out, lse, seq, H);
-  else k_attn_fwd_tc<false><<<grid, 192, kSmemTotal, st>>>(m, out, lse, seq, H);
+  if (causal) k_attn_fwd_tc<true><<<grid, 192, kSmemTotal, st>>>(m, out, lse, seq, H, B * H);
+  else k_attn_fwd_tc<false><<<grid, 192, kSmemTotal, st>>>(m, out, lse, seq, H, B * H);
   CK_CUDA(cudaGetLastError());
 }
 

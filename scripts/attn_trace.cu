@@ -42,7 +42,7 @@ int main(int argc, char** argv) {
   static long long tr[32][16], cta[4096][3];
   cudaMemcpyFromSymbol(tr, chimera::ops::g_attn_trace, sizeof(tr));
   cudaMemcpyFromSymbol(cta, chimera::ops::g_attn_cta, sizeof(cta));
-  const int ncta = bwd ? std::min((seq + 127) / 128 * B * H, 148) : (seq + 127) / 128 * B * H;  // bwd: persistent
+  const int ncta = std::min((seq + 127) / 128 * B * H, bwd ? 148 : 296);  // persistent grids
   long long t0 = cta[0][1], tend = 0, tmin = cta[0][1];
   for (int i = 0; i < ncta; ++i) tmin = std::min(tmin, cta[i][1]), tend = std::max(tend, cta[i][2]);
   printf("kernel span %.1f us, %d CTAs\n", (tend - tmin) / 1e3, ncta);
@@ -59,7 +59,7 @@ int main(int argc, char** argv) {
   const int nev = bwd ? 13 : 10;
   for (int e = 0; e < nev; ++e) printf(" %12s", names[e]);
   printf("\n");
-  for (int j = 0; j < (bwd ? 20 : 8); ++j) {
+  for (int j = 0; j < 16; ++j) {
     printf("%-4d", j);
     for (int e = 0; e < nev; ++e) printf(" %12lld", tr[j][e] ? tr[j][e] - c0 : -1);
     printf("\n");
@@ -77,7 +77,7 @@ int main(int argc, char** argv) {
   long long e_min = tend, e_max = 0;
   for (int s = 0; s < 148; ++s) if (sm_busy[s]) e_min = std::min(e_min, last_end[s]), e_max = std::max(e_max, last_end[s]);
   printf("SM finish spread: first idle SM at %.1f us, last at %.1f us\n", (e_min - tmin) / 1e3, (e_max - tmin) / 1e3);
-  if (!bwd) {  // per-tile-class CTA durations (fwd: qb = tiles-1 - blockIdx/BH)
+  if (false) {  // (per-tile-class CTA durations: pre-persistent grids only)
     const int nt = (seq + 127) / 128, BH = B * H;
     for (int c = 0; c < nt; ++c) {
       double sum = 0, mx = 0, first = 1e30, last = 0;
@@ -92,7 +92,7 @@ int main(int argc, char** argv) {
   }
   double dur_sum = 0;
   for (int i = 0; i < ncta; ++i) dur_sum += cta[i][2] - cta[i][1];
-  printf("sum CTA durations / (148 SMs * %d) = %.1f us\n", bwd ? 1 : 2, dur_sum / 1e3 / (bwd ? 148 : 296));
+  printf("mean CTA duration = %.1f us\n", dur_sum / 1e3 / ncta);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
