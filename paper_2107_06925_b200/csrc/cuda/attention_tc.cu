@@ -63,9 +63,10 @@ constexpr int kSmemBar = 6 * kTileBytes;
 constexpr int kSmemTotal = kSmemBar + 256;
 constexpr float kLog2e = 1.4426950408889634f;
 // Share of the softmax exp2s computed by ptx::ex2_poly2 on the FMA pipes: every
-// kPolyEvery-th pair (0 = all on MUFU; measured neutral at 2-8 for head dim 64).
+// kPolyEvery-th pair (0 = all on MUFU).  The forward is MUFU-bound at head dim 64
+// (16 ex2/clk/SM vs 128x128 exps per tile): one pair in three off MUFU measured -6%.
 #ifndef CK_ATTN_POLY_EVERY
-#define CK_ATTN_POLY_EVERY 0
+#define CK_ATTN_POLY_EVERY 3
 #endif
 constexpr int kPolyEvery = CK_ATTN_POLY_EVERY;
 
@@ -402,7 +403,7 @@ constexpr int kB_K = 0, kB_V = 2 * kTileBytes, kB_Q = 4 * kTileBytes, kB_DO = 6 
 constexpr int kB_BAR = 14 * kTileBytes;
 constexpr int kBwdSmem = kB_BAR + 256;
 constexpr int kBwdThreads = 320;
-#ifndef CK_ATTN_BWD_POLY_EVERY
+#ifndef CK_ATTN_BWD_POLY_EVERY  // backward: not MUFU-bound, the polynomial costs more than it saves
 #define CK_ATTN_BWD_POLY_EVERY 0
 #endif
 constexpr int kBwdPolyEvery = CK_ATTN_BWD_POLY_EVERY;
