@@ -7,6 +7,7 @@
 #include "chimera_ck.h"
 #include "common.cuh"
 #include "ops.cuh"
+#include "ptx_sm100.cuh"
 
 namespace chimera::ops {
 
@@ -237,6 +238,78 @@ __global__ void __launch_bounds__(512) k_xent(bf16* __restrict__ logits, long lo
   if (threadIdx.x == 0) atomicAdd(loss_sum, (lse - x_lab) * loss_scale);
 }
 
+// Persistent variant (one 512-thread CTA per SM): rows are streamed into shared memory
+// by a 1-D bulk copy one row ahead (double buffer), so the next row's HBM read overlaps
+// this row's exps and gradient stores.  Each row is read once and written once (the
+// 2 x 2 B per element floor), with one exp per element kept in registers (NV 16-byte
+// chunks per thread): max, p = exp(x - max), sum, grad = p / sum - onehot.
+template <int NV>
+__global__ void __launch_bounds__(512, 1) k_xent_pipe(bf16* __restrict__ logits, long long ld,
+                                                      const int32_t* __restrict__ labels, int M, int V, int Vp,
+                                                      float grad_scale, float loss_scale, float* __restrict__ loss_sum) {
+  extern __shared__ __align__(128) uint8_t xsm[];
+  __shared__ float scratch[32];
+  __shared__ __align__(8) uint64_t full[2];
+  const uint32_t row_bytes = uint32_t(Vp) * 2;
+  const uint32_t buf_bytes = (row_bytes + 127) / 128 * 128;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&full[0], 1);
+    ptx::mbar_init(&full[1], 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int row, int b) {
+    ptx::mbar_arrive_expect_tx(&full[b], row_bytes);
+    ptx::bulk_load(xsm + b * buf_bytes, logits + (long long)row * ld, row_bytes, &full[b]);
+  };
+  if (threadIdx.x == 0 && blockIdx.x < M) issue(blockIdx.x, 0);
+  int it = 0;
+  for (int row = blockIdx.x; row < M; row += gridDim.x, ++it) {
+    const int b = it & 1;
+    // the other buffer was last read in the previous iteration (ended by a block barrier)
+    if (threadIdx.x == 0 && row + gridDim.x < M) issue(row + gridDim.x, b ^ 1);
+    ptx::mbar_wait(&full[b], (it >> 1) & 1);
+    const bf16* sr = reinterpret_cast<const bf16*>(xsm + b * buf_bytes);
+    bf16* lr = logits + (long long)row * ld;
+    const int lab = labels[row];
+    float f[NV][8];
+    float m = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * 512 + threadIdx.x) * 8;
+      Vec8 v;
+      if (c < Vp) v.load(sr + c);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        f[i][t] = (c < Vp && c + t < V) ? v.f[t] : -INFINITY;
+        m = fmaxf(m, f[i][t]);
+      }
+    }
+    const float gm = cuda::block_max(m, scratch);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        f[i][t] = __expf(f[i][t] - gm);
+        s += f[i][t];
+      }
+    const float gs = cuda::block_sum(s, scratch);
+    const float inv = grad_scale / gs;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * 512 + threadIdx.x) * 8;
+      if (c >= Vp) continue;
+      Vec8 o;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) o.f[t] = f[i][t] * inv - (c + t == lab ? grad_scale : 0.f);
+      o.store(lr + c);
+    }
+    if (threadIdx.x == 0) atomicAdd(loss_sum, (gm + __logf(gs) - __bfloat162float(sr[lab])) * loss_scale);
+    __syncthreads();  // this buffer is free for the row after next
+  }
+}
+
 // ------------------------------------------------------------------ bias grad --
 // CTA = 256 columns x 64 rows: 32 column groups of 8 (16-byte loads) x 8 row lanes;
 // per-thread fp32 partials, reduced over the 8 row lanes in shared memory, then one
@@ -365,7 +438,26 @@ void embed_bwd(const int32_t* tok, const bf16* dx, float* dwte, float* dwpe, int
 
 void xent_fwd_bwd(bf16* logits, long long ld, const int32_t* labels, int M, int V, int Vp,
                   float grad_scale, float loss_scale, float* loss_sum, cudaStream_t st) {
-  k_xent<<<M, 512, 0, st>>>(logits, ld, labels, V, Vp, grad_scale, loss_scale, loss_sum);
+  const int need = ceil_div(Vp, 8 * 512);  // smallest instantiated register footprint that holds the row
+  const bool bulk_ok = ld % 8 == 0 && Vp % 8 == 0 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0;
+  const int nv = !bulk_ok ? 0 : need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : need <= 8 ? 8 : need <= 13 ? 13 : 0;
+  const size_t smem = 2 * size_t((Vp * 2 + 127) / 128 * 128);  // two row buffers (<= 208 KB)
+  const int grid = std::min(M, cuda::kNumSMs);
+  switch (nv) {
+#define CK_XR(NV)                                                                                      \
+  case NV: {                                                                                           \
+    static bool attr = false;                                                                          \
+    if (!attr) {                                                                                       \
+      CK_CUDA(cudaFuncSetAttribute(k_xent_pipe<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024)); \
+      attr = true;                                                                                     \
+    }                                                                                                  \
+    k_xent_pipe<NV><<<grid, 512, smem, st>>>(logits, ld, labels, M, V, Vp, grad_scale, loss_scale, loss_sum); \
+    break;                                                                                             \
+  }
+    CK_XR(1) CK_XR(2) CK_XR(4) CK_XR(8) CK_XR(13)
+#undef CK_XR
+    default: k_xent<<<M, 512, 0, st>>>(logits, ld, labels, V, Vp, grad_scale, loss_scale, loss_sum);
+  }
   CK_CUDA(cudaGetLastError());
 }
 

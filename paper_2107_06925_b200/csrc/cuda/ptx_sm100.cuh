@@ -119,6 +119,14 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 }
 
 // --------------------------------------------------------------------- TMA --
+// 1-D bulk copy global -> shared (16-byte aligned, size % 16 == 0), completion on `bar`.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 // Bulk tensor reduce-add of a swizzled smem tile into global (fp32 add at L2), tracked
 // by the issuing thread's bulk async-group.
 __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int c0, int c1) {

@@ -48,5 +48,9 @@ for n in (h, 3 * h, f):
     d = torch.randn(M, n, device="cuda").bfloat16()
     bg = torch.zeros(n, device="cuda")
     res[f"bias_grad_{n}"] = timeit(lambda st: K.bias_grad(d, bg, stream=st))
+logits = torch.randn(M, 50304, device="cuda").bfloat16()
+labels = torch.randint(0, 50257, (M,), device="cuda", dtype=torch.int32)
+ls = torch.zeros(1, device="cuda")
+res["xent_4096x50304"] = timeit(lambda st: K.xent(logits, labels, 50257, 1.0, 1.0, ls, stream=st), it=10)
 for k, v in res.items():
     print(json.dumps({"op": k, "us": round(v, 2)}))

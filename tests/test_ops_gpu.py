@@ -63,7 +63,9 @@ def test_embedding():
     assert rel(dwte, rw) < 1e-5 and rel(dwpe, rp) < 1e-5
 
 
-@pytest.mark.parametrize("M,V,Vp", [(256, 50257, 50304), (64, 1000, 1024)])
+# register-resident row (Vp <= 16 * 4096: several footprints) and the two-pass fallback
+@pytest.mark.parametrize("M,V,Vp", [(256, 50257, 50304), (64, 1000, 1024), (32, 30522, 30592), (16, 5000, 5120),
+                                   (8, 120000, 120064)])
 def test_xent(M, V, Vp):
     logits = (3 * torch.randn(M, Vp, device="cuda")).bfloat16()
     labels = torch.randint(0, V, (M,), device="cuda", dtype=torch.int32)
