@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(128) k_attn_fwd(const bf16* __restrict__ qkv, 
 __global__ void __launch_bounds__(256) k_attn_bwd_dot(const bf16* __restrict__ out, const bf16* __restrict__ dout,
                                                       float* __restrict__ D, float* __restrict__ dq, int M, int seq,
                                                       int H) {
+  cuda::pdl_wait();
   const long long rows = (long long)M * H;
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const int part = threadIdx.x & 7;
@@ -373,6 +374,7 @@ __global__ void __launch_bounds__(128) k_attn_bwd(const bf16* __restrict__ qkv, 
 // dQ (fp32 accumulator, scaled by 1/sqrt(d)) -> bf16 Q-part of dqkv (L2-resident stream)
 __global__ void __launch_bounds__(256) k_dq_out(const float* __restrict__ acc, bf16* __restrict__ dqkv, int n_rows,
                                                 int H) {
+  cuda::pdl_wait();
   const int w = H * kHd;  // multiple of 64
   const int n8 = n_rows * w / 8;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
@@ -400,14 +402,14 @@ size_t attn_bwd_scratch_floats(int B, int seq, int H) {
 }
 
 void attn_bwd_dot(const bf16* out, const bf16* dout, float* D, int M, int seq, int H, cudaStream_t st, float* dq_zero) {
-  k_attn_bwd_dot<<<std::min<long long>(cuda::ceil_div((long long)M * H * 8, 512), 148LL * 8), 256, 0, st>>>(
-      out, dout, D, dq_zero, M, seq, H);
+  cuda::launch(k_attn_bwd_dot, dim3(std::min<long long>(cuda::ceil_div((long long)M * H * 8, 512), 148LL * 8)),
+               dim3(256), 0, st, out, dout, D, dq_zero, M, seq, H);
   CK_CUDA(cudaGetLastError());
 }
 
 void attn_dq_out(const float* dq, bf16* dqkv, int M, int H, cudaStream_t st) {
   const long long n = (long long)M * H * kHd;
-  k_dq_out<<<std::min<long long>((n / 8 + 255) / 256, 148LL * 8), 256, 0, st>>>(dq, dqkv, M, H);
+  cuda::launch(k_dq_out, dim3(std::min<long long>((n / 8 + 255) / 256, 148LL * 8)), dim3(256), 0, st, dq, dqkv, M, H);
   CK_CUDA(cudaGetLastError());
 }
 

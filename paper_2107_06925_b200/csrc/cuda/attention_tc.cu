@@ -158,6 +158,8 @@ __global__ void __launch_bounds__(192, 2)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;  // S: cols [0,128), O: [128,192), P (bf16 pairs): [192,256)
+  cuda::pdl_wait();
+  cuda::pdl_trigger();
 
   if (warp == 4) {
     if (lane == 0) {
@@ -481,6 +483,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  cuda::pdl_wait();
+  cuda::pdl_trigger();
   constexpr uint32_t kS = 0, kDP = 128, kDV = 256, kDK = 320, kDQ = 384;
 
   if (warp == 8) {
@@ -746,8 +750,8 @@ void attn_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int seq, int H, 
     CK_CUDA(cudaFuncSetAttribute(k_attn_fwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
     attr = true;
   }
-  if (causal) k_attn_fwd_tc<true><<<grid, 192, kSmemTotal, st>>>(m, out, lse, seq, H, B * H);
-  else k_attn_fwd_tc<false><<<grid, 192, kSmemTotal, st>>>(m, out, lse, seq, H, B * H);
+  cuda::launch(causal ? k_attn_fwd_tc<true> : k_attn_fwd_tc<false>, grid, dim3(192), kSmemTotal, st, m, out, lse, seq, H,
+               B * H);
   CK_CUDA(cudaGetLastError());
 }
 
@@ -771,8 +775,8 @@ void attn_bwd_tc(const bf16* qkv, const bf16* out, const bf16* dout, const float
   }
   const int items = (seq + kKV - 1) / kKV * B * H;
   const dim3 grid(std::min(items, cuda::kNumSMs));  // persistent: one CTA per SM
-  if (causal) k_attn_bwd_tc<true><<<grid, kBwdThreads, kBwdSmem, st>>>(mq, mo, mdq, mdqkv, lse, D, dqkv, seq, H, B * H);
-  else k_attn_bwd_tc<false><<<grid, kBwdThreads, kBwdSmem, st>>>(mq, mo, mdq, mdqkv, lse, D, dqkv, seq, H, B * H);
+  cuda::launch(causal ? k_attn_bwd_tc<true> : k_attn_bwd_tc<false>, grid, dim3(kBwdThreads), kBwdSmem, st, mq, mo, mdq,
+               mdqkv, lse, D, dqkv, seq, H, B * H);
   CK_CUDA(cudaGetLastError());
   attn_dq_out(dq, dqkv, M, H, st);
 }

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -73,5 +74,37 @@ __device__ __forceinline__ float block_max(float v, float* scratch) {
   v = lane < nwarps ? scratch[lane] : -INFINITY;
   return warp_max(v);
 }
+
+// Programmatic dependent launch.  Every kernel of the stage executor is launched with
+// programmatic stream serialisation, so it is scheduled while its predecessor in the
+// stream is still running (on SMs that predecessor leaves free) and overlaps its
+// prologue (barrier init, TMEM allocation, tensor-map prefetch) with the predecessor's
+// tail.  Each such kernel calls pdl_wait() before its first global-memory access (read
+// or write): griddepcontrol.wait returns once every prerequisite grid has completed and
+// flushed.  Persistent kernels (grid <= resident capacity) call pdl_trigger() right after
+// their prologue so their successors may be scheduled early.  CK_PDL=0 disables it.
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CK_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline void launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  CK_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 }  // namespace chimera::cuda

@@ -280,6 +280,8 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  cuda::pdl_wait();     // operands / outputs of the previous kernel in the stream
+  cuda::pdl_trigger();  // persistent grid: successors may be scheduled on free SMs
 
   if (warp == 0) {
     if (lane == 0) {
@@ -445,6 +447,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  cuda::pdl_wait();
+  cuda::pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -570,7 +574,7 @@ void launch_pair(int M, int N, int K, const __nv_bfloat16* A, long long lda, con
   const int ks = split_k(EPI, base, cuda::kNumSMs / 2, K);
   const int tiles = base * ks;
   const int pairs = tiles < cuda::kNumSMs / 2 ? tiles : cuda::kNumSMs / 2;
-  kern<<<2 * pairs, 128 + 32 * kPairEpiWarps, kPairSmem, st>>>(ta, tb, ep, M, N, K, ks);
+  cuda::launch(kern, dim3(2 * pairs), dim3(128 + 32 * kPairEpiWarps), kPairSmem, st, ta, tb, ep, M, N, K, ks);
   CK_CUDA(cudaGetLastError());
 }
 
@@ -592,7 +596,7 @@ void launch(int M, int N, int K, const __nv_bfloat16* A, long long lda, const __
   const int ks = split_k(EPI, base, cuda::kNumSMs, K);
   const int tiles = base * ks;
   const int grid = tiles < cuda::kNumSMs ? tiles : cuda::kNumSMs;
-  kern<<<grid, 256, C::kSmem, st>>>(ta, tb, ep, M, N, K, ks);
+  cuda::launch(kern, dim3(grid), dim3(256), C::kSmem, st, ta, tb, ep, M, N, K, ks);
   CK_CUDA(cudaGetLastError());
 }
 

@@ -41,6 +41,7 @@ template <int VPL>
 __global__ void __launch_bounds__(256) k_ln_fwd(const bf16* __restrict__ x, const bf16* __restrict__ g,
                                                 const bf16* __restrict__ b, bf16* __restrict__ y,
                                                 float* __restrict__ mean, float* __restrict__ rstd, int M) {
+  cuda::pdl_wait();
   constexpr int h = VPL * 256;
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -82,6 +83,7 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const bf16* __restrict__ dy, con
                                                 const bf16* __restrict__ g, const bf16* __restrict__ dres,
                                                 bf16* __restrict__ dx, float* __restrict__ dgamma,
                                                 float* __restrict__ dbeta, int M) {
+  cuda::pdl_wait();
   constexpr int h = VPL * 256;
   extern __shared__ float red[];  // [8 warps][2][h]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -169,6 +171,7 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const bf16* __restrict__ dy, con
 // ------------------------------------------------------------------ embedding --
 __global__ void k_embed_fwd(const int32_t* __restrict__ tok, const bf16* __restrict__ wte,
                             const bf16* __restrict__ wpe, bf16* __restrict__ x, int M, int seq, int h) {
+  cuda::pdl_wait();
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (row >= M) return;
   const bf16* a = wte + (long long)tok[row] * h;
@@ -185,6 +188,7 @@ __global__ void k_embed_fwd(const int32_t* __restrict__ tok, const bf16* __restr
 
 __global__ void k_embed_bwd(const int32_t* __restrict__ tok, const bf16* __restrict__ dx,
                             float* __restrict__ dwte, float* __restrict__ dwpe, int M, int seq, int h) {
+  cuda::pdl_wait();
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (row >= M) return;
   float* a = dwte + (long long)tok[row] * h;
@@ -203,6 +207,7 @@ __global__ void k_embed_bwd(const int32_t* __restrict__ tok, const bf16* __restr
 __global__ void __launch_bounds__(512) k_xent(bf16* __restrict__ logits, long long ld,
                                               const int32_t* __restrict__ labels, int V, int Vp,
                                               float grad_scale, float loss_scale, float* __restrict__ loss_sum) {
+  cuda::pdl_wait();
   __shared__ float scratch[32];
   const int row = blockIdx.x;
   bf16* lr = logits + (long long)row * ld;
@@ -258,6 +263,8 @@ __global__ void __launch_bounds__(512, 1) k_xent_pipe(bf16* __restrict__ logits,
     ptx::fence_barrier_init();
   }
   __syncthreads();
+  cuda::pdl_wait();
+  cuda::pdl_trigger();
   auto issue = [&](int row, int b) {
     ptx::mbar_arrive_expect_tx(&full[b], row_bytes);
     ptx::bulk_load(xsm + b * buf_bytes, logits + (long long)row * ld, row_bytes, &full[b]);
@@ -316,6 +323,7 @@ __global__ void __launch_bounds__(512, 1) k_xent_pipe(bf16* __restrict__ logits,
 // atomic per column per CTA.
 __global__ void __launch_bounds__(256) k_bias_grad(const bf16* __restrict__ dy, float* __restrict__ db,
                                                    int M, int N) {
+  cuda::pdl_wait();
   __shared__ float red[8][256 + 8];
   const int cg = threadIdx.x & 31, rl = threadIdx.x >> 5;
   const int col = blockIdx.x * 256 + cg * 8;
@@ -349,6 +357,7 @@ struct GradPtrs {
 template <int COPIES>
 __global__ void __launch_bounds__(256) k_sgd(float* __restrict__ w32, bf16* __restrict__ w16, GradPtrs g,
                                              long long n, float lr) {
+  cuda::pdl_wait();
   const long long stride = (long long)gridDim.x * blockDim.x * 4;
   for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
     float4 v[COPIES];
@@ -368,6 +377,7 @@ __global__ void __launch_bounds__(256) k_sgd(float* __restrict__ w32, bf16* __re
 }
 
 __global__ void k_reduce(float* __restrict__ dst, GradPtrs g, int copies, long long n) {
+  cuda::pdl_wait();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     float s = 0.f;
@@ -377,6 +387,7 @@ __global__ void k_reduce(float* __restrict__ dst, GradPtrs g, int copies, long l
 }
 
 __global__ void k_cast(const float* __restrict__ s, bf16* __restrict__ d, long long n) {
+  cuda::pdl_wait();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     d[i] = __float2bfloat16_rn(s[i]);
@@ -393,7 +404,7 @@ void layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* 
                    int M, int h, cudaStream_t st) {
   const int grid = ceil_div(M, 8);
   switch (h) {
-#define CK_LN(V) case V * 256: k_ln_fwd<V><<<grid, 256, 0, st>>>(x, g, b, y, mean, rstd, M); break;
+#define CK_LN(V) case V * 256: cuda::launch(k_ln_fwd<V>, dim3(grid), dim3(256), 0, st, x, g, b, y, mean, rstd, M); break;
     CK_LN(1) CK_LN(2) CK_LN(3) CK_LN(4) CK_LN(5) CK_LN(6) CK_LN(8)
 #undef CK_LN
     default: throw chimera::capi::InternalError("layernorm: unsupported hidden size");
@@ -414,7 +425,7 @@ void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float
       CK_CUDA(cudaFuncSetAttribute(k_ln_bwd<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * V * 256 * 4)); \
       attr = true;                                                                                 \
     }                                                                                              \
-    k_ln_bwd<V><<<grid, 256, smem, st>>>(dy, x, mean, rstd, g, dres, dx, dgamma, dbeta, M);        \
+    cuda::launch(k_ln_bwd<V>, dim3(grid), dim3(256), smem, st, dy, x, mean, rstd, g, dres, dx, dgamma, dbeta, M); \
     break;                                                                                         \
   }
     CK_LN(1) CK_LN(2) CK_LN(3) CK_LN(4) CK_LN(5) CK_LN(6) CK_LN(8)
@@ -426,13 +437,13 @@ void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float
 
 void embed_fwd(const int32_t* tok, const bf16* wte, const bf16* wpe, bf16* x, int M, int seq, int h,
                cudaStream_t st) {
-  k_embed_fwd<<<ceil_div(M, 8), 256, 0, st>>>(tok, wte, wpe, x, M, seq, h);
+  cuda::launch(k_embed_fwd, dim3(ceil_div(M, 8)), dim3(256), 0, st, tok, wte, wpe, x, M, seq, h);
   CK_CUDA(cudaGetLastError());
 }
 
 void embed_bwd(const int32_t* tok, const bf16* dx, float* dwte, float* dwpe, int M, int seq, int h,
                cudaStream_t st) {
-  k_embed_bwd<<<ceil_div(M, 8), 256, 0, st>>>(tok, dx, dwte, dwpe, M, seq, h);
+  cuda::launch(k_embed_bwd, dim3(ceil_div(M, 8)), dim3(256), 0, st, tok, dx, dwte, dwpe, M, seq, h);
   CK_CUDA(cudaGetLastError());
 }
 
@@ -451,19 +462,20 @@ void xent_fwd_bwd(bf16* logits, long long ld, const int32_t* labels, int M, int 
       CK_CUDA(cudaFuncSetAttribute(k_xent_pipe<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024)); \
       attr = true;                                                                                     \
     }                                                                                                  \
-    k_xent_pipe<NV><<<grid, 512, smem, st>>>(logits, ld, labels, M, V, Vp, grad_scale, loss_scale, loss_sum); \
+    cuda::launch(k_xent_pipe<NV>, dim3(grid), dim3(512), smem, st, logits, ld, labels, M, V, Vp, grad_scale, loss_scale, \
+                 loss_sum);                                                                            \
     break;                                                                                             \
   }
     CK_XR(1) CK_XR(2) CK_XR(4) CK_XR(8) CK_XR(13)
 #undef CK_XR
-    default: k_xent<<<M, 512, 0, st>>>(logits, ld, labels, V, Vp, grad_scale, loss_scale, loss_sum);
+    default: cuda::launch(k_xent, dim3(M), dim3(512), 0, st, logits, ld, labels, V, Vp, grad_scale, loss_scale, loss_sum);
   }
   CK_CUDA(cudaGetLastError());
 }
 
 void bias_grad(const bf16* dy, float* db, int M, int N, cudaStream_t st) {
   if (N % 8) throw chimera::capi::InternalError("bias_grad: N % 8 != 0");
-  k_bias_grad<<<dim3(ceil_div(N, 256), ceil_div(M, 64)), 256, 0, st>>>(dy, db, M, N);
+  cuda::launch(k_bias_grad, dim3(ceil_div(N, 256), ceil_div(M, 64)), dim3(256), 0, st, dy, db, M, N);
   CK_CUDA(cudaGetLastError());
 }
 
@@ -475,7 +487,7 @@ void sgd_update(float* w32, bf16* w16, float* const* grads, int copies, long lon
   for (int c = 0; c < copies; ++c) g.p[c] = grads[c];
   const int grid = grid_for(n, 4);
   switch (copies) {
-#define CK_SGD(C) case C: k_sgd<C><<<grid, 256, 0, st>>>(w32, w16, g, n, lr); break;
+#define CK_SGD(C) case C: cuda::launch(k_sgd<C>, dim3(grid), dim3(256), 0, st, w32, w16, g, n, lr); break;
     CK_SGD(1) CK_SGD(2) CK_SGD(3) CK_SGD(4) CK_SGD(5) CK_SGD(6) CK_SGD(7) CK_SGD(8)
 #undef CK_SGD
   }
@@ -486,12 +498,12 @@ void reduce_copies(float* dst, float* const* srcs, int copies, long long n, cuda
   if (copies < 1 || copies > 8) throw chimera::capi::InternalError("reduce: 1..8 copies");
   GradPtrs g{};
   for (int c = 0; c < copies; ++c) g.p[c] = srcs[c];
-  k_reduce<<<grid_for(n, 1), 256, 0, st>>>(dst, g, copies, n);
+  cuda::launch(k_reduce, dim3(grid_for(n, 1)), dim3(256), 0, st, dst, g, copies, n);
   CK_CUDA(cudaGetLastError());
 }
 
 void cast_f32_bf16(const float* src, bf16* dst, long long n, cudaStream_t st) {
-  k_cast<<<grid_for(n, 1), 256, 0, st>>>(src, dst, n);
+  cuda::launch(k_cast, dim3(grid_for(n, 1)), dim3(256), 0, st, src, dst, n);
   CK_CUDA(cudaGetLastError());
 }
 
