@@ -100,6 +100,12 @@ CK_API int ck_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, const 
                         long long lda, const void* B, long long ldb, void* out, long long ldo,
                         const void* bias, const void* aux, long long ld_aux, void* out2,
                         long long ld_out2, void* stream);
+/* ck_gemm_bf16 plus, for epi 3, colsum[N] += column sums of the bf16 output (the fused bias
+   gradient of the layer whose pre-activation gradient this GEMM produces). */
+CK_API int ck_gemm_bf16_ex(int epi, int a_mn, int b_mn, int M, int N, int K, const void* A,
+                           long long lda, const void* B, long long ldb, void* out, long long ldo,
+                           const void* bias, const void* aux, long long ld_aux, void* out2,
+                           long long ld_out2, float* colsum, void* stream);
 
 /* LayerNorm (eps 1e-5), rows of h (h % 256 == 0); stats fp32. */
 CK_API int ck_layernorm_fwd(const void* x, const void* g, const void* b, void* y, float* mean,
@@ -107,6 +113,12 @@ CK_API int ck_layernorm_fwd(const void* x, const void* g, const void* b, void* y
 CK_API int ck_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd,
                             const void* g, const void* dres, void* dx, float* dgamma,
                             float* dbeta, int M, int h, void* stream);
+/* ck_layernorm_bwd that also accumulates dsum[h] += sum over rows of the (bf16) dx: the
+   bias gradient of the linear layer that produced the residual stream (fused bias grad,
+   replaces a ck_bias_grad pass over dx). */
+CK_API int ck_layernorm_bwd_dsum(const void* dy, const void* x, const float* mean, const float* rstd,
+                                 const void* g, const void* dres, void* dx, float* dgamma,
+                                 float* dbeta, float* dsum, int M, int h, void* stream);
 /* token + position embedding and its scatter-add backward (fp32 grads). */
 CK_API int ck_embed_fwd(const int32_t* tok, const void* wte, const void* wpe, void* x, int M,
                         int seq, int h, void* stream);

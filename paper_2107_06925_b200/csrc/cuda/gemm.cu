@@ -175,6 +175,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiArgs& ep, int row0, int 
     float2 bias[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) bias[e] = bf2f((&pre.bias.x)[e]);
+    float2 csum[4] = {};  // kGeluBwd + colsum: this lane's 8 columns over its rows
 #pragma unroll
     for (int it = 0; it < 4; ++it) {  // 32 rows x 4 segments of 8 columns
       const int rr = it * 8 + (lane >> 2), row = row0 + rr;
@@ -207,6 +208,12 @@ __device__ __forceinline__ void epilogue_chunk(const EpiArgs& ep, int row0, int 
       }
       uint4 q;
       q.x = f2bf(v[0].x, v[0].y), q.y = f2bf(v[1].x, v[1].y), q.z = f2bf(v[2].x, v[2].y), q.w = f2bf(v[3].x, v[3].y);
+      if constexpr (EPI == kGeluBwd) {
+        if (ep.colsum) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) csum[e] = ptx::add2(csum[e], bf2f((&q.x)[e]));
+        }
+      }
       __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + col;
       if (vec_o) {
         *reinterpret_cast<uint4*>(dst) = q;
@@ -233,6 +240,26 @@ __device__ __forceinline__ void epilogue_chunk(const EpiArgs& ep, int row0, int 
         } else {
           const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&g);
           for (int t = 0; t < 8 && col + t < N; ++t) dst2[t] = h[t];
+        }
+      }
+    }
+    if constexpr (EPI == kGeluBwd) {
+      if (ep.colsum) {  // reduce over the 8 lanes sharing these columns, one atomic per column
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+#pragma unroll
+          for (int off = 4; off < 32; off <<= 1) {
+            csum[e].x += __shfl_xor_sync(0xffffffffu, csum[e].x, off);
+            csum[e].y += __shfl_xor_sync(0xffffffffu, csum[e].y, off);
+          }
+        if (lane < 4 && col < N) {
+          if ((N % 8) == 0 && col + 8 <= N) {
+            float4* d = reinterpret_cast<float4*>(ep.colsum + col);
+            atomicAdd(d, make_float4(csum[0].x, csum[0].y, csum[1].x, csum[1].y));
+            atomicAdd(d + 1, make_float4(csum[2].x, csum[2].y, csum[3].x, csum[3].y));
+          } else {
+            for (int t = 0; t < 8 && col + t < N; ++t) atomicAdd(ep.colsum + col + t, (&csum[t >> 1].x)[t & 1]);
+          }
         }
       }
     }
@@ -404,45 +431,54 @@ inline int split_k(int epi, int tiles, int slots, int K) {
 }
 
 // ---------------------------------------------------------- 2-SM variant ----
-// A CTA pair (cluster of 2 on one TPC) computes a 256 x 256 tile with
-// tcgen05.mma.cta_group::2 (M = 256): each CTA stages its 128 rows of A and 128 of
-// the 256 rows of B per K-block, so per-SM operand traffic per MMA drops by 1/3 versus
-// the 128 x 256 single-CTA tile.  The leader (even) CTA issues the MMAs and owns the
-// smem-full and TMEM-empty barriers; commits are multicast to both CTAs.
-constexpr int kPairStages = 5;
-constexpr int kPairEpiWarps = 8;  // two per TMEM lane quarter, each owning 128 of the 256 columns
-constexpr int kPairHalfBytes = 128 * BK * 2;            // one operand half per CTA
-constexpr int kPairStageBytes = 2 * kPairHalfBytes;     // A half + B half
-constexpr int kPairSmem = kPairStages * kPairStageBytes + 1024 + 256 + kPairEpiWarps * kEpiWarpBytes;
+// A CTA pair (cluster of 2 on one TPC) computes a 256 x PBN tile with
+// tcgen05.mma.cta_group::2 (M = 256): each CTA stages its 128 rows of A and PBN/2 of
+// the PBN rows of B per K-block, so per-SM operand traffic per MMA drops versus a
+// single-CTA tile.  The leader (even) CTA issues the MMAs and owns the smem-full and
+// TMEM-empty barriers; commits are multicast to both CTAs.  PBN = 256 is the default;
+// PBN = 128 halves the tile so single-wave problems get two tiles per pair, the first
+// tile's epilogue hiding under the second's mainloop (and the exposed last epilogue
+// is half as long).
+constexpr int kPairEpiWarps = 8;  // two per TMEM lane quarter, each owning half of the columns
+template <int PBN>
+struct PairCfg {
+  static constexpr int kABytes = 128 * BK * 2;               // this CTA's 128 rows of A
+  static constexpr int kBBytes = (PBN / 2) * BK * 2;         // this CTA's PBN/2 rows of B
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = PBN == 256 ? 5 : 7;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256 + kPairEpiWarps * kEpiWarpBytes;
+  static constexpr int kChunks = PBN / 64;                   // 32-column chunks per epilogue warp
+};
 
-template <bool A_MN, bool B_MN, int EPI>
+template <int PBN, bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiWarps, 1)
     k_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const EpiArgs ep,
             int M, int N, int K, int ksplit) {
+  using C = PairCfg<PBN>;
   extern __shared__ uint8_t smem_raw[];
   GEMM_TRACE(threadIdx.x == 32, 0, 6);
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPairStages * kPairStageBytes);
-  uint64_t* empty = full + kPairStages;
-  uint64_t* tfull = empty + kPairStages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = ptx::cluster_ctarank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int num_m = (M + 255) / 256, num_n = (N + 255) / 256;
+  const int num_m = (M + 255) / 256, num_n = (N + PBN - 1) / PBN;
   const int num_kb = (K + BK - 1) / BK, kb_per = (num_kb + ksplit - 1) / ksplit;
   const int tiles = num_m * num_n * ksplit;
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&ta);
     ptx::tma_prefetch(&tb);
-    for (int s = 0; s < kPairStages; ++s) ptx::mbar_init(&full[s], 1), ptx::mbar_init(&empty[s], 1);
+    for (int s = 0; s < C::kStages; ++s) ptx::mbar_init(&full[s], 1), ptx::mbar_init(&empty[s], 1);
     for (int a = 0; a < 2; ++a) ptx::mbar_init(&tfull[a], 1), ptx::mbar_init(&tempty[a], 2 * kPairEpiWarps);
     ptx::fence_barrier_init();
   }
-  if (warp == 2) ptx::tmem_alloc2(tmem_slot, 512);
+  if (warp == 2) ptx::tmem_alloc2(tmem_slot, 2 * PBN);
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
@@ -458,13 +494,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
         int mb, nb;
         tile_coords(tile, num_m, num_n, mb, nb);
         const int ks = tile / (num_m * num_n);
-        const int m0 = mb * 256 + int(cta) * 128, n0 = nb * 256 + int(cta) * 128;
+        const int m0 = mb * 256 + int(cta) * 128, n0 = nb * PBN + int(cta) * (PBN / 2);
         const int kb1 = min(num_kb, (ks + 1) * kb_per);
         for (int kb = ks * kb_per; kb < kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * kPairStageBytes;
-          uint8_t* sb = sa + kPairHalfBytes;
-          if (cta == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
+          uint8_t* sa = smem + stage * C::kStageBytes;
+          uint8_t* sb = sa + C::kABytes;
+          if (cta == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
           if constexpr (!A_MN) {
             ptx::tma_load_2d_pair(sa, &ta, &full[stage], kb * BK, m0);
           } else {
@@ -475,15 +511,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
             ptx::tma_load_2d_pair(sb, &tb, &full[stage], kb * BK, n0);
           } else {
 #pragma unroll
-            for (int c = 0; c < 2; ++c) ptx::tma_load_2d_pair(sb + c * (BK * 128), &tb, &full[stage], n0 + c * 64, kb * BK);
+            for (int c = 0; c < PBN / 128; ++c)
+              ptx::tma_load_2d_pair(sb + c * (BK * 128), &tb, &full[stage], n0 + c * 64, kb * BK);
           }
-          if (++stage == kPairStages) stage = 0, phase ^= 1;
+          if (++stage == C::kStages) stage = 0, phase ^= 1;
         }
       }
     }
   } else if (warp == 1) {
     if (cta == 0 && lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16(256, 256, A_MN, B_MN);
+      constexpr uint32_t idesc = ptx::idesc_bf16(256, PBN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -492,14 +529,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
         ptx::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         GEMM_TRACE(true, it, 0);
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * 256;
+        const uint32_t d_tmem = tmem_base + acc * PBN;
         const int ks = tile / (num_m * num_n);
         const int kb0 = ks * kb_per, kb1 = min(num_kb, (ks + 1) * kb_per);
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t sa = ptx::smem_u32(smem + stage * kPairStageBytes);
-          const uint32_t sb = sa + kPairHalfBytes;
+          const uint32_t sa = ptx::smem_u32(smem + stage * C::kStageBytes);
+          const uint32_t sb = sa + C::kABytes;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = A_MN ? ptx::smem_desc_sw128(sa + k * 2048, BK * 128, 1024)
@@ -509,7 +546,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
             ptx::umma_f16_pair(d_tmem, ad, bd, idesc, (kb > kb0 || k) ? 1u : 0u);
           }
           ptx::umma_commit_pair(&empty[stage]);
-          if (++stage == kPairStages) stage = 0, phase ^= 1;
+          if (++stage == C::kStages) stage = 0, phase ^= 1;
         }
         GEMM_TRACE(true, it, 1);
         ptx::umma_commit_pair(&tfull[acc]);
@@ -517,28 +554,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
     }
   } else if (warp >= 4) {
     const int q = warp & 3, half = (warp - 4) >> 2;  // lane quarter, column half
+    constexpr int NC = C::kChunks;
     int it = 0;
     for (int tile = pair; tile < tiles; tile += npairs, ++it) {
       const int acc = it & 1;
       int mb, nb;
       tile_coords(tile, num_m, num_n, mb, nb);
       EpiPre pre;  // this tile's first-chunk operands are fetched while the MMAs run
-      epilogue_prefetch<EPI>(ep, mb * 256 + int(cta) * 128 + q * 32, nb * 256 + half * 128, M, N, lane, ksplit > 1,
-                             pre);
+      epilogue_prefetch<EPI>(ep, mb * 256 + int(cta) * 128 + q * 32, nb * PBN + half * (PBN / 2), M, N, lane,
+                             ksplit > 1, pre);
       ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
       GEMM_TRACE(warp == 4 && lane == 0, it, 2);
       GEMM_TRACE(warp == 11 && lane == 0, it, 4);
       ptx::tc_fence_after();
       const int row0 = mb * 256 + int(cta) * 128 + q * 32;
-      const uint32_t t0 = tmem_base + (uint32_t(q * 32) << 16) + acc * 256;
-      uint8_t* stg = smem + kPairStages * kPairStageBytes + 256 + (warp - 4) * kEpiWarpBytes;
+      const uint32_t t0 = tmem_base + (uint32_t(q * 32) << 16) + acc * PBN;
+      uint8_t* stg = smem + C::kStages * C::kStageBytes + 256 + (warp - 4) * kEpiWarpBytes;
 #pragma unroll 1
-      for (int c = half * 4; c < half * 4 + 4; ++c) {
+      for (int c = half * NC; c < half * NC + NC; ++c) {
         uint32_t r[32];
         ptx::tmem_ld32(t0 + c * 32, r);
-        const int col0 = nb * 256 + c * 32;
+        const int col0 = nb * PBN + c * 32;
         EpiPre cur = pre;
-        if (c + 1 < half * 4 + 4) epilogue_prefetch<EPI>(ep, row0, col0 + 32, M, N, lane, ksplit > 1, pre);
+        if (c + 1 < half * NC + NC) epilogue_prefetch<EPI>(ep, row0, col0 + 32, M, N, lane, ksplit > 1, pre);
         ptx::tmem_ld_wait();
         if (row0 < M && col0 < N) epilogue_chunk<EPI>(ep, row0, col0, M, N, r, stg, lane, ksplit > 1, cur);
       }
@@ -553,28 +591,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
   ptx::cluster_sync();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc2(tmem_base, 512);
+    ptx::tmem_dealloc2(tmem_base, 2 * PBN);
   }
 }
 
-template <bool A_MN, bool B_MN, int EPI>
+template <int PBN, bool A_MN, bool B_MN, int EPI>
 void launch_pair(int M, int N, int K, const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B,
                  long long ldb, const EpiArgs& ep, cudaStream_t st) {
+  using C = PairCfg<PBN>;
   const CUtensorMap ta = A_MN ? cuda::make_map_2d_bf16(A, M, K, lda, 64, BK)
                               : cuda::make_map_2d_bf16(A, K, M, lda, 64, 128);
   const CUtensorMap tb = B_MN ? cuda::make_map_2d_bf16(B, N, K, ldb, 64, BK)
-                              : cuda::make_map_2d_bf16(B, K, N, ldb, 64, 128);
-  auto kern = k_gemm2<A_MN, B_MN, EPI>;
+                              : cuda::make_map_2d_bf16(B, K, N, ldb, 64, PBN / 2);
+  auto kern = k_gemm2<PBN, A_MN, B_MN, EPI>;
   static bool attr = false;
   if (!attr) {
-    CK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));
+    CK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr = true;
   }
-  const int base = ((M + 255) / 256) * ((N + 255) / 256);
+  const int base = ((M + 255) / 256) * ((N + PBN - 1) / PBN);
   const int ks = split_k(EPI, base, cuda::kNumSMs / 2, K);
   const int tiles = base * ks;
   const int pairs = tiles < cuda::kNumSMs / 2 ? tiles : cuda::kNumSMs / 2;
-  cuda::launch(kern, dim3(2 * pairs), dim3(128 + 32 * kPairEpiWarps), kPairSmem, st, ta, tb, ep, M, N, K, ks);
+  cuda::launch(kern, dim3(2 * pairs), dim3(128 + 32 * kPairEpiWarps), C::kSmem, st, ta, tb, ep, M, N, K, ks);
   CK_CUDA(cudaGetLastError());
 }
 
@@ -603,7 +642,8 @@ void launch(int M, int N, int K, const __nv_bfloat16* A, long long lda, const __
 template <int BN, bool A_MN, bool B_MN, int EPI>
 void launch_any(int M, int N, int K, const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B,
                 long long ldb, const EpiArgs& ep, cudaStream_t st) {
-  if constexpr (BN == 0) launch_pair<A_MN, B_MN, EPI>(M, N, K, A, lda, B, ldb, ep, st);
+  if constexpr (BN == 0) launch_pair<256, A_MN, B_MN, EPI>(M, N, K, A, lda, B, ldb, ep, st);
+  else if constexpr (BN == 1) launch_pair<128, A_MN, B_MN, EPI>(M, N, K, A, lda, B, ldb, ep, st);
   else launch<BN, A_MN, B_MN, EPI>(M, N, K, A, lda, B, ldb, ep, st);
 }
 
@@ -645,16 +685,19 @@ void gemm(Epi epi, bool a_mn, bool b_mn, int M, int N, int K, const __nv_bfloat1
     throw chimera::capi::InternalError("gemm: operands must be 16-byte aligned with ld % 8 == 0");
   // CTA-pair 256 x 256 tiles for large problems, else single-CTA 128 x 256 / 128 x 128.
   static const int force = [] {
-    const char* e = std::getenv("CK_GEMM_TILE");  // "pair" | "256" | "128" (benchmarks)
-    return !e ? -1 : std::string(e) == "pair" ? 0 : std::string(e) == "256" ? 256 : 128;
+    const char* e = std::getenv("CK_GEMM_TILE");  // "pair" | "pair128" | "256" | "128" (benchmarks)
+    if (!e) return -1;
+    const std::string v(e);
+    return v == "pair" ? 0 : v == "pair128" ? 1 : v == "256" ? 256 : 128;
   }();
   const long long tiles_pair = (long long)((M + 255) / 256) * ((N + 255) / 256);
   const long long tiles256 = (long long)((M + BM - 1) / BM) * ((N + 255) / 256);
   int choice = force;
   (void)tiles256;
   if (choice < 0) choice = (M >= 256 && N >= 256 && tiles_pair >= 48) ? 0 : (N > 128) ? 256 : 128;
-  if (choice == 0 && (M < 256 || N < 256)) choice = 128;
+  if (choice <= 1 && (M < 256 || N < 256)) choice = 128;
   if (choice == 0) by_layout<0>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
+  else if (choice == 1) by_layout<1>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
   else if (choice == 256) by_layout<256>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
   else by_layout<128>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
 }
@@ -664,10 +707,10 @@ void gemm(Epi epi, bool a_mn, bool b_mn, int M, int N, int K, const __nv_bfloat1
 extern "C" {
 
 // Test / integration entry: all pointers are device pointers; stream may be 0.
-CK_API int ck_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, const void* A,
-                        long long lda, const void* B, long long ldb, void* out, long long ldo,
-                        const void* bias, const void* aux, long long ld_aux, void* out2,
-                        long long ld_out2, void* stream) {
+CK_API int ck_gemm_bf16_ex(int epi, int a_mn, int b_mn, int M, int N, int K, const void* A,
+                           long long lda, const void* B, long long ldb, void* out, long long ldo,
+                           const void* bias, const void* aux, long long ld_aux, void* out2,
+                           long long ld_out2, float* colsum, void* stream) {
   return chimera::capi::guarded([&] {
     chimera::gemm::EpiArgs ep;
     ep.out = out;
@@ -677,10 +720,19 @@ CK_API int ck_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, const 
     ep.ld_aux = ld_aux;
     ep.out2 = static_cast<__nv_bfloat16*>(out2);
     ep.ld_out2 = ld_out2;
+    ep.colsum = colsum;
     chimera::gemm::gemm(static_cast<chimera::gemm::Epi>(epi), a_mn != 0, b_mn != 0, M, N, K,
                         static_cast<const __nv_bfloat16*>(A), lda, static_cast<const __nv_bfloat16*>(B),
                         ldb, ep, static_cast<cudaStream_t>(stream));
   });
+}
+
+CK_API int ck_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, const void* A,
+                        long long lda, const void* B, long long ldb, void* out, long long ldo,
+                        const void* bias, const void* aux, long long ld_aux, void* out2,
+                        long long ld_out2, void* stream) {
+  return ck_gemm_bf16_ex(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, out, ldo, bias, aux, ld_aux, out2, ld_out2,
+                         nullptr, stream);
 }
 
 }  // extern "C"

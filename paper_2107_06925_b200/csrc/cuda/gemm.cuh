@@ -24,6 +24,7 @@ struct EpiArgs {
   long long ld_aux = 0;
   __nv_bfloat16* out2 = nullptr;  // kBiasGelu second output
   long long ld_out2 = 0;
+  float* colsum = nullptr;  // kGeluBwd: colsum[n] += sum_m out[m][n] (the fused bias gradient)
 };
 
 // Operand layouts: A(m,k) is A[m*lda+k] when !a_mn (K-major) else A[k*lda+m];

@@ -84,9 +84,16 @@ struct Stash {
   bf16* logits = nullptr;  // dlogits after the fused cross-entropy
 };
 
+// Backward temporaries of one rank.  Weight / bias gradients run on a side stream one
+// layer behind the activation-gradient chain, so the buffers that stream reads rotate:
+// the chain's dx over 3 (written at layer l, read by the side stream at layer l-1), the
+// per-layer du / dx2 / dqkv over 2; the chain at layer l first waits for the side
+// stream's layer l+2, the last reader of the buffers it is about to overwrite.
 struct Scratch {
-  bf16 *dxa, *dxb, *dx2, *dh, *du, *da, *dqkv;
+  bf16 *dx[3], *dx2[2], *du[2], *dqkv[2], *dh, *da;
   float* attn;
+  cudaStream_t side = nullptr;  // weight-gradient stream (== the rank stream when serialised)
+  cudaEvent_t fork[4], join[3];
 };
 
 struct StageState {
@@ -348,20 +355,30 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
   // ---- per-rank scratch and streams
   for (int k = 0; k < n_ranks; ++k) {
     Scratch sc;
-    sc.dxa = I.arena.alloc<bf16>((size_t)M * h);
-    sc.dxb = I.arena.alloc<bf16>((size_t)M * h);
-    sc.dx2 = I.arena.alloc<bf16>((size_t)M * h);
+    for (auto& b : sc.dx) b = I.arena.alloc<bf16>((size_t)M * h);
+    for (int j = 0; j < 2; ++j) {
+      sc.dx2[j] = I.arena.alloc<bf16>((size_t)M * h);
+      sc.du[j] = I.arena.alloc<bf16>((size_t)M * f);
+      sc.dqkv[j] = I.arena.alloc<bf16>((size_t)M * 3 * h);
+    }
     sc.dh = I.arena.alloc<bf16>((size_t)M * h);
     sc.da = I.arena.alloc<bf16>((size_t)M * h);
-    sc.du = I.arena.alloc<bf16>((size_t)M * f);
-    sc.dqkv = I.arena.alloc<bf16>((size_t)M * 3 * h);
     sc.attn = I.arena.alloc<float>(ops::attn_bwd_scratch_floats(I.B, shape.seq, H));
-    I.scratch.push_back(sc);
     cudaStream_t s;
     // CK_SERIALIZE=1: every rank issues on one stream (debug: rules out cross-stream races)
-    if (k > 0 && std::getenv("CK_SERIALIZE")) s = I.streams[0];
+    const bool serial = std::getenv("CK_SERIALIZE") != nullptr;
+    if (k > 0 && serial) s = I.streams[0];
     else CK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     I.streams.push_back(s);
+    // CK_WGRAD_SIDE=0: weight gradients stay on the rank stream (default under CK_SERIALIZE
+    // unless CK_WGRAD_SIDE=1: one chain stream + side streams, the one-rank-per-GPU shape)
+    const char* ws = std::getenv("CK_WGRAD_SIDE");
+    const bool on = ws ? std::string(ws) != "0" : !serial;
+    if (!on) sc.side = s;
+    else CK_CUDA(cudaStreamCreateWithFlags(&sc.side, cudaStreamNonBlocking));
+    for (auto& e : sc.fork) CK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : sc.join) CK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    I.scratch.push_back(sc);
     cudaEvent_t e;
     CK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     I.rank_done.push_back(e);
@@ -434,6 +451,12 @@ Trainer::~Trainer() {
   if (I.comm_stream) cudaStreamDestroy(I.comm_stream);
   cudaEventDestroy(I.start_ev);
   cudaEventDestroy(I.upd_ev);
+  for (size_t k = 0; k < I.scratch.size(); ++k) {
+    Scratch& sc = I.scratch[k];
+    for (auto e : sc.fork) cudaEventDestroy(e);
+    for (auto e : sc.join) cudaEventDestroy(e);
+    if (sc.side && sc.side != I.streams[k]) cudaStreamDestroy(sc.side);
+  }
   for (size_t k = 0; k < I.streams.size(); ++k)
     if (k == 0 || I.streams[k] != I.streams[0]) cudaStreamDestroy(I.streams[k]);
   cudaStreamDestroy(I.main_stream);
@@ -550,15 +573,37 @@ void Trainer::backward_task(int rank, int p, int mb, int s) {
     stage_forward(rank, s, Wk, stage_in, L.has_head ? Wk.xfinal : Wk.layers.back().xo, tok0, I.loss_dummy);
   }
 
+  // Activation-gradient chain on the rank stream `st`; weight and bias gradients on the
+  // side stream (fork after each producer, join per layer: see Scratch).
+  cudaStream_t ws = sc.side;
+  const bool side = ws != st;
+  int fork_i = 0;
+  auto fork = [&] {  // the side stream waits for everything issued so far on st
+    if (!side) return;
+    cudaEvent_t e = sc.fork[fork_i++ & 3];
+    CK_CUDA(cudaEventRecord(e, st));
+    CK_CUDA(cudaStreamWaitEvent(ws, e, 0));
+  };
+  const int top = L.has_head ? L.n_layers : L.n_layers - 1;  // highest side-stream "layer" index
+  auto side_done = [&](int l) {
+    if (side) CK_CUDA(cudaEventRecord(sc.join[l % 3], ws));
+  };
+  auto wait_side = [&](int l) {  // the chain is about to overwrite buffers side layer l read
+    if (side && l <= top) CK_CUDA(cudaStreamWaitEvent(st, sc.join[l % 3], 0));
+  };
   const bf16* dxo;
   if (L.has_head) {
+    fork();
+    gemm::gemm(gemm::kAccF32, true, true, m.vocab_padded, h, M, X.logits, m.vocab_padded, X.hf, h,
+               epi(gw + L.w_head, h), ws);
+    side_done(L.n_layers);
     gemm::gemm(gemm::kStoreBF16, false, true, M, h, m.vocab_padded, X.logits, m.vocab_padded, w + L.w_head, h,
                epi(sc.dh, h), st);
-    gemm::gemm(gemm::kAccF32, true, true, m.vocab_padded, h, M, X.logits, m.vocab_padded, X.hf, h,
-               epi(gw + L.w_head, h), st);
-    ops::layernorm_bwd(sc.dh, X.xfinal, X.meanf, X.rstdf, w + L.lnf_g, nullptr, sc.dxa, gw + L.lnf_g,
-                       gw + L.lnf_b, M, h, st);
-    dxo = sc.dxa;
+    bf16* d = sc.dx[L.n_layers % 3];
+    // (+ the top layer's FC2 bias gradient: column sums of this dx)
+    ops::layernorm_bwd(sc.dh, X.xfinal, X.meanf, X.rstdf, w + L.lnf_g, nullptr, d, gw + L.lnf_g,
+                       gw + L.lnf_b, gw + L.layers[L.n_layers - 1].b_fc2, M, h, st);
+    dxo = d;
     I.launches_per_step += 3;
   } else {
     const Msg& in = I.msgs.at(I.msg_key(r, mb, s, 1));
@@ -572,32 +617,54 @@ void Trainer::backward_task(int rank, int p, int mb, int s) {
     const LayerOffsets& o = L.layers[l];
     LayerStash& A = X.layers[l];
     const bf16* xin = (l > 0) ? X.layers[l - 1].xo : stage_in;
-    bf16* dxin = (l > 0) ? (dxo == sc.dxa ? sc.dxb : sc.dxa) : (dx_stage ? dx_stage : (dxo == sc.dxa ? sc.dxb : sc.dxa));
+    bf16* dxin = (l == 0 && dx_stage) ? dx_stage : sc.dx[l % 3];
+    bf16 *du = sc.du[l & 1], *dx2 = sc.dx2[l & 1], *dqkv = sc.dqkv[l & 1];
+    wait_side(l + 2);
     // MLP
-    ops::bias_grad(dxo, gw + o.b_fc2, M, h, st);
-    gemm::gemm(gemm::kAccF32, true, true, h, f, M, dxo, h, A.g, f, epi(gw + o.w_fc2, f), st);
-    gemm::gemm(gemm::kGeluBwd, false, true, M, f, h, dxo, h, w + o.w_fc2, f, epi(sc.du, f, nullptr, A.u, f), st);
-    ops::bias_grad(sc.du, gw + o.b_fc1, M, f, st);
-    gemm::gemm(gemm::kAccF32, true, true, f, h, M, sc.du, f, A.h2, h, epi(gw + o.w_fc1, h), st);
-    gemm::gemm(gemm::kStoreBF16, false, true, M, h, f, sc.du, f, w + o.w_fc1, h, epi(sc.dh, h), st);
-    ops::layernorm_bwd(sc.dh, A.x2, A.mean2, A.rstd2, w + o.ln2_g, dxo, sc.dx2, gw + o.ln2_g, gw + o.ln2_b, M, h, st);
+    // Bias gradients ride on the kernels producing the gradient they sum: FC1's in the
+    // GELU' epilogue, O-proj's in LN2-backward, FC2's in the LN1-backward of the layer
+    // above (or the final LN's); only the stage's top layer input gradient, arriving as
+    // a message, and the attention's dqkv keep a separate column-sum pass.
+    fork();
+    if (l == L.n_layers - 1 && !L.has_head) {
+      ops::bias_grad(dxo, gw + o.b_fc2, M, h, ws);
+      I.launches_per_step += 1;
+    }
+    gemm::gemm(gemm::kAccF32, true, true, h, f, M, dxo, h, A.g, f, epi(gw + o.w_fc2, f), ws);
+    {
+      EpiArgs e = epi(du, f, nullptr, A.u, f);
+      e.colsum = gw + o.b_fc1;
+      gemm::gemm(gemm::kGeluBwd, false, true, M, f, h, dxo, h, w + o.w_fc2, f, e, st);
+    }
+    fork();
+    gemm::gemm(gemm::kAccF32, true, true, f, h, M, du, f, A.h2, h, epi(gw + o.w_fc1, h), ws);
+    gemm::gemm(gemm::kStoreBF16, false, true, M, h, f, du, f, w + o.w_fc1, h, epi(sc.dh, h), st);
+    ops::layernorm_bwd(sc.dh, A.x2, A.mean2, A.rstd2, w + o.ln2_g, dxo, dx2, gw + o.ln2_g, gw + o.ln2_b,
+                       gw + o.b_o, M, h, st);
     // attention
-    ops::bias_grad(sc.dx2, gw + o.b_o, M, h, st);
-    gemm::gemm(gemm::kAccF32, true, true, h, h, M, sc.dx2, h, A.a, h, epi(gw + o.w_o, h), st);
-    gemm::gemm(gemm::kStoreBF16, false, true, M, h, h, sc.dx2, h, w + o.w_o, h, epi(sc.da, h), st);
-    ops::attn_bwd_tc(A.qkv, A.a, sc.da, A.lse, sc.dqkv, sc.attn, I.B, m.seq, H, m.causal, st);
-    ops::bias_grad(sc.dqkv, gw + o.b_qkv, M, 3 * h, st);
-    gemm::gemm(gemm::kAccF32, true, true, 3 * h, h, M, sc.dqkv, 3 * h, A.h1, h, epi(gw + o.w_qkv, h), st);
-    gemm::gemm(gemm::kStoreBF16, false, true, M, h, 3 * h, sc.dqkv, 3 * h, w + o.w_qkv, h, epi(sc.dh, h), st);
-    ops::layernorm_bwd(sc.dh, xin, A.mean1, A.rstd1, w + o.ln1_g, sc.dx2, dxin, gw + o.ln1_g, gw + o.ln1_b, M, h, st);
+    fork();
+    gemm::gemm(gemm::kAccF32, true, true, h, h, M, dx2, h, A.a, h, epi(gw + o.w_o, h), ws);
+    gemm::gemm(gemm::kStoreBF16, false, true, M, h, h, dx2, h, w + o.w_o, h, epi(sc.da, h), st);
+    ops::attn_bwd_tc(A.qkv, A.a, sc.da, A.lse, dqkv, sc.attn, I.B, m.seq, H, m.causal, st);
+    fork();
+    ops::bias_grad(dqkv, gw + o.b_qkv, M, 3 * h, ws);
+    gemm::gemm(gemm::kAccF32, true, true, 3 * h, h, M, dqkv, 3 * h, A.h1, h, epi(gw + o.w_qkv, h), ws);
+    side_done(l);
+    gemm::gemm(gemm::kStoreBF16, false, true, M, h, 3 * h, dqkv, 3 * h, w + o.w_qkv, h, epi(sc.dh, h), st);
+    ops::layernorm_bwd(sc.dh, xin, A.mean1, A.rstd1, w + o.ln1_g, dx2, dxin, gw + o.ln1_g, gw + o.ln1_b,
+                       l > 0 ? gw + L.layers[l - 1].b_fc2 : nullptr, M, h, st);
     dxo = dxin;
-    I.launches_per_step += 18;  // attn_bwd = 3 kernels (+ a memset node)
+    I.launches_per_step += 15;  // attn_bwd = 3 kernels (+ a memset node)
   }
   if (s == 0) {
     ops::embed_bwd(I.tokens + tok0, dxo, gw + L.wte, gw + L.wpe, M, m.seq, h, st);
     I.launches_per_step += 1;
   } else {
-    out_msg->after_produce(st);
+    out_msg->after_produce(st);  // the gradient leaves before the side stream is joined
+  }
+  if (side) {  // join: the side stream read the input message and the stash
+    CK_CUDA(cudaEventRecord(sc.join[0], ws));
+    CK_CUDA(cudaStreamWaitEvent(st, sc.join[0], 0));
   }
   // this task was the last reader of its input messages
   if (s > 0) I.msgs.at(I.msg_key(r, mb, s - 1, 0)).after_last_use(st);

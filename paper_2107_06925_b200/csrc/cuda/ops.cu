@@ -33,6 +33,12 @@ struct Vec8 {  // 8 bf16 <-> 8 fp32
     for (int t = 0; t < 4; ++t) h[t] = __floats2bfloat162_rn(f[2 * t], f[2 * t + 1]);
     *reinterpret_cast<uint4*>(p) = q;
   }
+  __device__ __forceinline__ Vec8 rounded() const {  // the values store() writes
+    Vec8 r;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) r.f[t] = __bfloat162float(__float2bfloat16_rn(f[t]));
+    return r;
+  }
 };
 
 // ------------------------------------------------------------------ LayerNorm --
@@ -82,10 +88,13 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const bf16* __restrict__ dy, con
                                                 const float* __restrict__ mean, const float* __restrict__ rstd,
                                                 const bf16* __restrict__ g, const bf16* __restrict__ dres,
                                                 bf16* __restrict__ dx, float* __restrict__ dgamma,
-                                                float* __restrict__ dbeta, int M) {
+                                                float* __restrict__ dbeta, float* __restrict__ dsum, int M) {
   cuda::pdl_wait();
   constexpr int h = VPL * 256;
-  extern __shared__ float red[];  // [8 warps][2][h]
+  extern __shared__ float red[];  // [8 warps][2][h] (+ [8 warps][h] column sums of dx when dsum)
+  float* colsum = red + 16 * h + (threadIdx.x >> 5) * h;
+  if (dsum)
+    for (int i = threadIdx.x & 31; i < h; i += 32) colsum[i] = 0.f;  // warp-private slice
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float acc_g[VPL][8], acc_b[VPL][8];
   Vec8 gam[VPL];
@@ -148,6 +157,14 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const bf16* __restrict__ dy, con
       for (int t = 0; t < 8; ++t)
         o.f[t] = rs * (dv.f[t] * gam[c].f[t] - s1 - (xv.f[t] - mu) * rs * s2) + rv.f[t];
       o.store(dx + (long long)row * h + col);
+      if (dsum) {  // column sums of the bf16 dx (the next bias gradient), lane-private smem
+        float4* cs = reinterpret_cast<float4*>(colsum + col);
+        const Vec8 ob = o.rounded();
+        float4 a = cs[0], b = cs[1];
+        a.x += ob.f[0], a.y += ob.f[1], a.z += ob.f[2], a.w += ob.f[3];
+        b.x += ob.f[4], b.y += ob.f[5], b.z += ob.f[6], b.w += ob.f[7];
+        cs[0] = a, cs[1] = b;
+      }
     }
   }
   // reduce the per-lane column partials over the 8 warps, then one atomic per column
@@ -165,6 +182,11 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const bf16* __restrict__ dy, con
     for (int w = 0; w < 8; ++w) sg += red[(w * 2) * h + col], sb += red[(w * 2 + 1) * h + col];
     atomicAdd(dgamma + col, sg);
     atomicAdd(dbeta + col, sb);
+    if (dsum) {
+      float sd = 0.f;
+      for (int w = 0; w < 8; ++w) sd += red[16 * h + w * h + col];
+      atomicAdd(dsum + col, sd);
+    }
   }
 }
 
@@ -413,19 +435,19 @@ void layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* 
 }
 
 void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* g,
-                   const bf16* dres, bf16* dx, float* dgamma, float* dbeta, int M, int h,
+                   const bf16* dres, bf16* dx, float* dgamma, float* dbeta, float* dsum, int M, int h,
                    cudaStream_t st) {
   const int grid = std::min(ceil_div(M, 8), cuda::kNumSMs);  // one 8-warp CTA per SM (255 registers)
-  const size_t smem = size_t(16) * h * sizeof(float);
+  const size_t smem = size_t(dsum ? 24 : 16) * h * sizeof(float);
   switch (h) {
 #define CK_LN(V)                                                                                   \
   case V * 256: {                                                                                  \
     static bool attr = false;                                                                      \
     if (!attr) {                                                                                   \
-      CK_CUDA(cudaFuncSetAttribute(k_ln_bwd<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * V * 256 * 4)); \
+      CK_CUDA(cudaFuncSetAttribute(k_ln_bwd<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * V * 256 * 4)); \
       attr = true;                                                                                 \
     }                                                                                              \
-    cuda::launch(k_ln_bwd<V>, dim3(grid), dim3(256), smem, st, dy, x, mean, rstd, g, dres, dx, dgamma, dbeta, M); \
+    cuda::launch(k_ln_bwd<V>, dim3(grid), dim3(256), smem, st, dy, x, mean, rstd, g, dres, dx, dgamma, dbeta, dsum, M); \
     break;                                                                                         \
   }
     CK_LN(1) CK_LN(2) CK_LN(3) CK_LN(4) CK_LN(5) CK_LN(6) CK_LN(8)
@@ -525,7 +547,15 @@ CK_API int ck_layernorm_bwd(const void* dy, const void* x, const float* mean, co
                             int h, void* st) {
   return chimera::capi::guarded([&] {
     chimera::ops::layernorm_bwd((const bf16*)dy, (const bf16*)x, mean, rstd, (const bf16*)g,
-                                (const bf16*)dres, (bf16*)dx, dg, db, M, h, (cudaStream_t)st);
+                                (const bf16*)dres, (bf16*)dx, dg, db, nullptr, M, h, (cudaStream_t)st);
+  });
+}
+CK_API int ck_layernorm_bwd_dsum(const void* dy, const void* x, const float* mean, const float* rstd,
+                                 const void* g, const void* dres, void* dx, float* dg, float* db, float* dsum,
+                                 int M, int h, void* st) {
+  return chimera::capi::guarded([&] {
+    chimera::ops::layernorm_bwd((const bf16*)dy, (const bf16*)x, mean, rstd, (const bf16*)g,
+                                (const bf16*)dres, (bf16*)dx, dg, db, dsum, M, h, (cudaStream_t)st);
   });
 }
 CK_API int ck_embed_fwd(const int32_t* tok, const void* wte, const void* wpe, void* x, int M, int seq,

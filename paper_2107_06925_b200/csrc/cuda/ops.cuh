@@ -18,7 +18,7 @@ void layernorm_fwd(const bf16* x, const bf16* gamma, const bf16* beta, bf16* y, 
 // dgamma += sum_rows dy * xhat; dbeta += sum_rows dy.  dres may be null.
 void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd,
                    const bf16* gamma, const bf16* dres, bf16* dx, float* dgamma, float* dbeta,
-                   int M, int h, cudaStream_t st);
+                   float* dsum, int M, int h, cudaStream_t st);  // dsum (nullable) += column sums of dx
 // x[t] = wte[tok[t]] + wpe[t % seq]
 void embed_fwd(const int32_t* tok, const bf16* wte, const bf16* wpe, bf16* x, int M, int seq,
                int h, cudaStream_t st);

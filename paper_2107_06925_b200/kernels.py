@@ -12,6 +12,8 @@ from ._lib import check, lib
 _vp, _ll, _i = C.c_void_p, C.c_longlong, C.c_int
 _lib.register("ck_gemm_bf16", _i, [_i, _i, _i, _i, _i, _i, _vp, _ll, _vp, _ll, _vp, _ll, _vp, _vp, _ll,
                                    _vp, _ll, _vp])
+_lib.register("ck_gemm_bf16_ex", _i, [_i, _i, _i, _i, _i, _i, _vp, _ll, _vp, _ll, _vp, _ll, _vp, _vp, _ll,
+                                      _vp, _ll, _vp, _vp])
 
 EPI = {"bf16": 0, "bias_gelu": 1, "bias_resid": 2, "gelu_bwd": 3, "acc_f32": 4, "f32": 5}
 
@@ -27,20 +29,25 @@ def _stream(stream):
 
 
 def gemm(epi, A, B, out, *, a_mn=False, b_mn=False, M=None, N=None, K=None, bias=None, aux=None,
-         out2=None, stream=None):
-    """D[m,n] = sum_k A(m,k) B(n,k) with A/B K-major ([M,K]/[N,K]) or MN-major ([K,M]/[K,N])."""
+         out2=None, stream=None, colsum=None):
+    """D[m,n] = sum_k A(m,k) B(n,k) with A/B K-major ([M,K]/[N,K]) or MN-major ([K,M]/[K,N]).
+    `colsum` (fp32 [N], gelu_bwd only) accumulates the column sums of the bf16 output."""
     M = M if M is not None else (A.shape[1] if a_mn else A.shape[0])
     K = K if K is not None else (A.shape[0] if a_mn else A.shape[1])
     N = N if N is not None else (B.shape[1] if b_mn else B.shape[0])
-    check(lib().ck_gemm_bf16(EPI[epi], int(a_mn), int(b_mn), M, N, K, _p(A), A.stride(0), _p(B),
-                             B.stride(0), _p(out), out.stride(0), _p(bias), _p(aux),
-                             aux.stride(0) if aux is not None else 0, _p(out2),
-                             out2.stride(0) if out2 is not None else 0, _stream(stream)))
+    args = (EPI[epi], int(a_mn), int(b_mn), M, N, K, _p(A), A.stride(0), _p(B), B.stride(0), _p(out),
+            out.stride(0), _p(bias), _p(aux), aux.stride(0) if aux is not None else 0, _p(out2),
+            out2.stride(0) if out2 is not None else 0)
+    if colsum is None:
+        check(lib().ck_gemm_bf16(*args, _stream(stream)))
+    else:
+        check(lib().ck_gemm_bf16_ex(*args, _p(colsum), _stream(stream)))
     return out
 
 _fp = C.POINTER(C.c_float)
 _lib.register("ck_layernorm_fwd", _i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp])
 _lib.register("ck_layernorm_bwd", _i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp])
+_lib.register("ck_layernorm_bwd_dsum", _i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp])
 _lib.register("ck_embed_fwd", _i, [_vp, _vp, _vp, _vp, _i, _i, _i, _vp])
 _lib.register("ck_embed_bwd", _i, [_vp, _vp, _vp, _vp, _i, _i, _i, _vp])
 _lib.register("ck_xent_fwd_bwd", _i, [_vp, _ll, _vp, _i, _i, _i, C.c_float, C.c_float, _vp, _vp])
@@ -58,10 +65,14 @@ def layernorm_fwd(x, g, b, y, mean, rstd, stream=None):
     check(lib().ck_layernorm_fwd(_p(x), _p(g), _p(b), _p(y), _p(mean), _p(rstd), M, h, _stream(stream)))
 
 
-def layernorm_bwd(dy, x, mean, rstd, g, dres, dx, dgamma, dbeta, stream=None):
+def layernorm_bwd(dy, x, mean, rstd, g, dres, dx, dgamma, dbeta, stream=None, dsum=None):
     M, h = x.shape
-    check(lib().ck_layernorm_bwd(_p(dy), _p(x), _p(mean), _p(rstd), _p(g), _p(dres), _p(dx), _p(dgamma),
-                                 _p(dbeta), M, h, _stream(stream)))
+    if dsum is None:
+        check(lib().ck_layernorm_bwd(_p(dy), _p(x), _p(mean), _p(rstd), _p(g), _p(dres), _p(dx), _p(dgamma),
+                                     _p(dbeta), M, h, _stream(stream)))
+    else:
+        check(lib().ck_layernorm_bwd_dsum(_p(dy), _p(x), _p(mean), _p(rstd), _p(g), _p(dres), _p(dx),
+                                          _p(dgamma), _p(dbeta), _p(dsum), M, h, _stream(stream)))
 
 
 def embed_fwd(tok, wte, wpe, x, seq, stream=None):

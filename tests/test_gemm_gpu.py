@@ -11,7 +11,11 @@ pytestmark = pytest.mark.gpu
 from paper_2107_06925_b200 import kernels as ck  # noqa: E402
 
 SHAPES = [(128, 128, 64), (256, 384, 192), (4096, 3072, 1024), (304, 200, 136), (632, 5120, 1280),
-          (1000, 1000, 72), (1024, 1024, 4096), (768, 256, 4096)]
+          (1000, 1000, 72), (1024, 1024, 4096), (768, 256, 4096),
+          # the stage shapes (64 / 256 CTA-pair tiles, split-K weight gradient) and
+          # ragged multi-wave ones
+          (4096, 1024, 1024), (4096, 1024, 4096), (4096, 4096, 1024), (3000, 1800, 1000),
+          (3072, 1024, 4096), (2560, 2048, 520)]
 
 
 def _rand(*shape):
@@ -39,7 +43,7 @@ def test_layouts_f32(a_mn, b_mn, M, N, K):
     assert _rel(acc, ref + 1) < 1e-3
 
 
-@pytest.mark.parametrize("M,N,K", SHAPES[:4])
+@pytest.mark.parametrize("M,N,K", SHAPES[:4] + SHAPES[8:12])
 def test_fused_epilogues(M, N, K):
     A, B = _rand(M, K), _rand(N, K)
     bias = _rand(N)
@@ -64,3 +68,30 @@ def test_fused_epilogues(M, N, K):
     gl = torch.nn.functional.gelu(u, approximate="tanh")
     (gp,) = torch.autograd.grad(gl.sum(), u)
     assert _rel(d, (dY.float() @ Wt.float()) * gp) < 8e-3
+
+
+@pytest.mark.parametrize("M,N,K", [(4096, 1024, 4096), (4096, 4096, 1024), (3000, 1800, 1000)])
+def test_deterministic(M, N, K):
+    """Repeated runs of a bf16-output GEMM are bit-identical."""
+    A, B = _rand(M, K), _rand(N, K)
+    outs = []
+    for _ in range(3):
+        o = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        ck.gemm("bf16", A, B, o)
+        outs.append(o)
+    torch.cuda.synchronize()
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
+
+
+def test_gelu_bwd_colsum():
+    """kGeluBwd with the fused bias gradient: colsum += column sums of the bf16 output."""
+    M, N, K = 4096, 4096, 1024
+    dY, Wt, U = _rand(M, K), _rand(K, N), _rand(M, N)
+    d = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    cs = torch.full((N,), 0.25, device="cuda")
+    ck.gemm("gelu_bwd", dY, Wt, d, b_mn=True, aux=U, colsum=cs)
+    d0 = torch.empty_like(d)
+    ck.gemm("gelu_bwd", dY, Wt, d0, b_mn=True, aux=U)
+    torch.cuda.synchronize()
+    assert torch.equal(d, d0)
+    assert _rel(cs, d.float().sum(0) + 0.25) < 1e-5

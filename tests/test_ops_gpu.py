@@ -43,6 +43,13 @@ def test_layernorm(M, h):
     rdx, rdg, rdb = torch.autograd.grad(ref, (xf, gf, bf), dy.float())
     assert rel(dx, rdx + dres.float()) < 1e-2
     assert rel(dg, rdg) < 1e-3 and rel(db, rdb) < 1e-3
+    # fused bias gradient: dsum += column sums of the bf16 dx the kernel wrote
+    dx2 = torch.empty_like(x)
+    ds = torch.full((h,), 0.5, device="cuda")
+    ck.layernorm_bwd(dy, x, mean, rstd, g, dres, dx2, torch.zeros(h, device="cuda"), torch.zeros(h, device="cuda"),
+                     dsum=ds)
+    assert torch.equal(dx2, dx)
+    assert rel(ds, dx.float().sum(0) + 0.5) < 1e-5
 
 
 def test_embedding():
