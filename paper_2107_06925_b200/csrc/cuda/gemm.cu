@@ -435,10 +435,10 @@ inline int split_k(int epi, int tiles, int slots, int K) {
 // tcgen05.mma.cta_group::2 (M = 256): each CTA stages its 128 rows of A and PBN/2 of
 // the PBN rows of B per K-block, so per-SM operand traffic per MMA drops versus a
 // single-CTA tile.  The leader (even) CTA issues the MMAs and owns the smem-full and
-// TMEM-empty barriers; commits are multicast to both CTAs.  PBN = 256 is the default;
-// PBN = 128 halves the tile so single-wave problems get two tiles per pair, the first
-// tile's epilogue hiding under the second's mainloop (and the exposed last epilogue
-// is half as long).
+// TMEM-empty barriers; commits are multicast to both CTAs.  PBN = 256 is the one used:
+// a 256 x 128 tile (two per pair on the single-wave stage shapes, the first epilogue
+// under the second mainloop) measured 0.6-0.7x of it on every stage shape -- per-SM
+// operand traffic per MMA grows by half and the mainloop becomes operand-bound.
 constexpr int kPairEpiWarps = 8;  // two per TMEM lane quarter, each owning half of the columns
 template <int PBN>
 struct PairCfg {
@@ -643,7 +643,6 @@ template <int BN, bool A_MN, bool B_MN, int EPI>
 void launch_any(int M, int N, int K, const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B,
                 long long ldb, const EpiArgs& ep, cudaStream_t st) {
   if constexpr (BN == 0) launch_pair<256, A_MN, B_MN, EPI>(M, N, K, A, lda, B, ldb, ep, st);
-  else if constexpr (BN == 1) launch_pair<128, A_MN, B_MN, EPI>(M, N, K, A, lda, B, ldb, ep, st);
   else launch<BN, A_MN, B_MN, EPI>(M, N, K, A, lda, B, ldb, ep, st);
 }
 
@@ -685,19 +684,18 @@ void gemm(Epi epi, bool a_mn, bool b_mn, int M, int N, int K, const __nv_bfloat1
     throw chimera::capi::InternalError("gemm: operands must be 16-byte aligned with ld % 8 == 0");
   // CTA-pair 256 x 256 tiles for large problems, else single-CTA 128 x 256 / 128 x 128.
   static const int force = [] {
-    const char* e = std::getenv("CK_GEMM_TILE");  // "pair" | "pair128" | "256" | "128" (benchmarks)
+    const char* e = std::getenv("CK_GEMM_TILE");  // "pair" | "256" | "128" (benchmarks)
     if (!e) return -1;
     const std::string v(e);
-    return v == "pair" ? 0 : v == "pair128" ? 1 : v == "256" ? 256 : 128;
+    return v == "pair" ? 0 : v == "256" ? 256 : 128;
   }();
   const long long tiles_pair = (long long)((M + 255) / 256) * ((N + 255) / 256);
   const long long tiles256 = (long long)((M + BM - 1) / BM) * ((N + 255) / 256);
   int choice = force;
   (void)tiles256;
   if (choice < 0) choice = (M >= 256 && N >= 256 && tiles_pair >= 48) ? 0 : (N > 128) ? 256 : 128;
-  if (choice <= 1 && (M < 256 || N < 256)) choice = 128;
+  if (choice == 0 && (M < 256 || N < 256)) choice = 128;
   if (choice == 0) by_layout<0>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
-  else if (choice == 1) by_layout<1>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
   else if (choice == 256) by_layout<256>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
   else by_layout<128>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
 }

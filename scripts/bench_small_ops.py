@@ -44,6 +44,8 @@ db = torch.zeros(h, device="cuda")
 res = {}
 res["ln_fwd"] = timeit(lambda st: K.layernorm_fwd(x, g, b, y, mean, rstd, stream=st))
 res["ln_bwd"] = timeit(lambda st: K.layernorm_bwd(dy, x, mean, rstd, g, dres, dx, dg, db, stream=st))
+dsum = torch.zeros(h, device="cuda")
+res["ln_bwd_dsum"] = timeit(lambda st: K.layernorm_bwd(dy, x, mean, rstd, g, dres, dx, dg, db, stream=st, dsum=dsum))
 for n in (h, 3 * h, f):
     d = torch.randn(M, n, device="cuda").bfloat16()
     bg = torch.zeros(n, device="cuda")
