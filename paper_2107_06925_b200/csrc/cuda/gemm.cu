@@ -283,7 +283,9 @@ __global__ void __launch_bounds__(256, 1)
            const EpiArgs ep, int M, int N, int K, int ksplit) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1 KB aligned (128-byte swizzle atoms); pointer arithmetic on the __shared__ array keeps
+  // the state space visible, so the epilogue staging compiles to STS/LDS, not generic ST/LD
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
@@ -457,7 +459,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
   using C = PairCfg<PBN>;
   extern __shared__ uint8_t smem_raw[];
   GEMM_TRACE(threadIdx.x == 32, 0, 6);
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1 KB aligned (128-byte swizzle atoms); pointer arithmetic on the __shared__ array keeps
+  // the state space visible, so the epilogue staging compiles to STS/LDS, not generic ST/LD
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
@@ -584,7 +588,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
       __syncwarp();
       GEMM_TRACE(warp == 4 && lane == 0, it, 3);
       GEMM_TRACE(warp == 11 && lane == 0, it, 5);
-      if (lane == 0) ptx::mbar_arrive_leader(&tempty[acc]);
+      if (lane == 0) ptx::mbar_arrive_leader_relaxed(&tempty[acc]);
     }
   }
   ptx::tc_fence_before();

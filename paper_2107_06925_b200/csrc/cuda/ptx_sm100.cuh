@@ -287,6 +287,14 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerBitMask)
                : "memory");
 }
+// Relaxed arrive on the leader's barrier: orders nothing but the arrive itself.  For the
+// TMEM-empty handshake -- tcgen05.wait::ld has already completed this thread's TMEM reads
+// (and tcgen05.fence::before_thread_sync precedes it), so the epilogue's outstanding
+// global stores need not drain first (a release.cluster arrive waits for them).
+__device__ __forceinline__ void mbar_arrive_leader_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerBitMask)
+               : "memory");
+}
 
 // ------------------------------------------------------------- descriptors --
 // Shared-memory matrix descriptor, SWIZZLE_128B (layout type 2), version 1 (sm_100).
