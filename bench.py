@@ -193,7 +193,7 @@ def measure_alpha_beta(world):
     ppg = int(os.environ.get("CK_PROCS_PER_GPU", "1"))
     members = list(range(0, world, ppg))
     g = dist.new_group(members, backend="nccl")
-    out = torch.zeros(2, dtype=torch.float64)
+    out = torch.zeros(4, dtype=torch.float64)
     if len(members) > 1 and dist.get_rank() in members:
         times = []
         for n in (1 << 10, 1 << 24):  # 4 KiB and 64 MiB of fp32
@@ -214,10 +214,50 @@ def measure_alpha_beta(world):
         slope = max(0.0, (t1 - t0) / (s1 - s0))
         icpt = max(0.0, t0 - slope * s0)
         r = float(len(members))
-        out = torch.tensor([icpt / (2.0 * math.log2(r)), slope * r / (2.0 * (r - 1.0))], dtype=torch.float64)
+        out = torch.tensor([icpt / (2.0 * math.log2(r)), slope * r / (2.0 * (r - 1.0)), s1, t1], dtype=torch.float64)
     dist.broadcast(out, src=0)  # default (gloo) group
     dist.destroy_process_group(g)
+    measure_alpha_beta.big = (float(out[2]), float(out[3]), len(members))
     return float(out[0]), float(out[1])
+
+
+def comm_report(world, msg_bytes):
+    """Achieved NVLink bandwidths: the 64 MiB NCCL allreduce of the alpha/beta fit (algorithmic
+    and bus bandwidth, 2(r-1)/r), and a peer copy of one stage message (cudaMemcpyPeerAsync on
+    the copy engines, GPU 0 -> GPU 1, timed by rank 0 while the other ranks wait).  The
+    executor's own messages are stored into the peer slot by the producing kernel, so they
+    have no separately timed transfer."""
+    import torch
+    import torch.distributed as dist
+    rep = {}
+    big = getattr(measure_alpha_beta, "big", None)
+    if big and big[1] > 0 and big[2] > 1:
+        nbytes, t_ms, r = big
+        alg = nbytes / (t_ms * 1e-3) / 1e9
+        rep["allreduce"] = {"ranks": r, "bytes": int(nbytes), "ms": round(t_ms, 4), "algbw_GBs": round(alg, 1),
+                            "busbw_GBs": round(alg * 2.0 * (r - 1) / r, 1), "impl": "NCCL ring/NVLS (torch nccl)"}
+    dist.barrier()
+    if dist.get_rank() == 0 and torch.cuda.device_count() > 1 and int(os.environ.get("CK_PROCS_PER_GPU", "1")) == 1:
+        src = torch.empty(msg_bytes // 2, dtype=torch.bfloat16, device="cuda:0")
+        dst = torch.empty(msg_bytes // 2, dtype=torch.bfloat16, device="cuda:1")
+        for _ in range(3):
+            dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize(0)
+        torch.cuda.synchronize(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0 = torch.cuda.current_stream(0)
+        e0.record(s0)
+        for _ in range(20):
+            dst.copy_(src, non_blocking=True)
+        e1.record(s0)
+        torch.cuda.synchronize(0)
+        torch.cuda.synchronize(1)
+        t = e0.elapsed_time(e1) / 20
+        rep["p2p_copy"] = {"bytes": int(msg_bytes), "ms": round(t, 4), "GBs": round(msg_bytes / (t * 1e-3) / 1e9, 1),
+                           "path": "cuda:0 -> cuda:1, copy engine over NVLink"}
+        del src, dst
+    dist.barrier()
+    return rep or None
 
 
 def run_reference(args, shape):
@@ -349,6 +389,7 @@ def main():
 
     # ---- alpha / beta of the collective fabric (Eq. 1's allreduce term), NCCL over all ranks
     ab = measure_alpha_beta(world) if world > 1 else (0.0, 0.0)
+    comm = comm_report(world, 2 * CFG["B"] * shape.seq * shape.hidden) if world > 1 else None
 
     stats = tr.stats()
     launches = int(stats["launches_per_step"] * args.steps)
@@ -431,6 +472,7 @@ def main():
                           "note": ("Eq. 1 assumes one worker per GPU" if not one_rank_per_gpu else
                                    "p2p term: alpha + beta * L_act with the allreduce fit (upper bound; "
                                    "stage outputs are stored into the peer slot by the producing kernel)")},
+            "comm": comm,
             "act_counts_per_worker": mp["act_counts"],
             "peak_stash_per_rank": stats["peak_stash_per_rank"],
             "peak_stash_bytes_per_rank": stats["peak_stash_bytes_per_rank"],

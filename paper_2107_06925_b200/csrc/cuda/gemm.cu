@@ -504,6 +504,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::kStageBytes;
           uint8_t* sb = sa + C::kABytes;
+#ifdef CK_GEMM_NOFEED  // scripts/gemm_trace.cu: the MMA rate with no operand traffic (timing only)
+          if (cta == 0) ptx::mbar_arrive(&full[stage]);
+          if (++stage == C::kStages) stage = 0, phase ^= 1;
+          continue;
+#endif
           if (cta == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
           if constexpr (!A_MN) {
             ptx::tma_load_2d_pair(sa, &ta, &full[stage], kb * BK, m0);
