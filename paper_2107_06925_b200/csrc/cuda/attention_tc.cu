@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(192, 2)
 // items -- heaviest first (key tile 0 sees every query tile under causal masking),
 // dealt boustrophedon-wise over the CTAs (the order balances like dynamic LPT) --
 // and pipelines across items: the next item's K/V land in the second K/V buffer and
-// its first S/dP MMAs run while the current item's dK/dV are written out.  10 warps:
+// its first S/dP MMAs run while the current item's dK/dV are written out.  16 warps:
 //   warp 8   TMA producer: per item K, V (2 buffers); per 128-query tile Q and dO
 //            (2-stage ring)
 //   warp 9   TMEM allocator + single-thread MMA issuer
@@ -395,16 +395,22 @@ __global__ void __launch_bounds__(192, 2)
 //     -- P / dS read as MN-major A operands
 //   dQ_g = dS K                      (M128 q, N64, K128 keys)  TMEM [384 + 64 (g&1), ..)
 //     double-buffered so the MMA never waits for the drain
-//   dQ_g is drained one tile later (underneath the next tile's math) by the compute
-//   WGs, 32 columns each, through a swizzled smem stage and one TMA bulk tensor
-//   reduce-add into the fp32 dQ accumulator -- no per-thread atomics.
+//   dQ_g is drained by a 4th warpgroup (warps 12-15, one per TMEM lane quarter) as soon
+//   as its MMA completes (dq_full), underneath the compute warpgroups' next tile:
+//   TMEM -> swizzled smem stage -> two TMA bulk tensor reduce-adds into the fp32 dQ
+//   accumulator (no per-thread atomics).  Draining it in the compute warps cost ~1.3 k
+//   of the ~3.6 k cycles per tile on their critical path.  setmaxnreg moves registers
+//   from the TMA/MMA and drain warpgroups (56) to the compute ones (200).
 // Item epilogue: dK (x 1/sqrt(d)) / dV leave TMEM (acc_free lets the next item's MMAs
-// accumulate), are staged bf16 in the same swizzled stage and written by TMA stores.
+// accumulate), are staged bf16 in the WG's P tile (free once the item's last MMAs are
+// done) and written by TMA stores.
 constexpr int kB_K = 0, kB_V = 2 * kTileBytes, kB_Q = 4 * kTileBytes, kB_DO = 6 * kTileBytes,
               kB_P = 8 * kTileBytes, kB_DS = 10 * kTileBytes, kB_DQ = 12 * kTileBytes;  // stage [WG][128][128 B]
 constexpr int kB_BAR = 14 * kTileBytes;
 constexpr int kBwdSmem = kB_BAR + 256;
-constexpr int kBwdThreads = 320;
+constexpr int kBwdThreads = 512;  // WG0-1 compute, WG2 = TMA + MMA warps, WG3 dQ drain
+// Register split per SM sub-partition (one warp of each warpgroup): 2 x 200 + 56 + 56 = 512.
+constexpr int kBwdRegsCompute = 192, kBwdRegsOther = 64;
 #ifndef CK_ATTN_BWD_POLY_EVERY  // backward: not MUFU-bound, the polynomial costs more than it saves
 #define CK_ATTN_BWD_POLY_EVERY 0
 #endif
@@ -451,7 +457,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kB_BAR);
   uint64_t *kv_full = bar, *kv_empty = bar + 2, *qd_full = bar + 4, *qd_empty = bar + 6, *s_full = bar + 8,
            *st_free = bar + 9, *ds_full = bar + 10, *mm_done = bar + 11, *dq_free = bar + 12,  // [2]
-      *acc_free = bar + 14;
+      *acc_free = bar + 14, *dq_full = bar + 16;  // dq_full [2]: dQ_g in TMEM buffer g & 1
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 15);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -469,7 +475,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int b2 = 0; b2 < 2; ++b2) {
       ptx::mbar_init(&kv_full[b2], 1), ptx::mbar_init(&kv_empty[b2], 1);
       ptx::mbar_init(&qd_full[b2], 1), ptx::mbar_init(&qd_empty[b2], 1);
-      ptx::mbar_init(&dq_free[b2], 256);
+      ptx::mbar_init(&dq_free[b2], 128);
+      ptx::mbar_init(&dq_full[b2], 1);
     }
     ptx::mbar_init(s_full, 1);
     ptx::mbar_init(st_free, 256);
@@ -487,6 +494,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   cuda::pdl_trigger();
   constexpr uint32_t kS = 0, kDP = 128, kDV = 256, kDK = 320, kDQ = 384;
 
+  // setmaxnreg is warpgroup-aligned: one instruction for warps 8-15 (TMA, MMA, two idle,
+  // the drain warpgroup), one for the compute warpgroups, each heading its role block
+  if (warp >= 8) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kBwdRegsOther));
   if (warp == 8) {
     if (lane == 0) {
       int g = 0;
@@ -572,11 +583,50 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           ptx::umma_f16(tmem + kDQ + 64 * st, ptx::smem_desc_sw128(sds + (k >> 2) * kTileBytes + (k & 3) * 32, 16, 1024),
                         ptx::smem_desc_sw128(sk + k * 2048, kTileBytes, 1024), id_q, k > 0);
         ptx::umma_commit(mm_done);
+        ptx::umma_commit(&dq_full[st]);
         if (last) ptx::umma_commit(&kv_empty[kvb]);  // this item's K / V no longer read
         q = nx;
       }
     }
+  } else if (warp >= 12) {  // dQ drain warpgroup
+    const int r = (warp & 3) * 32 + lane;  // TMEM lane: query row
+    const int dt = threadIdx.x - 384;
+    const uint32_t trow = tmem + (uint32_t((warp & 3) * 32) << 16);
+    uint8_t* stage = smem + kB_DQ;  // [2 column halves][128 rows][128 B]
+    int g = 0;
+    for (BwdSeq q = seq0; q.valid(); ++g) {
+      const int b = q.bh / H, hd = q.bh % H, row_base = b * seq, q0 = (q.j0 + q.it) * kQ;
+      if (dt == 0) ptx::bulk_wait_read0();  // the previous reduce-adds have read the stage
+      named_bar_sync(4, 128);
+      ptx::mbar_wait(&dq_full[g & 1], (g >> 1) & 1);
+      ptx::tc_fence_after();
+#pragma unroll 1
+      for (int hh = 0; hh < 2; ++hh) {  // 32 columns at a time (few registers in this WG)
+        uint32_t v[32];
+        ptx::tmem_ld32(trow + kDQ + 64 * (g & 1) + 32 * hh, v);
+        ptx::tmem_ld_wait();
+        if (hh == 1) {
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&dq_free[g & 1]);
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(stage + hh * kTileBytes + r * 128 + ((c ^ (r & 7)) << 4)) =
+              make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+      }
+      ptx::fence_proxy_async();
+      named_bar_sync(4, 128);
+      if (dt == 0) {
+        ptx::tma_reduce_add_2d(&tdq, stage, hd * kD, row_base + q0);
+        ptx::tma_reduce_add_2d(&tdq, stage + kTileBytes, hd * kD + 32, row_base + q0);
+        ptx::bulk_commit();
+      }
+      q.advance();
+    }
+    if (dt == 0) ptx::bulk_wait0();
+  }
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kBwdRegsCompute));
     const int g2 = warp >> 2;               // compute warpgroup: key columns [64 g2, 64 g2 + 64)
     const int r = (warp & 3) * 32 + lane;   // TMEM lane: query row (S, dP, dQ) / key row (dK, dV)
     const int ct = threadIdx.x & 127;       // thread within the WG
@@ -584,33 +634,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const float sl2 = 0.125f * kLog2e;
     uint8_t* sp = smem + kB_P + g2 * kTileBytes;
     uint8_t* sds = smem + kB_DS + g2 * kTileBytes;
-    uint8_t* stage = smem + kB_DQ + g2 * kTileBytes;
-    // the WG's stage is free once its previous bulk op has read it
-    auto stage_acquire = [&] {
-      if (ct == 0) ptx::bulk_wait_read0();
-      named_bar_sync(2 + g2, 128);
-    };
+    // the WG's P tile doubles as the item epilogue's dK / dV stage; before the next P is
+    // written there, the TMA store issued from it must have read it (epi_pending)
+    bool epi_pending = false;
     auto stage_release = [&] {
       ptx::fence_proxy_async();
       named_bar_sync(2 + g2, 128);
-    };
-    // dQ of global iteration g (query tile q0, head (b, hd)) -> TMA reduce-add; 32 columns
-    auto drain_dq = [&](int g, int q0, int row_base, int hd) {
-      stage_acquire();
-      uint32_t v[32];
-      ptx::tmem_ld32(trow + kDQ + 64 * (g & 1) + 32 * g2, v);
-      ptx::tmem_ld_wait();
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&dq_free[g & 1]);
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        *reinterpret_cast<uint4*>(stage + r * 128 + ((c ^ (r & 7)) << 4)) =
-            make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-      stage_release();
-      if (ct == 0) {
-        ptx::tma_reduce_add_2d(&tdq, stage, hd * kD + 32 * g2, row_base + q0);
-        ptx::bulk_commit();
-      }
     };
     auto fetch = [&](const BwdSeq& q, float& nl, float& nd) {  // -lse*log2(e), -D of this row
       nl = 0.f, nd = 0.f;
@@ -674,6 +703,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ptx::mbar_wait(mm_done, (g - 1) & 1);
         ptx::tc_fence_after();
       }
+      if (epi_pending) {  // the previous item's dK / dV store has read this WG's P tile
+        if (ct == 0) ptx::bulk_wait_read0();
+        named_bar_sync(2 + g2, 128);
+        epi_pending = false;
+      }
 #pragma unroll
       for (int k8 = 0; k8 < 8; ++k8) {  // 8 keys -> one 16-byte chunk of this WG's block
         const int off = r * 128 + ((k8 ^ (r & 7)) << 4);
@@ -684,11 +718,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       ptx::fence_proxy_async();
       ptx::tc_fence_before();
       ptx::mbar_arrive(ds_full);
-      if (it > 0) drain_dq(g - 1, q0 - kQ, row_base, hd);
-      if (last) {  // item epilogue: last dQ, then dK (WG 0, x 1/sqrt(d)) or dV (WG 1)
+      if (last) {  // item epilogue: dK (WG 0, x 1/sqrt(d)) or dV (WG 1)
         ptx::mbar_wait(mm_done, g & 1);
         ptx::tc_fence_after();
-        drain_dq(g, q0, row_base, hd);
         uint32_t v[2][32];
         ptx::tmem_ld32(trow + (g2 == 0 ? kDK : kDV), v[0]);
         ptx::tmem_ld32(trow + (g2 == 0 ? kDK : kDV) + 32, v[1]);
@@ -709,15 +741,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
           w[c] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
         }
-        if (k0 + kKV <= seq) {  // whole tile inside the sequence: swizzled stage + TMA store
-          stage_acquire();
+        if (k0 + kKV <= seq) {  // whole tile inside the sequence: swizzled stage (P tile) + TMA store
 #pragma unroll
-          for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(stage + r * 128 + ((c ^ (r & 7)) << 4)) = w[c];
+          for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(sp + r * 128 + ((c ^ (r & 7)) << 4)) = w[c];
           stage_release();
           if (ct == 0) {
-            ptx::tma_store_2d(&tdqkv, stage, (1 + g2) * H * kD + hd * kD, row_base + k0);
+            ptx::tma_store_2d(&tdqkv, sp, (1 + g2) * H * kD + hd * kD, row_base + k0);
             ptx::bulk_commit();
           }
+          epi_pending = true;
         } else if (k0 + r < seq) {  // sequence tail: rows past seq belong to the next sequence
           bf16* dst = dqkv + ((long long)row_base + k0 + r) * (3LL * H * kD) + (1 + g2) * (long long)H * kD + hd * kD;
 #pragma unroll
