@@ -441,6 +441,82 @@ inline int split_k(int epi, int tiles, int slots, int K) {
 // a 256 x 128 tile (two per pair on the single-wave stage shapes, the first epilogue
 // under the second mainloop) measured 0.6-0.7x of it on every stage shape -- per-SM
 // operand traffic per MMA grows by half and the mainloop becomes operand-bound.
+// TMA-store epilogue (kStoreBF16, kBiasResid, kAccF32) of one 32 x 32 accumulator chunk in the
+// tcgen05.ld layout (lane = row, 32 consecutive fp32 columns): the warp writes it to its
+// swizzled smem staging and one lane issues a bulk tensor store (bf16, 64-byte swizzle,
+// two alternating 2 KB buffers) or a bulk tensor reduce-add (fp32 += D at L2: the weight-
+// gradient accumulate, split-K included, with no read-back of the output) -- no
+// shared-memory round trip to a store layout, no per-thread global stores, and the
+// stores drain asynchronously while the next chunk (or tile) proceeds.
+// The residual operand of a kBiasResid chunk in the same layout: this lane's row, 32
+// columns (four 16-byte loads), fetched one chunk ahead.
+template <int EPI>
+__device__ __forceinline__ void aux_row_prefetch(const EpiArgs& ep, int row, int col0, int M, int N, uint4 (&a)[4]) {
+  if constexpr (EPI == kBiasResid) {
+    const bool ok = row < M && col0 < N;  // N % 32 == 0 on this path: whole chunks
+    const __nv_bfloat16* p = ep.aux + (long long)row * ep.ld_aux + col0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a[k] = ok ? *reinterpret_cast<const uint4*>(p + 8 * k) : make_uint4(0, 0, 0, 0);
+  }
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& ep, const CUtensorMap* to, int row0, int col0,
+                                                   const uint32_t (&r)[32], uint8_t* stg, int lane, int& nbuf,
+                                                   const uint4 (&aux)[4]) {
+  if constexpr (EPI == kAccF32) {
+    if (lane == 0) ptx::bulk_wait_read0();  // the previous reduce has read the staging
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      *reinterpret_cast<uint4*>(stg + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+          make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+    ptx::fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      ptx::tma_reduce_add_2d(to, stg, col0, row0);
+      ptx::bulk_commit();
+    }
+  } else {
+    uint32_t q[16];
+    if (ep.bias) {  // the chunk's 32 bias values (one broadcast line for the warp)
+      uint4 b[4];
+      const __nv_bfloat16* bp = ep.bias + col0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) b[k] = *reinterpret_cast<const uint4*>(bp + 8 * k);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        float2 bb = bf2f((&b[i >> 2].x)[i & 3]);
+        if constexpr (EPI == kBiasResid) bb = ptx::add2(bb, bf2f((&aux[i >> 2].x)[i & 3]));
+        q[i] = f2bf(__uint_as_float(r[2 * i]) + bb.x, __uint_as_float(r[2 * i + 1]) + bb.y);
+      }
+    } else if constexpr (EPI == kBiasResid) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float2 a = bf2f((&aux[i >> 2].x)[i & 3]);
+        q[i] = f2bf(__uint_as_float(r[2 * i]) + a.x, __uint_as_float(r[2 * i + 1]) + a.y);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) q[i] = f2bf(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+    }
+    uint8_t* buf = stg + (nbuf & 1) * 2048;
+    if (lane == 0) ptx::bulk_wait_read1();  // the store issued from this buffer two chunks ago
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      *reinterpret_cast<uint4*>(buf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+          make_uint4(q[4 * j], q[4 * j + 1], q[4 * j + 2], q[4 * j + 3]);
+    ptx::fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      ptx::tma_store_2d(to, buf, col0, row0);
+      ptx::bulk_commit();
+    }
+    ++nbuf;
+  }
+}
+
 constexpr int kPairEpiWarps = 8;  // two per TMEM lane quarter, each owning half of the columns
 template <int PBN>
 struct PairCfg {
@@ -448,21 +524,27 @@ struct PairCfg {
   static constexpr int kBBytes = (PBN / 2) * BK * 2;         // this CTA's PBN/2 rows of B
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = PBN == 256 ? 5 : 7;
-  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256 + kPairEpiWarps * kEpiWarpBytes;
+  // per-warp epilogue staging, 1 KB aligned for the swizzled TMA-store layouts
+  static constexpr int kStgBytes = 5120;
+  static_assert(kStgBytes >= kEpiWarpBytes, "staging");
+  static constexpr int kSmem = kStages * kStageBytes + kPairEpiWarps * kStgBytes + 256 + 1024;
   static constexpr int kChunks = PBN / 64;                   // 32-column chunks per epilogue warp
 };
 
-template <int PBN, bool A_MN, bool B_MN, int EPI>
+template <int PBN, bool A_MN, bool B_MN, int EPI, bool TO>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiWarps, 1)
-    k_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const EpiArgs ep,
-            int M, int N, int K, int ksplit) {
+    k_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+            const __grid_constant__ CUtensorMap to, const EpiArgs ep, int M, int N, int K, int ksplit) {
+  static_assert(!TO || EPI == kStoreBF16 || EPI == kBiasResid || EPI == kAccF32,
+                "TMA-store epilogue: bf16 store (+bias, +residual) / fp32 accumulate");
   using C = PairCfg<PBN>;
   extern __shared__ uint8_t smem_raw[];
   GEMM_TRACE(threadIdx.x == 32, 0, 6);
   // 1 KB aligned (128-byte swizzle atoms); pointer arithmetic on the __shared__ array keeps
   // the state space visible, so the epilogue staging compiles to STS/LDS, not generic ST/LD
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint8_t* stg_base = smem + C::kStages * C::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg_base + kPairEpiWarps * C::kStgBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
@@ -478,6 +560,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&ta);
     ptx::tma_prefetch(&tb);
+    if constexpr (TO) ptx::tma_prefetch(&to);
     for (int s = 0; s < C::kStages; ++s) ptx::mbar_init(&full[s], 1), ptx::mbar_init(&empty[s], 1);
     for (int a = 0; a < 2; ++a) ptx::mbar_init(&tfull[a], 1), ptx::mbar_init(&tempty[a], 2 * kPairEpiWarps);
     ptx::fence_barrier_init();
@@ -564,30 +647,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
   } else if (warp >= 4) {
     const int q = warp & 3, half = (warp - 4) >> 2;  // lane quarter, column half
     constexpr int NC = C::kChunks;
-    int it = 0;
+    uint8_t* stg = stg_base + (warp - 4) * C::kStgBytes;
+    int it = 0, nbuf = 0;
     for (int tile = pair; tile < tiles; tile += npairs, ++it) {
       const int acc = it & 1;
       int mb, nb;
       tile_coords(tile, num_m, num_n, mb, nb);
       EpiPre pre;  // this tile's first-chunk operands are fetched while the MMAs run
-      epilogue_prefetch<EPI>(ep, mb * 256 + int(cta) * 128 + q * 32, nb * PBN + half * (PBN / 2), M, N, lane,
-                             ksplit > 1, pre);
+      uint4 auxn[4];
+      if constexpr (!TO)
+        epilogue_prefetch<EPI>(ep, mb * 256 + int(cta) * 128 + q * 32, nb * PBN + half * (PBN / 2), M, N, lane,
+                               ksplit > 1, pre);
+      else
+        aux_row_prefetch<EPI>(ep, mb * 256 + int(cta) * 128 + q * 32 + lane, nb * PBN + half * (PBN / 2), M, N, auxn);
       ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
       GEMM_TRACE(warp == 4 && lane == 0, it, 2);
       GEMM_TRACE(warp == 11 && lane == 0, it, 4);
       ptx::tc_fence_after();
       const int row0 = mb * 256 + int(cta) * 128 + q * 32;
       const uint32_t t0 = tmem_base + (uint32_t(q * 32) << 16) + acc * PBN;
-      uint8_t* stg = smem + C::kStages * C::kStageBytes + 256 + (warp - 4) * kEpiWarpBytes;
 #pragma unroll 1
       for (int c = half * NC; c < half * NC + NC; ++c) {
         uint32_t r[32];
         ptx::tmem_ld32(t0 + c * 32, r);
         const int col0 = nb * PBN + c * 32;
-        EpiPre cur = pre;
-        if (c + 1 < half * NC + NC) epilogue_prefetch<EPI>(ep, row0, col0 + 32, M, N, lane, ksplit > 1, pre);
-        ptx::tmem_ld_wait();
-        if (row0 < M && col0 < N) epilogue_chunk<EPI>(ep, row0, col0, M, N, r, stg, lane, ksplit > 1, cur);
+        if constexpr (TO) {
+          uint4 auxc[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) auxc[k] = auxn[k];
+          if (c + 1 < half * NC + NC) aux_row_prefetch<EPI>(ep, row0 + lane, col0 + 32, M, N, auxn);
+          ptx::tmem_ld_wait();
+          if (row0 < M && col0 < N) epilogue_chunk_tma<EPI>(ep, &to, row0, col0, r, stg, lane, nbuf, auxc);
+        } else {
+          EpiPre cur = pre;
+          if (c + 1 < half * NC + NC) epilogue_prefetch<EPI>(ep, row0, col0 + 32, M, N, lane, ksplit > 1, pre);
+          ptx::tmem_ld_wait();
+          if (row0 < M && col0 < N) epilogue_chunk<EPI>(ep, row0, col0, M, N, r, stg, lane, ksplit > 1, cur);
+        }
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -595,6 +691,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
       GEMM_TRACE(warp == 11 && lane == 0, it, 5);
       if (lane == 0) ptx::mbar_arrive_leader_relaxed(&tempty[acc]);
     }
+    if constexpr (TO)
+      if (lane == 0) ptx::bulk_wait0();  // the bulk stores / reduces have completed
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();
@@ -612,17 +710,46 @@ void launch_pair(int M, int N, int K, const __nv_bfloat16* A, long long lda, con
                               : cuda::make_map_2d_bf16(A, K, M, lda, 64, 128);
   const CUtensorMap tb = B_MN ? cuda::make_map_2d_bf16(B, N, K, ldb, 64, BK)
                               : cuda::make_map_2d_bf16(B, K, N, ldb, 64, PBN / 2);
-  auto kern = k_gemm2<PBN, A_MN, B_MN, EPI>;
+  const int base = ((M + 255) / 256) * ((N + PBN - 1) / PBN);
+  const int ks = split_k(EPI, base, cuda::kNumSMs / 2, K);
+  const int tiles = base * ks;
+  const int pairs = tiles < cuda::kNumSMs / 2 ? tiles : cuda::kNumSMs / 2;
+  // TMA-store epilogue for bf16 stores / fp32 accumulates when the output rows are
+  // 16-byte aligned (CK_GEMM_TMA_OUT=0: the register epilogue everywhere; =1: not for
+  // bias+residual)
+  static const int tma_out_mode = [] {  // 0 off, 1 stores + accumulates, 2 also bias+residual
+    const char* e = std::getenv("CK_GEMM_TMA_OUT");
+    return e ? atoi(e) : 2;
+  }();
+  const bool tma_out_on = tma_out_mode >= (EPI == kBiasResid ? 2 : 1);
+  constexpr bool kTmaCapable = EPI == kStoreBF16 || EPI == kBiasResid || EPI == kAccF32;
+  constexpr int esz = EPI == kAccF32 ? 4 : 2;
+  const bool use_tma = kTmaCapable && tma_out_on && (reinterpret_cast<uintptr_t>(ep.out) % 16) == 0 &&
+                       (ep.ldo * esz) % 16 == 0 && (!ep.bias || (reinterpret_cast<uintptr_t>(ep.bias) % 16) == 0) &&
+                       (EPI != kBiasResid || ((reinterpret_cast<uintptr_t>(ep.aux) % 16) == 0 && ep.ld_aux % 8 == 0)) &&
+                       (N % 32) == 0;
+  if constexpr (kTmaCapable) {
+    if (use_tma) {
+      const CUtensorMap to = EPI == kAccF32 ? cuda::make_map_2d_f32(ep.out, N, M, ep.ldo, 32, 32)
+                                           : cuda::make_map_2d_bf16(ep.out, N, M, ep.ldo, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+      auto kern = k_gemm2<PBN, A_MN, B_MN, EPI, true>;
+      static bool attr = false;
+      if (!attr) {
+        CK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+        attr = true;
+      }
+      cuda::launch(kern, dim3(2 * pairs), dim3(128 + 32 * kPairEpiWarps), C::kSmem, st, ta, tb, to, ep, M, N, K, ks);
+      CK_CUDA(cudaGetLastError());
+      return;
+    }
+  }
+  auto kern = k_gemm2<PBN, A_MN, B_MN, EPI, false>;
   static bool attr = false;
   if (!attr) {
     CK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr = true;
   }
-  const int base = ((M + 255) / 256) * ((N + PBN - 1) / PBN);
-  const int ks = split_k(EPI, base, cuda::kNumSMs / 2, K);
-  const int tiles = base * ks;
-  const int pairs = tiles < cuda::kNumSMs / 2 ? tiles : cuda::kNumSMs / 2;
-  cuda::launch(kern, dim3(2 * pairs), dim3(128 + 32 * kPairEpiWarps), C::kSmem, st, ta, tb, ep, M, N, K, ks);
+  cuda::launch(kern, dim3(2 * pairs), dim3(128 + 32 * kPairEpiWarps), C::kSmem, st, ta, tb, ta, ep, M, N, K, ks);
   CK_CUDA(cudaGetLastError());
 }
 

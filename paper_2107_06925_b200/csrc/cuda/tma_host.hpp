@@ -33,9 +33,10 @@ inline EncodeTiledFn encode_fn() {
 }
 
 // 2-D bf16 tensor: `inner` contiguous elements per row, `outer` rows `row_stride`
-// elements apart; box = {box_inner, box_outer}; 128-byte swizzle (box_inner = 64).
+// elements apart; box = {box_inner, box_outer}; 128-byte swizzle (box_inner = 64) unless given.
 inline CUtensorMap make_map_2d_bf16(const void* base, uint64_t inner, uint64_t outer,
-                                    uint64_t row_stride, uint32_t box_inner, uint32_t box_outer) {
+                                    uint64_t row_stride, uint32_t box_inner, uint32_t box_outer,
+                                    CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {inner, outer};
   const cuuint64_t strides[1] = {row_stride * 2};
@@ -43,7 +44,7 @@ inline CUtensorMap make_map_2d_bf16(const void* base, uint64_t inner, uint64_t o
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
                                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw chimera::capi::InternalError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) +
