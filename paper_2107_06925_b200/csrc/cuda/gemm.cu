@@ -417,6 +417,11 @@ __global__ void __launch_bounds__(256, 1)
 // last wave is (nearly) as full as the best achievable; slices combine with fp32 vector
 // atomics.
 inline int split_k(int epi, int tiles, int slots, int K) {
+  static const int force = [] {  // CK_GEMM_KSPLIT=n: fixed slice count (benchmarks)
+    const char* e = std::getenv("CK_GEMM_KSPLIT");
+    return e ? atoi(e) : 0;
+  }();
+  if (epi == kAccF32 && force > 0) return force;
   if (epi != kAccF32 || tiles >= slots) return 1;
   const int kb = (K + BK - 1) / BK;
   // (more than 4 slices: the extra fp32 atomic traffic costs more than the wave it fills)
