@@ -389,16 +389,16 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t t0 = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
       uint8_t* stg = smem + C::kStages * C::kStageBytes + 256 + q * kEpiWarpBytes;
       EpiPre pre;
-      epilogue_prefetch<EPI>(ep, row0, nb * BN, M, N, lane, ksplit > 1, pre);
+      epilogue_prefetch<EPI>(ep, row0, nb * BN, M, N, lane, (ksplit > 1 || ep.atomic_acc), pre);
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
         ptx::tmem_ld32(t0 + c * 32, r);
         const int col0 = nb * BN + c * 32;
         EpiPre cur = pre;
-        if (c + 1 < BN / 32) epilogue_prefetch<EPI>(ep, row0, col0 + 32, M, N, lane, ksplit > 1, pre);
+        if (c + 1 < BN / 32) epilogue_prefetch<EPI>(ep, row0, col0 + 32, M, N, lane, (ksplit > 1 || ep.atomic_acc), pre);
         ptx::tmem_ld_wait();
-        if (row0 < M && col0 < N) epilogue_chunk<EPI>(ep, row0, col0, M, N, r, stg, lane, ksplit > 1, cur);
+        if (row0 < M && col0 < N) epilogue_chunk<EPI>(ep, row0, col0, M, N, r, stg, lane, (ksplit > 1 || ep.atomic_acc), cur);
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -662,7 +662,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
       uint4 auxn[4];
       if constexpr (!TO)
         epilogue_prefetch<EPI>(ep, mb * 256 + int(cta) * 128 + q * 32, nb * PBN + half * (PBN / 2), M, N, lane,
-                               ksplit > 1, pre);
+                               (ksplit > 1 || ep.atomic_acc), pre);
       else
         aux_row_prefetch<EPI>(ep, mb * 256 + int(cta) * 128 + q * 32 + lane, nb * PBN + half * (PBN / 2), M, N, auxn);
       ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
@@ -685,9 +685,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
           if (row0 < M && col0 < N) epilogue_chunk_tma<EPI>(ep, &to, row0, col0, r, stg, lane, nbuf, auxc);
         } else {
           EpiPre cur = pre;
-          if (c + 1 < half * NC + NC) epilogue_prefetch<EPI>(ep, row0, col0 + 32, M, N, lane, ksplit > 1, pre);
+          if (c + 1 < half * NC + NC) epilogue_prefetch<EPI>(ep, row0, col0 + 32, M, N, lane, (ksplit > 1 || ep.atomic_acc), pre);
           ptx::tmem_ld_wait();
-          if (row0 < M && col0 < N) epilogue_chunk<EPI>(ep, row0, col0, M, N, r, stg, lane, ksplit > 1, cur);
+          if (row0 < M && col0 < N) epilogue_chunk<EPI>(ep, row0, col0, M, N, r, stg, lane, (ksplit > 1 || ep.atomic_acc), cur);
         }
       }
       ptx::tc_fence_before();

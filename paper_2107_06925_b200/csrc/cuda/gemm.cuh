@@ -25,6 +25,7 @@ struct EpiArgs {
   __nv_bfloat16* out2 = nullptr;  // kBiasGelu second output
   long long ld_out2 = 0;
   float* colsum = nullptr;  // kGeluBwd: colsum[n] += sum_m out[m][n] (the fused bias gradient)
+  bool atomic_acc = false;  // kAccF32: always accumulate atomically (outf shared by concurrent GEMMs)
 };
 
 // Operand layouts: A(m,k) is A[m*lda+k] when !a_mn (K-major) else A[k*lda+m];

@@ -100,7 +100,8 @@ struct StageState {
   StageLayout L;
   float* w32 = nullptr;
   bf16* w16 = nullptr;
-  std::vector<float*> grads;  // one per local copy holding this stage
+  std::vector<float*> grads;  // gradient buffers of the local copies (one, shared, by default)
+  int copies = 0;             // local copies (rank, pipeline) holding this stage
 };
 
 struct Copy {  // one (local rank, pipeline) stage replica
@@ -270,10 +271,26 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
         CK_CUDA(cudaMemset(st.w16, 0, st.L.total * sizeof(bf16)));
         I.stages[s] = std::move(st);
       }
+      // The local copies of a stage accumulate into ONE fp32 gradient buffer (every
+      // gradient accumulation is atomic: TMA reduce-add / vector red in the GEMMs,
+      // atomics in LayerNorm, bias, embedding backward), so the optimizer step reads one
+      // gradient per parameter instead of one per copy -- Engine::apply_stage_update's
+      // sum over copies (oracle.cpp:283-299) happens as the gradients are produced.
+      // CK_SHARED_GRADS=0: one buffer per copy, summed by the update kernel.
+      static const bool shared = [] {
+        const char* e = std::getenv("CK_SHARED_GRADS");
+        return !(e && e[0] == '0');
+      }();
+      StageState& S = I.stages[s];
       Copy cp{rank, p, s, nullptr, {}, {}};
-      cp.grad = I.arena.alloc<float>(I.stages[s].L.total);
-      CK_CUDA(cudaMemset(cp.grad, 0, I.stages[s].L.total * sizeof(float)));
-      I.stages[s].grads.push_back(cp.grad);
+      if (shared && !S.grads.empty()) {
+        cp.grad = S.grads[0];
+      } else {
+        cp.grad = I.arena.alloc<float>(S.L.total);
+        CK_CUDA(cudaMemset(cp.grad, 0, S.L.total * sizeof(float)));
+        S.grads.push_back(cp.grad);
+      }
+      S.copies++;
       I.copies[{rank, p}] = std::move(cp);
     }
   }
@@ -471,6 +488,7 @@ EpiArgs epi(void* out, long long ldo, const bf16* bias = nullptr, const bf16* au
             long long ld_aux = 0, bf16* out2 = nullptr, long long ld_out2 = 0) {
   EpiArgs e;
   e.out = out, e.ldo = ldo, e.bias = bias, e.aux = aux, e.ld_aux = ld_aux, e.out2 = out2, e.ld_out2 = ld_out2;
+  e.atomic_acc = true;  // weight gradients: copies on concurrent streams share the buffer
   return e;
 }
 
@@ -718,7 +736,7 @@ void plan_sync(Trainer::Impl& I) {
   }
   for (auto& [st, S] : I.stages) {
     auto& evs = I.stage_done_ev[st];
-    while (evs.size() < S.grads.size()) {
+    while (int(evs.size()) < S.copies) {
       cudaEvent_t e;
       CK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       evs.push_back(e);
