@@ -818,26 +818,52 @@ void by_layout(Epi epi, bool a_mn, bool b_mn, int M, int N, int K, const __nv_bf
 
 }  // namespace
 
+// Tile configuration by a wave model calibrated on B200 (scripts/gemm_tile_sweep.py):
+// time = waves x per-tile work / per-slot rate, waves over the slots the configuration
+// keeps resident (74 CTA pairs or 148 CTAs), split-K included for the fp32 accumulate.
+// Per-slot rates (TFLOP/s): CTA pair 256x256 24.6, 128x256 11.4, 128x128 7.0, 128x64 3.6
+// -- the narrow tiles are operand-bound but put more SMs on problems with few output
+// tiles and a deep K (the small-M stage shapes of GPT-2 1.3B / Bert-48).
+int pick_tile(Epi epi, int M, int N, int K) {
+  struct Cand {
+    int choice, bm, bn, slots;
+    double rate;
+  };
+  const Cand cands[] = {{0, 256, 256, cuda::kNumSMs / 2, 24.6}, {256, BM, 256, cuda::kNumSMs, 11.4},
+                        {128, BM, 128, cuda::kNumSMs, 7.0}, {64, BM, 64, cuda::kNumSMs, 3.6}};
+  int best = 128;
+  double best_t = 1e300;
+  for (const Cand& c : cands) {
+    if (c.choice == 0 && (M < 256 || N < 256)) continue;
+    if (c.choice == 256 && N <= 128) continue;
+    const long long tiles = (long long)((M + c.bm - 1) / c.bm) * ((N + c.bn - 1) / c.bn);
+    const int ks = split_k(epi, int(std::min<long long>(tiles, 1 << 30)), c.slots, K);
+    const long long units = tiles * ks, waves = (units + c.slots - 1) / c.slots;
+    const double kdepth = double((K + ks - 1) / ks);
+    const double t = double(waves) * (2.0 * c.bm * c.bn * kdepth) / c.rate;
+    if (t < best_t * 0.98) best_t = t, best = c.choice;  // prefer the larger tile on a near-tie
+  }
+  return best;
+}
+
 void gemm(Epi epi, bool a_mn, bool b_mn, int M, int N, int K, const __nv_bfloat16* A, long long lda,
           const __nv_bfloat16* B, long long ldb, const EpiArgs& ep, cudaStream_t st) {
   if (M <= 0 || N <= 0 || K <= 0) return;
   if ((lda % 8) || (ldb % 8) || (reinterpret_cast<uintptr_t>(A) % 16) || (reinterpret_cast<uintptr_t>(B) % 16))
     throw chimera::capi::InternalError("gemm: operands must be 16-byte aligned with ld % 8 == 0");
-  // CTA-pair 256 x 256 tiles for large problems, else single-CTA 128 x 256 / 128 x 128.
+  // CTA-pair 256 x 256 or single-CTA 128 x {256, 128, 64} tiles (pick_tile).
   static const int force = [] {
-    const char* e = std::getenv("CK_GEMM_TILE");  // "pair" | "256" | "128" (benchmarks)
+    const char* e = std::getenv("CK_GEMM_TILE");  // "pair" | "256" | "128" | "64" (benchmarks)
     if (!e) return -1;
     const std::string v(e);
-    return v == "pair" ? 0 : v == "256" ? 256 : 128;
+    return v == "pair" ? 0 : v == "256" ? 256 : v == "64" ? 64 : 128;
   }();
-  const long long tiles_pair = (long long)((M + 255) / 256) * ((N + 255) / 256);
-  const long long tiles256 = (long long)((M + BM - 1) / BM) * ((N + 255) / 256);
   int choice = force;
-  (void)tiles256;
-  if (choice < 0) choice = (M >= 256 && N >= 256 && tiles_pair >= 48) ? 0 : (N > 128) ? 256 : 128;
+  if (choice < 0) choice = pick_tile(epi, M, N, K);
   if (choice == 0 && (M < 256 || N < 256)) choice = 128;
   if (choice == 0) by_layout<0>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
   else if (choice == 256) by_layout<256>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
+  else if (choice == 64) by_layout<64>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
   else by_layout<128>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
 }
 
