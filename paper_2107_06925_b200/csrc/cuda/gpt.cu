@@ -144,6 +144,11 @@ struct Trainer::Impl {
   // activation recomputation (config.recompute, forced by forward doubling): slots keep
   // only the stage input; one full per-rank workspace is rebuilt by each backward
   bool recompute = false;
+  // forward doubling: adjacent forwards of micro-batches (m, m+1) of one copy run as one
+  // 2B-row pass (the recompute workspace holds 2M rows; fd_in / fd_out per rank gather the
+  // two stage inputs and scatter the two outputs).  CK_FD_FUSE=0 disables.
+  bool fd_fuse = false;
+  std::vector<bf16*> fd_in, fd_out;
   std::vector<Stash> rscratch;  // per local rank
   float* loss_dummy = nullptr;  // sink for the recomputed last-stage loss
   std::map<std::array<int, 2>, long long> slot_bytes;  // (rank, pipeline) -> bytes of one stash
@@ -318,7 +323,12 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
     }
   }
   I.recompute = c.recompute;
-  auto alloc_full = [&](Stash& st, bool embed, bool head, int Ls) {
+  {
+    const char* e = std::getenv("CK_FD_FUSE");
+    I.fd_fuse = I.recompute && c.scaling == pipesim::ScalingStrategy::ForwardDoubling && !(e && e[0] == '0');
+  }
+  auto alloc_full = [&](Stash& st, bool embed, bool head, int Ls, int pairs = 1) {
+      const int M = I.M * pairs;  // rows
       if (embed) st.x0 = I.arena.alloc<bf16>((size_t)M * h);
       for (int l = 0; l < Ls; ++l) {
         LayerStash ls;
@@ -334,7 +344,7 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
         ls.rstd1 = I.arena.alloc<float>(M);
         ls.mean2 = I.arena.alloc<float>(M);
         ls.rstd2 = I.arena.alloc<float>(M);
-        ls.lse = I.arena.alloc<float>((size_t)I.B * H * shape.seq);
+        ls.lse = I.arena.alloc<float>((size_t)pairs * I.B * H * shape.seq);
         st.layers.push_back(ls);
       }
       if (head) {
@@ -348,7 +358,11 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
   if (I.recompute) {  // one full workspace per rank; xo of the last layer is a sink
     for (int k = 0; k < n_ranks; ++k) {
       Stash st;
-      alloc_full(st, false, true, Lmax);
+      alloc_full(st, false, true, Lmax, I.fd_fuse ? 2 : 1);
+      if (I.fd_fuse) {
+        I.fd_in.push_back(I.arena.alloc<bf16>((size_t)2 * M * h));
+        I.fd_out.push_back(I.arena.alloc<bf16>((size_t)2 * M * h));
+      }
       st.layers.back().xo = I.arena.alloc<bf16>((size_t)M * h);
       I.rscratch.push_back(std::move(st));
     }
@@ -528,13 +542,62 @@ void Trainer::forward_task(int rank, int p, int mb, int s) {
   if (s == 0) I.launches_per_step += 1;
 }
 
+// Forward doubling (schedgen.cpp:104-111): the two real micro-batches mb, mb+1
+// that one virtual micro-batch expands to run as ONE pass of 2B sequences -- GEMMs of 2M
+// rows instead of two of M (the 632-row GPT-2 1.3B stage GEMMs fill 3 of their 256-row
+// tiles 2.5 times) -- through the 2M-row recompute workspace: the two stage inputs are
+// gathered into fd_in, the 2M-row output is scattered to the two outgoing messages (peer
+// copies over NVLink when the consumer is remote).  Stash discipline, slot accounting and
+// message handshakes are exactly those of two forward_task calls.
+void Trainer::forward_pair(int rank, int p, int mb, int s) {
+  Impl& I = *d_;
+  const ModelShape& m = I.m;
+  const int h = m.hidden, M = I.M, r = rank / I.D;
+  const size_t bytes = (size_t)M * h * sizeof(bf16);
+  cudaStream_t st = I.stream_of(rank);
+  Copy& cp = I.copies.at({rank, p});
+  const StageLayout& L = I.stages.at(s).L;
+  const bf16* w = I.stages.at(s).w16;
+  bf16* xin = I.fd_in[rank - I.first];
+  const Msg* outs[2] = {nullptr, nullptr};
+  for (int k = 0; k < 2; ++k) {
+    if (cp.free_slots.empty()) throw capi::InternalError("stash pool exhausted");
+    const int slot = cp.free_slots.back();
+    cp.free_slots.pop_back();
+    I.slot_of[{rank, p, mb + k, s}] = slot;
+    Stash& X = cp.slots[slot];
+    const size_t tok0 = (size_t)(r * I.N + mb + k) * I.B * m.seq;
+    if (s == 0) {
+      ops::embed_fwd(I.tokens + tok0, w + L.wte, w + L.wpe, X.x0, M, m.seq, h, st);
+      CK_CUDA(cudaMemcpyAsync(xin + (size_t)k * M * h, X.x0, bytes, cudaMemcpyDeviceToDevice, st));
+      I.launches_per_step += 1;
+    } else {
+      const Msg& in = I.msgs.at(I.msg_key(r, mb + k, s - 1, 0));
+      in.before_consume(st);
+      CK_CUDA(cudaMemcpyAsync(xin + (size_t)k * M * h, in.buf, bytes, cudaMemcpyDeviceToDevice, st));
+    }
+    if (s + 1 < I.D) {
+      outs[k] = &I.msgs.at(I.msg_key(r, mb + k, s, 0));
+      outs[k]->before_produce(st);
+    }
+  }
+  Stash& Wk = I.rscratch[rank - I.first];
+  bf16* out_final = L.has_head ? Wk.xfinal : I.fd_out[rank - I.first];
+  stage_forward(rank, s, Wk, xin, out_final, (size_t)(r * I.N + mb) * I.B * m.seq, I.loss, 2);
+  if (!L.has_head)
+    for (int k = 0; k < 2; ++k) {
+      CK_CUDA(cudaMemcpyAsync(outs[k]->buf, out_final + (size_t)k * M * h, bytes, cudaMemcpyDeviceToDevice, st));
+      outs[k]->after_produce(st);
+    }
+}
+
 // The layers (+ final LN, LM head, fused cross-entropy) of stage s for one
 // micro-batch: activations into X, stage output into out_final.
 void Trainer::stage_forward(int rank, int s, Stash& X, const bf16* x, bf16* out_final, size_t tok0,
-                            float* loss) {
+                            float* loss, int pairs) {
   Impl& I = *d_;
   const ModelShape& m = I.m;
-  const int h = m.hidden, f = m.ffn, M = I.M, H = m.heads;
+  const int h = m.hidden, f = m.ffn, M = I.M * pairs, H = m.heads, Bq = I.B * pairs;  // rows, sequences
   cudaStream_t st = I.stream_of(rank);
   const StageLayout& L = I.stages.at(s).L;
   const bf16* w = I.stages.at(s).w16;
@@ -545,7 +608,7 @@ void Trainer::stage_forward(int rank, int s, Stash& X, const bf16* x, bf16* out_
     ops::layernorm_fwd(x, w + o.ln1_g, w + o.ln1_b, A.h1, A.mean1, A.rstd1, M, h, st);
     gemm::gemm(gemm::kStoreBF16, false, false, M, 3 * h, h, A.h1, h, w + o.w_qkv, h,
                epi(A.qkv, 3 * h, w + o.b_qkv), st);
-    ops::attn_fwd_tc(A.qkv, A.a, A.lse, I.B, m.seq, H, m.causal, st);
+    ops::attn_fwd_tc(A.qkv, A.a, A.lse, Bq, m.seq, H, m.causal, st);
     gemm::gemm(gemm::kBiasResid, false, false, M, h, h, A.a, h, w + o.w_o, h,
                epi(A.x2, h, w + o.b_o, x, h), st);
     ops::layernorm_fwd(A.x2, w + o.ln2_g, w + o.ln2_b, A.h2, A.mean2, A.rstd2, M, h, st);
@@ -901,8 +964,57 @@ void Trainer::end_iteration() {
 void Trainer::issue_iteration() {
   Impl& I = *d_;
   begin_iteration();
-  for (const auto& [w, i] : I.order) run_task(I.sched.per_worker[w][i]);
+  std::set<std::pair<int, int>> fused;  // (worker, index) issued as the second of a pair
+  for (const auto& [w, i] : I.order) {
+    if (fused.count({w, i})) continue;
+    const auto& wl = I.sched.per_worker[w];
+    if (I.fd_fuse && i + 1 < int(wl.size()) && fuse_forward_pair(wl[i], wl[i + 1])) {
+      fused.insert({w, i + 1});
+      continue;
+    }
+    run_task(wl[i]);
+  }
   end_iteration();
+}
+
+// Adjacent forwards of micro-batches (m, m+1) of the same copy in a worker's order (the
+// forward-doubling expansion) run as one forward_pair; same checks and bookkeeping as
+// two run_task calls.  Stream order is unchanged -- the two tasks were consecutive on
+// the worker -- so no new cross-rank waits arise.  Returns false if (t, next) is no pair.
+bool Trainer::fuse_forward_pair(const pipesim::Task& t, const pipesim::Task& next) {
+  Impl& I = *d_;
+  Impl::IterState& S = I.it;
+  if (t.kind != TaskKind::Forward || next.kind != TaskKind::Forward || next.pipeline_id != t.pipeline_id ||
+      next.stage != t.stage || next.worker != t.worker || next.micro_batch != t.micro_batch + 1)
+    return false;
+  for (const pipesim::Task* u : {&t, &next}) {
+    const std::array<int, 4> self{0, u->pipeline_id, u->micro_batch, u->stage};
+    if (S.issued.count(self)) throw pipesim::InvalidConfigError("task issued twice in one iteration");
+    if (u->stage > 0 && !S.issued.count({0, u->pipeline_id, u->micro_batch, u->stage - 1}))
+      throw MissingActivation("no stashed activation for (pipeline " + std::to_string(u->pipeline_id) +
+                              ", micro " + std::to_string(u->micro_batch) + ", stage " +
+                              std::to_string(u->stage) + ")");
+  }
+  S.issued.insert({0, t.pipeline_id, t.micro_batch, t.stage});
+  S.issued.insert({0, next.pipeline_id, next.micro_batch, next.stage});
+  for (int r = 0; r < I.W; ++r) {
+    const int rank = r * I.D + t.worker;
+    if (!I.local(rank)) continue;
+    Impl::TaskSpan sp{rank, int(t.kind), t.pipeline_id, t.micro_batch, t.stage, nullptr, nullptr};
+    if (I.profiling) {
+      sp.a = I.timed_event();
+      CK_CUDA(cudaEventRecord(sp.a, I.stream_of(rank)));
+    }
+    forward_pair(rank, t.pipeline_id, t.micro_batch, t.stage);
+    if (I.profiling) {  // the pair's span goes to its first task, the second gets an empty one
+      sp.b = I.timed_event();
+      CK_CUDA(cudaEventRecord(sp.b, I.stream_of(rank)));
+      I.spans.push_back(sp);
+      Impl::TaskSpan sp2{rank, int(next.kind), next.pipeline_id, next.micro_batch, next.stage, sp.b, sp.b};
+      I.spans.push_back(sp2);
+    }
+  }
+  return true;
 }
 
 float Trainer::finish_step() {

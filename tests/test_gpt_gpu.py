@@ -109,6 +109,28 @@ def test_forward_doubling_with_recompute():
     assert st["graph"]
 
 
+def test_forward_doubling_pair_fusion_matches_unfused(monkeypatch):
+    # adjacent forwards (m, m+1) of a copy run as one 2B-row pass; the result must be the
+    # one of two separate passes (same per-row arithmetic; only the atomic loss sum and
+    # gradient accumulation orders differ)
+    cfg = P.PipelineConfig("chimera", 4, 1, 8, 1, 1, "forward-doubling")
+    shape = PRESETS["tiny"]
+    out = {}
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("CK_FD_FUSE", fuse)
+        tr = Trainer(shape, cfg, lr=0.5)
+        tr.init_params(0)
+        tok, lab = synthetic_batch(shape, cfg.mini_batch(), 7)
+        tr.set_batch(tok, lab)
+        losses = [tr.step() for _ in range(2)]
+        out[fuse] = (losses, [tr.get_params(s).astype(np.float64) for s in range(cfg.D)])
+        tr.close()
+    (l1, p1), (l0, p0) = out["1"], out["0"]
+    assert np.allclose(l1, l0, rtol=1e-5), (l1, l0)
+    for a, b in zip(p1, p0):
+        assert np.max(np.abs(a - b)) <= 1e-5 * max(1.0, np.max(np.abs(b)))
+
+
 def test_recompute_flag_on_direct_schedule():
     cfg = P.PipelineConfig("chimera", 4, 2, 4, 2, 1, "direct", True)
     _check_iteration(PRESETS["tiny"], cfg)
