@@ -12,7 +12,9 @@ dist.init_process_group("gloo")
 world, rank = dist.get_world_size(), dist.get_rank()
 torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) // int(os.environ.get("CK_PROCS_PER_GPU", "1")))
 shape = PRESETS["tiny"]
-cfg = P.PipelineConfig("chimera", 4, 2, 4, 2, 1)
+# MP_CFG=fd: forward doubling + recompute (D=4 W=1 N=8), else Chimera D=4 W=2 N=4 direct
+cfg = (P.PipelineConfig("chimera", 4, 1, 8, 1, 1, "forward-doubling") if os.environ.get("MP_CFG") == "fd"
+       else P.PipelineConfig("chimera", 4, 2, 4, 2, 1))
 per = cfg.W * cfg.D // world
 tr = Trainer(shape, cfg, lr=0.5, first_rank=rank * per, n_ranks=per)
 tr.connect()
@@ -42,6 +44,8 @@ if rank == 0:
         ref.set_batch(tok, lab)
         rl.append(ref.step())
     md = max(float(np.abs(merged[s] - ref.get_params(s)).max()) for s in range(cfg.D))
-    print(json.dumps({"world": world, "losses": losses, "ref_losses": rl, "max_abs_param_diff": md}))
+    print(json.dumps({"world": world, "cfg": os.environ.get("MP_CFG", "direct"), "losses": losses, "ref_losses": rl,
+                      "max_abs_param_diff": md}))
+    assert md < 1e-3 and all(abs(a - b) <= 1e-4 * abs(b) for a, b in zip(losses, rl)), "multi-process != single"
 dist.barrier()
 tr.close()
