@@ -641,11 +641,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       ptx::fence_proxy_async();
       named_bar_sync(2 + g2, 128);
     };
-    auto fetch = [&](const BwdSeq& q, float& nl, float& nd) {  // -lse*log2(e), -D of this row
-      nl = 0.f, nd = 0.f;
+    // lse and D of this thread's row in tile q (raw; 0 past the sequence / the last tile)
+    auto fetch_raw = [&](const BwdSeq& q, float& l, float& d) {
+      l = 0.f, d = 0.f;
       if (!q.valid()) return;
       const int qi = (q.j0 + q.it) * kQ + r;
-      if (qi < seq) nl = -lse[(long long)q.bh * seq + qi] * kLog2e, nd = -Dv[(long long)q.bh * seq + qi];
+      if (qi < seq) l = lse[(long long)q.bh * seq + qi], d = Dv[(long long)q.bh * seq + qi];
+    };
+    auto fetch = [&](const BwdSeq& q, float& nl, float& nd) {  // -lse*log2(e), -D of this row
+      fetch_raw(q, nl, nd);
+      nl = -nl * kLog2e, nd = -nd;
     };
     const float2 sc2 = make_float2(sl2, sl2);
     float nl, nd;
@@ -655,6 +660,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int b = q.bh / H, hd = q.bh % H, row_base = b * seq;
       const int k0 = q.kb * kKV, q0 = (q.j0 + q.it) * kQ, qr = q0 + r, it = q.it;
       const bool last = it + 1 == q.niter;
+      float raw_l, raw_d;  // the next tile's lse / D: requested now, consumed after this tile's math
+      {
+        BwdSeq nq = q;
+        nq.advance();
+        fetch_raw(nq, raw_l, raw_d);
+      }
       ATTN_TRACE(threadIdx.x == 0, g, 3);
       ptx::mbar_wait(s_full, g & 1);
       ATTN_TRACE(threadIdx.x == 0, g, 5);
@@ -698,7 +709,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
       BwdSeq nx = q;
       nx.advance();
-      fetch(nx, nl, nd);
+      nl = -raw_l * kLog2e, nd = -raw_d;  // the next tile's, loaded a tile ago
       if (g > 0) {  // the previous tile's dV / dK / dQ MMAs have read the P / dS tiles
         ptx::mbar_wait(mm_done, (g - 1) & 1);
         ptx::tc_fence_after();
