@@ -466,9 +466,9 @@ __device__ __forceinline__ void aux_row_prefetch(const EpiArgs& ep, int row, int
 }
 
 template <int EPI>
-__device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& ep, const CUtensorMap* to, int row0, int col0,
-                                                   const uint32_t (&r)[32], uint8_t* stg, int lane, int& nbuf,
-                                                   const uint4 (&aux)[4]) {
+__device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& ep, const CUtensorMap* to, const CUtensorMap* to2,
+                                                   int row0, int col0, const uint32_t (&r)[32], uint8_t* stg,
+                                                   int lane, int& nbuf, const uint4 (&aux)[4]) {
   if constexpr (EPI == kAccF32) {
     if (lane == 0) ptx::bulk_wait_read0();  // the previous reduce has read the staging
     __syncwarp();
@@ -506,16 +506,38 @@ __device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& ep, const CUte
       for (int i = 0; i < 16; ++i) q[i] = f2bf(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
     }
     uint8_t* buf = stg + (nbuf & 1) * 2048;
-    if (lane == 0) ptx::bulk_wait_read1();  // the store issued from this buffer two chunks ago
+    // the stores issued from these buffers two chunks ago have read them (one bulk group
+    // per chunk: U alone, or U + G)
+    if (lane == 0) ptx::bulk_wait_read1();
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       *reinterpret_cast<uint4*>(buf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
           make_uint4(q[4 * j], q[4 * j + 1], q[4 * j + 2], q[4 * j + 3]);
+    if constexpr (EPI == kBiasGelu) {  // G = gelu_tanh(U) of the bf16-rounded U
+      const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+      uint32_t gq[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float2 u = bf2f(q[i]);
+        const float2 u2 = ptx::mul2(u, u);
+        const float2 z = ptx::mul2(u, ptx::fma2(u2, make_float2(k0 * k1, k0 * k1), make_float2(k0, k0)));
+        const float2 t = make_float2(tanh_fast(z.x), tanh_fast(z.y));
+        const float2 hu = ptx::mul2(u, make_float2(0.5f, 0.5f));
+        const float2 y = ptx::fma2(hu, t, hu);
+        gq[i] = f2bf(y.x, y.y);
+      }
+      uint8_t* buf2 = buf + 4096;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        *reinterpret_cast<uint4*>(buf2 + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+            make_uint4(gq[4 * j], gq[4 * j + 1], gq[4 * j + 2], gq[4 * j + 3]);
+    }
     ptx::fence_proxy_async();
     __syncwarp();
     if (lane == 0) {
       ptx::tma_store_2d(to, buf, col0, row0);
+      if constexpr (EPI == kBiasGelu) ptx::tma_store_2d(to2, buf + 4096, col0, row0);
       ptx::bulk_commit();
     }
     ++nbuf;
@@ -530,7 +552,7 @@ struct PairCfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = PBN == 256 ? 5 : 7;
   // per-warp epilogue staging, 1 KB aligned for the swizzled TMA-store layouts
-  static constexpr int kStgBytes = 5120;
+  static constexpr int kStgBytes = 8192;  // TMA epilogue: 2 x (U, G) 2 KB bf16 chunk buffers
   static_assert(kStgBytes >= kEpiWarpBytes, "staging");
   static constexpr int kSmem = kStages * kStageBytes + kPairEpiWarps * kStgBytes + 256 + 1024;
   static constexpr int kChunks = PBN / 64;                   // 32-column chunks per epilogue warp
@@ -539,9 +561,10 @@ struct PairCfg {
 template <int PBN, bool A_MN, bool B_MN, int EPI, bool TO>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiWarps, 1)
     k_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-            const __grid_constant__ CUtensorMap to, const EpiArgs ep, int M, int N, int K, int ksplit) {
-  static_assert(!TO || EPI == kStoreBF16 || EPI == kBiasResid || EPI == kAccF32,
-                "TMA-store epilogue: bf16 store (+bias, +residual) / fp32 accumulate");
+            const __grid_constant__ CUtensorMap to, const __grid_constant__ CUtensorMap to2, const EpiArgs ep,
+            int M, int N, int K, int ksplit) {
+  static_assert(!TO || EPI == kStoreBF16 || EPI == kBiasResid || EPI == kBiasGelu || EPI == kAccF32,
+                "TMA-store epilogue: bf16 store (+bias, +residual, +GELU) / fp32 accumulate");
   using C = PairCfg<PBN>;
   extern __shared__ uint8_t smem_raw[];
   GEMM_TRACE(threadIdx.x == 32, 0, 6);
@@ -566,6 +589,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
     ptx::tma_prefetch(&ta);
     ptx::tma_prefetch(&tb);
     if constexpr (TO) ptx::tma_prefetch(&to);
+    if constexpr (TO && EPI == kBiasGelu) ptx::tma_prefetch(&to2);
     for (int s = 0; s < C::kStages; ++s) ptx::mbar_init(&full[s], 1), ptx::mbar_init(&empty[s], 1);
     for (int a = 0; a < 2; ++a) ptx::mbar_init(&tfull[a], 1), ptx::mbar_init(&tempty[a], 2 * kPairEpiWarps);
     ptx::fence_barrier_init();
@@ -682,7 +706,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
           for (int k = 0; k < 4; ++k) auxc[k] = auxn[k];
           if (c + 1 < half * NC + NC) aux_row_prefetch<EPI>(ep, row0 + lane, col0 + 32, M, N, auxn);
           ptx::tmem_ld_wait();
-          if (row0 < M && col0 < N) epilogue_chunk_tma<EPI>(ep, &to, row0, col0, r, stg, lane, nbuf, auxc);
+          if (row0 < M && col0 < N) epilogue_chunk_tma<EPI>(ep, &to, &to2, row0, col0, r, stg, lane, nbuf, auxc);
         } else {
           EpiPre cur = pre;
           if (c + 1 < half * NC + NC) epilogue_prefetch<EPI>(ep, row0, col0 + 32, M, N, lane, (ksplit > 1 || ep.atomic_acc), pre);
@@ -727,23 +751,28 @@ void launch_pair(int M, int N, int K, const __nv_bfloat16* A, long long lda, con
     return e ? atoi(e) : 2;
   }();
   const bool tma_out_on = tma_out_mode >= (EPI == kBiasResid ? 2 : 1);
-  constexpr bool kTmaCapable = EPI == kStoreBF16 || EPI == kBiasResid || EPI == kAccF32;
+  constexpr bool kTmaCapable = EPI == kStoreBF16 || EPI == kBiasResid || EPI == kBiasGelu || EPI == kAccF32;
   constexpr int esz = EPI == kAccF32 ? 4 : 2;
   const bool use_tma = kTmaCapable && tma_out_on && (reinterpret_cast<uintptr_t>(ep.out) % 16) == 0 &&
                        (ep.ldo * esz) % 16 == 0 && (!ep.bias || (reinterpret_cast<uintptr_t>(ep.bias) % 16) == 0) &&
                        (EPI != kBiasResid || ((reinterpret_cast<uintptr_t>(ep.aux) % 16) == 0 && ep.ld_aux % 8 == 0)) &&
+                       (EPI != kBiasGelu || ((reinterpret_cast<uintptr_t>(ep.out2) % 16) == 0 && ep.ld_out2 % 8 == 0)) &&
                        (N % 32) == 0;
   if constexpr (kTmaCapable) {
     if (use_tma) {
       const CUtensorMap to = EPI == kAccF32 ? cuda::make_map_2d_f32(ep.out, N, M, ep.ldo, 32, 32)
                                            : cuda::make_map_2d_bf16(ep.out, N, M, ep.ldo, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+      const CUtensorMap to2 = EPI == kBiasGelu
+                                  ? cuda::make_map_2d_bf16(ep.out2, N, M, ep.ld_out2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)
+                                  : to;
       auto kern = k_gemm2<PBN, A_MN, B_MN, EPI, true>;
       static bool attr = false;
       if (!attr) {
         CK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
         attr = true;
       }
-      cuda::launch(kern, dim3(2 * pairs), dim3(128 + 32 * kPairEpiWarps), C::kSmem, st, ta, tb, to, ep, M, N, K, ks);
+      cuda::launch(kern, dim3(2 * pairs), dim3(128 + 32 * kPairEpiWarps), C::kSmem, st, ta, tb, to, to2, ep, M, N, K,
+                   ks);
       CK_CUDA(cudaGetLastError());
       return;
     }
@@ -754,7 +783,7 @@ void launch_pair(int M, int N, int K, const __nv_bfloat16* A, long long lda, con
     CK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr = true;
   }
-  cuda::launch(kern, dim3(2 * pairs), dim3(128 + 32 * kPairEpiWarps), C::kSmem, st, ta, tb, ta, ep, M, N, K, ks);
+  cuda::launch(kern, dim3(2 * pairs), dim3(128 + 32 * kPairEpiWarps), C::kSmem, st, ta, tb, ta, ta, ep, M, N, K, ks);
   CK_CUDA(cudaGetLastError());
 }
 
