@@ -446,7 +446,7 @@ inline int split_k(int epi, int tiles, int slots, int K) {
 // a 256 x 128 tile (two per pair on the single-wave stage shapes, the first epilogue
 // under the second mainloop) measured 0.6-0.7x of it on every stage shape -- per-SM
 // operand traffic per MMA grows by half and the mainloop becomes operand-bound.
-// TMA-store epilogue (kStoreBF16, kBiasResid, kAccF32) of one 32 x 32 accumulator chunk in the
+// TMA-store epilogue (every bf16 output epilogue, and kAccF32) of one 32 x 32 accumulator chunk in the
 // tcgen05.ld layout (lane = row, 32 consecutive fp32 columns): the warp writes it to its
 // swizzled smem staging and one lane issues a bulk tensor store (bf16, 64-byte swizzle,
 // two alternating 2 KB buffers) or a bulk tensor reduce-add (fp32 += D at L2: the weight-
@@ -457,7 +457,7 @@ inline int split_k(int epi, int tiles, int slots, int K) {
 // columns (four 16-byte loads), fetched one chunk ahead.
 template <int EPI>
 __device__ __forceinline__ void aux_row_prefetch(const EpiArgs& ep, int row, int col0, int M, int N, uint4 (&a)[4]) {
-  if constexpr (EPI == kBiasResid) {
+  if constexpr (EPI == kBiasResid || EPI == kGeluBwd) {
     const bool ok = row < M && col0 < N;  // N % 32 == 0 on this path: whole chunks
     const __nv_bfloat16* p = ep.aux + (long long)row * ep.ld_aux + col0;
 #pragma unroll
@@ -501,6 +501,22 @@ __device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& ep, const CUte
         const float2 a = bf2f((&aux[i >> 2].x)[i & 3]);
         q[i] = f2bf(__uint_as_float(r[2 * i]) + a.x, __uint_as_float(r[2 * i + 1]) + a.y);
       }
+    } else if constexpr (EPI == kGeluBwd) {  // D * gelu_tanh'(U), U = aux
+      const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float2 u = bf2f((&aux[i >> 2].x)[i & 3]);
+        const float2 u2 = ptx::mul2(u, u);
+        const float2 z = ptx::mul2(u, ptx::fma2(u2, make_float2(k0 * k1, k0 * k1), make_float2(k0, k0)));
+        const float2 t = make_float2(tanh_fast(z.x), tanh_fast(z.y));
+        const float2 a = ptx::fma2(t, make_float2(0.5f, 0.5f), make_float2(0.5f, 0.5f));
+        const float2 om = ptx::fma2(make_float2(-t.x, -t.y), t, make_float2(1.f, 1.f));
+        const float2 c = ptx::fma2(u2, make_float2(3.f * k0 * k1, 3.f * k0 * k1), make_float2(k0, k0));
+        const float2 hb = ptx::mul2(ptx::mul2(u, make_float2(0.5f, 0.5f)), om);
+        const float2 v = ptx::mul2(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])),
+                                   ptx::fma2(hb, c, a));
+        q[i] = f2bf(v.x, v.y);
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < 16; ++i) q[i] = f2bf(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
@@ -540,6 +556,16 @@ __device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& ep, const CUte
       if constexpr (EPI == kBiasGelu) ptx::tma_store_2d(to2, buf + 4096, col0, row0);
       ptx::bulk_commit();
     }
+    if constexpr (EPI == kGeluBwd) {
+      if (ep.colsum) {  // the fused bias gradient: lane sums its column of the staged bf16 chunk
+        float cs = 0.f;
+#pragma unroll 8
+        for (int rr = 0; rr < 32; ++rr)
+          cs += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
+              buf + rr * 64 + ((((lane >> 3) ^ ((rr >> 1) & 3))) << 4) + (lane & 7) * 2));
+        atomicAdd(ep.colsum + col0 + lane, cs);  // rows past M: zero-filled A rows and aux -> 0
+      }
+    }
     ++nbuf;
   }
 }
@@ -563,8 +589,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
     k_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
             const __grid_constant__ CUtensorMap to, const __grid_constant__ CUtensorMap to2, const EpiArgs ep,
             int M, int N, int K, int ksplit) {
-  static_assert(!TO || EPI == kStoreBF16 || EPI == kBiasResid || EPI == kBiasGelu || EPI == kAccF32,
-                "TMA-store epilogue: bf16 store (+bias, +residual, +GELU) / fp32 accumulate");
+  static_assert(!TO || EPI != kStoreF32, "TMA-store epilogue: bf16 outputs / fp32 accumulate");
   using C = PairCfg<PBN>;
   extern __shared__ uint8_t smem_raw[];
   GEMM_TRACE(threadIdx.x == 32, 0, 6);
@@ -751,11 +776,12 @@ void launch_pair(int M, int N, int K, const __nv_bfloat16* A, long long lda, con
     return e ? atoi(e) : 2;
   }();
   const bool tma_out_on = tma_out_mode >= (EPI == kBiasResid ? 2 : 1);
-  constexpr bool kTmaCapable = EPI == kStoreBF16 || EPI == kBiasResid || EPI == kBiasGelu || EPI == kAccF32;
+  constexpr bool kTmaCapable = EPI != kStoreF32;
   constexpr int esz = EPI == kAccF32 ? 4 : 2;
   const bool use_tma = kTmaCapable && tma_out_on && (reinterpret_cast<uintptr_t>(ep.out) % 16) == 0 &&
                        (ep.ldo * esz) % 16 == 0 && (!ep.bias || (reinterpret_cast<uintptr_t>(ep.bias) % 16) == 0) &&
-                       (EPI != kBiasResid || ((reinterpret_cast<uintptr_t>(ep.aux) % 16) == 0 && ep.ld_aux % 8 == 0)) &&
+                       ((EPI != kBiasResid && EPI != kGeluBwd) ||
+                        ((reinterpret_cast<uintptr_t>(ep.aux) % 16) == 0 && ep.ld_aux % 8 == 0)) &&
                        (EPI != kBiasGelu || ((reinterpret_cast<uintptr_t>(ep.out2) % 16) == 0 && ep.ld_out2 % 8 == 0)) &&
                        (N % 32) == 0;
   if constexpr (kTmaCapable) {
