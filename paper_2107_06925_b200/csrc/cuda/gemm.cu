@@ -267,185 +267,6 @@ __device__ __forceinline__ void epilogue_chunk(const EpiArgs& ep, int row0, int 
   __syncwarp();
 }
 
-template <int BN>
-struct Cfg {
-  static constexpr int kStages = BN == 256 ? 4 : 6;
-  static constexpr int kABytes = BM * BK * 2;
-  static constexpr int kBBytes = BN * BK * 2;
-  static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kTmemCols = 2 * BN;
-  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256 + 4 * kEpiWarpBytes;
-};
-
-template <int BN, bool A_MN, bool B_MN, int EPI>
-__global__ void __launch_bounds__(256, 1)
-    k_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-           const EpiArgs ep, int M, int N, int K, int ksplit) {
-  using C = Cfg<BN>;
-  extern __shared__ uint8_t smem_raw[];
-  // 1 KB aligned (128-byte swizzle atoms); pointer arithmetic on the __shared__ array keeps
-  // the state space visible, so the epilogue staging compiles to STS/LDS, not generic ST/LD
-  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
-  uint64_t* empty = full + C::kStages;
-  uint64_t* tfull = empty + C::kStages;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
-  const int num_kb = (K + BK - 1) / BK, kb_per = (num_kb + ksplit - 1) / ksplit;
-  const int tiles = num_m * num_n * ksplit;
-
-  if (warp == 0 && lane == 0) {
-    ptx::tma_prefetch(&ta);
-    ptx::tma_prefetch(&tb);
-    for (int s = 0; s < C::kStages; ++s) ptx::mbar_init(&full[s], 1), ptx::mbar_init(&empty[s], 1);
-    for (int a = 0; a < 2; ++a) ptx::mbar_init(&tfull[a], 1), ptx::mbar_init(&tempty[a], 4);
-    ptx::fence_barrier_init();
-  }
-  if (warp == 2) ptx::tmem_alloc(tmem_slot, C::kTmemCols);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  cuda::pdl_wait();     // operands / outputs of the previous kernel in the stream
-  cuda::pdl_trigger();  // persistent grid: successors may be scheduled on free SMs
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        int mb, nb;
-        tile_coords(tile, num_m, num_n, mb, nb);
-        const int ks = tile / (num_m * num_n);
-        const int kb1 = min(num_kb, (ks + 1) * kb_per);
-        for (int kb = ks * kb_per; kb < kb1; ++kb) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * C::kStageBytes;
-          uint8_t* sb = sa + C::kABytes;
-          ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-          if constexpr (!A_MN) {
-            ptx::tma_load_2d(sa, &ta, &full[stage], kb * BK, mb * BM);
-          } else {
-#pragma unroll
-            for (int c = 0; c < BM / 64; ++c)
-              ptx::tma_load_2d(sa + c * (BK * 128), &ta, &full[stage], mb * BM + c * 64, kb * BK);
-          }
-          if constexpr (!B_MN) {
-            ptx::tma_load_2d(sb, &tb, &full[stage], kb * BK, nb * BN);
-          } else {
-#pragma unroll
-            for (int c = 0; c < BN / 64; ++c)
-              ptx::tma_load_2d(sb + c * (BK * 128), &tb, &full[stage], nb * BN + c * 64, kb * BK);
-          }
-          if (++stage == C::kStages) stage = 0, phase ^= 1;
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16(BM, BN, A_MN, B_MN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
-        const int acc = it & 1;
-        ptx::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
-        ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        const int ks = tile / (num_m * num_n);
-        const int kb0 = ks * kb_per, kb1 = min(num_kb, (ks + 1) * kb_per);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          ptx::mbar_wait(&full[stage], phase);
-          ptx::tc_fence_after();
-          const uint32_t sa = ptx::smem_u32(smem + stage * C::kStageBytes);
-          const uint32_t sb = sa + C::kABytes;
-#pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = A_MN ? ptx::smem_desc_sw128(sa + k * 2048, BK * 128, 1024)
-                                     : ptx::smem_desc_sw128(sa + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? ptx::smem_desc_sw128(sb + k * 2048, BK * 128, 1024)
-                                     : ptx::smem_desc_sw128(sb + k * 32, 16, 1024);
-            ptx::umma_f16(d_tmem, ad, bd, idesc, (kb > kb0 || k) ? 1u : 0u);
-          }
-          ptx::umma_commit(&empty[stage]);
-          if (++stage == C::kStages) stage = 0, phase ^= 1;
-        }
-        ptx::umma_commit(&tfull[acc]);
-      }
-    }
-  } else if (warp >= 4) {
-    const int q = warp - 4;  // TMEM lane quarter owned by this warp
-    int it = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
-      const int acc = it & 1;
-      int mb, nb;
-      tile_coords(tile, num_m, num_n, mb, nb);
-      ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
-      ptx::tc_fence_after();
-      const int row0 = mb * BM + q * 32;
-      const uint32_t t0 = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
-      uint8_t* stg = smem + C::kStages * C::kStageBytes + 256 + q * kEpiWarpBytes;
-      EpiPre pre;
-      epilogue_prefetch<EPI>(ep, row0, nb * BN, M, N, lane, (ksplit > 1 || ep.atomic_acc), pre);
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        ptx::tmem_ld32(t0 + c * 32, r);
-        const int col0 = nb * BN + c * 32;
-        EpiPre cur = pre;
-        if (c + 1 < BN / 32) epilogue_prefetch<EPI>(ep, row0, col0 + 32, M, N, lane, (ksplit > 1 || ep.atomic_acc), pre);
-        ptx::tmem_ld_wait();
-        if (row0 < M && col0 < N) epilogue_chunk<EPI>(ep, row0, col0, M, N, r, stg, lane, (ksplit > 1 || ep.atomic_acc), cur);
-      }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-    }
-  }
-  __syncthreads();
-  if (warp == 2) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, C::kTmemCols);
-  }
-}
-
-// Split-K for the fp32-accumulate (weight-gradient) epilogue when the output tiles alone
-// cannot fill the machine: the smallest slice count (each >= 8 K-blocks deep) whose
-// last wave is (nearly) as full as the best achievable; slices combine with fp32 vector
-// atomics.
-inline int split_k(int epi, int tiles, int slots, int K) {
-  static const int force = [] {  // CK_GEMM_KSPLIT=n: fixed slice count (benchmarks)
-    const char* e = std::getenv("CK_GEMM_KSPLIT");
-    return e ? atoi(e) : 0;
-  }();
-  if (epi == kAccF32 && force > 0) return force;
-  if (epi != kAccF32 || tiles >= slots) return 1;
-  const int kb = (K + BK - 1) / BK;
-  // (more than 4 slices: the extra fp32 atomic traffic costs more than the wave it fills)
-  const int kmax = kb / 8 < 1 ? 1 : (kb / 8 > 4 ? 4 : kb / 8);
-  auto eff = [&](int ks) {
-    const long long u = (long long)tiles * ks, waves = (u + slots - 1) / slots;
-    return double(u) / double(waves * slots);
-  };
-  double best = 0.0;
-  for (int ks = 1; ks <= kmax; ++ks) best = eff(ks) > best ? eff(ks) : best;
-  for (int ks = 1; ks <= kmax; ++ks)
-    if (eff(ks) >= best - 0.03) return ks;
-  return 1;
-}
-
-// ---------------------------------------------------------- 2-SM variant ----
-// A CTA pair (cluster of 2 on one TPC) computes a 256 x PBN tile with
-// tcgen05.mma.cta_group::2 (M = 256): each CTA stages its 128 rows of A and PBN/2 of
-// the PBN rows of B per K-block, so per-SM operand traffic per MMA drops versus a
-// single-CTA tile.  The leader (even) CTA issues the MMAs and owns the smem-full and
-// TMEM-empty barriers; commits are multicast to both CTAs.  PBN = 256 is the one used:
-// a 256 x 128 tile (two per pair on the single-wave stage shapes, the first epilogue
-// under the second mainloop) measured 0.6-0.7x of it on every stage shape -- per-SM
-// operand traffic per MMA grows by half and the mainloop becomes operand-bound.
 // TMA-store epilogue (every bf16 output epilogue, and kAccF32) of one 32 x 32 accumulator chunk in the
 // tcgen05.ld layout (lane = row, 32 consecutive fp32 columns): the warp writes it to its
 // swizzled smem staging and one lane issues a bulk tensor store (bf16, 64-byte swizzle,
@@ -570,6 +391,202 @@ __device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& ep, const CUte
   }
 }
 
+template <int BN>
+struct Cfg {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kStgBytes = 8192;  // per epilogue warp, 1 KB aligned (TMA-store layouts)
+  static constexpr int kSmem = kStages * kStageBytes + 4 * kStgBytes + 256 + 1024;
+};
+
+template <int BN, bool A_MN, bool B_MN, int EPI, bool TO>
+__global__ void __launch_bounds__(256, 1)
+    k_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+           const __grid_constant__ CUtensorMap to, const __grid_constant__ CUtensorMap to2, const EpiArgs ep, int M,
+           int N, int K, int ksplit) {
+  static_assert(!TO || EPI != kStoreF32, "TMA-store epilogue: bf16 outputs / fp32 accumulate");
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  // 1 KB aligned (128-byte swizzle atoms); pointer arithmetic on the __shared__ array keeps
+  // the state space visible, so the epilogue staging compiles to STS/LDS, not generic ST/LD
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* stg_base = smem + C::kStages * C::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg_base + 4 * C::kStgBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
+  const int num_kb = (K + BK - 1) / BK, kb_per = (num_kb + ksplit - 1) / ksplit;
+  const int tiles = num_m * num_n * ksplit;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&ta);
+    ptx::tma_prefetch(&tb);
+    for (int s = 0; s < C::kStages; ++s) ptx::mbar_init(&full[s], 1), ptx::mbar_init(&empty[s], 1);
+    for (int a = 0; a < 2; ++a) ptx::mbar_init(&tfull[a], 1), ptx::mbar_init(&tempty[a], 4);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tmem_slot, C::kTmemCols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  cuda::pdl_wait();     // operands / outputs of the previous kernel in the stream
+  cuda::pdl_trigger();  // persistent grid: successors may be scheduled on free SMs
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, mb, nb);
+        const int ks = tile / (num_m * num_n);
+        const int kb1 = min(num_kb, (ks + 1) * kb_per);
+        for (int kb = ks * kb_per; kb < kb1; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::kStageBytes;
+          uint8_t* sb = sa + C::kABytes;
+          ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+          if constexpr (!A_MN) {
+            ptx::tma_load_2d(sa, &ta, &full[stage], kb * BK, mb * BM);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BM / 64; ++c)
+              ptx::tma_load_2d(sa + c * (BK * 128), &ta, &full[stage], mb * BM + c * 64, kb * BK);
+          }
+          if constexpr (!B_MN) {
+            ptx::tma_load_2d(sb, &tb, &full[stage], kb * BK, nb * BN);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c)
+              ptx::tma_load_2d(sb + c * (BK * 128), &tb, &full[stage], nb * BN + c * 64, kb * BK);
+          }
+          if (++stage == C::kStages) stage = 0, phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16(BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        ptx::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        const int ks = tile / (num_m * num_n);
+        const int kb0 = ks * kb_per, kb1 = min(num_kb, (ks + 1) * kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(smem + stage * C::kStageBytes);
+          const uint32_t sb = sa + C::kABytes;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? ptx::smem_desc_sw128(sa + k * 2048, BK * 128, 1024)
+                                     : ptx::smem_desc_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? ptx::smem_desc_sw128(sb + k * 2048, BK * 128, 1024)
+                                     : ptx::smem_desc_sw128(sb + k * 32, 16, 1024);
+            ptx::umma_f16(d_tmem, ad, bd, idesc, (kb > kb0 || k) ? 1u : 0u);
+          }
+          ptx::umma_commit(&empty[stage]);
+          if (++stage == C::kStages) stage = 0, phase ^= 1;
+        }
+        ptx::umma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;  // TMEM lane quarter owned by this warp
+    uint8_t* stg = stg_base + q * C::kStgBytes;
+    int it = 0, nbuf = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      int mb, nb;
+      tile_coords(tile, num_m, num_n, mb, nb);
+      const int row0 = mb * BM + q * 32;
+      EpiPre pre;
+      uint4 auxn[4];
+      if constexpr (!TO) epilogue_prefetch<EPI>(ep, row0, nb * BN, M, N, lane, (ksplit > 1 || ep.atomic_acc), pre);
+      else aux_row_prefetch<EPI>(ep, row0 + lane, nb * BN, M, N, auxn);
+      ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      ptx::tc_fence_after();
+      const uint32_t t0 = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        ptx::tmem_ld32(t0 + c * 32, r);
+        const int col0 = nb * BN + c * 32;
+        if constexpr (TO) {
+          uint4 auxc[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) auxc[k] = auxn[k];
+          if (c + 1 < BN / 32) aux_row_prefetch<EPI>(ep, row0 + lane, col0 + 32, M, N, auxn);
+          ptx::tmem_ld_wait();
+          if (row0 < M && col0 < N) epilogue_chunk_tma<EPI>(ep, &to, &to2, row0, col0, r, stg, lane, nbuf, auxc);
+        } else {
+          EpiPre cur = pre;
+          if (c + 1 < BN / 32) epilogue_prefetch<EPI>(ep, row0, col0 + 32, M, N, lane, (ksplit > 1 || ep.atomic_acc), pre);
+          ptx::tmem_ld_wait();
+          if (row0 < M && col0 < N) epilogue_chunk<EPI>(ep, row0, col0, M, N, r, stg, lane, (ksplit > 1 || ep.atomic_acc), cur);
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+    }
+    if constexpr (TO)
+      if (lane == 0) ptx::bulk_wait0();
+  }
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, C::kTmemCols);
+  }
+}
+
+// Split-K for the fp32-accumulate (weight-gradient) epilogue when the output tiles alone
+// cannot fill the machine: the smallest slice count (each >= 8 K-blocks deep) whose
+// last wave is (nearly) as full as the best achievable; slices combine with fp32 vector
+// atomics.
+inline int split_k(int epi, int tiles, int slots, int K) {
+  static const int force = [] {  // CK_GEMM_KSPLIT=n: fixed slice count (benchmarks)
+    const char* e = std::getenv("CK_GEMM_KSPLIT");
+    return e ? atoi(e) : 0;
+  }();
+  if (epi == kAccF32 && force > 0) return force;
+  if (epi != kAccF32 || tiles >= slots) return 1;
+  const int kb = (K + BK - 1) / BK;
+  // (more than 4 slices: the extra fp32 atomic traffic costs more than the wave it fills)
+  const int kmax = kb / 8 < 1 ? 1 : (kb / 8 > 4 ? 4 : kb / 8);
+  auto eff = [&](int ks) {
+    const long long u = (long long)tiles * ks, waves = (u + slots - 1) / slots;
+    return double(u) / double(waves * slots);
+  };
+  double best = 0.0;
+  for (int ks = 1; ks <= kmax; ++ks) best = eff(ks) > best ? eff(ks) : best;
+  for (int ks = 1; ks <= kmax; ++ks)
+    if (eff(ks) >= best - 0.03) return ks;
+  return 1;
+}
+
+// ---------------------------------------------------------- 2-SM variant ----
+// A CTA pair (cluster of 2 on one TPC) computes a 256 x PBN tile with
+// tcgen05.mma.cta_group::2 (M = 256): each CTA stages its 128 rows of A and PBN/2 of
+// the PBN rows of B per K-block, so per-SM operand traffic per MMA drops versus a
+// single-CTA tile.  The leader (even) CTA issues the MMAs and owns the smem-full and
+// TMEM-empty barriers; commits are multicast to both CTAs.  PBN = 256 is the one used:
+// a 256 x 128 tile (two per pair on the single-wave stage shapes, the first epilogue
+// under the second mainloop) measured 0.6-0.7x of it on every stage shape -- per-SM
+// operand traffic per MMA grows by half and the mainloop becomes operand-bound.
 constexpr int kPairEpiWarps = 8;  // two per TMEM lane quarter, each owning half of the columns
 template <int PBN>
 struct PairCfg {
@@ -756,21 +773,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
   }
 }
 
-template <int PBN, bool A_MN, bool B_MN, int EPI>
-void launch_pair(int M, int N, int K, const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B,
-                 long long ldb, const EpiArgs& ep, cudaStream_t st) {
-  using C = PairCfg<PBN>;
-  const CUtensorMap ta = A_MN ? cuda::make_map_2d_bf16(A, M, K, lda, 64, BK)
-                              : cuda::make_map_2d_bf16(A, K, M, lda, 64, 128);
-  const CUtensorMap tb = B_MN ? cuda::make_map_2d_bf16(B, N, K, ldb, 64, BK)
-                              : cuda::make_map_2d_bf16(B, K, N, ldb, 64, PBN / 2);
-  const int base = ((M + 255) / 256) * ((N + PBN - 1) / PBN);
-  const int ks = split_k(EPI, base, cuda::kNumSMs / 2, K);
-  const int tiles = base * ks;
-  const int pairs = tiles < cuda::kNumSMs / 2 ? tiles : cuda::kNumSMs / 2;
-  // TMA-store epilogue for bf16 stores / fp32 accumulates when the output rows are
-  // 16-byte aligned (CK_GEMM_TMA_OUT=0: the register epilogue everywhere; =1: not for
-  // bias+residual)
+// Whether a launch takes the TMA-store epilogue, and its output tensor maps: every epilogue
+// but kStoreF32, when the output rows (and the aux / out2 operands) are 16-byte aligned and
+// N is whole 32-column chunks (CK_GEMM_TMA_OUT=0: the register epilogue everywhere; =1:
+// not for bias+residual).
+template <int EPI>
+bool tma_out(const EpiArgs& ep, int M, int N, CUtensorMap& to, CUtensorMap& to2) {
   static const int tma_out_mode = [] {  // 0 off, 1 stores + accumulates, 2 also bias+residual
     const char* e = std::getenv("CK_GEMM_TMA_OUT");
     return e ? atoi(e) : 2;
@@ -783,14 +791,29 @@ void launch_pair(int M, int N, int K, const __nv_bfloat16* A, long long lda, con
                        ((EPI != kBiasResid && EPI != kGeluBwd) ||
                         ((reinterpret_cast<uintptr_t>(ep.aux) % 16) == 0 && ep.ld_aux % 8 == 0)) &&
                        (EPI != kBiasGelu || ((reinterpret_cast<uintptr_t>(ep.out2) % 16) == 0 && ep.ld_out2 % 8 == 0)) &&
-                       (N % 32) == 0;
-  if constexpr (kTmaCapable) {
-    if (use_tma) {
-      const CUtensorMap to = EPI == kAccF32 ? cuda::make_map_2d_f32(ep.out, N, M, ep.ldo, 32, 32)
-                                           : cuda::make_map_2d_bf16(ep.out, N, M, ep.ldo, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
-      const CUtensorMap to2 = EPI == kBiasGelu
-                                  ? cuda::make_map_2d_bf16(ep.out2, N, M, ep.ld_out2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)
-                                  : to;
+                       (N % 32) == 0 && M >= 32;
+  if (!use_tma) return false;
+  to = EPI == kAccF32 ? cuda::make_map_2d_f32(ep.out, N, M, ep.ldo, 32, 32)
+                      : cuda::make_map_2d_bf16(ep.out, N, M, ep.ldo, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+  to2 = EPI == kBiasGelu ? cuda::make_map_2d_bf16(ep.out2, N, M, ep.ld_out2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B) : to;
+  return true;
+}
+
+template <int PBN, bool A_MN, bool B_MN, int EPI>
+void launch_pair(int M, int N, int K, const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B,
+                 long long ldb, const EpiArgs& ep, cudaStream_t st) {
+  using C = PairCfg<PBN>;
+  const CUtensorMap ta = A_MN ? cuda::make_map_2d_bf16(A, M, K, lda, 64, BK)
+                              : cuda::make_map_2d_bf16(A, K, M, lda, 64, 128);
+  const CUtensorMap tb = B_MN ? cuda::make_map_2d_bf16(B, N, K, ldb, 64, BK)
+                              : cuda::make_map_2d_bf16(B, K, N, ldb, 64, PBN / 2);
+  const int base = ((M + 255) / 256) * ((N + PBN - 1) / PBN);
+  const int ks = split_k(EPI, base, cuda::kNumSMs / 2, K);
+  const int tiles = base * ks;
+  const int pairs = tiles < cuda::kNumSMs / 2 ? tiles : cuda::kNumSMs / 2;
+  CUtensorMap to, to2;
+  if constexpr (EPI != kStoreF32) {
+    if (tma_out<EPI>(ep, M, N, to, to2)) {
       auto kern = k_gemm2<PBN, A_MN, B_MN, EPI, true>;
       static bool attr = false;
       if (!attr) {
@@ -821,17 +844,31 @@ void launch(int M, int N, int K, const __nv_bfloat16* A, long long lda, const __
                               : cuda::make_map_2d_bf16(A, K, M, lda, 64, BM);
   const CUtensorMap tb = B_MN ? cuda::make_map_2d_bf16(B, N, K, ldb, 64, BK)
                               : cuda::make_map_2d_bf16(B, K, N, ldb, 64, BN);
-  auto kern = k_gemm<BN, A_MN, B_MN, EPI>;
+  const int base = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int ks = split_k(EPI, base, cuda::kNumSMs, K);
+  const int tiles = base * ks;
+  const int grid = tiles < cuda::kNumSMs ? tiles : cuda::kNumSMs;
+  CUtensorMap to, to2;
+  if constexpr (EPI != kStoreF32) {
+    if (tma_out<EPI>(ep, M, N, to, to2)) {
+      auto kern = k_gemm<BN, A_MN, B_MN, EPI, true>;
+      static bool attr = false;
+      if (!attr) {
+        CK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+        attr = true;
+      }
+      cuda::launch(kern, dim3(grid), dim3(256), C::kSmem, st, ta, tb, to, to2, ep, M, N, K, ks);
+      CK_CUDA(cudaGetLastError());
+      return;
+    }
+  }
+  auto kern = k_gemm<BN, A_MN, B_MN, EPI, false>;
   static bool attr = false;  // one-time per instantiation
   if (!attr) {
     CK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr = true;
   }
-  const int base = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const int ks = split_k(EPI, base, cuda::kNumSMs, K);
-  const int tiles = base * ks;
-  const int grid = tiles < cuda::kNumSMs ? tiles : cuda::kNumSMs;
-  cuda::launch(kern, dim3(grid), dim3(256), C::kSmem, st, ta, tb, ep, M, N, K, ks);
+  cuda::launch(kern, dim3(grid), dim3(256), C::kSmem, st, ta, tb, ta, ta, ep, M, N, K, ks);
   CK_CUDA(cudaGetLastError());
 }
 
