@@ -286,10 +286,17 @@ __device__ __forceinline__ void aux_row_prefetch(const EpiArgs& ep, int row, int
   }
 }
 
+// The chunk's 32 bias values as bf16 pairs, pair i in lane i (broadcast by shuffles in
+// the epilogue): one 4-byte load per lane, issued a chunk ahead like the residual rows.
+__device__ __forceinline__ uint32_t bias_prefetch(const EpiArgs& ep, int col0, int N, int lane) {
+  if (!ep.bias || lane >= 16 || col0 >= N) return 0u;
+  return *reinterpret_cast<const uint32_t*>(ep.bias + col0 + 2 * lane);
+}
+
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& ep, const CUtensorMap* to, const CUtensorMap* to2,
                                                    int row0, int col0, const uint32_t (&r)[32], uint8_t* stg,
-                                                   int lane, int& nbuf, const uint4 (&aux)[4]) {
+                                                   int lane, int& nbuf, const uint4 (&aux)[4], uint32_t bias2) {
   if constexpr (EPI == kAccF32) {
     if (lane == 0) ptx::bulk_wait_read0();  // the previous reduce has read the staging
     __syncwarp();
@@ -305,14 +312,10 @@ __device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& ep, const CUte
     }
   } else {
     uint32_t q[16];
-    if (ep.bias) {  // the chunk's 32 bias values (one broadcast line for the warp)
-      uint4 b[4];
-      const __nv_bfloat16* bp = ep.bias + col0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) b[k] = *reinterpret_cast<const uint4*>(bp + 8 * k);
+    if (ep.bias) {  // the chunk's 32 bias values: pair i from lane i
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        float2 bb = bf2f((&b[i >> 2].x)[i & 3]);
+        float2 bb = bf2f(__shfl_sync(0xffffffffu, bias2, i));
         if constexpr (EPI == kBiasResid) bb = ptx::add2(bb, bf2f((&aux[i >> 2].x)[i & 3]));
         q[i] = f2bf(__uint_as_float(r[2 * i]) + bb.x, __uint_as_float(r[2 * i + 1]) + bb.y);
       }
@@ -514,9 +517,14 @@ __global__ void __launch_bounds__(256, 1)
       tile_coords(tile, num_m, num_n, mb, nb);
       const int row0 = mb * BM + q * 32;
       EpiPre pre;
-      uint4 auxn[4];
-      if constexpr (!TO) epilogue_prefetch<EPI>(ep, row0, nb * BN, M, N, lane, (ksplit > 1 || ep.atomic_acc), pre);
-      else aux_row_prefetch<EPI>(ep, row0 + lane, nb * BN, M, N, auxn);
+      uint4 auxn[4], auxn2[4];  // residual / U rows of the next two chunks (TMA epilogue)
+      if constexpr (!TO) {
+        epilogue_prefetch<EPI>(ep, row0, nb * BN, M, N, lane, (ksplit > 1 || ep.atomic_acc), pre);
+      } else {
+        aux_row_prefetch<EPI>(ep, row0 + lane, nb * BN, M, N, auxn);
+        if (BN / 32 > 1) aux_row_prefetch<EPI>(ep, row0 + lane, nb * BN + 32, M, N, auxn2);
+      }
+      uint32_t biasn = TO ? bias_prefetch(ep, nb * BN, N, lane) : 0u;
       ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
       ptx::tc_fence_after();
       const uint32_t t0 = tmem_base + (uint32_t(q * 32) << 16) + acc * BN;
@@ -528,10 +536,13 @@ __global__ void __launch_bounds__(256, 1)
         if constexpr (TO) {
           uint4 auxc[4];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) auxc[k] = auxn[k];
-          if (c + 1 < BN / 32) aux_row_prefetch<EPI>(ep, row0 + lane, col0 + 32, M, N, auxn);
+          for (int k = 0; k < 4; ++k) auxc[k] = auxn[k], auxn[k] = auxn2[k];
+          if (c + 2 < BN / 32) aux_row_prefetch<EPI>(ep, row0 + lane, col0 + 64, M, N, auxn2);
+          const uint32_t biasc = biasn;
+          if (c + 1 < BN / 32) biasn = bias_prefetch(ep, col0 + 32, N, lane);
           ptx::tmem_ld_wait();
-          if (row0 < M && col0 < N) epilogue_chunk_tma<EPI>(ep, &to, &to2, row0, col0, r, stg, lane, nbuf, auxc);
+          if (row0 < M && col0 < N)
+            epilogue_chunk_tma<EPI>(ep, &to, &to2, row0, col0, r, stg, lane, nbuf, auxc, biasc);
         } else {
           EpiPre cur = pre;
           if (c + 1 < BN / 32) epilogue_prefetch<EPI>(ep, row0, col0 + 32, M, N, lane, (ksplit > 1 || ep.atomic_acc), pre);
@@ -725,12 +736,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
       int mb, nb;
       tile_coords(tile, num_m, num_n, mb, nb);
       EpiPre pre;  // this tile's first-chunk operands are fetched while the MMAs run
-      uint4 auxn[4];
-      if constexpr (!TO)
+      uint4 auxn[4], auxn2[4];  // residual / U rows of the next two chunks (TMA epilogue), in
+                                // flight under the mainloop: their HBM latency is what the
+                                // single-wave shapes' exposed epilogue otherwise waits on
+      if constexpr (!TO) {
         epilogue_prefetch<EPI>(ep, mb * 256 + int(cta) * 128 + q * 32, nb * PBN + half * (PBN / 2), M, N, lane,
                                (ksplit > 1 || ep.atomic_acc), pre);
-      else
-        aux_row_prefetch<EPI>(ep, mb * 256 + int(cta) * 128 + q * 32 + lane, nb * PBN + half * (PBN / 2), M, N, auxn);
+      } else {
+        const int rr = mb * 256 + int(cta) * 128 + q * 32 + lane, c0 = nb * PBN + half * (PBN / 2);
+        aux_row_prefetch<EPI>(ep, rr, c0, M, N, auxn);
+        if (NC > 1) aux_row_prefetch<EPI>(ep, rr, c0 + 32, M, N, auxn2);
+      }
+      uint32_t biasn = TO ? bias_prefetch(ep, nb * PBN + half * (PBN / 2), N, lane) : 0u;
       ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
       GEMM_TRACE(warp == 4 && lane == 0, it, 2);
       GEMM_TRACE(warp == 11 && lane == 0, it, 4);
@@ -745,10 +762,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
         if constexpr (TO) {
           uint4 auxc[4];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) auxc[k] = auxn[k];
-          if (c + 1 < half * NC + NC) aux_row_prefetch<EPI>(ep, row0 + lane, col0 + 32, M, N, auxn);
+          for (int k = 0; k < 4; ++k) auxc[k] = auxn[k], auxn[k] = auxn2[k];
+          if (c + 2 < half * NC + NC) aux_row_prefetch<EPI>(ep, row0 + lane, col0 + 64, M, N, auxn2);
+          const uint32_t biasc = biasn;
+          if (c + 1 < half * NC + NC) biasn = bias_prefetch(ep, col0 + 32, N, lane);
           ptx::tmem_ld_wait();
-          if (row0 < M && col0 < N) epilogue_chunk_tma<EPI>(ep, &to, &to2, row0, col0, r, stg, lane, nbuf, auxc);
+          if (row0 < M && col0 < N)
+            epilogue_chunk_tma<EPI>(ep, &to, &to2, row0, col0, r, stg, lane, nbuf, auxc, biasc);
         } else {
           EpiPre cur = pre;
           if (c + 1 < half * NC + NC) epilogue_prefetch<EPI>(ep, row0, col0 + 32, M, N, lane, (ksplit > 1 || ep.atomic_acc), pre);
