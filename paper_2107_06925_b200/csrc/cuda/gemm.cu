@@ -6,9 +6,13 @@
 //               two TMEM accumulators; tcgen05.commit frees smem stages / hands the
 //               finished accumulator to the epilogue
 //   warp 2      TMEM allocator (2*BN fp32 columns)
-//   warps 4..7  epilogue: tcgen05.ld 32x32b -> registers -> fused op -> global
+//   warps 4..7  epilogue: tcgen05.ld 32x32b -> registers -> fused op -> swizzled smem
+//               chunk -> TMA bulk tensor store (bf16) / reduce-add (fp32 accumulate);
+//               a register epilogue with coalesced stores covers the other cases
 // Double-buffered TMEM accumulators let tile i's epilogue overlap tile i+1's
-// mainloop.  Grid = min(#tiles, 148): one resident CTA per SM.
+// mainloop.  Grid = min(#tiles, 148): one resident CTA per SM.  The CTA-pair variant
+// (k_gemm2, 256 x 256 tiles on tcgen05.mma.cta_group::2) carries most stage GEMMs;
+// pick_tile chooses among the two by a calibrated wave model.
 //
 // This single kernel family serves every linear layer of the transformer stage:
 // forward (A=X K-major, B=W K-major), activation gradient dX = dY W (B MN-major) and
