@@ -171,11 +171,11 @@ def gemm_roofline(stream_handle, peak_tflops):
     # DRAM bytes per launch of the same 12 shapes from the committed `ncu --set full`
     # capture (scripts/roofline_shapes.py); below the algorithmic operand+output bytes
     traffic, tsrc = None, None
-    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01m_gemm_roofline_ncu.json")
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01y_gemm_roofline_ncu.json")
     if SHAPE_NAME == "gpt2-medium" and os.path.exists(tpath):
         with open(tpath) as fh:
             traffic = json.load(fh)["avg_dram_bytes_per_launch"]
-        tsrc = "profiles/r01m_gemm_roofline_ncu.json"
+        tsrc = "profiles/r01y_gemm_roofline_ncu.json"
     return {"bound": "tensor", "kernel": "ck gemm_bf16 (tcgen05.mma kind::f16, TMA, TMEM), 12 stage GEMM shapes",
             "achieved": round(achieved, 1), "peak": peak_tflops, "unit": "TFLOP/s",
             "frac": round(achieved / peak_tflops, 4), "traffic": traffic, "traffic_unit": "bytes/launch",
