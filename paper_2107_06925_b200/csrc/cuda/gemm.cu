@@ -603,16 +603,21 @@ inline int split_k(int epi, int tiles, int slots, int K) {
 // under the second mainloop) measured 0.6-0.7x of it on every stage shape -- per-SM
 // operand traffic per MMA grows by half and the mainloop becomes operand-bound.
 constexpr int kPairEpiWarps = 8;  // two per TMEM lane quarter, each owning half of the columns
-template <int PBN>
+// AUX: the bias+residual TMA epilogue stages each warp's 32 x 128 residual block in shared
+// memory with one TMA load issued under the mainloop (4-stage ring to make room).
+template <int PBN, bool AUX = false>
 struct PairCfg {
   static constexpr int kABytes = 128 * BK * 2;               // this CTA's 128 rows of A
   static constexpr int kBBytes = (PBN / 2) * BK * 2;         // this CTA's PBN/2 rows of B
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = PBN == 256 ? 5 : 7;
-  // per-warp epilogue staging, 1 KB aligned for the swizzled TMA-store layouts
-  static constexpr int kStgBytes = 8192;  // TMA epilogue: 2 x (U, G) 2 KB bf16 chunk buffers
+  static constexpr int kStages = AUX ? 4 : PBN == 256 ? 5 : 7;
+  // per-warp epilogue staging, 1 KB aligned for the swizzled TMA-store layouts: 2 x (U, G)
+  // 2 KB bf16 chunk buffers; when AUX, 2 x 2 KB output buffers + the 8 KB residual block
+  static constexpr int kAuxOff = 4096;
+  static constexpr int kStgBytes = AUX ? 4096 + 8192 : 8192;
   static_assert(kStgBytes >= kEpiWarpBytes, "staging");
   static constexpr int kSmem = kStages * kStageBytes + kPairEpiWarps * kStgBytes + 256 + 1024;
+  static_assert(kSmem <= 227 * 1024, "shared memory");
   static constexpr int kChunks = PBN / 64;                   // 32-column chunks per epilogue warp
 };
 
@@ -622,7 +627,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
             const __grid_constant__ CUtensorMap to, const __grid_constant__ CUtensorMap to2, const EpiArgs ep,
             int M, int N, int K, int ksplit) {
   static_assert(!TO || EPI != kStoreF32, "TMA-store epilogue: bf16 outputs / fp32 accumulate");
-  using C = PairCfg<PBN>;
+  constexpr bool AUX = TO && EPI == kBiasResid;  // residual block via TMA (tensor map `to2`)
+  using C = PairCfg<PBN, AUX>;
   extern __shared__ uint8_t smem_raw[];
   GEMM_TRACE(threadIdx.x == 32, 0, 6);
   // 1 KB aligned (128-byte swizzle atoms); pointer arithmetic on the __shared__ array keeps
@@ -633,7 +639,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* auxbar = tempty + 2;  // [kPairEpiWarps] residual block landed (AUX)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(auxbar + kPairEpiWarps);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = ptx::cluster_ctarank();
@@ -649,6 +656,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
     if constexpr (TO && EPI == kBiasGelu) ptx::tma_prefetch(&to2);
     for (int s = 0; s < C::kStages; ++s) ptx::mbar_init(&full[s], 1), ptx::mbar_init(&empty[s], 1);
     for (int a = 0; a < 2; ++a) ptx::mbar_init(&tfull[a], 1), ptx::mbar_init(&tempty[a], 2 * kPairEpiWarps);
+    for (int w = 0; w < kPairEpiWarps; ++w) ptx::mbar_init(&auxbar[w], 1);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc2(tmem_slot, 2 * PBN);
@@ -746,6 +754,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
       if constexpr (!TO) {
         epilogue_prefetch<EPI>(ep, mb * 256 + int(cta) * 128 + q * 32, nb * PBN + half * (PBN / 2), M, N, lane,
                                (ksplit > 1 || ep.atomic_acc), pre);
+      } else if constexpr (AUX) {  // this warp's residual block, one TMA box per chunk
+        ptx::fence_proxy_async();  // the previous tile's reads of the block precede the refill
+        __syncwarp();
+        if (lane == 0) {
+          const int rw = mb * 256 + int(cta) * 128 + q * 32, c0 = nb * PBN + half * (PBN / 2);
+          ptx::mbar_arrive_expect_tx(&auxbar[warp - 4], NC * 2048);
+          for (int c = 0; c < NC; ++c)
+            ptx::tma_load_2d(stg + C::kAuxOff + c * 2048, &to2, &auxbar[warp - 4], c0 + 32 * c, rw);
+        }
       } else {
         const int rr = mb * 256 + int(cta) * 128 + q * 32 + lane, c0 = nb * PBN + half * (PBN / 2);
         aux_row_prefetch<EPI>(ep, rr, c0, M, N, auxn);
@@ -765,9 +782,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
         const int col0 = nb * PBN + c * 32;
         if constexpr (TO) {
           uint4 auxc[4];
+          if constexpr (AUX) {  // this lane's row of the staged residual chunk
+            if (c == half * NC) ptx::mbar_wait(&auxbar[warp - 4], it & 1);
+            const uint8_t* ab = stg + C::kAuxOff + (c - half * NC) * 2048;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) auxc[k] = auxn[k], auxn[k] = auxn2[k];
-          if (c + 2 < half * NC + NC) aux_row_prefetch<EPI>(ep, row0 + lane, col0 + 64, M, N, auxn2);
+            for (int k = 0; k < 4; ++k)
+              auxc[k] = *reinterpret_cast<const uint4*>(ab + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4));
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) auxc[k] = auxn[k], auxn[k] = auxn2[k];
+            if (c + 2 < half * NC + NC) aux_row_prefetch<EPI>(ep, row0 + lane, col0 + 64, M, N, auxn2);
+          }
           const uint32_t biasc = biasn;
           if (c + 1 < half * NC + NC) biasn = bias_prefetch(ep, col0 + 32, N, lane);
           ptx::tmem_ld_wait();
@@ -838,14 +863,17 @@ void launch_pair(int M, int N, int K, const __nv_bfloat16* A, long long lda, con
   CUtensorMap to, to2;
   if constexpr (EPI != kStoreF32) {
     if (tma_out<EPI>(ep, M, N, to, to2)) {
+      using CT = PairCfg<PBN, EPI == kBiasResid>;
+      if constexpr (EPI == kBiasResid)  // the residual, in the output's 32 x 32 swizzled chunk layout
+        to2 = cuda::make_map_2d_bf16(ep.aux, N, M, ep.ld_aux, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
       auto kern = k_gemm2<PBN, A_MN, B_MN, EPI, true>;
       static bool attr = false;
       if (!attr) {
-        CK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+        CK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CT::kSmem));
         attr = true;
       }
-      cuda::launch(kern, dim3(2 * pairs), dim3(128 + 32 * kPairEpiWarps), C::kSmem, st, ta, tb, to, to2, ep, M, N, K,
-                   ks);
+      cuda::launch(kern, dim3(2 * pairs), dim3(128 + 32 * kPairEpiWarps), CT::kSmem, st, ta, tb, to, to2, ep, M, N,
+                   K, ks);
       CK_CUDA(cudaGetLastError());
       return;
     }
