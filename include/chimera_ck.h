@@ -142,6 +142,11 @@ CK_API long long ck_attn_bwd_scratch_floats(int B, int seq, int H);
 /* tcgen05/TMEM flash attention backward (same contract / scratch as ck_attn_bwd). */
 CK_API int ck_attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float* lse,
                           void* dqkv, float* scratch, int B, int seq, int H, int causal, void* stream);
+/* ck_attn_bwd_tc that also accumulates dbias[3 H 64] += column sums of the bf16 dqkv it
+   writes: the QKV bias gradient, summed in the dQ conversion and the dK / dV epilogue. */
+CK_API int ck_attn_bwd_tc_dbias(const void* qkv, const void* out, const void* dout, const float* lse,
+                                void* dqkv, float* scratch, float* dbias, int B, int seq, int H, int causal,
+                                void* stream);
 
 /* ------------------------------------------------------- GPT-2 stage executor */
 /* Transformer shape (head dim 64; vocab padded to a multiple of 8, e.g. 50304). */

@@ -372,18 +372,30 @@ __global__ void __launch_bounds__(128) k_attn_bwd(const bf16* __restrict__ qkv, 
 
 // dqkv[:, q-part] = bf16(dq_acc * scale)
 // dQ (fp32 accumulator, scaled by 1/sqrt(d)) -> bf16 Q-part of dqkv (L2-resident stream)
-__global__ void __launch_bounds__(256) k_dq_out(const float* __restrict__ acc, bf16* __restrict__ dqkv, int n_rows,
-                                                int H) {
+// dQ (fp32 accumulator, scaled by 1/sqrt(d) here) -> the Q columns of dqkv in bf16; with
+// dbias, also the Q part of the QKV bias gradient: column sums of the bf16 values written.
+// threadIdx.x <-> 8-column group (blockDim.x = w / 8), threadIdx.y <-> one of 4 rows in
+// flight; CTAs stride over row quads.
+__global__ void __launch_bounds__(1024) k_dq_out(const float* __restrict__ acc, bf16* __restrict__ dqkv, int n_rows,
+                                                 int H, float* __restrict__ dbias) {
   cuda::pdl_wait();
-  const int w = H * kHd;  // multiple of 64
-  const int n8 = n_rows * w / 8;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
-    const float4* p = reinterpret_cast<const float4*>(acc) + 2 * i;
+  const int w = H * kHd, g = threadIdx.x;  // w is a multiple of 64
+  float cs[8] = {};
+  for (int r = blockIdx.x * 4 + threadIdx.y; r < n_rows; r += gridDim.x * 4) {
+    const float4* p = reinterpret_cast<const float4*>(acc + (long long)r * w) + 2 * g;
     const float4 a = __ldcs(p), b = __ldcs(p + 1);
-    const int e = i * 8, r = e / w, c = e - r * w;
-    *reinterpret_cast<uint4*>(dqkv + (long long)r * 3 * w + c) =
-        make_uint4(pack(a.x * 0.125f, a.y * 0.125f), pack(a.z * 0.125f, a.w * 0.125f), pack(b.x * 0.125f, b.y * 0.125f),
-                   pack(b.z * 0.125f, b.w * 0.125f));
+    const uint4 q = make_uint4(pack(a.x * 0.125f, a.y * 0.125f), pack(a.z * 0.125f, a.w * 0.125f),
+                               pack(b.x * 0.125f, b.y * 0.125f), pack(b.z * 0.125f, b.w * 0.125f));
+    *reinterpret_cast<uint4*>(dqkv + (long long)r * 3 * w + 8 * g) = q;
+    if (dbias) {
+      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) cs[t] += __bfloat162float(h[t]);
+    }
+  }
+  if (dbias) {
+    atomicAdd(reinterpret_cast<float4*>(dbias + 8 * g), make_float4(cs[0], cs[1], cs[2], cs[3]));
+    atomicAdd(reinterpret_cast<float4*>(dbias + 8 * g + 4), make_float4(cs[4], cs[5], cs[6], cs[7]));
   }
 }
 
@@ -407,9 +419,10 @@ void attn_bwd_dot(const bf16* out, const bf16* dout, float* D, int M, int seq, i
   CK_CUDA(cudaGetLastError());
 }
 
-void attn_dq_out(const float* dq, bf16* dqkv, int M, int H, cudaStream_t st) {
-  const long long n = (long long)M * H * kHd;
-  cuda::launch(k_dq_out, dim3(std::min<long long>((n / 8 + 255) / 256, 148LL * 8)), dim3(256), 0, st, dq, dqkv, M, H);
+void attn_dq_out(const float* dq, bf16* dqkv, int M, int H, cudaStream_t st, float* dbias) {
+  const int ng = H * kHd / 8;  // 8-column groups per row
+  if (ng * 4 > 1024) throw chimera::capi::InternalError("attention: H * 64 > 2048");
+  cuda::launch(k_dq_out, dim3(std::min((M + 3) / 4, 148 * 4)), dim3(ng, 4), 0, st, dq, dqkv, M, H, dbias);
   CK_CUDA(cudaGetLastError());
 }
 
@@ -422,7 +435,7 @@ void attn_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* l
   const dim3 grid((seq + kTile - 1) / kTile, B * H);
   if (causal) k_attn_bwd<true><<<grid, 128, 0, st>>>(qkv, dout, lse, D, dq, dqkv, seq, H);
   else k_attn_bwd<false><<<grid, 128, 0, st>>>(qkv, dout, lse, D, dq, dqkv, seq, H);
-  attn_dq_out(dq, dqkv, M, H, st);
+  attn_dq_out(dq, dqkv, M, H, st, nullptr);
   CK_CUDA(cudaGetLastError());
 }
 

@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     k_attn_bwd_tc(const __grid_constant__ CUtensorMap tqkv, const __grid_constant__ CUtensorMap tdo,
                   const __grid_constant__ CUtensorMap tdq, const __grid_constant__ CUtensorMap tdqkv,
                   const float* __restrict__ lse, const float* __restrict__ Dv, bf16* __restrict__ dqkv, int seq, int H,
-                  int BH) {
+                  int BH, float* __restrict__ dbias) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((ptx::smem_u32(smem) & 1023) != 0) __trap();
   ATTN_CTA(0);
@@ -752,19 +752,29 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
           w[c] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
         }
-        if (k0 + kKV <= seq) {  // whole tile inside the sequence: swizzled stage (P tile) + TMA store
+        // staged in the swizzled P tile: the TMA store's source and the bias-gradient sums'
 #pragma unroll
-          for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(sp + r * 128 + ((c ^ (r & 7)) << 4)) = w[c];
-          stage_release();
+        for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(sp + r * 128 + ((c ^ (r & 7)) << 4)) = w[c];
+        stage_release();
+        epi_pending = true;
+        if (k0 + kKV <= seq) {  // whole tile inside the sequence: TMA store
           if (ct == 0) {
             ptx::tma_store_2d(&tdqkv, sp, (1 + g2) * H * kD + hd * kD, row_base + k0);
             ptx::bulk_commit();
           }
-          epi_pending = true;
         } else if (k0 + r < seq) {  // sequence tail: rows past seq belong to the next sequence
           bf16* dst = dqkv + ((long long)row_base + k0 + r) * (3LL * H * kD) + (1 + g2) * (long long)H * kD + hd * kD;
 #pragma unroll
           for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(dst + c * 8) = w[c];
+        }
+        if (dbias) {  // K / V part of the QKV bias gradient: this item's 128 key rows per column
+          const int col = ct & 63, r0 = (ct >> 6) * 64;  // keys past seq hold zeros
+          float cs = 0.f;
+#pragma unroll 8
+          for (int rr = r0; rr < r0 + 64; ++rr)
+            cs += __bfloat162float(*reinterpret_cast<const bf16*>(sp + rr * 128 + (((col >> 3) ^ (rr & 7)) << 4) +
+                                                                 (col & 7) * 2));
+          atomicAdd(dbias + (1 + g2) * H * kD + hd * kD + col, cs);
         }
       }
       q = nx;
@@ -800,7 +810,7 @@ void attn_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int seq, int H, 
 
 // dqkv from dout on the tensor cores; `scratch` as attn_bwd (row dots D, fp32 dQ).
 void attn_bwd_tc(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, bf16* dqkv, float* scratch,
-                 int B, int seq, int H, bool causal, cudaStream_t st) {
+                 int B, int seq, int H, bool causal, cudaStream_t st, float* dbias) {
   float* D = scratch;
   float* dq = scratch + size_t(B) * H * seq;
   const int M = B * seq;
@@ -819,9 +829,9 @@ void attn_bwd_tc(const bf16* qkv, const bf16* out, const bf16* dout, const float
   const int items = (seq + kKV - 1) / kKV * B * H;
   const dim3 grid(std::min(items, cuda::kNumSMs));  // persistent: one CTA per SM
   cuda::launch(causal ? k_attn_bwd_tc<true> : k_attn_bwd_tc<false>, grid, dim3(kBwdThreads), kBwdSmem, st, mq, mo, mdq,
-               mdqkv, lse, D, dqkv, seq, H, B * H);
+               mdqkv, lse, D, dqkv, seq, H, B * H, dbias);
   CK_CUDA(cudaGetLastError());
-  attn_dq_out(dq, dqkv, M, H, st);
+  attn_dq_out(dq, dqkv, M, H, st, dbias);
 }
 
 }  // namespace chimera::ops
@@ -831,7 +841,17 @@ extern "C" CK_API int ck_attn_bwd_tc(const void* qkv, const void* out, const voi
   using chimera::ops::bf16;
   return chimera::capi::guarded([&] {
     chimera::ops::attn_bwd_tc((const bf16*)qkv, (const bf16*)out, (const bf16*)dout, lse, (bf16*)dqkv, scratch, B, seq,
-                              H, causal != 0, (cudaStream_t)st);
+                              H, causal != 0, (cudaStream_t)st, nullptr);
+  });
+}
+
+extern "C" CK_API int ck_attn_bwd_tc_dbias(const void* qkv, const void* out, const void* dout, const float* lse,
+                                           void* dqkv, float* scratch, float* dbias, int B, int seq, int H, int causal,
+                                           void* st) {
+  using chimera::ops::bf16;
+  return chimera::capi::guarded([&] {
+    chimera::ops::attn_bwd_tc((const bf16*)qkv, (const bf16*)out, (const bf16*)dout, lse, (bf16*)dqkv, scratch, B, seq,
+                              H, causal != 0, (cudaStream_t)st, dbias);
   });
 }
 

@@ -704,8 +704,9 @@ void Trainer::backward_task(int rank, int p, int mb, int s) {
     // MLP
     // Bias gradients ride on the kernels producing the gradient they sum: FC1's in the
     // GELU' epilogue, O-proj's in LN2-backward, FC2's in the LN1-backward of the layer
-    // above (or the final LN's); only the stage's top layer input gradient, arriving as
-    // a message, and the attention's dqkv keep a separate column-sum pass.
+    // above (or the final LN's), QKV's in the attention backward (dQ conversion, dK / dV
+    // epilogue); only the stage's top layer input gradient, arriving as a message, keeps
+    // a separate column-sum pass.
     fork();
     if (l == L.n_layers - 1 && !L.has_head) {
       ops::bias_grad(dxo, gw + o.b_fc2, M, h, ws);
@@ -726,16 +727,15 @@ void Trainer::backward_task(int rank, int p, int mb, int s) {
     fork();
     gemm::gemm(gemm::kAccF32, true, true, h, h, M, dx2, h, A.a, h, epi(gw + o.w_o, h), ws);
     gemm::gemm(gemm::kStoreBF16, false, true, M, h, h, dx2, h, w + o.w_o, h, epi(sc.da, h), st);
-    ops::attn_bwd_tc(A.qkv, A.a, sc.da, A.lse, dqkv, sc.attn, I.B, m.seq, H, m.causal, st);
+    ops::attn_bwd_tc(A.qkv, A.a, sc.da, A.lse, dqkv, sc.attn, I.B, m.seq, H, m.causal, st, gw + o.b_qkv);
     fork();
-    ops::bias_grad(dqkv, gw + o.b_qkv, M, 3 * h, ws);
     gemm::gemm(gemm::kAccF32, true, true, 3 * h, h, M, dqkv, 3 * h, A.h1, h, epi(gw + o.w_qkv, h), ws);
     side_done(l);
     gemm::gemm(gemm::kStoreBF16, false, true, M, h, 3 * h, dqkv, 3 * h, w + o.w_qkv, h, epi(sc.dh, h), st);
     ops::layernorm_bwd(sc.dh, xin, A.mean1, A.rstd1, w + o.ln1_g, dx2, dxin, gw + o.ln1_g, gw + o.ln1_b,
                        l > 0 ? gw + L.layers[l - 1].b_fc2 : nullptr, M, h, st);
     dxo = dxin;
-    I.launches_per_step += 15;  // attn_bwd = 3 kernels (+ a memset node)
+    I.launches_per_step += 14;  // attn_bwd = 3 kernels (+ a memset node)
   }
   if (s == 0) {
     ops::embed_bwd(I.tokens + tok0, dxo, gw + L.wte, gw + L.wpe, M, m.seq, h, st);

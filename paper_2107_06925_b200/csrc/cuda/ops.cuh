@@ -51,13 +51,14 @@ void attn_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int seq, int H, 
 void attn_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, bf16* dqkv,
               float* scratch, int B, int seq, int H, bool causal, cudaStream_t st);
 size_t attn_bwd_scratch_floats(int B, int seq, int H);
+// dbias (nullable, fp32 [3 H 64]) += column sums of the bf16 dqkv written (the QKV bias gradient)
 void attn_bwd_tc(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, bf16* dqkv,
-                 float* scratch, int B, int seq, int H, bool causal, cudaStream_t st);
+                 float* scratch, int B, int seq, int H, bool causal, cudaStream_t st, float* dbias = nullptr);
 // pieces shared by both backward implementations
 // D = rowsum(dO * O) per (token, head); zeroes the fp32 dQ accumulator `dq_zero` if given
 void attn_bwd_dot(const bf16* out, const bf16* dout, float* D, int M, int seq, int H, cudaStream_t st,
                   float* dq_zero = nullptr);
 // dq (scaled by 1/8) -> Q columns of dqkv
-void attn_dq_out(const float* dq, bf16* dqkv, int M, int H, cudaStream_t st);
+void attn_dq_out(const float* dq, bf16* dqkv, int M, int H, cudaStream_t st, float* dbias = nullptr);
 
 }  // namespace chimera::ops

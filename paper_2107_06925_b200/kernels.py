@@ -58,6 +58,7 @@ _lib.register("ck_attn_fwd_tc", _i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp])
 _lib.register("ck_attn_bwd", _i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp])
 _lib.register("ck_attn_bwd_scratch_floats", _ll, [_i, _i, _i])
 _lib.register("ck_attn_bwd_tc", _i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp])
+_lib.register("ck_attn_bwd_tc_dbias", _i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp])
 
 
 def layernorm_fwd(x, g, b, y, mean, rstd, stream=None):
@@ -102,10 +103,15 @@ def attn_fwd_tc(qkv, out, lse, B, seq, H, causal=True, stream=None):
     check(lib().ck_attn_fwd_tc(_p(qkv), _p(out), _p(lse), B, seq, H, int(causal), _stream(stream)))
 
 
-def attn_bwd(qkv, out, dout, lse, dqkv, B, seq, H, causal=True, stream=None, impl="mma_sync"):
+def attn_bwd(qkv, out, dout, lse, dqkv, B, seq, H, causal=True, stream=None, impl="mma_sync", dbias=None):
+    """dbias (fp32 [3 H 64], tcgen05 only) accumulates the column sums of dqkv (QKV bias grad)."""
     import torch
     n = lib().ck_attn_bwd_scratch_floats(B, seq, H)
     scratch = torch.empty(n, device=qkv.device, dtype=torch.float32)
+    if dbias is not None:
+        check(lib().ck_attn_bwd_tc_dbias(_p(qkv), _p(out), _p(dout), _p(lse), _p(dqkv), _p(scratch), _p(dbias), B,
+                                         seq, H, int(causal), _stream(stream)))
+        return
     fn = lib().ck_attn_bwd if impl == "mma_sync" else lib().ck_attn_bwd_tc
     check(fn(_p(qkv), _p(out), _p(dout), _p(lse), _p(dqkv), _p(scratch), B, seq, H,
                             int(causal), _stream(stream)))

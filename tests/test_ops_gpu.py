@@ -121,3 +121,9 @@ def test_attention(B, seq, H, causal, impl):
     assert rel(got[0], dq) < 2e-2
     assert rel(got[1], dk) < 2e-2
     assert rel(got[2], dv) < 2e-2
+    if impl == "tcgen05":  # fused QKV bias gradient: column sums of the dqkv written
+        db = torch.full((3 * H * d,), 0.5, device="cuda")
+        dqkv2 = torch.empty_like(qkv)
+        ck.attn_bwd(qkv, out, dout, lse, dqkv2, B, seq, H, causal, impl=impl, dbias=db)
+        assert rel(dqkv2, dqkv) < 1e-3  # dQ is reduce-added in L2: order-dependent fp32 sums
+        assert rel(db, dqkv2.float().sum(0) + 0.5) < 1e-5
