@@ -393,9 +393,17 @@ __global__ void __launch_bounds__(1024) k_dq_out(const float* __restrict__ acc, 
       for (int t = 0; t < 8; ++t) cs[t] += __bfloat162float(h[t]);
     }
   }
-  if (dbias) {
-    atomicAdd(reinterpret_cast<float4*>(dbias + 8 * g), make_float4(cs[0], cs[1], cs[2], cs[3]));
-    atomicAdd(reinterpret_cast<float4*>(dbias + 8 * g + 4), make_float4(cs[4], cs[5], cs[6], cs[7]));
+  if (dbias) {  // reduce the 4 row lanes in shared memory: one atomic set per CTA and column group
+    __shared__ float red[4][2048];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) red[threadIdx.y][8 * g + t] = cs[t];
+    __syncthreads();
+    if (threadIdx.y == 0) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) cs[t] = red[0][8 * g + t] + red[1][8 * g + t] + red[2][8 * g + t] + red[3][8 * g + t];
+      atomicAdd(reinterpret_cast<float4*>(dbias + 8 * g), make_float4(cs[0], cs[1], cs[2], cs[3]));
+      atomicAdd(reinterpret_cast<float4*>(dbias + 8 * g + 4), make_float4(cs[4], cs[5], cs[6], cs[7]));
+    }
   }
 }
 
@@ -422,7 +430,8 @@ void attn_bwd_dot(const bf16* out, const bf16* dout, float* D, int M, int seq, i
 void attn_dq_out(const float* dq, bf16* dqkv, int M, int H, cudaStream_t st, float* dbias) {
   const int ng = H * kHd / 8;  // 8-column groups per row
   if (ng * 4 > 1024) throw chimera::capi::InternalError("attention: H * 64 > 2048");
-  cuda::launch(k_dq_out, dim3(std::min((M + 3) / 4, 148 * 4)), dim3(ng, 4), 0, st, dq, dqkv, M, H, dbias);
+  // one CTA per SM: the bias-gradient atomics are one set per CTA (contended addresses)
+  cuda::launch(k_dq_out, dim3(std::min((M + 3) / 4, cuda::kNumSMs)), dim3(ng, 4), 0, st, dq, dqkv, M, H, dbias);
   CK_CUDA(cudaGetLastError());
 }
 
