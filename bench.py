@@ -114,21 +114,25 @@ def cpu_port_sample(shape, seconds_hint=20.0):
     P = O.unpack(params, stage.layout)
     rng = np.random.default_rng(0)
     x = rng.standard_normal((m.seq, m.hidden))
-    t0 = time.perf_counter()
-    n = 0
-    while True:
-        y, _, cache = stage.forward(P, x, None, 1, 1.0)
-        G = {k: np.zeros_like(v) for k, v in P.items()}
-        stage.backward(P, G, cache, np.ones_like(y) * 1e-3, 1)
-        n += 1
-        if time.perf_counter() - t0 > seconds_hint or n >= 50:
-            break
-    dt = (time.perf_counter() - t0) / n
+    # torchrun exports OMP_NUM_THREADS=1; the baseline uses every host core regardless
+    from threadpoolctl import threadpool_info, threadpool_limits
+    with threadpool_limits(limits=os.cpu_count()):
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+        t0 = time.perf_counter()
+        n = 0
+        while True:
+            y, _, cache = stage.forward(P, x, None, 1, 1.0)
+            G = {k: np.zeros_like(v) for k, v in P.items()}
+            stage.backward(P, G, cache, np.ones_like(y) * 1e-3, 1)
+            n += 1
+            if time.perf_counter() - t0 > seconds_hint or n >= 50:
+                break
+        dt = (time.perf_counter() - t0) / n
     s, h = m.seq, m.hidden
     stage_flops = 3 * stage.per * (24 * s * h * h + 4 * s * s * h)  # fwd+bwd, no head
     rate = stage_flops / dt
     seqs_per_s = rate / shape.flops_per_seq()
-    return {"value": seqs_per_s, "unit": "seqs/s", "cores": os.cpu_count(), "kind": "port",
+    return {"value": seqs_per_s, "unit": "seqs/s", "cores": cores, "kind": "port",
             "sample": f"numpy fp64 oracle, 1 sequence x 1 stage ({stage.per} layers) fwd+bwd x{n} "
                       f"({dt:.2f} s each, {rate / 1e9:.1f} GFLOP/s), scaled by FLOPs to the full model"}
 
@@ -277,7 +281,7 @@ def run_reference(args, shape):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "model": SHAPE_NAME, "global_batch": CFG["B"] * CFG["N"] * CFG["W"],
                        "seq_len": shape.seq},
-            "cpu_baseline": {"value": v, "unit": "seqs/s", "cores": os.cpu_count(), "kind": "port",
+            "cpu_baseline": {"value": v, "unit": "seqs/s", "cores": s["cores"], "kind": "port",
                              "sample": s["sample"]},
             "e2e": {"value": v, "unit": "seqs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
