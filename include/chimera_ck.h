@@ -71,6 +71,14 @@ CK_API int pipesim_replicas_per_stage(const char* config_json);
 CK_API int pipesim_critical_path(const char* schedule_json, const char* profile_json, int* C_f,
                           int* C_b);
 CK_API int pipesim_predict_T(const char* config_json, const char* profile_json, double* T);
+/* analysis::validate_dependencies / bubble_ratio_per_worker / steady_state_idle /
+ * memory_profile (proj/include/pipesim/analysis.hpp:41-60) and perfmodel::free_regions /
+ * critical_path (proj/include/pipesim/perfmodel.hpp:63-70) in one JSON document
+ * {"violations", "bubble", "steady_state_idle", "memory", "free_regions", "critical_path"}. */
+CK_API int pipesim_analysis_report(const char* schedule_json, const char* profile_json, char** out_json);
+/* perfmodel::plan (proj/include/pipesim/perfmodel.hpp:78-83): JSON list of
+ * {"W","D","B","N","scaling","recompute","T_predicted"}, fastest first. */
+CK_API int pipesim_plan(int P, long long B_hat, const char* profile_json, const char* scheme, char** out_json);
 /* Issue order used by the executors: (worker, index) sorted by unit-tick start,
  * the reference oracle's replay order (proj/src/oracle.cpp:312-327). */
 CK_API int pipesim_replay_order(const char* schedule_json, int* worker, int* index, int cap);

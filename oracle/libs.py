@@ -72,6 +72,8 @@ class RefLib:
         L.ref_simulate_timeline.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_double, C.POINTER(C.c_void_p)]
         L.ref_critical_path.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.ref_predict_T.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_double)]
+        L.ref_analysis_report.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]
+        L.ref_plan.argtypes = [C.c_int, C.c_longlong, C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]
         L.ref_toy_make_model.argtypes = [_ip, C.c_int, C.c_uint64, _dp]
         L.ref_toy_make_batch.argtypes = [_ip, C.c_int, C.c_int, C.c_uint64, _dp, _dp]
         L.ref_toy_run_iteration.argtypes = [C.c_char_p, _ip, C.c_int, _dp, _dp, _dp, C.c_int,
@@ -147,6 +149,12 @@ class RefLib:
         t = C.c_double()
         self._chk(self.L.ref_predict_T(cfg_json.encode(), prof_json.encode(), C.byref(t)))
         return t.value
+
+    def analysis_report(self, sched_json: str, prof_json: str) -> dict:
+        return json.loads(self._str(self.L.ref_analysis_report, sched_json.encode(), prof_json.encode()))
+
+    def plan(self, P: int, B_hat: int, prof_json: str, scheme: str = "chimera") -> list:
+        return json.loads(self._str(self.L.ref_plan, int(P), int(B_hat), prof_json.encode(), scheme.encode()))
 
     # ToyModel oracle (proj/src/oracle.cpp)
     def make_model(self, dims, seed):

@@ -320,3 +320,71 @@ int ref_simulate_timeline(const char* sched, const char* prof, int policy, doubl
 }
 
 }  // extern "C"
+
+namespace {
+
+nlohmann::ordered_json task_j(const Task& t) {
+  return nlohmann::ordered_json::array({to_string(t.kind), t.pipeline_id, t.micro_batch, t.stage, t.worker});
+}
+
+}  // namespace
+
+extern "C" {
+
+// One JSON document of every schedule metric: analysis::validate_dependencies,
+// bubble_ratio_per_worker and steady_state_idle (proj/src/analysis.cpp:40-152),
+// memory_profile (:155-214), perfmodel::free_regions and critical_path
+// (proj/src/perfmodel.cpp:54-155), all on the schedule timed by dessim::simulate
+// with zero communication (as pipesim_bubble_ratio_per_worker does).
+int ref_analysis_report(const char* sched, const char* prof, char** out) {
+  return guard([&] {
+    using oj = nlohmann::ordered_json;
+    const Schedule s = schedule_from_json(sched);
+    const CostProfile p = profile_from_json(prof);
+    oj j;
+    j["violations"] = analysis::validate_dependencies(s);
+    if (!j["violations"].empty()) {
+      *out = dup(j.dump());
+      return;
+    }
+    dessim::SimOptions o;
+    o.zero_comm = true;
+    const auto sim = dessim::simulate(s, p, o);
+    oj b = oj::array();
+    for (const auto& r : analysis::bubble_ratio_per_worker(sim.timed, p)) b.push_back({r.num, r.den});
+    j["bubble"] = b;
+    j["steady_state_idle"] = analysis::steady_state_idle(s, p);
+    const auto mp = analysis::memory_profile(s, p);
+    j["memory"] = {{"weight_counts", mp.weight_counts}, {"act_counts", mp.act_counts},
+                   {"weight_bytes", mp.weight_bytes}, {"act_bytes", mp.act_bytes},
+                   {"peak_worker", mp.peak_worker}, {"peak_bytes", mp.peak_bytes}};
+    oj fr = oj::array();
+    for (const auto& w : perfmodel::free_regions(sim.timed, p).per_worker) {
+      oj x = oj::array();
+      for (const auto& st : w) x.push_back({st.stage, st.slack});
+      fr.push_back(x);
+    }
+    j["free_regions"] = fr;
+    const auto cp = perfmodel::critical_path(s, p);
+    oj path = oj::array();
+    for (const auto& t : cp.path) path.push_back(task_j(t));
+    j["critical_path"] = {{"C_f", cp.C_f}, {"C_b", cp.C_b}, {"path", path}};
+    *out = dup(j.dump());
+  });
+}
+
+// perfmodel::plan (proj/src/perfmodel.cpp:225-298) as a JSON list of entries.
+int ref_plan(int P, long long B_hat, const char* prof, const char* scheme, char** out) {
+  return guard([&] {
+    using oj = nlohmann::ordered_json;
+    const auto sc = scheme_from_string(scheme);
+    if (!sc) throw InvalidConfigError("unknown scheme");
+    oj a = oj::array();
+    for (const auto& e : perfmodel::plan(P, B_hat, profile_from_json(prof), *sc))
+      a.push_back({{"W", e.W}, {"D", e.D}, {"B", e.B}, {"N", e.N}, {"scaling", to_string(e.scaling)},
+                   {"recompute", e.recompute}, {"T_predicted", e.T_predicted}});
+    *out = dup(a.dump());
+  });
+}
+
+}  // extern "C"

@@ -41,6 +41,8 @@ SIGNATURES = {
                                         C.POINTER(C.c_int)]),
     "pipesim_predict_T": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(C.c_double)]),
     "pipesim_replay_order": (C.c_int, [C.c_char_p, _ip, _ip, C.c_int]),
+    "pipesim_analysis_report": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]),
+    "pipesim_plan": (C.c_int, [C.c_int, C.c_longlong, C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]),
 }
 
 _lib = None

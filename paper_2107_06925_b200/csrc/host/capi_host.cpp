@@ -197,3 +197,111 @@ const char* ck_last_error(void) { return chimera::capi::last_error().c_str(); }
 void ck_free(void* p) { std::free(p); }
 
 }  // extern "C"
+
+namespace {
+
+using chimera::json::Value;
+
+Value int_list(const std::vector<int>& v) {
+  Value a = Value::array();
+  for (int x : v) a.push(Value::integer(x));
+  return a;
+}
+
+Value num_list(const std::vector<double>& v) {
+  Value a = Value::array();
+  for (double x : v) a.push(Value::number(x));
+  return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+// Every schedule metric in one document (validate_dependencies, per-worker bubble,
+// steady-state idle, memory profile, free regions, critical path), the schedule
+// timed by a zero-communication dessim::simulate like pipesim_bubble_ratio_per_worker.
+int pipesim_analysis_report(const char* schedule_json, const char* profile_json, char** out_json) {
+  return guarded([&] {
+    const Schedule s = schedule_from_json(schedule_json);
+    const CostProfile p = profile_from_json(profile_json);
+    Value j = Value::object();
+    Value bad = Value::array();
+    for (const auto& v : analysis::validate_dependencies(s)) bad.push(Value::string(v));
+    const bool ok = bad.arr.empty();
+    j.set("violations", std::move(bad));
+    if (ok) {
+      dessim::SimOptions o;
+      o.zero_comm = true;
+      const auto sim = dessim::simulate(s, p, o);
+      Value b = Value::array();
+      for (const auto& r : analysis::bubble_ratio_per_worker(sim.timed, p)) {
+        Value x = Value::array();
+        x.push(Value::integer(r.num));
+        x.push(Value::integer(r.den));
+        b.push(std::move(x));
+      }
+      j.set("bubble", std::move(b));
+      j.set("steady_state_idle", Value::number(analysis::steady_state_idle(s, p)));
+      const auto mp = analysis::memory_profile(s, p);
+      Value m = Value::object();
+      m.set("weight_counts", int_list(mp.weight_counts));
+      m.set("act_counts", int_list(mp.act_counts));
+      m.set("weight_bytes", num_list(mp.weight_bytes));
+      m.set("act_bytes", num_list(mp.act_bytes));
+      m.set("peak_worker", Value::integer(mp.peak_worker));
+      m.set("peak_bytes", Value::number(mp.peak_bytes));
+      j.set("memory", std::move(m));
+      Value fr = Value::array();
+      for (const auto& w : perfmodel::free_regions(sim.timed, p).per_worker) {
+        Value x = Value::array();
+        for (const auto& st : w) {
+          Value e = Value::array();
+          e.push(Value::integer(st.stage));
+          e.push(Value::number(st.slack));
+          x.push(std::move(e));
+        }
+        fr.push(std::move(x));
+      }
+      j.set("free_regions", std::move(fr));
+      const auto cp = perfmodel::critical_path(s, p);
+      Value path = Value::array();
+      for (const Task& t : cp.path) {
+        Value e = Value::array();
+        e.push(Value::string(to_string(t.kind)));
+        for (int x : {t.pipeline_id, t.micro_batch, t.stage, t.worker}) e.push(Value::integer(x));
+        path.push(std::move(e));
+      }
+      Value c = Value::object();
+      c.set("C_f", Value::integer(cp.C_f));
+      c.set("C_b", Value::integer(cp.C_b));
+      c.set("path", std::move(path));
+      j.set("critical_path", std::move(c));
+    }
+    *out_json = dup_string(chimera::json::dump(j, -1));
+  });
+}
+
+// perfmodel::plan (proj/src/perfmodel.cpp:225-298): candidate (W, D, B, N, scaling)
+// ranked by predicted iteration time, as a JSON list.
+int pipesim_plan(int P, long long B_hat, const char* profile_json, const char* scheme, char** out_json) {
+  return guarded([&] {
+    const auto sc = scheme_from_string(scheme);
+    if (!sc) throw InvalidConfigError("unknown scheme");
+    Value a = Value::array();
+    for (const auto& e : perfmodel::plan(P, B_hat, profile_from_json(profile_json), *sc)) {
+      Value x = Value::object();
+      x.set("W", Value::integer(e.W));
+      x.set("D", Value::integer(e.D));
+      x.set("B", Value::integer(e.B));
+      x.set("N", Value::integer(e.N));
+      x.set("scaling", Value::string(to_string(e.scaling)));
+      x.set("recompute", Value::boolean(e.recompute));
+      x.set("T_predicted", Value::number(e.T_predicted));
+      a.push(std::move(x));
+    }
+    *out_json = dup_string(chimera::json::dump(a, -1));
+  });
+}
+
+}  // extern "C"

@@ -15,7 +15,7 @@ from typing import List, Optional
 
 import numpy as np
 
-from ._lib import InvalidConfigError, call_str, check, lib  # noqa: F401
+from ._lib import CKError, InvalidConfigError, call_str, check, lib  # noqa: F401
 
 SCHEMES = ("gpipe", "dapple", "gems", "pipedream", "pipedream-2bw", "chimera")
 SCALINGS = ("direct", "forward-doubling", "backward-halving")
@@ -210,6 +210,18 @@ def predict_T(config, profile=None) -> float:
     t = C.c_double()
     check(lib().pipesim_predict_T(_cfg(config), _prof(profile), C.byref(t)))
     return t.value
+
+
+def analysis_report(schedule, profile=None) -> dict:
+    """validate_dependencies, per-worker bubble, steady-state idle, memory profile, free
+    regions and critical path of one schedule (pipesim_analysis_report)."""
+    return json.loads(call_str(lib().pipesim_analysis_report, _sched(schedule), _prof(profile)))
+
+
+def plan(P: int, B_hat: int, profile=None, scheme: str = "chimera") -> list:
+    """perfmodel::plan (proj/src/perfmodel.cpp:225-298): feasible (W, D, B, N, scaling)
+    configurations for P workers and mini-batch B_hat, fastest predicted first."""
+    return json.loads(call_str(lib().pipesim_plan, int(P), int(B_hat), _prof(profile), scheme.encode()))
 
 
 def replay_order(schedule):
