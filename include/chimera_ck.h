@@ -95,6 +95,11 @@ CK_API int ck_toy_run_iteration(const char* schedule_json, const int* dims, int 
 CK_API int ck_toy_make_model(const int* dims, int n_dims, uint64_t seed, double* params);
 CK_API int ck_toy_make_batch(const int* dims, int n_dims, int size, uint64_t seed,
                              double* inputs, double* targets);
+/* oracle::check_gradients (proj/include/pipesim/oracle.hpp:77, oracle.cpp:358-410):
+ * central finite differences (fp64, one CTA per parameter and sign) vs the analytic
+ * gradient, both on the GPU; *max_rel_err = max |fd - g| / max(1, |fd|, |g|). */
+CK_API int ck_toy_check_gradients(const int* dims, int n_dims, const double* params, const double* inputs,
+                                  const double* targets, int batch, double step, double* max_rel_err);
 /* oracle::sequential_sgd (oracle.hpp:56): plain mini-batch SGD on the GPU. */
 CK_API int ck_toy_sequential_sgd(const int* dims, int n_dims, const double* params_in,
                                  const double* inputs, const double* targets, int batch,

@@ -39,6 +39,12 @@ struct MissingActivationError : std::runtime_error {
 struct VersionMismatchError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+/// Chimera-B200 extension (not in the reference): the GPU could not run the request --
+/// no sm_100 device, a CUDA / NCCL failure, out of device memory.  Every GPU-executed
+/// entry point below reports device trouble with this type (C boundary: status 3).
+struct DeviceError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 
 ToyModel sequential_sgd(const ToyModel& model, const Batch& batch, double lr);
 ToyModel run_iteration(const Schedule& s, const ToyModel& model, const Batch& batch, double lr);
@@ -50,6 +56,11 @@ struct IterationTrace {
 
 IterationTrace run_iteration_traced(const Schedule& s, const ToyModel& model, const Batch& batch,
                                     double lr);
+/// Central finite differences of the mean squared-error loss on every weight and bias
+/// against the analytic gradient (proj/src/oracle.cpp:358-410); returns the maximum
+/// relative error max|fd - g| / max(1, |fd|, |g|).  Both sides run on the GPU in fp64.
+double check_gradients(const ToyModel& model, const Batch& batch, double step = 1e-5);
+
 double max_relative_diff(const ToyModel& a, const ToyModel& b);
 
 }  // namespace pipesim::oracle

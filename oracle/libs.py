@@ -26,7 +26,7 @@ def build(ref: bool = True) -> None:
     """Compile the C restatement (always) and oracle/_ref (when the reference is mounted)."""
     subprocess.check_call(["make", "-s", "-C", HERE, "all"])
     if ref and os.path.isdir(REF_SRC):
-        subprocess.check_call(["make", "-s", "-j8", "-C", HERE, "ref"])
+        subprocess.check_call(["make", "-s", "-j8", "-C", HERE, "ref", "reftests"])
 
 
 def ref_available() -> bool:

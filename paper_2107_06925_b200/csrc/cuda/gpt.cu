@@ -1323,6 +1323,13 @@ CK_API int ck_gpt_create(const ck_gpt_model* mdl, const char* schedule_json, flo
     const auto s = pipesim::schedule_from_json(schedule_json);
     const auto v = pipesim::validate_config_shape(s.config);
     if (!v.empty()) throw pipesim::InvalidConfigError(v.front());
+    // PipeDream updates each stage after every micro-batch under stashed weight
+    // versions (proj/src/oracle.cpp:205-214,337-345); this executor is synchronous
+    // (one update per stage per iteration), so it refuses rather than diverge.
+    if (s.config.scheme == pipesim::Scheme::PipeDream)
+      throw pipesim::InvalidConfigError("the GPT executor runs synchronous schemes only (pipedream needs "
+                                        "per-micro-batch weight versions)");
+    chimera::capi::require_executable(s);
     auto* h = new ck_gpt;
     try {
       h->t = std::make_unique<chimera::gpt::Trainer>(m, s, lr, first_rank, n_ranks);

@@ -1,6 +1,8 @@
 // GPT-2 Chimera trainer (cuda/gpt.cu).
 #pragma once
 
+#include "pipesim/oracle.hpp"
+
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -15,10 +17,8 @@ namespace chimera::gpt {
 
 struct Stash;
 
-// oracle::MissingActivationError analogue (status 3 at the C-ABI)
-struct MissingActivation : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
+// oracle::MissingActivationError itself (status 3 at the C-ABI)
+using MissingActivation = pipesim::oracle::MissingActivationError;
 
 class Trainer {
  public:

@@ -10,7 +10,9 @@
 #include <utility>
 #include <vector>
 
+#include "pipesim/analysis.hpp"
 #include "pipesim/core.hpp"
+#include "pipesim/oracle.hpp"
 #include "sched_engine.hpp"
 
 namespace chimera::capi {
@@ -22,9 +24,8 @@ inline std::string& last_error() {
 
 // Status convention of the C boundary: 0 ok, 2 invalid input,
 // 3 internal (CUDA / NCCL failure, missing activation, deadlock timeout).
-struct InternalError : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
+// Device-side failures surface to C++ callers as pipesim::oracle::DeviceError.
+using InternalError = pipesim::oracle::DeviceError;
 
 template <class F>
 int guarded(F&& f) {
@@ -50,6 +51,24 @@ inline char* dup_string(const std::string& s) {
   char* p = static_cast<char*>(std::malloc(s.size() + 1));
   std::memcpy(p, s.c_str(), s.size() + 1);
   return p;
+}
+
+// Precondition of every executed schedule: the schedule must
+// pass analysis::validate_dependencies.  Violations map to the exception the
+// reference Engine would raise executing it (proj/src/oracle.cpp:210-280): a backward
+// whose forward never runs -> MissingActivationError, a dependency cycle ->
+// CyclicDependencyError (from the replay-order timing); anything else (duplicate
+// tasks, stage order) -> InvalidConfigError listing the violations.
+inline void require_executable(const pipesim::Schedule& s) {
+  const auto bad = pipesim::analysis::validate_dependencies(s);
+  if (bad.empty()) return;
+  std::string all;
+  for (const auto& v : bad) all += (all.empty() ? "" : "; ") + v;
+  for (const auto& v : bad)
+    if (v.rfind("backward without matching forward", 0) == 0) throw pipesim::oracle::MissingActivationError(all);
+  for (const auto& v : bad)
+    if (v.rfind("cyclic dependency", 0) == 0) throw pipesim::CyclicDependencyError(all);
+  throw pipesim::InvalidConfigError("schedule fails validate_dependencies: " + all);
 }
 
 // Global issue order of a schedule's tasks: unit-profile tick timing, sorted by

@@ -92,6 +92,12 @@ ToyModel run_iteration(const Schedule& s, const ToyModel& model, const Batch& ba
   return run_iteration_traced(s, model, batch, lr).model;
 }
 
+double check_gradients(const ToyModel& model, const Batch& batch, double step) {
+  const auto p = flat(model);
+  return chimera::toy::check_gradients(model.dims, p.data(), batch.inputs.data(), batch.targets.data(), batch.size,
+                                       step);
+}
+
 double max_relative_diff(const ToyModel& a, const ToyModel& b) {
   const auto x = flat(a), y = flat(b);
   double worst = 0;

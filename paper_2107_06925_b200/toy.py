@@ -18,6 +18,8 @@ from .pipesim import Schedule, generate_json
 _lib.register("ck_toy_run_iteration", C.c_int, [C.c_char_p, _ip, C.c_int, _dp, _dp, _dp, C.c_int,
                                                 C.c_double, _dp, _ip, C.c_int])
 _lib.register("ck_toy_sequential_sgd", C.c_int, [_ip, C.c_int, _dp, _dp, _dp, C.c_int, C.c_double, _dp])
+_lib.register("ck_toy_check_gradients", C.c_int, [_ip, C.c_int, _dp, _dp, _dp, C.c_int, C.c_double,
+                                                  C.POINTER(C.c_double)])
 _lib.register("ck_toy_make_model", C.c_int, [_ip, C.c_int, C.c_uint64, _dp])
 _lib.register("ck_toy_make_batch", C.c_int, [_ip, C.c_int, C.c_int, C.c_uint64, _dp, _dp])
 
@@ -71,3 +73,14 @@ def sequential_sgd(dims, params, inputs, targets, batch: int, lr: float) -> np.n
                                       np.ascontiguousarray(inputs, np.float64),
                                       np.ascontiguousarray(targets, np.float64), batch, lr, out))
     return out
+
+
+def check_gradients(dims, params, inputs, targets, batch: int, step: float = 1e-5) -> float:
+    """oracle::check_gradients (proj/src/oracle.cpp:358-410) on the GPU: max relative
+    error of central finite differences against the analytic gradient."""
+    d = np.asarray(dims, np.int32)
+    err = C.c_double()
+    check(lib().ck_toy_check_gradients(d, len(d), np.ascontiguousarray(params, np.float64),
+                                       np.ascontiguousarray(inputs, np.float64),
+                                       np.ascontiguousarray(targets, np.float64), batch, step, C.byref(err)))
+    return err.value

@@ -53,3 +53,14 @@ def test_library_does_not_pin_nccl_before_torch():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_gpt_executor_rejects_pipedream_before_touching_the_device():
+    """The GPT executor is synchronous: PipeDream (per-micro-batch updates under weight
+    versions, proj/src/oracle.cpp:205-214) is refused with InvalidConfigError (status
+    2) at ck_gpt_create, before any device work -- so this runs without a GPU."""
+    import pytest
+    from paper_2107_06925_b200 import pipesim as P
+    from paper_2107_06925_b200.gpt import PRESETS, Trainer
+    with pytest.raises(P.InvalidConfigError):
+        Trainer(PRESETS["tiny"], P.PipelineConfig("pipedream", 4, 1, 4), lr=0.1)

@@ -73,3 +73,53 @@ def test_bad_batch_size_is_invalid():
     x, t = toy.make_batch(dims, 3, 1)
     with pytest.raises(P.InvalidConfigError):
         toy.run_iteration(P.generate_json(cfg, None, -1), dims, p, x, t, 0.1)
+
+
+@pytest.mark.gpu
+def test_async_and_two_replica_schemes_vs_reference_fixtures(golden, toy_oracle):
+    """PipeDream (per-backward updates under stashed weight versions,
+    proj/src/oracle.cpp:205-214,337-345), PipeDream-2BW and GEMS on the GPU executor
+    against trajectories of the reference oracle (3 iterations)."""
+    for case in golden("toy_oracle.json")["async_cases"]:
+        c, dims = case["config"], case["dims"]
+        text = P.generate_json(P.PipelineConfig(**c), None, -1)
+        params = toy.make_model(dims, case["model_seed"])
+        batch = c["B"] * c["N"] * c["W"]
+        for it, seed in enumerate(case["batch_seeds"]):
+            x, t = toy.make_batch(dims, batch, seed)
+            params, peaks = toy.run_iteration(text, dims, params, x, t, case["lr"])
+            assert toy_oracle.max_relative_diff(dims, params, np.array(case["params_after"][it])) <= TOL, (c, it)
+        assert peaks == case["peak_stash"]
+
+
+@pytest.mark.gpu
+def test_check_gradients_gpu_vs_reference_pins(golden):
+    """oracle::check_gradients on the GPU (fp64 finite differences) next to the
+    reference's value on the same model / batch (proj/tests/test_oracle.cpp:56-62)."""
+    g = golden("toy_oracle.json")
+    for pin in g["fd_pins"]:
+        p = toy.make_model(pin["dims"], pin["seed"])
+        x, t = toy.make_batch(pin["dims"], pin["batch"], pin["seed"])
+        err = toy.check_gradients(pin["dims"], p, x, t, pin["batch"])
+        assert err <= 1e-5 and abs(err - pin["err"]) <= 1e-8, (pin, err)
+    dims = [4, 5, 4, 3]  # acceptance criterion 7 (proj/tests/acceptance.cpp:306-313)
+    p = toy.make_model(dims, 0)
+    x, t = toy.make_batch(dims, 8, 0)
+    err = toy.check_gradients(dims, p, x, t, 8)
+    assert err <= 1e-5 and abs(err - g["generators"]["fd_error_crit7"]) <= 1e-8
+
+
+@pytest.mark.gpu
+def test_executor_rejects_malformed_schedules():
+    """Precondition (a28): validate_dependencies before execution; an orphan backward
+    raises MissingActivationError (status 3) like the reference Engine."""
+    from paper_2107_06925_b200._lib import CKError
+    dims = [4, 4, 3]
+    sched = {"config": P.PipelineConfig("gpipe", 2, 1, 1).__dict__,
+             "per_worker": [[], [{"kind": "Backward", "pipeline_id": 0, "micro_batch": 0, "stage": 1,
+                                  "worker": 1, "replica_group": 0}]]}
+    p = toy.make_model(dims, 0)
+    x, t = toy.make_batch(dims, 1, 0)
+    with pytest.raises(CKError) as e:
+        toy.run_iteration(json.dumps(sched), dims, p, x, t, 0.1)
+    assert e.value.status == 3 and "backward without matching forward" in str(e.value)
