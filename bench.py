@@ -1,11 +1,13 @@
 """Chimera-B200 benchmark: GPT-2 training throughput under a Chimera schedule.
 
-Workload (BASELINE.json configs[1]): GPT-2 medium (24 layers, h=1024, 16 heads,
-s=1024, V=50257), Chimera D=4, N=4 micro-batches of B=4 sequences, W=2 data-parallel
-pipeline replicas -> 8 logical ranks, 32 sequences per iteration.  At --gpus G the 8
-ranks are spread over G GPUs (G | 8); one process per GPU under torchrun.  A "step" is
-one full training iteration (all micro-batches forward+backward, stage gradient
-allreduce, SGD update) on synthetic tokens and random-init weights.
+Workload (BASELINE.json `metric` "GPT-2 seqs/sec at D=8" -> configs[3]): GPT-2 1.3B
+(64 layers, h=1280, 20 heads, s=632, V=50257), Chimera D=8 with N=32 micro-batches of
+B=2 sequences (B 1-2), forward doubling + recompute -> 8 logical
+ranks, 64 sequences per iteration.  At --gpus G the 8 ranks are spread over G GPUs
+(G | 8); one process per GPU under torchrun.  A "step" is one full training iteration
+(all micro-batches forward+backward, stage gradient allreduce, SGD update) on
+synthetic tokens and random-init weights.  `--config gpt2-medium` runs configs[1]
+(GPT-2 medium D=4 W=2) as a secondary line; bert48 / q4* the other configs.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
@@ -34,8 +36,8 @@ CONFIGS = {
                     "GPT-2 medium Chimera D=4 N=4 W=2 B=4 (BASELINE configs[1])"),
     "bert48": ("bert48", dict(scheme="chimera", D=8, W=1, N=8, B=8, f=1, scaling="direct"),
                "Bert-48 shape (bidirectional, dense MLM head) Chimera D=8 N=8 B=8 (BASELINE configs[2])"),
-    "gpt2-1.3b": ("gpt2-1.3b", dict(scheme="chimera", D=8, W=1, N=32, B=1, f=1, scaling="forward-doubling"),
-                  "GPT-2 1.3B s=632 Chimera D=8 N=32 forward-doubling + recompute (BASELINE configs[3])"),
+    "gpt2-1.3b": ("gpt2-1.3b", dict(scheme="chimera", D=8, W=1, N=32, B=2, f=1, scaling="forward-doubling"),
+                  "GPT-2 1.3B s=632 Chimera D=8 N=32 B=2 forward-doubling + recompute (BASELINE configs[3])"),
     "q4": ("gpt2-32l", dict(scheme="chimera", D=8, W=1, N=16, B=1, f=2, scaling="direct"),
            "GPT-2 32-layer s=632 Chimera f=2 (4 pipelines) D=8 N=16 (BASELINE configs[4])"),
     "q4-gpipe": ("gpt2-32l", dict(scheme="gpipe", D=8, W=1, N=16, B=1, f=1, scaling="direct"),
@@ -43,7 +45,8 @@ CONFIGS = {
     "q4-dapple": ("gpt2-32l", dict(scheme="dapple", D=8, W=1, N=16, B=1, f=1, scaling="direct"),
                   "GPT-2 32-layer s=632 1F1B/DAPPLE D=8 N=16 (configs[4] baseline)"),
 }
-SHAPE_NAME, CFG, WORKLOAD = CONFIGS["gpt2-medium"]
+DEFAULT_CONFIG = "gpt2-1.3b"
+SHAPE_NAME, CFG, WORKLOAD = CONFIGS[DEFAULT_CONFIG]
 
 
 def peaks():
@@ -100,91 +103,203 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_port_sample(shape, seconds_hint=20.0):
-    """The numpy oracle (oracle/gpt_oracle.py, fp64, all BLAS threads) on a bounded
-    sample: forward+backward of one GPT-2 medium pipeline stage (6 layers, no head) for
-    one sequence, repeated until ~`seconds_hint`; scaled to full-model seqs/s by
-    algorithmic FLOPs."""
-    import numpy as np
-    from oracle import gpt_oracle as O
-    m = O.Shape(**shape.__dict__)
-    D = CFG["D"]
-    stage = O.StageModel(m, D, 1)
-    params = O.init_params(m, D, 0)[1]
-    P = O.unpack(params, stage.layout)
-    rng = np.random.default_rng(0)
-    x = rng.standard_normal((m.seq, m.hidden))
-    # torchrun exports OMP_NUM_THREADS=1; the baseline uses every host core regardless
-    from threadpoolctl import threadpool_info, threadpool_limits
-    with threadpool_limits(limits=os.cpu_count()):
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
-        t0 = time.perf_counter()
-        n = 0
-        while True:
-            y, _, cache = stage.forward(P, x, None, 1, 1.0)
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class PortStages:
+    """The numpy fp64 port of the reference Engine (oracle/gpt_oracle.py; the reference
+    itself has no transformer) timed stage by stage on ONE sequence of the workload:
+    stage s forward + backward (stage 0 from tokens, stage D-1 with the LM head and
+    cross-entropy), all host BLAS threads.  A sequence's full fwd+bwd time is the sum
+    over the D stages -- measured, not FLOP-scaled."""
+
+    def __init__(self, shape):
+        import numpy as np
+        from oracle import gpt_oracle as O
+        self.np, self.O = np, O
+        self.m = O.Shape(**shape.__dict__)
+        self.D = CFG["D"]
+        self.params = O.init_params(self.m, self.D, 0)
+        self.models = [O.StageModel(self.m, self.D, st) for st in range(self.D)]
+        tok, lab = O.synthetic_tokens(self.m, 1, 1)
+        self.tok, self.lab = tok, lab
+        self.times = {}
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=os.cpu_count()):  # spin up the BLAS threads untimed
+            w = np.ones((512, 512))
+            for _ in range(4):
+                w = w @ w * 1e-3
+
+    def time_stage(self, st):
+        import time as _t
+        np, O, m = self.np, self.O, self.m
+        sm = self.models[st]
+        P = O.unpack(self.params[st], sm.layout)
+        x = self.tok if st == 0 else np.random.default_rng(st).standard_normal((m.seq, m.hidden))
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=os.cpu_count()):  # torchrun exports OMP_NUM_THREADS=1
+            t0 = _t.perf_counter()
+            y, _, cache = sm.forward(P, x, self.lab, 1, 1.0 / m.seq)
             G = {k: np.zeros_like(v) for k, v in P.items()}
-            stage.backward(P, G, cache, np.ones_like(y) * 1e-3, 1)
-            n += 1
-            if time.perf_counter() - t0 > seconds_hint or n >= 50:
-                break
-        dt = (time.perf_counter() - t0) / n
-    s, h = m.seq, m.hidden
-    stage_flops = 3 * stage.per * (24 * s * h * h + 4 * s * s * h)  # fwd+bwd, no head
-    rate = stage_flops / dt
-    seqs_per_s = rate / shape.flops_per_seq()
-    return {"value": seqs_per_s, "unit": "seqs/s", "cores": cores, "kind": "port",
-            "sample": f"numpy fp64 oracle, 1 sequence x 1 stage ({stage.per} layers) fwd+bwd x{n} "
-                      f"({dt:.2f} s each, {rate / 1e9:.1f} GFLOP/s), scaled by FLOPs to the full model"}
+            sm.backward(P, G, cache, None if st == self.D - 1 else np.ones_like(y) * 1e-3, 1)
+            dt = _t.perf_counter() - t0
+        self.times.setdefault(st, []).append(dt)
+        return dt
+
+    def seqs_per_s(self):
+        per = [sum(v) / len(v) for _, v in sorted(self.times.items())]
+        mean = sum(per) / len(per)
+        return 1.0 / (sum(per) + mean * (self.D - len(per)))
 
 
-def gemm_roofline(stream_handle, peak_tflops):
+def threads_used():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        return os.cpu_count()
+
+
+def reference_toy_iteration():
+    """The reference library itself (oracle/_ref, proj/src/oracle.cpp:304-356, single-
+    threaded by design) on SURVEY.md §8(d) CPU-baseline item 1: run_iteration on the
+    Chimera D=4 N=4 schedule, dims {256 x 5}, micro-batch B = 128 (B_hat = 512; the survey's
+    probe: 0.546 s / iteration) -- seconds per iteration."""
+    import time as _t
+    try:
+        from oracle.libs import RefLib, ref_available
+        if not ref_available():
+            return None
+        from paper_2107_06925_b200 import pipesim as P
+        R = RefLib()
+        cfg = P.PipelineConfig("chimera", 4, 1, 4, 128, 1)  # B_hat = 512
+        text = R.generate(cfg.to_json(), P.CostProfile().to_json(), -1)
+        dims = [256] * 5
+        p = R.make_model(dims, 42)
+        x, t = R.make_batch(dims, 512, 100)
+        t0 = _t.perf_counter()
+        R.run_iteration(text, dims, p, x, t, 512, 0.05, 4)
+        dt = _t.perf_counter() - t0
+        flops = 6.0 * 512 * sum(dims[i] * dims[i + 1] for i in range(4))
+        return {"s_per_iteration": round(dt, 4), "gflops": round(flops / dt / 1e9, 3), "cores": 1,
+                "config": "Chimera D=4 N=4 B=128 W=1, dims {256 x 5}, B_hat = 512 (ToyModel, fp64 + Kahan)"}
+    except Exception as e:  # the checker is optional on a box without the built reference
+        return {"unavailable": str(e)[:200]}
+
+
+def cpu_port_sample(shape, stages=None):
+    """cpu_baseline: one sequence through every pipeline stage (fwd+bwd, incl. the LM
+    head) on the numpy port, all host cores; plus the reference library's own ToyModel
+    iteration on 1 core."""
+    ps = PortStages(shape)
+    for st in (stages if stages is not None else range(ps.D)):
+        ps.time_stage(st)
+    v = ps.seqs_per_s()
+    per = {st: round(sum(t) / len(t), 3) for st, t in sorted(ps.times.items())}
+    return {"value": v, "unit": "seqs/s", "cores": threads_used(), "kind": "port", "cpu_model": cpu_model(),
+            "sample": f"numpy fp64 port of the reference Engine: ONE sequence of the workload, forward + backward "
+                      f"through each of the {ps.D} stages (s per stage {per}); seqs/s = 1 / sum over stages",
+            "reference_toy": reference_toy_iteration()}
+
+
+def roofline_shapes(shape, cfg):
+    """(M, N, K, a_mn, b_mn, weight): every stage-GEMM shape one iteration runs, weighted by
+    how often it runs per layer-micro-batch.  Forward doubling + recompute (configs[3]):
+    fused forward pairs on 2M rows (weight 1/2 per micro-batch), recompute forward,
+    activation gradient (dgrad) and weight gradient (K = M) on M rows; the LM head's
+    four GEMMs with weight 1/L (one head per L layers)."""
+    M, h, f, Vp = cfg["B"] * shape.seq, shape.hidden, shape.ffn, shape.vocab_padded
+    fd = cfg["scaling"] == "forward-doubling" and cfg["N"] > cfg["D"]
+    layer = lambda Mm: [(Mm, 3 * h, h), (Mm, h, h), (Mm, f, h), (Mm, h, f)]
+    out = []
+    if fd:
+        out += [(Mm, N, K, 0, 0, 0.5) for (Mm, N, K) in layer(2 * M)]  # fused pair forward
+        out += [(Mm, N, K, 0, 0, 1.0) for (Mm, N, K) in layer(M)]  # recompute forward
+    else:
+        out += [(Mm, N, K, 0, 0, 1.0) for (Mm, N, K) in layer(M)]
+    out += [(M, h, 3 * h, 0, 1, 1.0), (M, h, h, 0, 1, 1.0), (M, h, f, 0, 1, 1.0), (M, f, h, 0, 1, 1.0)]  # dgrad
+    out += [(3 * h, h, M, 1, 1, 1.0), (h, h, M, 1, 1, 1.0), (f, h, M, 1, 1, 1.0), (h, f, M, 1, 1, 1.0)]  # wgrad
+    wl = 1.0 / shape.n_layer
+    if fd:
+        out += [(2 * M, Vp, h, 0, 0, 0.5 * wl), (M, Vp, h, 0, 0, wl)]
+    else:
+        out += [(M, Vp, h, 0, 0, wl)]
+    out += [(M, h, Vp, 0, 1, wl), (Vp, h, M, 1, 1, wl)]
+    return out
+
+
+def gemm_roofline(stream_handle, peak_tflops, shape=None, cfg=None, workspace=True):
     """Live CUDA-event timing of the stage GEMMs (the dominant kernel family) at the
-    workload's shapes, on the trainer's device: achieved = 2MNK / avg launch time."""
+    workload's shapes as the step runs them (roofline_shapes), on the trainer's device,
+    with the split-K workspace the trainer's chain streams use:
+    achieved = sum_i w_i 2 M N K / sum_i w_i t_i."""
     import torch
     from paper_2107_06925_b200 import kernels as ck
     from paper_2107_06925_b200.gpt import PRESETS
-    m = PRESETS[SHAPE_NAME]
-    M, h, f = CFG["B"] * m.seq, m.hidden, m.ffn
-    shapes = [  # (M, N, K, a_mn, b_mn) one layer fwd + bwd, weight x tokens
-        (M, 3 * h, h, 0, 0), (M, h, h, 0, 0), (M, f, h, 0, 0), (M, h, f, 0, 0),
-        (M, h, 3 * h, 0, 1), (M, h, h, 0, 1), (M, h, f, 0, 1), (M, f, h, 0, 1),
-        (3 * h, h, M, 1, 1), (h, h, M, 1, 1), (f, h, M, 1, 1), (h, f, M, 1, 1)]
+    shape = shape or PRESETS[SHAPE_NAME]
+    cfg = cfg or CFG
+    shapes = roofline_shapes(shape, cfg)
     st = torch.cuda.ExternalStream(stream_handle) if stream_handle else torch.cuda.current_stream()
-    tot_flops, tot_ms = 0.0, 0.0
+    tot_flops, tot_ms, wsum, n_launch = 0.0, 0.0, 0.0, 0
+    rows = []
     with torch.cuda.stream(st):
+        ws = torch.zeros(max(Mm * N for (Mm, N, K, a, b, w) in shapes if not (a and b)), device="cuda") \
+            if workspace else None
         bufs = []
-        for (Mm, N, K, a, b) in shapes:
+        for (Mm, N, K, a, b, w) in shapes:
             A = torch.randn((K, Mm) if a else (Mm, K), device="cuda").bfloat16()
             B = torch.randn((K, N) if b else (N, K), device="cuda").bfloat16()
             out = torch.zeros(Mm, N, device="cuda", dtype=torch.float32 if (a and b) else torch.bfloat16)
-            bufs.append((Mm, N, K, a, b, A, B, out))
+            bufs.append((Mm, N, K, a, b, w, A, B, out))
+
+        def run(Mm, N, K, a, b, A, B, out):
+            ck.gemm("acc_f32" if (a and b) else "bf16", A, B, out, a_mn=bool(a), b_mn=bool(b),
+                    ws=None if (a and b) else ws, stream=st)
         for it in range(2):
-            for (Mm, N, K, a, b, A, B, out) in bufs:
-                ck.gemm("acc_f32" if (a and b) else "bf16", A, B, out, a_mn=bool(a), b_mn=bool(b), stream=st)
+            for (Mm, N, K, a, b, w, A, B, out) in bufs:
+                run(Mm, N, K, a, b, A, B, out)
         reps = 20
-        for (Mm, N, K, a, b, A, B, out) in bufs:
+        for (Mm, N, K, a, b, w, A, B, out) in bufs:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
             for _ in range(reps):
-                ck.gemm("acc_f32" if (a and b) else "bf16", A, B, out, a_mn=bool(a), b_mn=bool(b), stream=st)
+                run(Mm, N, K, a, b, A, B, out)
             e1.record(st)
             e1.synchronize()
-            tot_ms += e0.elapsed_time(e1) / reps
-            tot_flops += 2.0 * Mm * N * K
+            ms = e0.elapsed_time(e1) / reps
+            fl = 2.0 * Mm * N * K
+            tot_ms += w * ms
+            tot_flops += w * fl
+            wsum += w
+            rows.append({"shape": [Mm, N, K, a, b], "weight": round(w, 4), "us": round(ms * 1e3, 2),
+                         "tflops": round(fl / (ms * 1e-3) / 1e12, 1)})
+        del ws
     achieved = tot_flops / (tot_ms * 1e-3) / 1e12
-    # DRAM bytes per launch of the same 12 shapes from the committed `ncu --set full`
-    # capture (scripts/roofline_shapes.py); below the algorithmic operand+output bytes
+    # DRAM bytes per launch of the same shapes from the committed `ncu --set full`
+    # capture (scripts/roofline_shapes.py --config ...); null when not captured
     traffic, tsrc = None, None
-    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01y_gemm_roofline_ncu.json")
-    if SHAPE_NAME == "gpt2-medium" and os.path.exists(tpath):
-        with open(tpath) as fh:
-            traffic = json.load(fh)["avg_dram_bytes_per_launch"]
-        tsrc = "profiles/r01y_gemm_roofline_ncu.json"
-    return {"bound": "tensor", "kernel": "ck gemm_bf16 (tcgen05.mma kind::f16, TMA, TMEM), 12 stage GEMM shapes",
+    root = os.path.dirname(os.path.abspath(__file__))
+    for cand in (f"profiles/r02_gemm_roofline_ncu_{SHAPE_NAME}_B{cfg['B']}.json",
+                 "profiles/r01y_gemm_roofline_ncu.json" if SHAPE_NAME == "gpt2-medium" and cfg["B"] == 4 else None):
+        if cand and os.path.exists(os.path.join(root, cand)):
+            with open(os.path.join(root, cand)) as fh:
+                traffic = json.load(fh)["avg_dram_bytes_per_launch"]
+            tsrc = cand
+            break
+    return {"bound": "tensor", "kernel": "ck gemm_bf16 (tcgen05.mma kind::f16, TMA, TMEM; split-K + finalize "
+                                        "where chosen), every stage-GEMM shape of the step, run-count weighted",
             "achieved": round(achieved, 1), "peak": peak_tflops, "unit": "TFLOP/s",
             "frac": round(achieved / peak_tflops, 4), "traffic": traffic, "traffic_unit": "bytes/launch",
             "traffic_source": tsrc,
-            "flops_per_launch_avg": tot_flops / len(shapes), "avg_launch_ms": tot_ms / len(shapes)}
+            "flops_per_launch_avg": tot_flops / wsum, "avg_launch_ms": tot_ms / wsum, "shapes": rows}
 
 
 def measure_alpha_beta(world):
@@ -266,23 +381,30 @@ def comm_report(world, msg_bytes):
 
 def run_reference(args, shape):
     """--impl reference: the reference path's CPU implementation (the numpy port of the
-    reference Engine; the reference itself has no transformer), all host threads."""
+    reference Engine -- the reference itself has no transformer), all host threads, on
+    the SAME workload: every step times one sequence's forward + backward through one
+    pipeline stage (stages in turn), so the run covers every stage; value = 1 / (sum over
+    stages of the mean per-stage time) sequences/s."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    samples = []
-    for k in range(args.warmup + args.steps):
-        s = cpu_port_sample(shape, seconds_hint=3.0)
-        if k >= args.warmup:
-            samples.append(s["value"])
-    v = sum(samples) / len(samples)
+    ps = PortStages(shape)
+    for k in range(args.warmup):
+        ps.time_stage(k % ps.D)
+    ps.times = {}
+    for k in range(args.steps):
+        ps.time_stage((args.warmup + k) % ps.D)
+    v = ps.seqs_per_s()
+    per = {st: round(sum(t) / len(t), 3) for st, t in sorted(ps.times.items())}
     line = {"metric": METRIC, "value": v, "unit": "seqs/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "model": SHAPE_NAME, "global_batch": CFG["B"] * CFG["N"] * CFG["W"],
                        "seq_len": shape.seq},
-            "cpu_baseline": {"value": v, "unit": "seqs/s", "cores": s["cores"], "kind": "port",
-                             "sample": s["sample"]},
+            "cpu_baseline": {"value": v, "unit": "seqs/s", "cores": threads_used(), "kind": "port",
+                             "cpu_model": cpu_model(),
+                             "sample": f"numpy fp64 port of the reference Engine, one sequence per step through one "
+                                       f"stage (stages in turn; s per stage {per}); 1 / sum over the {ps.D} stages"},
             "e2e": {"value": v, "unit": "seqs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -294,13 +416,17 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="chimera")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", default="gpt2-medium", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--B", type=int, default=0, help="override the config's micro-batch size")
     ap.add_argument("--partition", default="balanced", choices=["balanced", "even"],
                     help="layers per stage: balanced per pipeline worker (LM-head stage shorter) or even")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     global SHAPE_NAME, CFG, WORKLOAD
     SHAPE_NAME, CFG, WORKLOAD = CONFIGS[args.config]
+    if args.B:
+        CFG = dict(CFG, B=args.B)
+        WORKLOAD = WORKLOAD.replace(f"B={CONFIGS[args.config][1]['B']}", f"B={args.B}")
 
     from paper_2107_06925_b200.gpt import PRESETS
     shape = PRESETS[SHAPE_NAME]
@@ -438,7 +564,7 @@ def main():
                                   alpha=ab[0], beta=ab[1], L_grad=l_grad,
                                   L_act=2.0 * CFG["B"] * shape.seq * shape.hidden)
         pred = P.predict_T(cfg, prof_b200)
-        rl = gemm_roofline(tr.stream_handle(), peak)
+        rl = gemm_roofline(tr.stream_handle(), peak, shape, CFG)
         flops_seq = shape.flops_per_seq()
         cpu = None if args.no_cpu_baseline else cpu_port_sample(shape)
         line = {

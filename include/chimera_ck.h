@@ -109,6 +109,13 @@ CK_API int ck_toy_sequential_sgd(const int* dims, int n_dims, const double* para
 /* tcgen05/TMA GEMM with fused epilogue (cuda/gemm.cu).  epi: 0 bf16 store (+bias),
  * 1 bias+GELU (out=U, out2=gelu(U)), 2 bias+residual(aux), 3 x gelu'(aux), 4 fp32 +=,
  * 5 fp32 store.  a_mn/b_mn select MN-major operands (see cuda/gemm.cuh). */
+/* Split-K variant for the bf16 epilogues: ws = fp32 workspace (zero-filled, >= M*N,
+ * left zeroed); K-slices reduce-add into it, one finalize pass applies the epilogue.
+ * ksplit > 1 forces the slice count, 0 lets the wave model decide (it may not split). */
+CK_API int ck_gemm_bf16_split(int epi, int a_mn, int b_mn, int M, int N, int K, const void* A, long long lda,
+                              const void* B, long long ldb, void* out, long long ldo, const void* bias,
+                              const void* aux, long long ld_aux, void* out2, long long ld_out2, float* colsum,
+                              float* ws, long long ws_elems, int ksplit, void* stream);
 CK_API int ck_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, const void* A,
                         long long lda, const void* B, long long ldb, void* out, long long ldo,
                         const void* bias, const void* aux, long long ld_aux, void* out2,

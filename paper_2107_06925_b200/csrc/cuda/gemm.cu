@@ -572,11 +572,12 @@ __global__ void __launch_bounds__(256, 1)
 // cannot fill the machine: the smallest slice count (each >= 8 K-blocks deep) whose
 // last wave is (nearly) as full as the best achievable; slices combine with fp32 vector
 // atomics.
-inline int split_k(int epi, int tiles, int slots, int K) {
+inline int split_k(int epi, int tiles, int slots, int K, int chosen = 0) {
   static const int force = [] {  // CK_GEMM_KSPLIT=n: fixed slice count (benchmarks)
     const char* e = std::getenv("CK_GEMM_KSPLIT");
     return e ? atoi(e) : 0;
   }();
+  if (chosen > 0) return chosen;
   if (epi == kAccF32 && force > 0) return force;
   if (epi != kAccF32 || tiles >= slots) return 1;
   const int kb = (K + BK - 1) / BK;
@@ -591,6 +592,91 @@ inline int split_k(int epi, int tiles, int slots, int K) {
   for (int ks = 1; ks <= kmax; ++ks)
     if (eff(ks) >= best - 0.03) return ks;
   return 1;
+}
+
+
+// ------------------------------------------------ split-K for bf16 epilogues --
+// Problems whose output tiles cannot fill 148 SMs (the 632 / 1264-row stage GEMMs of
+// GPT-2 1.3B with N = h, deep K) run as K-slices: every slice reduce-adds its fp32
+// partial tile into a zero-filled workspace (the kAccF32 kernels, TMA bulk reduce-add
+// at L2), then this pass applies the epilogue to the reduced rows with the arithmetic
+// of epilogue_chunk_tma (bias + residual summed first, gelu_tanh / gelu_tanh' on the
+// same formulas, bf16 rounding, the fused bias-gradient column sums of the bf16
+// values), writes the outputs and re-zeroes the workspace for the stream's next call.
+// Thread = 8 consecutive columns x kFinRows rows (16-byte loads and stores).
+constexpr int kFinRows = 8;
+
+template <int EPI>
+__global__ void __launch_bounds__(128) k_splitk_finalize(float* __restrict__ ws, EpiArgs ep, int M, int N) {
+  const int col = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (col >= N) return;
+  const int row0 = blockIdx.y * kFinRows;
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  float2 bias[4] = {};
+  if (ep.bias && EPI != kGeluBwd) {
+    const uint4 b = *reinterpret_cast<const uint4*>(ep.bias + col);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) bias[e] = bf2f((&b.x)[e]);
+  }
+  float2 csum[4] = {};
+  for (int rr = 0; rr < kFinRows; ++rr) {
+    const int row = row0 + rr;
+    if (row >= M) break;
+    float4* src = reinterpret_cast<float4*>(ws + (long long)row * N + col);
+    const float4 x0 = src[0], x1 = src[1];
+    src[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    src[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float2 v[4] = {make_float2(x0.x, x0.y), make_float2(x0.z, x0.w), make_float2(x1.x, x1.y), make_float2(x1.z, x1.w)};
+    uint4 q;
+    if constexpr (EPI == kGeluBwd) {
+      const uint4 a = *reinterpret_cast<const uint4*>(ep.aux + (long long)row * ep.ld_aux + col);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 u = bf2f((&a.x)[e]);
+        const float2 u2 = ptx::mul2(u, u);
+        const float2 z = ptx::mul2(u, ptx::fma2(u2, make_float2(k0 * k1, k0 * k1), make_float2(k0, k0)));
+        const float2 t = make_float2(tanh_fast(z.x), tanh_fast(z.y));
+        const float2 g = ptx::fma2(t, make_float2(0.5f, 0.5f), make_float2(0.5f, 0.5f));
+        const float2 om = ptx::fma2(make_float2(-t.x, -t.y), t, make_float2(1.f, 1.f));
+        const float2 c = ptx::fma2(u2, make_float2(3.f * k0 * k1, 3.f * k0 * k1), make_float2(k0, k0));
+        const float2 hb = ptx::mul2(ptx::mul2(u, make_float2(0.5f, 0.5f)), om);
+        const float2 y = ptx::mul2(v[e], ptx::fma2(hb, c, g));
+        (&q.x)[e] = f2bf(y.x, y.y);
+        if (ep.colsum) csum[e] = ptx::add2(csum[e], bf2f((&q.x)[e]));
+      }
+    } else {
+      uint4 a = make_uint4(0, 0, 0, 0);
+      if constexpr (EPI == kBiasResid) a = *reinterpret_cast<const uint4*>(ep.aux + (long long)row * ep.ld_aux + col);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float2 bb = bias[e];
+        if constexpr (EPI == kBiasResid) bb = ep.bias ? ptx::add2(bb, bf2f((&a.x)[e])) : bf2f((&a.x)[e]);
+        (&q.x)[e] = (ep.bias || EPI == kBiasResid) ? f2bf(v[e].x + bb.x, v[e].y + bb.y) : f2bf(v[e].x, v[e].y);
+      }
+    }
+    *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + col) = q;
+    if constexpr (EPI == kBiasGelu) {  // G = gelu_tanh(U) of the bf16-rounded U
+      uint4 gq;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 u = bf2f((&q.x)[e]);
+        const float2 u2 = ptx::mul2(u, u);
+        const float2 z = ptx::mul2(u, ptx::fma2(u2, make_float2(k0 * k1, k0 * k1), make_float2(k0, k0)));
+        const float2 t = make_float2(tanh_fast(z.x), tanh_fast(z.y));
+        const float2 hu = ptx::mul2(u, make_float2(0.5f, 0.5f));
+        const float2 y = ptx::fma2(hu, t, hu);
+        (&gq.x)[e] = f2bf(y.x, y.y);
+      }
+      *reinterpret_cast<uint4*>(ep.out2 + (long long)row * ep.ld_out2 + col) = gq;
+    }
+  }
+  if constexpr (EPI == kGeluBwd) {
+    if (ep.colsum) {
+      float4* d = reinterpret_cast<float4*>(ep.colsum + col);
+      atomicAdd(d, make_float4(csum[0].x, csum[0].y, csum[1].x, csum[1].y));
+      atomicAdd(d + 1, make_float4(csum[2].x, csum[2].y, csum[3].x, csum[3].y));
+    }
+  }
 }
 
 // ---------------------------------------------------------- 2-SM variant ----
@@ -857,7 +943,7 @@ void launch_pair(int M, int N, int K, const __nv_bfloat16* A, long long lda, con
   const CUtensorMap tb = B_MN ? cuda::make_map_2d_bf16(B, N, K, ldb, 64, BK)
                               : cuda::make_map_2d_bf16(B, K, N, ldb, 64, PBN / 2);
   const int base = ((M + 255) / 256) * ((N + PBN - 1) / PBN);
-  const int ks = split_k(EPI, base, cuda::kNumSMs / 2, K);
+  const int ks = split_k(EPI, base, cuda::kNumSMs / 2, K, ep.ksplit);
   const int tiles = base * ks;
   const int pairs = tiles < cuda::kNumSMs / 2 ? tiles : cuda::kNumSMs / 2;
   CUtensorMap to, to2;
@@ -897,7 +983,7 @@ void launch(int M, int N, int K, const __nv_bfloat16* A, long long lda, const __
   const CUtensorMap tb = B_MN ? cuda::make_map_2d_bf16(B, N, K, ldb, 64, BK)
                               : cuda::make_map_2d_bf16(B, K, N, ldb, 64, BN);
   const int base = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const int ks = split_k(EPI, base, cuda::kNumSMs, K);
+  const int ks = split_k(EPI, base, cuda::kNumSMs, K, ep.ksplit);
   const int tiles = base * ks;
   const int grid = tiles < cuda::kNumSMs ? tiles : cuda::kNumSMs;
   CUtensorMap to, to2;
@@ -968,47 +1054,120 @@ void by_layout(Epi epi, bool a_mn, bool b_mn, int M, int N, int K, const __nv_bf
 // Per-slot rates (TFLOP/s): CTA pair 256x256 24.6, 128x256 11.4, 128x128 7.0, 128x64 3.6
 // -- the narrow tiles are operand-bound but put more SMs on problems with few output
 // tiles and a deep K (the small-M stage shapes of GPT-2 1.3B / Bert-48).
-int pick_tile(Epi epi, int M, int N, int K) {
+// With a split-K workspace the bf16 epilogues may also be cut into 2-4 K-slices (each
+// >= 8 K-blocks deep); that variant pays the finalize pass: a launch plus M*N*(8+2)
+// bytes (+2 residual / gelu operand, +2 second output) at ~4 TB/s, and a per-wave
+// fixed cost for the shallower tiles.
+struct TilePlan {
+  int choice;  // 0 = CTA pair 256x256, else single-CTA 128 x choice
+  int ks;      // K-slices (bf16 epilogues through the workspace when > 1)
+};
+
+TilePlan pick_tile(Epi epi, int M, int N, int K, bool can_split) {
   struct Cand {
     int choice, bm, bn, slots;
     double rate;
   };
   const Cand cands[] = {{0, 256, 256, cuda::kNumSMs / 2, 24.6}, {256, BM, 256, cuda::kNumSMs, 11.4},
                         {128, BM, 128, cuda::kNumSMs, 7.0}, {64, BM, 64, cuda::kNumSMs, 3.6}};
-  int best = 128;
+  const int kb = (K + BK - 1) / BK;
+  const int kmax = can_split ? std::max(1, std::min(4, kb / 8)) : 1;
+  const double wave_fixed = 1.5e6;  // ps: prologue / fill / exposed epilogue per wave
+  const double fin = 2.5e6 + double(M) * N * (10.0 + (epi == kBiasResid || epi == kGeluBwd || epi == kBiasGelu ? 2.0 : 0.0)) /
+                                 4.0e12 * 1e12;
+  TilePlan best{128, 1};
   double best_t = 1e300;
   for (const Cand& c : cands) {
     if (c.choice == 0 && (M < 256 || N < 256)) continue;
     if (c.choice == 256 && N <= 128) continue;
     const long long tiles = (long long)((M + c.bm - 1) / c.bm) * ((N + c.bn - 1) / c.bn);
-    const int ks = split_k(epi, int(std::min<long long>(tiles, 1 << 30)), c.slots, K);
-    const long long units = tiles * ks, waves = (units + c.slots - 1) / c.slots;
-    const double kdepth = double((K + ks - 1) / ks);
-    const double t = double(waves) * (2.0 * c.bm * c.bn * kdepth) / c.rate;
-    if (t < best_t * 0.98) best_t = t, best = c.choice;  // prefer the larger tile on a near-tie
+    for (int kq = 1; kq <= (epi == kAccF32 ? 1 : kmax); ++kq) {
+      const int ks = epi == kAccF32 ? split_k(epi, int(std::min<long long>(tiles, 1 << 30)), c.slots, K) : kq;
+      const long long units = tiles * ks, waves = (units + c.slots - 1) / c.slots;
+      const double kdepth = double((K + ks - 1) / ks);
+      double t = double(waves) * (2.0 * c.bm * c.bn * kdepth) / c.rate;
+      if (epi != kAccF32 && ks > 1) t += double(waves) * wave_fixed + fin;
+      if (t < best_t * 0.98) best_t = t, best = {c.choice, epi == kAccF32 ? 0 : ks};  // prefer earlier (larger) on near-ties
+    }
   }
   return best;
 }
+
+int pick_tile(Epi epi, int M, int N, int K) { return pick_tile(epi, M, N, K, false).choice; }
+
+namespace {
+
+void dispatch(int choice, Epi epi, bool a_mn, bool b_mn, int M, int N, int K, const __nv_bfloat16* A, long long lda,
+              const __nv_bfloat16* B, long long ldb, const EpiArgs& ep, cudaStream_t st) {
+  if (choice == 0 && (M < 256 || N < 256)) choice = 128;
+  if (choice == 0) by_layout<0>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
+  else if (choice == 256) by_layout<256>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
+  else if (choice == 64) by_layout<64>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
+  else by_layout<128>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) % 16) == 0; }
+
+// The workspace route needs whole 8-column groups and 16-byte aligned operands.
+bool split_ok(Epi epi, int M, int N, const EpiArgs& ep) {
+  if (!ep.ws || epi == kAccF32 || epi == kStoreF32 || ep.ws_elems < (long long)M * N) return false;
+  if (N % 8 || ep.ldo % 8 || !aligned16(ep.out) || !aligned16(ep.ws)) return false;
+  if (ep.bias && !aligned16(ep.bias)) return false;
+  if ((epi == kBiasResid || epi == kGeluBwd) && (!ep.aux || ep.ld_aux % 8 || !aligned16(ep.aux))) return false;
+  if (epi == kBiasGelu && (!ep.out2 || ep.ld_out2 % 8 || !aligned16(ep.out2))) return false;
+  if (epi == kGeluBwd && ep.colsum && !aligned16(ep.colsum)) return false;
+  return true;
+}
+
+template <int EPI>
+void finalize(const EpiArgs& ep, int M, int N, cudaStream_t st) {
+  const dim3 grid((N / 8 + 127) / 128, (M + kFinRows - 1) / kFinRows);
+  cuda::launch(k_splitk_finalize<EPI>, grid, dim3(128), 0, st, ep.ws, ep, M, N);
+  CK_CUDA(cudaGetLastError());
+}
+
+}  // namespace
 
 void gemm(Epi epi, bool a_mn, bool b_mn, int M, int N, int K, const __nv_bfloat16* A, long long lda,
           const __nv_bfloat16* B, long long ldb, const EpiArgs& ep, cudaStream_t st) {
   if (M <= 0 || N <= 0 || K <= 0) return;
   if ((lda % 8) || (ldb % 8) || (reinterpret_cast<uintptr_t>(A) % 16) || (reinterpret_cast<uintptr_t>(B) % 16))
     throw chimera::capi::InternalError("gemm: operands must be 16-byte aligned with ld % 8 == 0");
-  // CTA-pair 256 x 256 or single-CTA 128 x {256, 128, 64} tiles (pick_tile).
+  // CTA-pair 256 x 256 or single-CTA 128 x {256, 128, 64} tiles, split-K slices (pick_tile).
   static const int force = [] {
     const char* e = std::getenv("CK_GEMM_TILE");  // "pair" | "256" | "128" | "64" (benchmarks)
     if (!e) return -1;
     const std::string v(e);
     return v == "pair" ? 0 : v == "256" ? 256 : v == "64" ? 64 : 128;
   }();
-  int choice = force;
-  if (choice < 0) choice = pick_tile(epi, M, N, K);
-  if (choice == 0 && (M < 256 || N < 256)) choice = 128;
-  if (choice == 0) by_layout<0>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
-  else if (choice == 256) by_layout<256>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
-  else if (choice == 64) by_layout<64>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
-  else by_layout<128>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
+  static const int force_split = [] {  // CK_GEMM_SPLIT_BF16=0 disables the workspace route; n>1 forces n slices
+    const char* e = std::getenv("CK_GEMM_SPLIT_BF16");
+    return e ? atoi(e) : -1;
+  }();
+  const bool can_split = force_split != 0 && split_ok(epi, M, N, ep);
+  TilePlan plan = pick_tile(epi, M, N, K, can_split);
+  if (force >= 0) plan.choice = force;
+  if (can_split && force_split > 1) plan.ks = force_split;
+  if (can_split && ep.ksplit > 1) plan.ks = ep.ksplit;  // caller-forced (tests / benchmarks)
+  if (plan.ks > 1 && can_split) {  // K-slices into the workspace, then the epilogue pass
+    EpiArgs part;
+    part.out = ep.ws;
+    part.ldo = N;
+    part.atomic_acc = true;
+    part.ksplit = plan.ks;
+    dispatch(plan.choice, kAccF32, a_mn, b_mn, M, N, K, A, lda, B, ldb, part, st);
+    switch (epi) {
+      case kStoreBF16: return finalize<kStoreBF16>(ep, M, N, st);
+      case kBiasGelu: return finalize<kBiasGelu>(ep, M, N, st);
+      case kBiasResid: return finalize<kBiasResid>(ep, M, N, st);
+      case kGeluBwd: return finalize<kGeluBwd>(ep, M, N, st);
+      default: break;
+    }
+    throw chimera::capi::InternalError("gemm: split-K epilogue not supported");
+  }
+  EpiArgs e2 = ep;
+  e2.ksplit = 0;
+  dispatch(plan.choice, epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, e2, st);
 }
 
 }  // namespace chimera::gemm
@@ -1030,6 +1189,31 @@ CK_API int ck_gemm_bf16_ex(int epi, int a_mn, int b_mn, int M, int N, int K, con
     ep.out2 = static_cast<__nv_bfloat16*>(out2);
     ep.ld_out2 = ld_out2;
     ep.colsum = colsum;
+    chimera::gemm::gemm(static_cast<chimera::gemm::Epi>(epi), a_mn != 0, b_mn != 0, M, N, K,
+                        static_cast<const __nv_bfloat16*>(A), lda, static_cast<const __nv_bfloat16*>(B),
+                        ldb, ep, static_cast<cudaStream_t>(stream));
+  });
+}
+
+// ck_gemm_bf16_ex with a split-K workspace (fp32, zero-filled, >= M*N; left zeroed):
+// ksplit > 1 forces that many K-slices for a bf16 epilogue, 0 lets the wave model choose.
+CK_API int ck_gemm_bf16_split(int epi, int a_mn, int b_mn, int M, int N, int K, const void* A, long long lda,
+                              const void* B, long long ldb, void* out, long long ldo, const void* bias,
+                              const void* aux, long long ld_aux, void* out2, long long ld_out2, float* colsum,
+                              float* ws, long long ws_elems, int ksplit, void* stream) {
+  return chimera::capi::guarded([&] {
+    chimera::gemm::EpiArgs ep;
+    ep.out = out;
+    ep.ldo = ldo;
+    ep.bias = static_cast<const __nv_bfloat16*>(bias);
+    ep.aux = static_cast<const __nv_bfloat16*>(aux);
+    ep.ld_aux = ld_aux;
+    ep.out2 = static_cast<__nv_bfloat16*>(out2);
+    ep.ld_out2 = ld_out2;
+    ep.colsum = colsum;
+    ep.ws = ws;
+    ep.ws_elems = ws_elems;
+    ep.ksplit = ksplit;  // honoured by gemm() as the forced slice count when > 1
     chimera::gemm::gemm(static_cast<chimera::gemm::Epi>(epi), a_mn != 0, b_mn != 0, M, N, K,
                         static_cast<const __nv_bfloat16*>(A), lda, static_cast<const __nv_bfloat16*>(B),
                         ldb, ep, static_cast<cudaStream_t>(stream));

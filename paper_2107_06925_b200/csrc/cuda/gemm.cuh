@@ -26,6 +26,13 @@ struct EpiArgs {
   long long ld_out2 = 0;
   float* colsum = nullptr;  // kGeluBwd: colsum[n] += sum_m out[m][n] (the fused bias gradient)
   bool atomic_acc = false;  // kAccF32: always accumulate atomically (outf shared by concurrent GEMMs)
+  // Split-K workspace for the bf16 epilogues (fp32, zero-filled, >= M*N elements, owned
+  // by the calling stream).  When present, problems whose output tiles cannot fill the
+  // machine run as K-slices reduce-added into it, then one finalize pass applies the
+  // epilogue and re-zeroes the workspace.  Null: never split a bf16 epilogue.
+  float* ws = nullptr;
+  long long ws_elems = 0;
+  int ksplit = 0;  // internal: slice count chosen by gemm() (0 = the kernels' own rule)
 };
 
 // Operand layouts: A(m,k) is A[m*lda+k] when !a_mn (K-major) else A[k*lda+m];

@@ -92,6 +92,8 @@ struct Stash {
 struct Scratch {
   bf16 *dx[3], *dx2[2], *du[2], *dqkv[2], *dh, *da;
   float* attn;
+  float* ws = nullptr;  // split-K workspace of the chain stream's bf16 GEMMs (gemm.cuh EpiArgs::ws)
+  long long ws_elems = 0;
   cudaStream_t side = nullptr;  // weight-gradient stream (== the rank stream when serialised)
   cudaEvent_t fork[4], join[3];
 };
@@ -188,6 +190,7 @@ struct Trainer::Impl {
   }
   int steps = 0;
   long long launches_per_step = 0;
+  long long graph_kernels = 0;  // kernel nodes of the captured iteration graph
   // issue state of the open iteration (begin_iteration .. end_iteration)
   struct IterState {
     bool open = false;
@@ -395,6 +398,13 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
     sc.dh = I.arena.alloc<bf16>((size_t)M * h);
     sc.da = I.arena.alloc<bf16>((size_t)M * h);
     sc.attn = I.arena.alloc<float>(ops::attn_bwd_scratch_floats(I.B, shape.seq, H));
+    // split-K workspace: the widest chain GEMM output (fused forward pairs: 2M rows)
+    sc.ws_elems = (long long)(I.fd_fuse ? 2 : 1) * M * std::max(3 * h, f);
+    if (std::getenv("CK_GEMM_SPLIT_BF16") && std::string(std::getenv("CK_GEMM_SPLIT_BF16")) == "0") sc.ws_elems = 0;
+    if (sc.ws_elems) {
+      sc.ws = I.arena.alloc<float>((size_t)sc.ws_elems);
+      CK_CUDA(cudaMemset(sc.ws, 0, (size_t)sc.ws_elems * sizeof(float)));
+    }
     cudaStream_t s;
     // CK_SERIALIZE=1: every rank issues on one stream (debug: rules out cross-stream races)
     const bool serial = std::getenv("CK_SERIALIZE") != nullptr;
@@ -506,6 +516,13 @@ EpiArgs epi(void* out, long long ldo, const bf16* bias = nullptr, const bf16* au
   return e;
 }
 
+// A bf16-epilogue GEMM on a rank's chain stream may split K through that stream's workspace.
+EpiArgs on_chain(EpiArgs e, const Scratch& sc) {
+  e.ws = sc.ws;
+  e.ws_elems = sc.ws_elems;
+  return e;
+}
+
 }  // namespace
 
 void Trainer::forward_task(int rank, int p, int mb, int s) {
@@ -601,21 +618,22 @@ void Trainer::stage_forward(int rank, int s, Stash& X, const bf16* x, bf16* out_
   cudaStream_t st = I.stream_of(rank);
   const StageLayout& L = I.stages.at(s).L;
   const bf16* w = I.stages.at(s).w16;
+  const Scratch& sc = I.scratch[rank - I.first];
   for (int l = 0; l < L.n_layers; ++l) {
     const LayerOffsets& o = L.layers[l];
     LayerStash& A = X.layers[l];
     bf16* xo = (l + 1 < L.n_layers) ? A.xo : out_final;
     ops::layernorm_fwd(x, w + o.ln1_g, w + o.ln1_b, A.h1, A.mean1, A.rstd1, M, h, st);
     gemm::gemm(gemm::kStoreBF16, false, false, M, 3 * h, h, A.h1, h, w + o.w_qkv, h,
-               epi(A.qkv, 3 * h, w + o.b_qkv), st);
+               on_chain(epi(A.qkv, 3 * h, w + o.b_qkv), sc), st);
     ops::attn_fwd_tc(A.qkv, A.a, A.lse, Bq, m.seq, H, m.causal, st);
     gemm::gemm(gemm::kBiasResid, false, false, M, h, h, A.a, h, w + o.w_o, h,
-               epi(A.x2, h, w + o.b_o, x, h), st);
+               on_chain(epi(A.x2, h, w + o.b_o, x, h), sc), st);
     ops::layernorm_fwd(A.x2, w + o.ln2_g, w + o.ln2_b, A.h2, A.mean2, A.rstd2, M, h, st);
     gemm::gemm(gemm::kBiasGelu, false, false, M, f, h, A.h2, h, w + o.w_fc1, h,
-               epi(A.u, f, w + o.b_fc1, nullptr, 0, A.g, f), st);
+               on_chain(epi(A.u, f, w + o.b_fc1, nullptr, 0, A.g, f), sc), st);
     gemm::gemm(gemm::kBiasResid, false, false, M, h, f, A.g, f, w + o.w_fc2, f,
-               epi(xo, h, w + o.b_fc2, A.x2, h), st);
+               on_chain(epi(xo, h, w + o.b_fc2, A.x2, h), sc), st);
     x = xo;
     I.launches_per_step += 7;
   }
@@ -679,7 +697,7 @@ void Trainer::backward_task(int rank, int p, int mb, int s) {
                epi(gw + L.w_head, h), ws);
     side_done(L.n_layers);
     gemm::gemm(gemm::kStoreBF16, false, true, M, h, m.vocab_padded, X.logits, m.vocab_padded, w + L.w_head, h,
-               epi(sc.dh, h), st);
+               on_chain(epi(sc.dh, h), sc), st);
     bf16* d = sc.dx[L.n_layers % 3];
     // (+ the top layer's FC2 bias gradient: column sums of this dx)
     ops::layernorm_bwd(sc.dh, X.xfinal, X.meanf, X.rstdf, w + L.lnf_g, nullptr, d, gw + L.lnf_g,
@@ -714,24 +732,25 @@ void Trainer::backward_task(int rank, int p, int mb, int s) {
     }
     gemm::gemm(gemm::kAccF32, true, true, h, f, M, dxo, h, A.g, f, epi(gw + o.w_fc2, f), ws);
     {
-      EpiArgs e = epi(du, f, nullptr, A.u, f);
+      EpiArgs e = on_chain(epi(du, f, nullptr, A.u, f), sc);
       e.colsum = gw + o.b_fc1;
       gemm::gemm(gemm::kGeluBwd, false, true, M, f, h, dxo, h, w + o.w_fc2, f, e, st);
     }
     fork();
     gemm::gemm(gemm::kAccF32, true, true, f, h, M, du, f, A.h2, h, epi(gw + o.w_fc1, h), ws);
-    gemm::gemm(gemm::kStoreBF16, false, true, M, h, f, du, f, w + o.w_fc1, h, epi(sc.dh, h), st);
+    gemm::gemm(gemm::kStoreBF16, false, true, M, h, f, du, f, w + o.w_fc1, h, on_chain(epi(sc.dh, h), sc), st);
     ops::layernorm_bwd(sc.dh, A.x2, A.mean2, A.rstd2, w + o.ln2_g, dxo, dx2, gw + o.ln2_g, gw + o.ln2_b,
                        gw + o.b_o, M, h, st);
     // attention
     fork();
     gemm::gemm(gemm::kAccF32, true, true, h, h, M, dx2, h, A.a, h, epi(gw + o.w_o, h), ws);
-    gemm::gemm(gemm::kStoreBF16, false, true, M, h, h, dx2, h, w + o.w_o, h, epi(sc.da, h), st);
+    gemm::gemm(gemm::kStoreBF16, false, true, M, h, h, dx2, h, w + o.w_o, h, on_chain(epi(sc.da, h), sc), st);
     ops::attn_bwd_tc(A.qkv, A.a, sc.da, A.lse, dqkv, sc.attn, I.B, m.seq, H, m.causal, st, gw + o.b_qkv);
     fork();
     gemm::gemm(gemm::kAccF32, true, true, 3 * h, h, M, dqkv, 3 * h, A.h1, h, epi(gw + o.w_qkv, h), ws);
     side_done(l);
-    gemm::gemm(gemm::kStoreBF16, false, true, M, h, 3 * h, dqkv, 3 * h, w + o.w_qkv, h, epi(sc.dh, h), st);
+    gemm::gemm(gemm::kStoreBF16, false, true, M, h, 3 * h, dqkv, 3 * h, w + o.w_qkv, h, on_chain(epi(sc.dh, h), sc),
+               st);
     ops::layernorm_bwd(sc.dh, xin, A.mean1, A.rstd1, w + o.ln1_g, dx2, dxin, gw + o.ln1_g, gw + o.ln1_b,
                        l > 0 ? gw + L.layers[l - 1].b_fc2 : nullptr, M, h, st);
     dxo = dxin;
@@ -1051,6 +1070,19 @@ float Trainer::step() {
       issue_iteration();
       CK_CUDA(cudaStreamEndCapture(I.main_stream, &I.graph));
       CK_CUDA(cudaGraphInstantiate(&I.graph_exec, I.graph, 0));
+      // launches per step = the kernel nodes of the captured iteration (the issue-time
+      // count above is an estimate: split-K finalize passes, NCCL kernels...)
+      size_t n = 0;
+      CK_CUDA(cudaGraphGetNodes(I.graph, nullptr, &n));
+      std::vector<cudaGraphNode_t> nodes(n);
+      CK_CUDA(cudaGraphGetNodes(I.graph, nodes.data(), &n));
+      long long kernels = 0;
+      for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType t;
+        CK_CUDA(cudaGraphNodeGetType(nd, &t));
+        kernels += t == cudaGraphNodeTypeKernel;
+      }
+      I.graph_kernels = kernels;
     }
     CK_CUDA(cudaGraphLaunch(I.graph_exec, I.main_stream));
   }
@@ -1298,7 +1330,7 @@ std::string Trainer::stats_json() const {
     sb.push(Value::integer(bytes * (long long)I.peak_live[k]));
   }
   j.set("peak_stash_bytes_per_rank", std::move(sb));
-  j.set("launches_per_step", Value::integer(I.launches_per_step));
+  j.set("launches_per_step", Value::integer(I.graph_exec ? I.graph_kernels : I.launches_per_step));
   j.set("graph", Value::boolean(I.graph_exec != nullptr));
   j.set("steps", Value::integer(I.steps));
   return json::dump(j, -1);

@@ -14,6 +14,8 @@ _lib.register("ck_gemm_bf16", _i, [_i, _i, _i, _i, _i, _i, _vp, _ll, _vp, _ll, _
                                    _vp, _ll, _vp])
 _lib.register("ck_gemm_bf16_ex", _i, [_i, _i, _i, _i, _i, _i, _vp, _ll, _vp, _ll, _vp, _ll, _vp, _vp, _ll,
                                       _vp, _ll, _vp, _vp])
+_lib.register("ck_gemm_bf16_split", _i, [_i, _i, _i, _i, _i, _i, _vp, _ll, _vp, _ll, _vp, _ll, _vp, _vp, _ll,
+                                         _vp, _ll, _vp, _vp, _ll, _i, _vp])
 
 EPI = {"bf16": 0, "bias_gelu": 1, "bias_resid": 2, "gelu_bwd": 3, "acc_f32": 4, "f32": 5}
 
@@ -29,7 +31,7 @@ def _stream(stream):
 
 
 def gemm(epi, A, B, out, *, a_mn=False, b_mn=False, M=None, N=None, K=None, bias=None, aux=None,
-         out2=None, stream=None, colsum=None):
+         out2=None, stream=None, colsum=None, ws=None, ksplit=0):
     """D[m,n] = sum_k A(m,k) B(n,k) with A/B K-major ([M,K]/[N,K]) or MN-major ([K,M]/[K,N]).
     `colsum` (fp32 [N], gelu_bwd only) accumulates the column sums of the bf16 output."""
     M = M if M is not None else (A.shape[1] if a_mn else A.shape[0])
@@ -38,7 +40,9 @@ def gemm(epi, A, B, out, *, a_mn=False, b_mn=False, M=None, N=None, K=None, bias
     args = (EPI[epi], int(a_mn), int(b_mn), M, N, K, _p(A), A.stride(0), _p(B), B.stride(0), _p(out),
             out.stride(0), _p(bias), _p(aux), aux.stride(0) if aux is not None else 0, _p(out2),
             out2.stride(0) if out2 is not None else 0)
-    if colsum is None:
+    if ws is not None:  # split-K workspace route (fp32, zero-filled, >= M*N)
+        check(lib().ck_gemm_bf16_split(*args, _p(colsum), _p(ws), ws.numel(), int(ksplit), _stream(stream)))
+    elif colsum is None:
         check(lib().ck_gemm_bf16(*args, _stream(stream)))
     else:
         check(lib().ck_gemm_bf16_ex(*args, _p(colsum), _stream(stream)))

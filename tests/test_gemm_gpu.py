@@ -95,3 +95,41 @@ def test_gelu_bwd_colsum():
     torch.cuda.synchronize()
     assert torch.equal(d, d0)
     assert _rel(cs, d.float().sum(0) + 0.25) < 1e-5
+
+
+# split-K through a workspace for the bf16 epilogues (the small-M stage shapes of
+# GPT-2 1.3B: N = h with a deep K) -- forced slice counts and the wave model's own choice
+SPLIT_SHAPES = [(632, 1280, 5120), (632, 1280, 3840), (1264, 1280, 5120), (632, 1280, 50304), (300, 264, 1000)]
+
+
+@pytest.mark.parametrize("M,N,K", SPLIT_SHAPES)
+@pytest.mark.parametrize("ks", [0, 2, 3, 4])
+def test_split_k_bf16_epilogues(M, N, K, ks):
+    ws = torch.zeros(M * max(N, K), device="cuda")
+    A, B = _rand(M, K), _rand(N, K)
+    bias = _rand(N)
+    ref = A.float() @ B.float().t() + bias.float()
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    ck.gemm("bf16", A, B, out, bias=bias, ws=ws, ksplit=ks)
+    assert _rel(out, ref) < 8e-3
+    resid = _rand(M, N)
+    ck.gemm("bias_resid", A, B, out, bias=bias, aux=resid, ws=ws, ksplit=ks)
+    assert _rel(out, ref + resid.float()) < 8e-3
+    g = torch.empty_like(out)
+    ck.gemm("bias_gelu", A, B, out, bias=bias, out2=g, ws=ws, ksplit=ks)
+    assert _rel(out, ref) < 8e-3
+    assert _rel(g, torch.nn.functional.gelu(out.float(), approximate="tanh")) < 8e-3
+    # dgrad layout (B MN-major) with gelu' and the fused column sums
+    Wt = _rand(K, N)
+    dY = _rand(M, K)
+    U = _rand(M, N)
+    d = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    cs = torch.zeros(N, device="cuda")
+    ck.gemm("gelu_bwd", dY, Wt, d, b_mn=True, aux=U, colsum=cs, ws=ws, ksplit=ks)
+    u = U.float().requires_grad_()
+    gl = torch.nn.functional.gelu(u, approximate="tanh")
+    (gp,) = torch.autograd.grad(gl.sum(), u)
+    assert _rel(d, (dY.float() @ Wt.float()) * gp) < 8e-3
+    assert _rel(cs, d.float().sum(0)) < 1e-4
+    torch.cuda.synchronize()
+    assert int(torch.count_nonzero(ws)) == 0  # the finalize pass leaves the workspace zeroed

@@ -1,0 +1,93 @@
+"""GPT stage executor vs the numpy fp64 oracle at the BENCHMARKED widths.
+
+Fixtures (tests/golden/gpt_wide.npz) are frozen on the CPU by
+oracle/make_gpt_wide_fixtures.py from oracle/gpt_oracle.py (the reference Engine
+semantics restated for a transformer); the GPU box only compares:
+  * GPT-2 medium width (h=1024, 16 heads, s=1024, V=50257), Chimera D=4 N=4 W=2;
+  * GPT-2 1.3B width (h=1280, 20 heads, s=632 -- not a multiple of 128 --, V=50257),
+    Chimera D=4 N=8 forward doubling + recompute (1264-row fused forward pairs),
+    uneven stage_layers (2, 1, 2, 1);
+  * Bert-48 width (bidirectional, s=128, V=30522), Chimera D=8 N=8.
+Per stage and PER TENSOR (LN gains/biases and every bias are checked on
+their own, so a zeroed or misrouted small gradient cannot hide in a stage norm):
+  * gradient norm within NORM_TOL of the oracle's;
+  * on the fixed index sample: cosine >= COS_MIN and ||g - g_ref|| / ||g_ref|| <= REL_TOL;
+and the mean loss within LOSS_TOL.  The gradient is recovered from one SGD step at
+lr = 64 (a power of two: (w - w') / lr is exact up to the fp32 rounding of w').
+Tolerances are the bf16-operand / fp32-accumulate bounds of SURVEY.md §8(c),
+tightened to the measured values (see profiles/ r02 parity summary).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle.make_gpt_wide_fixtures import CASES
+from paper_2107_06925_b200 import pipesim as P
+from paper_2107_06925_b200.gpt import GPTShape, Trainer
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "gpt_wide.npz")
+LR = 64.0
+LOSS_TOL = 5e-3
+NORM_TOL = 3e-2
+COS_MIN = 0.999
+REL_TOL = 5e-2
+
+
+@pytest.fixture(scope="module")
+def gold():
+    if not os.path.exists(GOLD):
+        pytest.skip("tests/golden/gpt_wide.npz not generated")
+    return dict(np.load(GOLD))
+
+
+@pytest.mark.parametrize("name", ["medium", "xl", "bert"])
+def test_wide_iteration_vs_oracle(gold, name):
+    if f"{name}/loss" not in gold:
+        pytest.skip(f"fixture {name} absent")
+    sh, cf = CASES[name]
+    shape = GPTShape(**sh)
+    cfg = P.PipelineConfig(**cf)
+    tr = Trainer(shape, cfg, lr=LR)
+    tr.init_params(0)
+    before = {st["stage"]: tr.get_params(st["stage"]).astype(np.float64) for st in tr.layout}
+    tr.set_batch(gold[f"{name}/tokens"], gold[f"{name}/labels"])
+    loss = tr.step()
+    ref_loss = float(gold[f"{name}/loss"][0])
+    report = {"case": name, "loss": loss, "ref_loss": ref_loss, "loss_rel": abs(loss - ref_loss) / abs(ref_loss),
+              "worst": {}}
+    bad = []
+    for st in tr.layout:
+        s = st["stage"]
+        g = (before[s] - tr.get_params(s).astype(np.float64)) / LR
+        for t in st["tensors"]:
+            key = f"{name}/s{s}/{t['name']}"
+            gt = g[t["offset"]:t["offset"] + t["rows"] * t["cols"]]
+            nref = float(gold[key + "/norm"][0])
+            idx, ref = gold[key + "/idx"], gold[key + "/val"]
+            mine = gt[idx]
+            nr = np.linalg.norm(ref)
+            if nref == 0.0:
+                if np.linalg.norm(gt) != 0.0:
+                    bad.append((key, "nonzero gradient where the oracle's is zero"))
+                continue
+            norm_err = abs(np.linalg.norm(gt) / nref - 1.0)
+            cos = float(mine @ ref / (np.linalg.norm(mine) * nr)) if nr > 0 and np.linalg.norm(mine) > 0 else 0.0
+            rel = float(np.linalg.norm(mine - ref) / nr) if nr > 0 else 0.0
+            for k, v in (("norm_err", norm_err), ("rel", rel), ("1-cos", 1.0 - cos)):
+                w = report["worst"].get(k)
+                if w is None or v > w[1]:
+                    report["worst"][k] = (key, v)
+            if norm_err > NORM_TOL or (nr > 0 and (cos < COS_MIN or rel > REL_TOL)):
+                bad.append((key, dict(norm_err=norm_err, cos=cos, rel=rel)))
+    stats = tr.stats()
+    tr.close()
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open(os.path.join("gpurun_out", "parity_wide.jsonl"), "a") as fh:
+        fh.write(json.dumps(report) + "\n")
+    assert report["loss_rel"] <= LOSS_TOL, report
+    assert not bad, bad[:10]
+    assert stats["peak_stash_per_rank"] == list(gold[f"{name}/peak"]) * cfg.W
