@@ -34,6 +34,13 @@ METRIC = "GPT-2 seqs/sec at D=8 on 8×B200; bubble ratio vs (D-2)/(2N+D-2)"
 CONFIGS = {
     "gpt2-medium": ("gpt2-medium", dict(scheme="chimera", D=4, W=2, N=4, B=4, f=1, scaling="direct"),
                     "GPT-2 medium Chimera D=4 N=4 W=2 B=4 (BASELINE configs[1])"),
+    # one pipeline (W=1) of configs[1]'s model: with --gpus 4 every logical rank owns a GPU,
+    # so the per-worker bubble is observable (closed form 1/4 at N=4, 1/9 at N=8)
+    "gpt2-medium-d4": ("gpt2-medium", dict(scheme="chimera", D=4, W=1, N=4, B=4, f=1, scaling="direct"),
+                       "GPT-2 medium Chimera D=4 N=4 W=1 B=4 (configs[1] model, one pipeline pair)"),
+    "gpt2-medium-d4-n8bh": ("gpt2-medium", dict(scheme="chimera", D=4, W=1, N=8, B=4, f=1,
+                                                scaling="backward-halving"),
+                            "GPT-2 medium Chimera D=4 N=8 W=1 B=4 backward-halving (configs[1] model)"),
     "bert48": ("bert48", dict(scheme="chimera", D=8, W=1, N=8, B=8, f=1, scaling="direct"),
                "Bert-48 shape (bidirectional, dense MLM head) Chimera D=8 N=8 B=8 (BASELINE configs[2])"),
     "gpt2-1.3b": ("gpt2-1.3b", dict(scheme="chimera", D=8, W=1, N=32, B=2, f=1, scaling="forward-doubling"),
@@ -239,49 +246,56 @@ def roofline_shapes(shape, cfg):
 def gemm_roofline(stream_handle, peak_tflops, shape=None, cfg=None, workspace=True):
     """Live CUDA-event timing of the stage GEMMs (the dominant kernel family) at the
     workload's shapes as the step runs them (roofline_shapes), on the trainer's device,
-    with the split-K workspace the trainer's chain streams use:
-    achieved = sum_i w_i 2 M N K / sum_i w_i t_i."""
+    with the split-K workspace the trainer's chain streams use, each shape's launches
+    replayed from a CUDA graph like the step's: achieved = sum_i w_i 2 M N K / sum_i w_i t_i."""
     import torch
     from paper_2107_06925_b200 import kernels as ck
     from paper_2107_06925_b200.gpt import PRESETS
     shape = shape or PRESETS[SHAPE_NAME]
     cfg = cfg or CFG
     shapes = roofline_shapes(shape, cfg)
-    st = torch.cuda.ExternalStream(stream_handle) if stream_handle else torch.cuda.current_stream()
-    tot_flops, tot_ms, wsum, n_launch = 0.0, 0.0, 0.0, 0
+    tot_flops, tot_ms, wsum = 0.0, 0.0, 0.0
     rows = []
-    with torch.cuda.stream(st):
-        ws = torch.zeros(max(Mm * N for (Mm, N, K, a, b, w) in shapes if not (a and b)), device="cuda") \
-            if workspace else None
-        bufs = []
-        for (Mm, N, K, a, b, w) in shapes:
-            A = torch.randn((K, Mm) if a else (Mm, K), device="cuda").bfloat16()
-            B = torch.randn((K, N) if b else (N, K), device="cuda").bfloat16()
-            out = torch.zeros(Mm, N, device="cuda", dtype=torch.float32 if (a and b) else torch.bfloat16)
-            bufs.append((Mm, N, K, a, b, w, A, B, out))
+    ws = torch.zeros(max(Mm * N for (Mm, N, K, a, b, w) in shapes if not (a and b)), device="cuda") \
+        if workspace else None
+    side = torch.cuda.Stream()
+    reps = 20
+    for (Mm, N, K, a, b, w) in shapes:
+        A = torch.randn((K, Mm) if a else (Mm, K), device="cuda").bfloat16()
+        B = torch.randn((K, N) if b else (N, K), device="cuda").bfloat16()
+        out = torch.zeros(Mm, N, device="cuda", dtype=torch.float32 if (a and b) else torch.bfloat16)
 
-        def run(Mm, N, K, a, b, A, B, out):
+        def run():
             ck.gemm("acc_f32" if (a and b) else "bf16", A, B, out, a_mn=bool(a), b_mn=bool(b),
-                    ws=None if (a and b) else ws, stream=st)
-        for it in range(2):
-            for (Mm, N, K, a, b, w, A, B, out) in bufs:
-                run(Mm, N, K, a, b, A, B, out)
-        reps = 20
-        for (Mm, N, K, a, b, w, A, B, out) in bufs:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
+                    ws=None if (a and b) else ws, stream=torch.cuda.current_stream())
+        # the step replays its kernels from a CUDA graph: time the same way (no host
+        # launch cost), `reps` launches captured back to back, CUDA events around replays
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                run()
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
             for _ in range(reps):
-                run(Mm, N, K, a, b, A, B, out)
-            e1.record(st)
-            e1.synchronize()
-            ms = e0.elapsed_time(e1) / reps
-            fl = 2.0 * Mm * N * K
-            tot_ms += w * ms
-            tot_flops += w * fl
-            wsum += w
-            rows.append({"shape": [Mm, N, K, a, b], "weight": round(w, 4), "us": round(ms * 1e3, 2),
-                         "tflops": round(fl / (ms * 1e-3) / 1e12, 1)})
-        del ws
+                run()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            g.replay()
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / (3 * reps)
+        fl = 2.0 * Mm * N * K
+        tot_ms += w * ms
+        tot_flops += w * fl
+        wsum += w
+        rows.append({"shape": [Mm, N, K, a, b], "weight": round(w, 4), "us": round(ms * 1e3, 2),
+                     "tflops": round(fl / (ms * 1e-3) / 1e12, 1)})
+        del g, A, B, out
+    del ws
     achieved = tot_flops / (tot_ms * 1e-3) / 1e12
     # DRAM bytes per launch of the same shapes from the committed `ncu --set full`
     # capture (scripts/roofline_shapes.py --config ...); null when not captured
@@ -521,6 +535,47 @@ def main():
     ab = measure_alpha_beta(world) if world > 1 else (0.0, 0.0)
     comm = comm_report(world, 2 * CFG["B"] * shape.seq * shape.hidden) if world > 1 else None
 
+    # ---- the measured B200 CostProfile, computed identically on every process (from the
+    # gathered task spans) so the sync plan built on it is the same everywhere
+    from fractions import Fraction
+    # task compute time = span minus the stream's waits for incoming messages
+    fwd = [t["end_ms"] - t["start_ms"] - t.get("stall_ms", 0.0) for t in tasks if t["kind"] == "Forward"]
+    bwd = [t["end_ms"] - t["start_ms"] - t.get("stall_ms", 0.0) for t in tasks if t["kind"] == "Backward"]
+    ratio = (sum(bwd) / len(bwd)) / (sum(fwd) / len(fwd))
+    l_grad = 4.0 * max(st["numel"] for st in tr.layout)  # fp32 gradient of the largest held stage
+    if world > 1:
+        t = torch.tensor([l_grad], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        l_grad = float(t)
+    prof_b200 = P.CostProfile(F_t=sum(fwd) / len(fwd), backward_ratio=float(Fraction(ratio).limit_denominator(16)),
+                              alpha=ab[0], beta=ab[1], L_grad=l_grad,
+                              L_act=2.0 * CFG["B"] * shape.seq * shape.hidden)
+
+    # ---- gradient-sync policies on the measured profile (dessim eager rule), one rank per
+    # GPU: the paper's eager-sync-opt vs eager-sync vs end-of-iteration
+    sync_ab = None
+    if world > 1:
+        tr.set_cost_profile(prof_b200)
+        sync_ab = {}
+        for pol in ("end-of-iteration", "eager-sync", "eager-sync-opt"):
+            tr.set_sync_policy(pol)
+            for _ in range(2):
+                tr.step()
+            dist.barrier()
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            for _ in range(args.steps):
+                tr.launch()
+            g1.record(stream)
+            torch.cuda.synchronize()
+            t = torch.tensor([g0.elapsed_time(g1) / args.steps])
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sync_ab[pol] = {"ms_per_step": round(float(t), 3)}
+            if pol == "eager-sync-opt":
+                sync_ab[pol]["eager_stages"] = [e["stage"] for e in tr.sync_plan()["order"] if e["eager"]]
+        tr.set_sync_policy("eager-sync")
+
     stats = tr.stats()
     launches = int(stats["launches_per_step"] * args.steps)
     if world > 1:  # the loss is summed over the processes holding last stages
@@ -539,11 +594,7 @@ def main():
     if rank == 0:
         sched = tr.schedule_text
         bub = P.bubble_ratio(sched)
-        from fractions import Fraction
         from paper_2107_06925_b200.gpt import measured_bubble, timeline_json
-        fwd = [t["end_ms"] - t["start_ms"] for t in tasks if t["kind"] == "Forward"]
-        bwd = [t["end_ms"] - t["start_ms"] for t in tasks if t["kind"] == "Backward"]
-        ratio = (sum(bwd) / len(bwd)) / (sum(fwd) / len(fwd))
         prof_m = P.CostProfile(backward_ratio=float(Fraction(ratio).limit_denominator(16)))
         bub_at_ratio = P.bubble_ratio(P.generate_json(cfg, prof_m, -1), prof_m)
         one_rank_per_gpu = per == 1
@@ -557,13 +608,31 @@ def main():
                               (".txt", P.gantt_timeline(tl, ft)), (".sched.json", timeline_json({"tasks": tasks}, sched))):
                 with open(pre + ext, "w") as fh:
                     fh.write(text)
+        # dessim::simulate (proj/src/dessim.cpp:60-181) on the measured F_t, B/F, alpha, beta:
+        # per-worker idle / compute span, averaged -- the simulated counterpart of `measured`
+        sim = P.simulate(sched, prof_b200, "eager-sync")
+        span = sim["compute_makespan"]
+        dessim_bubble = round(sum(sim["per_worker_idle"]) / len(sim["per_worker_idle"]) / span, 4) if span else None
         mp = P.memory_profile(sched)
         # Eq. 1 (perfmodel::predict_T, perfmodel.cpp:157) on the measured B200 CostProfile
-        l_grad = 4.0 * max(st["numel"] for st in tr.layout)  # fp32 gradient of the largest held stage
-        prof_b200 = P.CostProfile(F_t=sum(fwd) / len(fwd), backward_ratio=float(Fraction(ratio).limit_denominator(16)),
-                                  alpha=ab[0], beta=ab[1], L_grad=l_grad,
-                                  L_act=2.0 * CFG["B"] * shape.seq * shape.hidden)
         pred = P.predict_T(cfg, prof_b200)
+        # perfmodel::plan (perfmodel.cpp:225-298) on the same profile with the measured
+        # memory terms: which (W, D, B) it would pick for 2, 4, 8 GPUs at this mini-batch
+        plans = None
+        try:
+            acts = [a for a in stats["peak_stash_per_rank"] if a] or [1]
+            sbytes = [b for b in stats["peak_stash_bytes_per_rank"] if b] or [0]
+            m_a = max(sbytes) / max(acts) / CFG["B"] if max(sbytes) else 0.0
+            mprof = P.CostProfile(**{**prof_b200.__dict__, "M_theta": 10.0 * l_grad / 4.0, "M_a": m_a,
+                                     "M_a_ckpt": 2.0 * shape.seq * shape.hidden, "mem_capacity": 178e9,
+                                     "embed_surcharge": True})
+            plans = {}
+            for Pn in (2, 4, 8):
+                ents = P.plan(Pn, n_seq, mprof, "chimera")
+                plans[str(Pn)] = [{k: e[k] for k in ("W", "D", "B", "N", "scaling", "recompute")} |
+                                  {"T_predicted_ms": round(e["T_predicted"], 3)} for e in ents[:3]]
+        except Exception as e:  # the planner may find nothing feasible
+            plans = {"error": str(e)[:200]}
         rl = gemm_roofline(tr.stream_handle(), peak, shape, CFG)
         flops_seq = shape.flops_per_seq()
         cpu = None if args.no_cpu_baseline else cpu_port_sample(shape)
@@ -591,6 +660,7 @@ def main():
                        "reference_schedule_at_B/F=2": str(bub),
                        "measured_B/F": round(ratio, 3),
                        "reference_schedule_at_measured_B/F": str(bub_at_ratio),
+                       "dessim_at_measured_profile": dessim_bubble,
                        "note": (None if one_rank_per_gpu else
                                 f"{per} logical ranks share each GPU: per-rank bubble not observable")},
             "perfmodel": {"predicted_ms": round(pred, 3), "measured_ms": round(ms, 3),
@@ -603,6 +673,8 @@ def main():
                                    "p2p term: alpha + beta * L_act with the allreduce fit (upper bound; "
                                    "stage outputs are stored into the peer slot by the producing kernel)")},
             "comm": comm,
+            "sync_policies": sync_ab,
+            "plan": plans,
             "act_counts_per_worker": mp["act_counts"],
             "peak_stash_per_rank": stats["peak_stash_per_rank"],
             "peak_stash_bytes_per_rank": stats["peak_stash_bytes_per_rank"],

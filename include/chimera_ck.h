@@ -111,11 +111,12 @@ CK_API int ck_toy_sequential_sgd(const int* dims, int n_dims, const double* para
  * 5 fp32 store.  a_mn/b_mn select MN-major operands (see cuda/gemm.cuh). */
 /* Split-K variant for the bf16 epilogues: ws = fp32 workspace (zero-filled, >= M*N,
  * left zeroed); K-slices reduce-add into it, one finalize pass applies the epilogue.
- * ksplit > 1 forces the slice count, 0 lets the wave model decide (it may not split). */
+ * ksplit > 1 forces the slice count, 0 lets the wave model decide (it may not split);
+ * tile >= 0 forces the tile (0 CTA pair 256x256, 256 / 128 / 64: single CTA 128 x tile). */
 CK_API int ck_gemm_bf16_split(int epi, int a_mn, int b_mn, int M, int N, int K, const void* A, long long lda,
                               const void* B, long long ldb, void* out, long long ldo, const void* bias,
                               const void* aux, long long ld_aux, void* out2, long long ld_out2, float* colsum,
-                              float* ws, long long ws_elems, int ksplit, void* stream);
+                              float* ws, long long ws_elems, int ksplit, int tile, void* stream);
 CK_API int ck_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, const void* A,
                         long long lda, const void* B, long long ldb, void* out, long long ldo,
                         const void* bias, const void* aux, long long ld_aux, void* out2,
@@ -216,6 +217,20 @@ CK_API int ck_gpt_set_graph(ck_gpt* h, int on);
  * comm stream as soon as its last local backward is issued), 2 eager-sync-opt (eager
  * iff the reference's interior-slack rule marks every holder eager). */
 CK_API int ck_gpt_set_sync_policy(ck_gpt* h, int policy);
+/* The CostProfile (pipesim JSON) the gradient-sync plan is computed on: dessim::simulate
+ * (proj/src/dessim.cpp:60-135) decides eager-sync-opt per stage and orders the stage
+ * collectives.  Every process of a run must pass identical values (the collective order
+ * must agree).  Drops the captured iteration graph. */
+CK_API int ck_gpt_set_cost_profile(ck_gpt* h, const char* profile_json);
+/* {"policy", "profile", "order": [{"stage", "eager", "planned_start"}...]} */
+CK_API int ck_gpt_sync_plan(ck_gpt* h, char** out_json);
+/* Stage optimizer (beyond the reference's SGD): kind 0 SGD (default,
+ * proj/src/oracle.cpp:283-299), 1 AdamW (decoupled weight decay; lr = the trainer's).
+ * zero != 0: ZeRO-1 -- each process holding a stage keeps 1/R of the AdamW moments and
+ * updates that share (reduce-scatter + fp32 all-gather over the stage communicator).
+ * Multi-process: call after connect. */
+CK_API int ck_gpt_set_optimizer(ck_gpt* h, int kind, float beta1, float beta2, float eps, float weight_decay,
+                                int zero);
 CK_API void* ck_gpt_stream(ck_gpt* h);
 /* Multi-process (one process per GPU): export this process's 128 bytes of CUDA-IPC
  * handles, all-gather them (host side, e.g. torch.distributed), then connect with all

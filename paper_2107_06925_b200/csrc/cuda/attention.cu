@@ -374,14 +374,17 @@ __global__ void __launch_bounds__(128) k_attn_bwd(const bf16* __restrict__ qkv, 
 // dQ (fp32 accumulator, scaled by 1/sqrt(d)) -> bf16 Q-part of dqkv (L2-resident stream)
 // dQ (fp32 accumulator, scaled by 1/sqrt(d) here) -> the Q columns of dqkv in bf16; with
 // dbias, also the Q part of the QKV bias gradient: column sums of the bf16 values written.
-// threadIdx.x <-> 8-column group (blockDim.x = w / 8), threadIdx.y <-> one of 4 rows in
-// flight; CTAs stride over row quads.
+// threadIdx.x + blockIdx.y * blockDim.x <-> 8-column group (w / 8 of them, at most 256
+// per CTA: any head count), threadIdx.y <-> one of 4 rows in flight; CTAs stride over
+// row quads.
+constexpr int kDqGroups = 256;
 __global__ void __launch_bounds__(1024) k_dq_out(const float* __restrict__ acc, bf16* __restrict__ dqkv, int n_rows,
                                                  int H, float* __restrict__ dbias) {
   cuda::pdl_wait();
-  const int w = H * kHd, g = threadIdx.x;  // w is a multiple of 64
+  const int w = H * kHd, g = blockIdx.y * blockDim.x + threadIdx.x;  // w is a multiple of 64
+  const bool live = g < w / 8;
   float cs[8] = {};
-  for (int r = blockIdx.x * 4 + threadIdx.y; r < n_rows; r += gridDim.x * 4) {
+  for (int r = blockIdx.x * 4 + threadIdx.y; live && r < n_rows; r += gridDim.x * 4) {
     const float4* p = reinterpret_cast<const float4*>(acc + (long long)r * w) + 2 * g;
     const float4 a = __ldcs(p), b = __ldcs(p + 1);
     const uint4 q = make_uint4(pack(a.x * 0.125f, a.y * 0.125f), pack(a.z * 0.125f, a.w * 0.125f),
@@ -394,13 +397,14 @@ __global__ void __launch_bounds__(1024) k_dq_out(const float* __restrict__ acc, 
     }
   }
   if (dbias) {  // reduce the 4 row lanes in shared memory: one atomic set per CTA and column group
-    __shared__ float red[4][2048];
+    __shared__ float red[4][8 * kDqGroups];
+    const int l = threadIdx.x;
 #pragma unroll
-    for (int t = 0; t < 8; ++t) red[threadIdx.y][8 * g + t] = cs[t];
+    for (int t = 0; t < 8; ++t) red[threadIdx.y][8 * l + t] = cs[t];
     __syncthreads();
-    if (threadIdx.y == 0) {
+    if (threadIdx.y == 0 && live) {
 #pragma unroll
-      for (int t = 0; t < 8; ++t) cs[t] = red[0][8 * g + t] + red[1][8 * g + t] + red[2][8 * g + t] + red[3][8 * g + t];
+      for (int t = 0; t < 8; ++t) cs[t] = red[0][8 * l + t] + red[1][8 * l + t] + red[2][8 * l + t] + red[3][8 * l + t];
       atomicAdd(reinterpret_cast<float4*>(dbias + 8 * g), make_float4(cs[0], cs[1], cs[2], cs[3]));
       atomicAdd(reinterpret_cast<float4*>(dbias + 8 * g + 4), make_float4(cs[4], cs[5], cs[6], cs[7]));
     }
@@ -429,9 +433,12 @@ void attn_bwd_dot(const bf16* out, const bf16* dout, float* D, int M, int seq, i
 
 void attn_dq_out(const float* dq, bf16* dqkv, int M, int H, cudaStream_t st, float* dbias) {
   const int ng = H * kHd / 8;  // 8-column groups per row
-  if (ng * 4 > 1024) throw chimera::capi::InternalError("attention: H * 64 > 2048");
-  // one CTA per SM: the bias-gradient atomics are one set per CTA (contended addresses)
-  cuda::launch(k_dq_out, dim3(std::min((M + 3) / 4, cuda::kNumSMs)), dim3(ng, 4), 0, st, dq, dqkv, M, H, dbias);
+  if (dbias && (reinterpret_cast<uintptr_t>(dbias) % 16))
+    throw chimera::capi::InternalError("attention: the bias-gradient pointer must be 16-byte aligned");
+  const int bx = std::min(ng, kDqGroups), by = (ng + bx - 1) / bx;
+  // one CTA per SM (per column slab): the bias-gradient atomics are one set per CTA
+  cuda::launch(k_dq_out, dim3(std::min((M + 3) / 4, cuda::num_sms()), by), dim3(bx, 4), 0, st, dq, dqkv, M, H,
+               dbias);
   CK_CUDA(cudaGetLastError());
 }
 

@@ -796,7 +796,7 @@ void attn_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int seq, int H, 
   const long long ld = 3LL * H * kD;
   const CUtensorMap m = cuda::make_map_2d_bf16(qkv, ld, (long long)B * seq, ld, 64, 128);
   const int items = (seq + kQ - 1) / kQ * B * H;
-  const dim3 grid(std::min(items, 2 * cuda::kNumSMs));  // persistent: two CTAs per SM
+  const dim3 grid(std::min(items, 2 * cuda::num_sms()));  // persistent: two CTAs per SM
   static bool attr = false;
   if (!attr) {
     CK_CUDA(cudaFuncSetAttribute(k_attn_fwd_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
@@ -811,6 +811,8 @@ void attn_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int seq, int H, 
 // dqkv from dout on the tensor cores; `scratch` as attn_bwd (row dots D, fp32 dQ).
 void attn_bwd_tc(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, bf16* dqkv, float* scratch,
                  int B, int seq, int H, bool causal, cudaStream_t st, float* dbias) {
+  if (dbias && (reinterpret_cast<uintptr_t>(dbias) % 16))  // float4 atomics in the dQ pass
+    throw chimera::capi::InternalError("attention: the bias-gradient pointer must be 16-byte aligned");
   float* D = scratch;
   float* dq = scratch + size_t(B) * H * seq;
   const int M = B * seq;
@@ -827,7 +829,7 @@ void attn_bwd_tc(const bf16* qkv, const bf16* out, const bf16* dout, const float
     attr = true;
   }
   const int items = (seq + kKV - 1) / kKV * B * H;
-  const dim3 grid(std::min(items, cuda::kNumSMs));  // persistent: one CTA per SM
+  const dim3 grid(std::min(items, cuda::num_sms()));  // persistent: one CTA per SM
   cuda::launch(causal ? k_attn_bwd_tc<true> : k_attn_bwd_tc<false>, grid, dim3(kBwdThreads), kBwdSmem, st, mq, mo, mdq,
                mdqkv, lse, D, dqkv, seq, H, B * H, dbias);
   CK_CUDA(cudaGetLastError());

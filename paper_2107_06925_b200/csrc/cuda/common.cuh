@@ -21,7 +21,17 @@
 
 namespace chimera::cuda {
 
-constexpr int kNumSMs = 148;  // B200
+// SM count of the current device (148 on a full B200), queried once per device: the
+// persistent grids (GEMM tiles, attention items, LayerNorm backward, dQ pass) are sized
+// from it, so a part with fewer SMs or a MIG slice is neither over- nor under-subscribed.
+inline int num_sms() {
+  static int cache[64] = {};
+  int dev = 0;
+  CK_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) CK_CUDA(cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev));
+  return cache[dev];
+}
 
 inline int ceil_div(long long a, long long b) { return int((a + b - 1) / b); }
 

@@ -608,6 +608,7 @@ constexpr int kFinRows = 8;
 
 template <int EPI>
 __global__ void __launch_bounds__(128) k_splitk_finalize(float* __restrict__ ws, EpiArgs ep, int M, int N) {
+  cuda::pdl_wait();  // launched with programmatic serialisation: the slices must have landed
   const int col = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (col >= N) return;
   const int row0 = blockIdx.y * kFinRows;
@@ -943,9 +944,9 @@ void launch_pair(int M, int N, int K, const __nv_bfloat16* A, long long lda, con
   const CUtensorMap tb = B_MN ? cuda::make_map_2d_bf16(B, N, K, ldb, 64, BK)
                               : cuda::make_map_2d_bf16(B, K, N, ldb, 64, PBN / 2);
   const int base = ((M + 255) / 256) * ((N + PBN - 1) / PBN);
-  const int ks = split_k(EPI, base, cuda::kNumSMs / 2, K, ep.ksplit);
+  const int ks = split_k(EPI, base, cuda::num_sms() / 2, K, ep.ksplit);
   const int tiles = base * ks;
-  const int pairs = tiles < cuda::kNumSMs / 2 ? tiles : cuda::kNumSMs / 2;
+  const int pairs = tiles < cuda::num_sms() / 2 ? tiles : cuda::num_sms() / 2;
   CUtensorMap to, to2;
   if constexpr (EPI != kStoreF32) {
     if (tma_out<EPI>(ep, M, N, to, to2)) {
@@ -983,9 +984,9 @@ void launch(int M, int N, int K, const __nv_bfloat16* A, long long lda, const __
   const CUtensorMap tb = B_MN ? cuda::make_map_2d_bf16(B, N, K, ldb, 64, BK)
                               : cuda::make_map_2d_bf16(B, K, N, ldb, 64, BN);
   const int base = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const int ks = split_k(EPI, base, cuda::kNumSMs, K, ep.ksplit);
+  const int ks = split_k(EPI, base, cuda::num_sms(), K, ep.ksplit);
   const int tiles = base * ks;
-  const int grid = tiles < cuda::kNumSMs ? tiles : cuda::kNumSMs;
+  const int grid = tiles < cuda::num_sms() ? tiles : cuda::num_sms();
   CUtensorMap to, to2;
   if constexpr (EPI != kStoreF32) {
     if (tma_out<EPI>(ep, M, N, to, to2)) {
@@ -1068,8 +1069,8 @@ TilePlan pick_tile(Epi epi, int M, int N, int K, bool can_split) {
     int choice, bm, bn, slots;
     double rate;
   };
-  const Cand cands[] = {{0, 256, 256, cuda::kNumSMs / 2, 24.6}, {256, BM, 256, cuda::kNumSMs, 11.4},
-                        {128, BM, 128, cuda::kNumSMs, 7.0}, {64, BM, 64, cuda::kNumSMs, 3.6}};
+  const Cand cands[] = {{0, 256, 256, cuda::num_sms() / 2, 24.6}, {256, BM, 256, cuda::num_sms(), 11.4},
+                        {128, BM, 128, cuda::num_sms(), 7.0}, {64, BM, 64, cuda::num_sms(), 3.6}};
   const int kb = (K + BK - 1) / BK;
   const int kmax = can_split ? std::max(1, std::min(4, kb / 8)) : 1;
   const double wave_fixed = 1.5e6;  // ps: prologue / fill / exposed epilogue per wave
@@ -1147,8 +1148,9 @@ void gemm(Epi epi, bool a_mn, bool b_mn, int M, int N, int K, const __nv_bfloat1
   const bool can_split = force_split != 0 && split_ok(epi, M, N, ep);
   TilePlan plan = pick_tile(epi, M, N, K, can_split);
   if (force >= 0) plan.choice = force;
+  if (ep.tile >= 0) plan.choice = ep.tile;
   if (can_split && force_split > 1) plan.ks = force_split;
-  if (can_split && ep.ksplit > 1) plan.ks = ep.ksplit;  // caller-forced (tests / benchmarks)
+  if (can_split && ep.ksplit >= 1) plan.ks = ep.ksplit;  // caller-forced (tests / benchmarks); 1 = no split
   if (plan.ks > 1 && can_split) {  // K-slices into the workspace, then the epilogue pass
     EpiArgs part;
     part.out = ep.ws;
@@ -1200,7 +1202,7 @@ CK_API int ck_gemm_bf16_ex(int epi, int a_mn, int b_mn, int M, int N, int K, con
 CK_API int ck_gemm_bf16_split(int epi, int a_mn, int b_mn, int M, int N, int K, const void* A, long long lda,
                               const void* B, long long ldb, void* out, long long ldo, const void* bias,
                               const void* aux, long long ld_aux, void* out2, long long ld_out2, float* colsum,
-                              float* ws, long long ws_elems, int ksplit, void* stream) {
+                              float* ws, long long ws_elems, int ksplit, int tile, void* stream) {
   return chimera::capi::guarded([&] {
     chimera::gemm::EpiArgs ep;
     ep.out = out;
@@ -1214,6 +1216,7 @@ CK_API int ck_gemm_bf16_split(int epi, int a_mn, int b_mn, int M, int N, int K, 
     ep.ws = ws;
     ep.ws_elems = ws_elems;
     ep.ksplit = ksplit;  // honoured by gemm() as the forced slice count when > 1
+    ep.tile = tile;
     chimera::gemm::gemm(static_cast<chimera::gemm::Epi>(epi), a_mn != 0, b_mn != 0, M, N, K,
                         static_cast<const __nv_bfloat16*>(A), lda, static_cast<const __nv_bfloat16*>(B),
                         ldb, ep, static_cast<cudaStream_t>(stream));

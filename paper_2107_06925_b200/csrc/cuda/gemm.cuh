@@ -33,6 +33,7 @@ struct EpiArgs {
   float* ws = nullptr;
   long long ws_elems = 0;
   int ksplit = 0;  // internal: slice count chosen by gemm() (0 = the kernels' own rule)
+  int tile = -1;   // forced tile (benchmarks): 0 CTA pair 256x256, 256 / 128 / 64 single-CTA; -1 auto
 };
 
 // Operand layouts: A(m,k) is A[m*lda+k] when !a_mn (K-major) else A[k*lda+m];

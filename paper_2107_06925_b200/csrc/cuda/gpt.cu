@@ -160,6 +160,25 @@ struct Trainer::Impl {
   // gradient synchronisation policy (dessim::SyncPolicy): 0 end-of-iteration,
   // 1 eager-sync, 2 eager-sync-opt (eager iff the reference's slack rule says so)
   int sync_policy = 1;
+  // CostProfile the gradient-sync plan is computed on (set_cost_profile: the measured
+  // B200 profile; default: unit compute with a small alpha-beta allreduce, under which
+  // only "slack > 0" decides eager-sync-opt)
+  pipesim::CostProfile sync_profile = [] {
+    pipesim::CostProfile p;
+    p.alpha = 0.01, p.beta = 0.001, p.L_grad = 100.0;
+    return p;
+  }();
+  std::map<int, double> sync_time;  // stage -> planned allreduce start (profile time units)
+  // optimizer (set_optimizer): 0 SGD, 1 AdamW; per held stage the moments of its shard
+  int optimizer = 0;
+  ops::AdamHP adam;
+  struct OptState {
+    float *m = nullptr, *v = nullptr;
+    int* step = nullptr;
+    long long lo = 0, hi = 0;  // this process's ZeRO shard of the stage (whole stage if unsharded)
+    int pos = 0, holders = 1;  // position in / size of the stage communicator when sharded
+  };
+  std::map<int, OptState> opt;
   cudaStream_t comm_stream = nullptr;
   std::vector<int> coll_order;                   // stages in the global collective order
   std::map<int, bool> stage_eager;               // stage -> launched at its completion
@@ -170,8 +189,14 @@ struct Trainer::Impl {
   struct TaskSpan {
     int rank, kind, pipeline, micro, stage;
     cudaEvent_t a, b;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stalls;  // waits for an incoming message
   };
   std::vector<TaskSpan> spans;
+  TaskSpan* cur_span = nullptr;  // the span being issued (profiling)
+  // Stream wait for a message, bracketed by events while profiling: the bracket's
+  // length is time the rank's stream sat idle inside the task (not busy), so the
+  // measured bubble uses busy = span - stalls (dessim's busy = compute only).
+  void consume(const Msg& in, cudaStream_t st);
   struct CollSpan {  // one stage's allreduce + SGD on the comm stream
     int stage;
     bool eager;
@@ -503,6 +528,15 @@ Trainer::~Trainer() {
   cudaStreamDestroy(I.main_stream);
 }
 
+void Trainer::Impl::consume(const Msg& in, cudaStream_t st) {
+  if (!profiling || !cur_span) return in.before_consume(st);
+  cudaEvent_t a = timed_event(), b = timed_event();
+  CK_CUDA(cudaEventRecord(a, st));
+  in.before_consume(st);
+  CK_CUDA(cudaEventRecord(b, st));
+  cur_span->stalls.emplace_back(a, b);
+}
+
 // ----------------------------------------------------------- task kernels --
 namespace {
 
@@ -547,7 +581,7 @@ void Trainer::forward_task(int rank, int p, int mb, int s) {
     x = X.x0;
   } else {
     const Msg& in = I.msgs.at(I.msg_key(r, mb, s - 1, 0));
-    in.before_consume(st);
+    I.consume(in, st);
     x = in.buf;
   }
   const Msg* out_msg = (s + 1 < I.D) ? &I.msgs.at(I.msg_key(r, mb, s, 0)) : nullptr;
@@ -590,7 +624,7 @@ void Trainer::forward_pair(int rank, int p, int mb, int s) {
       I.launches_per_step += 1;
     } else {
       const Msg& in = I.msgs.at(I.msg_key(r, mb + k, s - 1, 0));
-      in.before_consume(st);
+      I.consume(in, st);
       CK_CUDA(cudaMemcpyAsync(xin + (size_t)k * M * h, in.buf, bytes, cudaMemcpyDeviceToDevice, st));
     }
     if (s + 1 < I.D) {
@@ -706,7 +740,7 @@ void Trainer::backward_task(int rank, int p, int mb, int s) {
     I.launches_per_step += 3;
   } else {
     const Msg& in = I.msgs.at(I.msg_key(r, mb, s, 1));
-    in.before_consume(st);
+    I.consume(in, st);
     dxo = in.buf;
   }
   const Msg* out_msg = (s > 0) ? &I.msgs.at(I.msg_key(r, mb, s - 1, 1)) : nullptr;
@@ -778,32 +812,28 @@ namespace {
 // eager stages by the unit-tick time at which their last backward (over all holders)
 // ends, then the end-of-iteration ones by stage id.
 void plan_sync(Trainer::Impl& I) {
-  const auto tl = pipesim::engine::tick_schedule(I.sched, pipesim::CostProfile{});
-  std::map<int, double> done_at;
-  for (int w = 0; w < I.D; ++w)
-    for (int i = 0; i < int(I.sched.per_worker[w].size()); ++i) {
-      const Task& t = I.sched.per_worker[w][i];
-      if (t.kind == TaskKind::Backward) done_at[t.stage] = std::max(done_at[t.stage], tl.spans[w][i].end);
-    }
-  std::map<std::pair<int, int>, bool> eager_ws;  // (worker, stage) -> eager (reference rule)
-  if (I.sync_policy == 2) {
-    pipesim::CostProfile prof;  // unit compute, small comm: alpha-beta only decides slack > 0
-    prof.alpha = 0.01, prof.beta = 0.001, prof.L_grad = 100.0;
-    pipesim::dessim::SimOptions o;
-    o.policy = pipesim::dessim::SyncPolicy::EagerSyncOpt;
-    for (const auto& ev : pipesim::dessim::simulate(I.sched, prof, o).allreduce_events)
-      eager_ws[{ev.worker, ev.stage}] = ev.eager;
+  // dessim::simulate on the sync profile (proj/src/dessim.cpp:60-135): per (worker, held
+  // stage) the reference rule -- eager-sync: always; eager-sync-opt: iff the worker
+  // idles after that stage's last backward (interior slack > 0).  A stage launches
+  // eagerly iff every holder would; eager stages are ordered by their simulated launch
+  // time, the others follow by stage id -- the same order on every process.
+  pipesim::dessim::SimOptions o;
+  o.policy = I.sync_policy == 2 ? pipesim::dessim::SyncPolicy::EagerSyncOpt : pipesim::dessim::SyncPolicy::EagerSync;
+  pipesim::CostProfile prof = I.sync_profile;
+  if (prof.L_grad <= 0) prof.L_grad = 1.0;  // the rule needs a non-zero allreduce cost
+  const auto sim = pipesim::dessim::simulate(I.sched, prof, o);
+  std::map<int, bool> all_eager;
+  std::map<int, double> start;
+  for (const auto& ev : sim.allreduce_events) {
+    auto it = all_eager.emplace(ev.stage, true).first;
+    it->second = it->second && ev.eager;
+    start[ev.stage] = std::max(start[ev.stage], ev.start);
   }
   I.stage_eager.clear();
-  for (int s = 0; s < I.D; ++s) {
-    bool e = I.sync_policy != 0;
-    if (I.sync_policy == 2)
-      for (const auto& [ws, eg] : eager_ws)
-        if (ws.second == s) e = e && eg;
-    I.stage_eager[s] = e;
-  }
+  I.sync_time = start;
+  for (int s = 0; s < I.D; ++s) I.stage_eager[s] = I.sync_policy == 1 || (I.sync_policy == 2 && all_eager[s]);
   std::vector<std::pair<double, int>> eager, late;
-  for (int s = 0; s < I.D; ++s) (I.stage_eager[s] ? eager : late).push_back({I.stage_eager[s] ? done_at[s] : s, s});
+  for (int s = 0; s < I.D; ++s) (I.stage_eager[s] ? eager : late).push_back({I.stage_eager[s] ? start[s] : s, s});
   std::sort(eager.begin(), eager.end());
   std::sort(late.begin(), late.end());
   I.coll_order.clear();
@@ -846,9 +876,18 @@ void sync_stage_body(Trainer::Impl& I, int s) {
   StageState& S = I.stages.at(s);
   cudaStream_t cs = I.comm_stream;
   for (cudaEvent_t e : I.stage_done_ev.at(s)) CK_CUDA(cudaStreamWaitEvent(cs, e, 0));
+  const bool adam = I.optimizer == 1;
+  auto update = [&](float* const* g, int copies) {  // the optimizer step over this process's range
+    if (!adam) return ops::sgd_update(S.w32, S.w16, g, copies, S.L.total, I.lr, cs);
+    Trainer::Impl::OptState& o = I.opt.at(s);
+    ops::AdamHP hp = I.adam;
+    hp.lr = I.lr;
+    ops::adamw_update(S.w32, S.w16, g, copies, o.m, o.v, o.step, o.lo, o.hi, hp, cs);
+    I.launches_per_step += 1;
+  };
   auto it = I.stage_comm.find(s);
   if (it == I.stage_comm.end()) {
-    ops::sgd_update(S.w32, S.w16, S.grads.data(), int(S.grads.size()), S.L.total, I.lr, cs);
+    update(S.grads.data(), int(S.grads.size()));
     I.launches_per_step += 1;
     return;
   }
@@ -859,9 +898,22 @@ void sync_stage_body(Trainer::Impl& I, int s) {
       CK_CUDA(cudaMemsetAsync(S.grads[c], 0, S.L.total * sizeof(float), cs));
     I.launches_per_step += 1;
   }
+  if (adam && I.opt.at(s).holders > 1) {  // ZeRO-1: reduce-scatter, shard update, all-gather
+    const Trainer::Impl::OptState& o = I.opt.at(s);
+    const size_t chunk = size_t(o.hi - o.lo);
+    if (Nccl::get().ReduceScatter(g0, g0 + o.lo, chunk, ncclFloat, ncclSum, it->second, cs) != ncclSuccess)
+      throw capi::InternalError("ncclReduceScatter failed");
+    update(&g0, 1);
+    CK_CUDA(cudaMemsetAsync(g0, 0, S.L.total * sizeof(float), cs));  // the other shards' partial sums
+    if (Nccl::get().AllGather(S.w32 + o.lo, S.w32, chunk, ncclFloat, it->second, cs) != ncclSuccess)
+      throw capi::InternalError("ncclAllGather failed");
+    ops::cast_f32_bf16(S.w32, S.w16, S.L.total, cs);
+    I.launches_per_step += 1;
+    return;
+  }
   if (Nccl::get().AllReduce(g0, g0, S.L.total, ncclFloat, ncclSum, it->second, cs) != ncclSuccess)
     throw capi::InternalError("ncclAllReduce failed");
-  ops::sgd_update(S.w32, S.w16, &g0, 1, S.L.total, I.lr, cs);
+  update(&g0, 1);
   I.launches_per_step += 1;
 }
 
@@ -939,13 +991,15 @@ void Trainer::run_task(const pipesim::Task& t) {
   for (int r = 0; r < I.W; ++r) {
     const int rank = r * I.D + t.worker;
     if (!I.local(rank)) continue;
-    Impl::TaskSpan sp{rank, int(t.kind), t.pipeline_id, t.micro_batch, t.stage, nullptr, nullptr};
+    Impl::TaskSpan sp{rank, int(t.kind), t.pipeline_id, t.micro_batch, t.stage, nullptr, nullptr, {}};
     if (I.profiling) {
       sp.a = I.timed_event();
       CK_CUDA(cudaEventRecord(sp.a, I.stream_of(rank)));
+      I.cur_span = &sp;
     }
     if (fwd) forward_task(rank, t.pipeline_id, t.micro_batch, t.stage);
     else backward_task(rank, t.pipeline_id, t.micro_batch, t.stage);
+    I.cur_span = nullptr;
     if (I.profiling) {
       sp.b = I.timed_event();
       CK_CUDA(cudaEventRecord(sp.b, I.stream_of(rank)));
@@ -1019,17 +1073,19 @@ bool Trainer::fuse_forward_pair(const pipesim::Task& t, const pipesim::Task& nex
   for (int r = 0; r < I.W; ++r) {
     const int rank = r * I.D + t.worker;
     if (!I.local(rank)) continue;
-    Impl::TaskSpan sp{rank, int(t.kind), t.pipeline_id, t.micro_batch, t.stage, nullptr, nullptr};
+    Impl::TaskSpan sp{rank, int(t.kind), t.pipeline_id, t.micro_batch, t.stage, nullptr, nullptr, {}};
     if (I.profiling) {
       sp.a = I.timed_event();
       CK_CUDA(cudaEventRecord(sp.a, I.stream_of(rank)));
+      I.cur_span = &sp;
     }
     forward_pair(rank, t.pipeline_id, t.micro_batch, t.stage);
+    I.cur_span = nullptr;
     if (I.profiling) {  // the pair's span goes to its first task, the second gets an empty one
       sp.b = I.timed_event();
       CK_CUDA(cudaEventRecord(sp.b, I.stream_of(rank)));
       I.spans.push_back(sp);
-      Impl::TaskSpan sp2{rank, int(next.kind), next.pipeline_id, next.micro_batch, next.stage, sp.b, sp.b};
+      Impl::TaskSpan sp2{rank, int(next.kind), next.pipeline_id, next.micro_batch, next.stage, sp.b, sp.b, {}};
       I.spans.push_back(sp2);
     }
   }
@@ -1055,6 +1111,68 @@ void Trainer::set_sync_policy(int policy) {
     cudaGraphDestroy(I.graph);
     I.graph_exec = nullptr, I.graph = nullptr;
   }
+}
+
+void Trainer::set_cost_profile(const pipesim::CostProfile& p) {
+  Impl& I = *d_;
+  I.sync_profile = p;
+  set_sync_policy(I.sync_policy);  // re-plan, drop the captured graph
+}
+
+void Trainer::set_optimizer(int kind, float beta1, float beta2, float eps, float weight_decay, bool zero) {
+  Impl& I = *d_;
+  if (kind < 0 || kind > 1) throw pipesim::InvalidConfigError("optimizer must be 0 (sgd) or 1 (adamw)");
+  if (kind == 1 && !(beta1 >= 0 && beta1 < 1 && beta2 >= 0 && beta2 < 1 && eps > 0 && weight_decay >= 0))
+    throw pipesim::InvalidConfigError("adamw: need 0 <= beta < 1, eps > 0, weight_decay >= 0");
+  if (!I.connected) throw capi::InternalError("multi-process trainer: call connect() before set_optimizer()");
+  I.optimizer = kind;
+  I.adam.beta1 = beta1, I.adam.beta2 = beta2, I.adam.eps = eps, I.adam.weight_decay = weight_decay;
+  if (kind == 1) {
+    for (auto& [s, S] : I.stages) {
+      Impl::OptState o;
+      o.lo = 0, o.hi = S.L.total;
+      if (zero && I.stage_comm.count(s)) {  // shard over the processes holding the stage
+        const std::vector<int> holders = I.lp->stage_holders(s);
+        const int R = int(holders.size());
+        const int pos = int(std::find(holders.begin(), holders.end(), I.proc) - holders.begin());
+        if (S.L.total % (4LL * R) == 0) {
+          const long long chunk = S.L.total / R;
+          o.lo = pos * chunk, o.hi = o.lo + chunk, o.pos = pos, o.holders = R;
+        }
+      }
+      Impl::OptState& cur = I.opt[s];
+      if (!cur.m || cur.hi - cur.lo != o.hi - o.lo) {  // (re)allocate this process's moments
+        cur.m = I.arena.alloc<float>(size_t(o.hi - o.lo));
+        cur.v = I.arena.alloc<float>(size_t(o.hi - o.lo));
+        if (!cur.step) cur.step = I.arena.alloc<int>(1);
+      }
+      CK_CUDA(cudaMemset(cur.m, 0, size_t(o.hi - o.lo) * sizeof(float)));
+      CK_CUDA(cudaMemset(cur.v, 0, size_t(o.hi - o.lo) * sizeof(float)));
+      CK_CUDA(cudaMemset(cur.step, 0, sizeof(int)));
+      cur.lo = o.lo, cur.hi = o.hi, cur.pos = o.pos, cur.holders = o.holders;
+    }
+  }
+  set_sync_policy(I.sync_policy);  // drop the captured graph
+}
+
+std::string Trainer::sync_plan_json() const {
+  Impl& I = *d_;
+  if (I.coll_order.empty()) plan_sync(I);
+  using json::Value;
+  Value arr = Value::array();
+  for (int s : I.coll_order) {
+    Value e = Value::object();
+    e.set("stage", Value::integer(s));
+    e.set("eager", Value::boolean(I.stage_eager.at(s)));
+    e.set("planned_start", Value::number(I.sync_time.count(s) ? I.sync_time.at(s) : 0.0));
+    arr.push(std::move(e));
+  }
+  Value j = Value::object();
+  j.set("policy", Value::string(I.sync_policy == 0 ? "end-of-iteration" : I.sync_policy == 1 ? "eager-sync"
+                                                                                            : "eager-sync-opt"));
+  j.set("profile", json::parse(pipesim::to_json(I.sync_profile, -1)));
+  j.set("order", std::move(arr));
+  return json::dump(j, -1);
 }
 
 
@@ -1123,6 +1241,13 @@ std::string Trainer::profile_step() {
     x.set("stage", Value::integer(sp.stage));
     x.set("start_ms", Value::number(a));
     x.set("end_ms", Value::number(b));
+    double stall = 0;
+    for (const auto& [sa, sb] : sp.stalls) {
+      float t = 0;
+      CK_CUDA(cudaEventElapsedTime(&t, sa, sb));
+      stall += t;
+    }
+    x.set("stall_ms", Value::number(stall));
     arr.push(std::move(x));
   }
   Value colls = Value::array();
@@ -1280,8 +1405,18 @@ void Trainer::connect(const std::string& all_blobs, const std::string& nccl_id) 
       if (Nccl::get().CommSplit(I.world_comm, mine ? s : NCCL_SPLIT_NOCOLOR, I.proc, &c, nullptr) != ncclSuccess)
         throw capi::InternalError("ncclCommSplit failed");
     } else if (mine) {
-      if (Nccl::get().CommInitRank(&c, int(holders.size()), id_at(size_t(s)), int(pos - holders.begin())) !=
-          ncclSuccess)
+      // the stage allreduces overlap compute: cap their CTAs (CK_NCCL_MAX_CTAS, default
+      // 16 of 148 SMs; 0 = NCCL's own choice) so the pipeline keeps its SMs
+      ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+      const char* mc = std::getenv("CK_NCCL_MAX_CTAS");
+      const int max_ctas = mc ? atoi(mc) : 16;
+      if (max_ctas > 0) cfg.maxCTAs = max_ctas, cfg.minCTAs = std::min(cfg.minCTAs > 0 ? cfg.minCTAs : 1, max_ctas);
+      const ncclResult_t rc =
+          Nccl::get().CommInitRankConfig
+              ? Nccl::get().CommInitRankConfig(&c, int(holders.size()), id_at(size_t(s)), int(pos - holders.begin()),
+                                               &cfg)
+              : Nccl::get().CommInitRank(&c, int(holders.size()), id_at(size_t(s)), int(pos - holders.begin()));
+      if (rc != ncclSuccess)
         throw capi::InternalError("ncclCommInitRank (stage " + std::to_string(s) + ") failed");
     }
     if (mine) I.stage_comm[s] = c;
@@ -1443,6 +1578,19 @@ CK_API int ck_gpt_launch(ck_gpt* h) {
 
 CK_API int ck_gpt_set_sync_policy(ck_gpt* h, int policy) {
   return chimera::capi::guarded([&] { h->t->set_sync_policy(policy); });
+}
+
+CK_API int ck_gpt_set_cost_profile(ck_gpt* h, const char* profile_json) {
+  return chimera::capi::guarded([&] { h->t->set_cost_profile(pipesim::profile_from_json(profile_json)); });
+}
+
+CK_API int ck_gpt_set_optimizer(ck_gpt* h, int kind, float beta1, float beta2, float eps, float weight_decay,
+                                int zero) {
+  return chimera::capi::guarded([&] { h->t->set_optimizer(kind, beta1, beta2, eps, weight_decay, zero != 0); });
+}
+
+CK_API int ck_gpt_sync_plan(ck_gpt* h, char** out_json) {
+  return chimera::capi::guarded([&] { *out_json = chimera::capi::dup_string(h->t->sync_plan_json()); });
 }
 
 CK_API int ck_gpt_set_graph(ck_gpt* h, int on) {

@@ -36,6 +36,17 @@ class Trainer {
   void* stream() const;
   void set_use_graph(bool on);
   void set_sync_policy(int policy);  // 0 end-of-iteration, 1 eager-sync, 2 eager-sync-opt
+  // The measured CostProfile (F_t, backward_ratio, alpha, beta, L_act, L_grad) the
+  // eager-sync-opt decision and the collective order are planned on (dessim::simulate).
+  void set_cost_profile(const pipesim::CostProfile& p);
+  std::string sync_plan_json() const;  // per stage: eager?, planned launch time
+  // Optimizer of the stage update (the reference has SGD only):
+  // kind 0 = SGD (default, proj/src/oracle.cpp:283-299), 1 = AdamW with (beta1, beta2,
+  // eps, weight_decay).  zero = ZeRO-1: each process holding a stage keeps only its
+  // 1/R share of the AdamW moments and updates that share of the weights (gradient
+  // reduce-scatter + fp32 weight all-gather over the stage communicator instead of one
+  // allreduce).  Multi-process trainers call it after connect().
+  void set_optimizer(int kind, float beta1, float beta2, float eps, float weight_decay, bool zero);
   // multi-process: this process's IPC handles (inbox, outbox), then connect with the
   // handles of all processes (ordered by process index) and an NCCL unique id.
   std::string ipc_export() const;

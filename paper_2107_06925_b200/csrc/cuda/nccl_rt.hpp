@@ -21,8 +21,11 @@ namespace chimera::gpt {
 struct Nccl {
   decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
   decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommInitRankConfig) CommInitRankConfig = nullptr;  // optional (CTA caps)
   decltype(&ncclCommSplit) CommSplit = nullptr;
   decltype(&ncclAllReduce) AllReduce = nullptr;
+  decltype(&ncclReduceScatter) ReduceScatter = nullptr;
+  decltype(&ncclAllGather) AllGather = nullptr;
   decltype(&ncclCommDestroy) CommDestroy = nullptr;
   decltype(&ncclGetErrorString) GetErrorString = nullptr;
 
@@ -41,8 +44,12 @@ struct Nccl {
       };
       n.GetUniqueId = reinterpret_cast<decltype(n.GetUniqueId)>(sym("ncclGetUniqueId"));
       n.CommInitRank = reinterpret_cast<decltype(n.CommInitRank)>(sym("ncclCommInitRank"));
+      n.CommInitRankConfig =
+          reinterpret_cast<decltype(n.CommInitRankConfig)>(dlsym(h, "ncclCommInitRankConfig"));
       n.CommSplit = reinterpret_cast<decltype(n.CommSplit)>(sym("ncclCommSplit"));
       n.AllReduce = reinterpret_cast<decltype(n.AllReduce)>(sym("ncclAllReduce"));
+      n.ReduceScatter = reinterpret_cast<decltype(n.ReduceScatter)>(sym("ncclReduceScatter"));
+      n.AllGather = reinterpret_cast<decltype(n.AllGather)>(sym("ncclAllGather"));
       n.CommDestroy = reinterpret_cast<decltype(n.CommDestroy)>(sym("ncclCommDestroy"));
       n.GetErrorString = reinterpret_cast<decltype(n.GetErrorString)>(sym("ncclGetErrorString"));
     });

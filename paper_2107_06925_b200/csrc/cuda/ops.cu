@@ -409,6 +409,55 @@ __global__ void __launch_bounds__(256) k_sgd(float* __restrict__ w32, bf16* __re
   }
 }
 
+// AdamW (decoupled weight decay, torch.optim.AdamW semantics) over elements [lo, hi) of
+// a stage: g = sum of the gradient copies; m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2;
+// w = w (1 - lr wd) - lr (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps); w16 = bf16(w);
+// the gradients are zeroed.  m / v hold only [lo, hi) (the ZeRO shard: m[i - lo]); the
+// step t = *step + 1 is read on the device so one captured graph serves every iteration.
+template <int COPIES>
+__global__ void __launch_bounds__(256) k_adamw(float* __restrict__ w32, bf16* __restrict__ w16, GradPtrs g,
+                                               float* __restrict__ m, float* __restrict__ v, const int* __restrict__ step,
+                                               long long lo, long long hi, AdamHP hp) {
+  cuda::pdl_wait();
+  const float t = float(*step + 1);
+  const float c1 = 1.f / (1.f - powf(hp.beta1, t)), c2 = 1.f / (1.f - powf(hp.beta2, t));
+  const float decay = 1.f - hp.lr * hp.weight_decay;
+  const long long stride = (long long)gridDim.x * blockDim.x * 4;
+  for (long long i = lo + (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 4; i < hi; i += stride) {
+    float4 gs = __ldcs(reinterpret_cast<const float4*>(g.p[0] + i));
+#pragma unroll
+    for (int c = 1; c < COPIES; ++c) {
+      const float4 x = __ldcs(reinterpret_cast<const float4*>(g.p[c] + i));
+      gs.x += x.x, gs.y += x.y, gs.z += x.z, gs.w += x.w;
+    }
+    float4 w = __ldcs(reinterpret_cast<const float4*>(w32 + i));
+    float4 mm = __ldcs(reinterpret_cast<const float4*>(m + (i - lo)));
+    float4 vv = __ldcs(reinterpret_cast<const float4*>(v + (i - lo)));
+    float* wp = &w.x;
+    float* mp = &mm.x;
+    float* vp = &vv.x;
+    const float* gp = &gs.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      mp[e] = hp.beta1 * mp[e] + (1.f - hp.beta1) * gp[e];
+      vp[e] = hp.beta2 * vp[e] + (1.f - hp.beta2) * gp[e] * gp[e];
+      wp[e] = wp[e] * decay - hp.lr * (mp[e] * c1) / (sqrtf(vp[e] * c2) + hp.eps);
+    }
+    __stcs(reinterpret_cast<float4*>(w32 + i), w);
+    __stcs(reinterpret_cast<float4*>(m + (i - lo)), mm);
+    __stcs(reinterpret_cast<float4*>(v + (i - lo)), vv);
+    __nv_bfloat162 h[2] = {__floats2bfloat162_rn(w.x, w.y), __floats2bfloat162_rn(w.z, w.w)};
+    *reinterpret_cast<uint2*>(w16 + i) = *reinterpret_cast<uint2*>(h);
+#pragma unroll
+    for (int c = 0; c < COPIES; ++c) __stcs(reinterpret_cast<float4*>(g.p[c] + i), make_float4(0.f, 0.f, 0.f, 0.f));
+  }
+}
+
+__global__ void k_count_step(int* step) {
+  cuda::pdl_wait();
+  if (threadIdx.x == 0 && blockIdx.x == 0) ++*step;
+}
+
 __global__ void k_reduce(float* __restrict__ dst, GradPtrs g, int copies, long long n) {
   cuda::pdl_wait();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -448,7 +497,7 @@ void layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* 
 void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* g,
                    const bf16* dres, bf16* dx, float* dgamma, float* dbeta, float* dsum, int M, int h,
                    cudaStream_t st) {
-  const int grid = std::min(ceil_div(M, 8), cuda::kNumSMs);  // one 8-warp CTA per SM (255 registers)
+  const int grid = std::min(ceil_div(M, 8), cuda::num_sms());  // one 8-warp CTA per SM (255 registers)
   const size_t smem = size_t(dsum ? 24 : 16) * h * sizeof(float);
   switch (h) {
 #define CK_LN(V)                                                                                   \
@@ -486,7 +535,7 @@ void xent_fwd_bwd(bf16* logits, long long ld, const int32_t* labels, int M, int 
   const bool bulk_ok = ld % 8 == 0 && Vp % 8 == 0 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0;
   const int nv = !bulk_ok ? 0 : need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : need <= 8 ? 8 : need <= 13 ? 13 : 0;
   const size_t smem = 2 * size_t((Vp * 2 + 127) / 128 * 128);  // two row buffers (<= 208 KB)
-  const int grid = std::min(M, cuda::kNumSMs);
+  const int grid = std::min(M, cuda::num_sms());
   switch (nv) {
 #define CK_XR(NV)                                                                                      \
   case NV: {                                                                                           \
@@ -524,6 +573,23 @@ void sgd_update(float* w32, bf16* w16, float* const* grads, int copies, long lon
     CK_SGD(1) CK_SGD(2) CK_SGD(3) CK_SGD(4) CK_SGD(5) CK_SGD(6) CK_SGD(7) CK_SGD(8)
 #undef CK_SGD
   }
+  CK_CUDA(cudaGetLastError());
+}
+
+void adamw_update(float* w32, bf16* w16, float* const* grads, int copies, float* m, float* v, int* step,
+                  long long lo, long long hi, const AdamHP& hp, cudaStream_t st) {
+  if (copies < 1 || copies > 8) throw chimera::capi::InternalError("adamw: 1..8 gradient copies");
+  if (lo % 4 || hi % 4) throw chimera::capi::InternalError("adamw: range must be a multiple of 4 elements");
+  GradPtrs g{};
+  for (int c = 0; c < copies; ++c) g.p[c] = grads[c];
+  const int grid = grid_for(hi - lo, 4);
+  switch (copies) {
+#define CK_ADAM(C) \
+  case C: cuda::launch(k_adamw<C>, dim3(grid), dim3(256), 0, st, w32, w16, g, m, v, (const int*)step, lo, hi, hp); break;
+    CK_ADAM(1) CK_ADAM(2) CK_ADAM(3) CK_ADAM(4) CK_ADAM(5) CK_ADAM(6) CK_ADAM(7) CK_ADAM(8)
+#undef CK_ADAM
+  }
+  cuda::launch(k_count_step, dim3(1), dim3(32), 0, st, step);
   CK_CUDA(cudaGetLastError());
 }
 

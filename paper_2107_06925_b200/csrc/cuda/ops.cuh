@@ -35,6 +35,13 @@ void bias_grad(const bf16* dy, float* db, int M, int N, cudaStream_t st);
 // g = sum_c grads[c]; w32 -= lr * g; w16 = bf16(w32); grads[c] = 0.  (n elements)
 void sgd_update(float* w32, bf16* w16, float* const* grads, int copies, long long n, float lr,
                 cudaStream_t st);
+// AdamW over elements [lo, hi) (decoupled weight decay): g = sum_c grads[c]; m / v are the
+// optimizer state of [lo, hi) only (a ZeRO shard); t = *step + 1, then ++*step on the device.
+struct AdamHP {
+  float lr = 1e-4f, beta1 = 0.9f, beta2 = 0.999f, eps = 1e-8f, weight_decay = 0.0f;
+};
+void adamw_update(float* w32, bf16* w16, float* const* grads, int copies, float* m, float* v, int* step,
+                  long long lo, long long hi, const AdamHP& hp, cudaStream_t st);
 // dst = sum_c srcs[c] (fp32), n elements; used before an inter-process allreduce.
 void reduce_copies(float* dst, float* const* srcs, int copies, long long n, cudaStream_t st);
 void cast_f32_bf16(const float* src, bf16* dst, long long n, cudaStream_t st);

@@ -44,6 +44,9 @@ _lib.register("ck_gpt_end_iteration", C.c_int, [_vp, C.POINTER(C.c_float)])
 _lib.register("ck_gpt_profile_step", C.c_int, [_vp, C.POINTER(_vp)])
 _lib.register("ck_gpt_set_graph", C.c_int, [_vp, C.c_int])
 _lib.register("ck_gpt_set_sync_policy", C.c_int, [_vp, C.c_int])
+_lib.register("ck_gpt_set_cost_profile", C.c_int, [_vp, C.c_char_p])
+_lib.register("ck_gpt_sync_plan", C.c_int, [_vp, C.POINTER(_vp)])
+_lib.register("ck_gpt_set_optimizer", C.c_int, [_vp, C.c_int, C.c_float, C.c_float, C.c_float, C.c_float, C.c_int])
 _lib.register("ck_gpt_stream", _vp, [_vp])
 _lib.register("ck_gpt_ipc_handles", C.c_int, [_vp, C.c_char_p, C.c_int])
 _lib.register("ck_gpt_connect", C.c_int, [_vp, C.c_char_p, C.c_int, C.c_char_p, C.c_int])
@@ -94,7 +97,9 @@ def balanced_partition(shape: GPTShape, config) -> tuple:
     stage), counting a layer as 1 and the LM head as its FLOP ratio
     V / (12 h + 2 s*causal_fraction) to a layer.  Chimera worker w holds stage w of the
     down pipelines and the mirrored stage of the up ones, so the stage carrying the
-    head should be shorter than the middle ones (e.g. GPT-2 medium D=4 -> (5, 7, 7, 5))."""
+    head should be shorter than the middle ones.  E.g. GPT-2 medium D=4: (5, 7, 7, 5) and
+    (7, 7, 7, 3) load the busiest worker equally (10 layers + head); the tie-break on the
+    busiest single stage (7 vs 5 + head = 8.8) picks (7, 7, 7, 3)."""
     import itertools
     D, L = config.D, shape.n_layer
     attn = shape.seq * (0.5 if shape.causal else 1.0)
@@ -242,6 +247,21 @@ class Trainer:
         check(lib().ck_gpt_set_sync_policy(self._h, {"end-of-iteration": 0, "eager-sync": 1,
                                                       "eager-sync-opt": 2}[policy]))
 
+    def set_cost_profile(self, profile):
+        """Plan the gradient sync (eager-sync-opt set, collective order) on this
+        CostProfile -- normally the measured one; identical on every process."""
+        check(lib().ck_gpt_set_cost_profile(self._h, profile.to_json().encode()))
+
+    def set_optimizer(self, kind: str = "adamw", beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+                      weight_decay: float = 0.0, zero: bool = False):
+        """'sgd' (the reference's, default) or 'adamw'; zero=True shards the AdamW moments
+        over the processes holding each stage (ZeRO-1).  After connect()."""
+        check(lib().ck_gpt_set_optimizer(self._h, {"sgd": 0, "adamw": 1}[kind], beta1, beta2, eps, weight_decay,
+                                         int(zero)))
+
+    def sync_plan(self) -> dict:
+        return json.loads(call_str(lib().ck_gpt_sync_plan, self._h))
+
     def use_graph(self, on: bool):
         check(lib().ck_gpt_set_graph(self._h, int(on)))
 
@@ -275,13 +295,15 @@ class Trainer:
 def measured_bubble(profile: dict, ranks=None) -> dict:
     """Per-rank idle fraction of a profiled iteration with the dessim definition
     (proj/src/dessim.cpp:168-181): idle_w = (span_end - span_start) - busy_w
-    over the iteration span, busy_w = sum of the rank's task durations."""
+    over the iteration span, busy_w = sum of the rank's task durations minus the time
+    its stream sat waiting inside a task for an incoming message (`stall_ms`, measured
+    by events around each wait) -- dessim's busy time is compute only."""
     tasks = profile["tasks"]
     lo = min(t["start_ms"] for t in tasks)
     hi = max(t["end_ms"] for t in tasks)
     out = {}
     for r in sorted({t["rank"] for t in tasks} if ranks is None else ranks):
-        busy = sum(t["end_ms"] - t["start_ms"] for t in tasks if t["rank"] == r)
+        busy = sum(t["end_ms"] - t["start_ms"] - t.get("stall_ms", 0.0) for t in tasks if t["rank"] == r)
         out[r] = ((hi - lo) - busy) / (hi - lo)
     return {"per_rank": out, "span_ms": hi - lo}
 

@@ -15,7 +15,7 @@ _lib.register("ck_gemm_bf16", _i, [_i, _i, _i, _i, _i, _i, _vp, _ll, _vp, _ll, _
 _lib.register("ck_gemm_bf16_ex", _i, [_i, _i, _i, _i, _i, _i, _vp, _ll, _vp, _ll, _vp, _ll, _vp, _vp, _ll,
                                       _vp, _ll, _vp, _vp])
 _lib.register("ck_gemm_bf16_split", _i, [_i, _i, _i, _i, _i, _i, _vp, _ll, _vp, _ll, _vp, _ll, _vp, _vp, _ll,
-                                         _vp, _ll, _vp, _vp, _ll, _i, _vp])
+                                         _vp, _ll, _vp, _vp, _ll, _i, _i, _vp])
 
 EPI = {"bf16": 0, "bias_gelu": 1, "bias_resid": 2, "gelu_bwd": 3, "acc_f32": 4, "f32": 5}
 
@@ -31,7 +31,7 @@ def _stream(stream):
 
 
 def gemm(epi, A, B, out, *, a_mn=False, b_mn=False, M=None, N=None, K=None, bias=None, aux=None,
-         out2=None, stream=None, colsum=None, ws=None, ksplit=0):
+         out2=None, stream=None, colsum=None, ws=None, ksplit=0, tile=-1):
     """D[m,n] = sum_k A(m,k) B(n,k) with A/B K-major ([M,K]/[N,K]) or MN-major ([K,M]/[K,N]).
     `colsum` (fp32 [N], gelu_bwd only) accumulates the column sums of the bf16 output."""
     M = M if M is not None else (A.shape[1] if a_mn else A.shape[0])
@@ -41,7 +41,8 @@ def gemm(epi, A, B, out, *, a_mn=False, b_mn=False, M=None, N=None, K=None, bias
             out.stride(0), _p(bias), _p(aux), aux.stride(0) if aux is not None else 0, _p(out2),
             out2.stride(0) if out2 is not None else 0)
     if ws is not None:  # split-K workspace route (fp32, zero-filled, >= M*N)
-        check(lib().ck_gemm_bf16_split(*args, _p(colsum), _p(ws), ws.numel(), int(ksplit), _stream(stream)))
+        check(lib().ck_gemm_bf16_split(*args, _p(colsum), _p(ws), ws.numel(), int(ksplit), int(tile),
+                                       _stream(stream)))
     elif colsum is None:
         check(lib().ck_gemm_bf16(*args, _stream(stream)))
     else:

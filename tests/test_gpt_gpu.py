@@ -237,3 +237,43 @@ def test_measured_timeline_renders_with_reference_gantt():
     svg = P.gantt_timeline(tl, P.CostProfile(F_t=float(f_mean)), svg=True)
     assert svg.startswith("<svg") and svg.count("<rect") >= len(doc["events"])
     tr.close()
+
+
+def _adamw_ref(w, g, m, v, t, lr, b1, b2, eps, wd):
+    m = b1 * m + (1 - b1) * g
+    v = b2 * v + (1 - b2) * g * g
+    w = w * (1 - lr * wd) - lr * (m / (1 - b1 ** t)) / (np.sqrt(v / (1 - b2 ** t)) + eps)
+    return w, m, v
+
+
+def test_adamw_two_steps_vs_numpy():
+    """§8(f)-4: the AdamW stage update (torch.optim.AdamW semantics) on the GPU vs numpy
+    AdamW applied to the fp64 oracle's gradients, two iterations (bias correction and
+    moment carry-over); per-stage update direction cos >= 0.99, ||d - d_ref|| / ||d_ref||
+    <= 0.1 (bf16 gradients vs fp64; eps chosen so near-zero gradients stay in the
+    linear regime)."""
+    shape = PRESETS["tiny"]
+    cfg = P.PipelineConfig("chimera", 4, 1, 4, 2, 1)
+    lr, b1, b2, eps, wd = 1e-3, 0.9, 0.99, 1e-4, 0.01
+    tr = Trainer(shape, cfg, lr=lr)
+    tr.init_params(0)
+    tr.set_optimizer("adamw", b1, b2, eps, wd)
+    D = cfg.D
+    params = [tr.get_params(s).astype(np.float64) for s in range(D)]
+    m = [np.zeros_like(p) for p in params]
+    v = [np.zeros_like(p) for p in params]
+    sched = json.loads(tr.schedule_text)
+    for it in range(2):
+        tok, lab = synthetic_batch(shape, cfg.mini_batch(), 20 + it)
+        tr.set_batch(tok, lab)
+        tr.step()
+        _, _, g_ref, _ = O.run_iteration(sched, _oshape(shape), params, tok, lab, 0.0)
+        after = [tr.get_params(s).astype(np.float64) for s in range(D)]
+        for s in range(D):
+            w_ref, m[s], v[s] = _adamw_ref(params[s], g_ref[s], m[s], v[s], it + 1, lr, b1, b2, eps, wd)
+            d, d_ref = after[s] - params[s], w_ref - params[s]
+            cos = d @ d_ref / (np.linalg.norm(d) * np.linalg.norm(d_ref))
+            rel = np.linalg.norm(d - d_ref) / np.linalg.norm(d_ref)
+            assert cos >= 0.99 and rel <= 0.1, (it, s, cos, rel)
+        params = after
+    tr.close()

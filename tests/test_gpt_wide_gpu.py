@@ -14,8 +14,8 @@ their own, so a zeroed or misrouted small gradient cannot hide in a stage norm):
   * on the fixed index sample: cosine >= COS_MIN and ||g - g_ref|| / ||g_ref|| <= REL_TOL;
 and the mean loss within LOSS_TOL.  The gradient is recovered from one SGD step at
 lr = 64 (a power of two: (w - w') / lr is exact up to the fp32 rounding of w').
-Tolerances are the bf16-operand / fp32-accumulate bounds of SURVEY.md §8(c),
-tightened to the measured values (see profiles/ r02 parity summary).
+Tolerances start from the bf16-operand / fp32-accumulate bounds of SURVEY.md §8(c)
+(loss 2e-2, cos 0.999, rel 3e-2) and are tightened to ~3x the measured worst case.
 """
 import json
 import os
@@ -31,10 +31,12 @@ pytestmark = pytest.mark.gpu
 
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "gpt_wide.npz")
 LR = 64.0
-LOSS_TOL = 5e-3
-NORM_TOL = 3e-2
-COS_MIN = 0.999
-REL_TOL = 5e-2
+# measured on B200 (r02, profiles/r02_parity_wide.jsonl): loss rel <= 1.1e-5, per-tensor
+# norm error <= 3.3e-3, sampled rel <= 1.3e-2, 1 - cos <= 8e-5
+LOSS_TOL = 1e-4
+NORM_TOL = 1e-2
+COS_MIN = 0.9995
+REL_TOL = 3e-2
 
 
 @pytest.fixture(scope="module")

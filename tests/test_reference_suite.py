@@ -61,10 +61,26 @@ def test_reference_unit_tests_oracle_on_gpu():
     assert "| 0 failed | assertions:" in r.stdout, r.stdout
 
 
+def _criteria(text):
+    return [ln for ln in text.splitlines() if ln.startswith("criterion")]
+
+
 @pytest.mark.gpu
 def test_reference_acceptance_on_gpu():
+    """Same report as the reference build's own run (proj/test_output.txt, frozen in
+    tests/golden/acceptance_reference_output.txt): criteria 2-10 PASS and criterion 1
+    FAIL with the identical detail -- the reference itself fails it (GEMS D=2 N=2 is
+    fixed at 5/11, outside the closed form's +-0.05).  Every line is byte-identical except
+    criterion 7's finite-difference error, which here comes from the GPU fp64 kernels."""
     r = _run("acceptance", env={"PIPESIM_GOLDEN_DIR": os.path.join(ROOT, "tests", "golden")})
-    assert r.returncode == 0, r.stdout + r.stderr
-    assert "all acceptance criteria passed" in r.stdout, r.stdout
-    for k in range(1, 11):
-        assert f"criterion {k}{' ' if k < 10 else ''}  PASS" in r.stdout, r.stdout
+    with open(os.path.join(ROOT, "tests", "golden", "acceptance_reference_output.txt")) as fh:
+        want = _criteria(fh.read())
+    got = _criteria(r.stdout)
+    assert len(got) == len(want) == 10, r.stdout + r.stderr
+    for g, w in zip(got, want):
+        if w.startswith("criterion 7 "):
+            assert g.startswith("criterion 7  PASS  finite-difference gradient check"), g
+            assert float(g.split("error ")[1].rstrip("]")) <= 1e-10, g
+        else:
+            assert g == w, (g, w)
+    assert "1 criterion(s) failed" in r.stdout
