@@ -217,33 +217,49 @@ def cpu_port_sample(shape, stages=None):
             "reference_toy": reference_toy_iteration()}
 
 
-def roofline_shapes(shape, cfg):
+def roofline_shapes(shape, cfg, bwd_pair_frac=None):
     """(M, N, K, a_mn, b_mn, weight): every stage-GEMM shape one iteration runs, weighted by
     how often it runs per layer-micro-batch.  Forward doubling + recompute (configs[3]):
-    fused forward pairs on 2M rows (weight 1/2 per micro-batch), recompute forward,
-    activation gradient (dgrad) and weight gradient (K = M) on M rows; the LM head's
-    four GEMMs with weight 1/L (one head per L layers)."""
+    fused forward pairs on 2M rows (weight 1/2 per micro-batch); the backward of a pair
+    (recompute forward, activation gradient, weight gradient with K = rows) on 2M rows
+    when fused (bwd_pair_frac of the micro-batches, from the trainer's stats; default
+    all) else on M rows; the LM head's GEMMs with weight 1/L (one head per L layers)."""
     M, h, f, Vp = cfg["B"] * shape.seq, shape.hidden, shape.ffn, shape.vocab_padded
     fd = cfg["scaling"] == "forward-doubling" and cfg["N"] > cfg["D"]
+    fp = (1.0 if bwd_pair_frac is None else bwd_pair_frac) if fd else 0.0
     layer = lambda Mm: [(Mm, 3 * h, h), (Mm, h, h), (Mm, f, h), (Mm, h, f)]
+    dgrad = lambda Mm: [(Mm, h, 3 * h), (Mm, h, h), (Mm, h, f), (Mm, f, h)]
+    wgrad = lambda Kk: [(3 * h, h, Kk), (h, h, Kk), (f, h, Kk), (h, f, Kk)]
     out = []
     if fd:
         out += [(Mm, N, K, 0, 0, 0.5) for (Mm, N, K) in layer(2 * M)]  # fused pair forward
-        out += [(Mm, N, K, 0, 0, 1.0) for (Mm, N, K) in layer(M)]  # recompute forward
     else:
         out += [(Mm, N, K, 0, 0, 1.0) for (Mm, N, K) in layer(M)]
-    out += [(M, h, 3 * h, 0, 1, 1.0), (M, h, h, 0, 1, 1.0), (M, h, f, 0, 1, 1.0), (M, f, h, 0, 1, 1.0)]  # dgrad
-    out += [(3 * h, h, M, 1, 1, 1.0), (h, h, M, 1, 1, 1.0), (f, h, M, 1, 1, 1.0), (h, f, M, 1, 1, 1.0)]  # wgrad
+    for rows, wt in ((2 * M, 0.5 * fp), (M, 1.0 - fp)) if fd else ((M, 1.0),):
+        if wt <= 0:
+            continue
+        if fd:
+            out += [(Mm, N, K, 0, 0, wt) for (Mm, N, K) in layer(rows)]  # recompute forward
+        out += [(Mm, N, K, 0, 1, wt) for (Mm, N, K) in dgrad(rows)]
+        out += [(Mm, N, K, 1, 1, wt) for (Mm, N, K) in wgrad(rows)]
     wl = 1.0 / shape.n_layer
     if fd:
-        out += [(2 * M, Vp, h, 0, 0, 0.5 * wl), (M, Vp, h, 0, 0, wl)]
-    else:
-        out += [(M, Vp, h, 0, 0, wl)]
-    out += [(M, h, Vp, 0, 1, wl), (Vp, h, M, 1, 1, wl)]
-    return out
+        out += [(2 * M, Vp, h, 0, 0, 0.5 * wl)]
+    for rows, wt in ((2 * M, 0.5 * fp), (M, 1.0 - fp)) if fd else ((M, 1.0),):
+        if wt <= 0:
+            continue
+        if fd:
+            out += [(rows, Vp, h, 0, 0, wt * wl)]
+        else:
+            out += [(rows, Vp, h, 0, 0, wt * wl)]
+        out += [(rows, h, Vp, 0, 1, wt * wl), (Vp, h, rows, 1, 1, wt * wl)]
+    merged = {}  # the same shape from several roles: one entry, weights summed
+    for (Mm, N, K, a, b, w) in out:
+        merged[(Mm, N, K, a, b)] = merged.get((Mm, N, K, a, b), 0.0) + w
+    return [k + (w,) for k, w in merged.items()]
 
 
-def gemm_roofline(stream_handle, peak_tflops, shape=None, cfg=None, workspace=True):
+def gemm_roofline(stream_handle, peak_tflops, shape=None, cfg=None, workspace=True, bwd_pair_frac=None):
     """Live CUDA-event timing of the stage GEMMs (the dominant kernel family) at the
     workload's shapes as the step runs them (roofline_shapes), on the trainer's device,
     with the split-K workspace the trainer's chain streams use, each shape's launches
@@ -253,7 +269,7 @@ def gemm_roofline(stream_handle, peak_tflops, shape=None, cfg=None, workspace=Tr
     from paper_2107_06925_b200.gpt import PRESETS
     shape = shape or PRESETS[SHAPE_NAME]
     cfg = cfg or CFG
-    shapes = roofline_shapes(shape, cfg)
+    shapes = roofline_shapes(shape, cfg, bwd_pair_frac)
     tot_flops, tot_ms, wsum = 0.0, 0.0, 0.0
     rows = []
     ws = torch.zeros(max(Mm * N for (Mm, N, K, a, b, w) in shapes if not (a and b)), device="cuda") \
@@ -633,7 +649,9 @@ def main():
                                   {"T_predicted_ms": round(e["T_predicted"], 3)} for e in ents[:3]]
         except Exception as e:  # the planner may find nothing feasible
             plans = {"error": str(e)[:200]}
-        rl = gemm_roofline(tr.stream_handle(), peak, shape, CFG)
+        bt = stats.get("backward_tasks") or 0
+        rl = gemm_roofline(tr.stream_handle(), peak, shape, CFG,
+                           bwd_pair_frac=(2.0 * stats.get("fused_backward_pairs", 0) / bt) if bt else None)
         flops_seq = shape.flops_per_seq()
         cpu = None if args.no_cpu_baseline else cpu_port_sample(shape)
         line = {

@@ -1141,11 +1141,16 @@ void gemm(Epi epi, bool a_mn, bool b_mn, int M, int N, int K, const __nv_bfloat1
     const std::string v(e);
     return v == "pair" ? 0 : v == "256" ? 256 : v == "64" ? 64 : 128;
   }();
-  static const int force_split = [] {  // CK_GEMM_SPLIT_BF16=0 disables the workspace route; n>1 forces n slices
+  // The workspace route is OFF unless CK_GEMM_SPLIT_BF16=1 (wave model decides) or n > 1
+  // (n slices), or a caller forces a slice count: graph-timed on B200 it never beat the
+  // best unsplit tile on the 632 / 1264 / 2528-row stage shapes -- the fp32 partial
+  // reduce-adds plus the finalize pass cost more than the wave they fill
+  // (profiles/r02f_gemm_split_sweep.jsonl).
+  static const int force_split = [] {
     const char* e = std::getenv("CK_GEMM_SPLIT_BF16");
-    return e ? atoi(e) : -1;
+    return e ? atoi(e) : 0;
   }();
-  const bool can_split = force_split != 0 && split_ok(epi, M, N, ep);
+  const bool can_split = (force_split != 0 || ep.ksplit >= 1) && split_ok(epi, M, N, ep);
   TilePlan plan = pick_tile(epi, M, N, K, can_split);
   if (force >= 0) plan.choice = force;
   if (ep.tile >= 0) plan.choice = ep.tile;

@@ -91,6 +91,7 @@ struct Stash {
 // stream's layer l+2, the last reader of the buffers it is about to overwrite.
 struct Scratch {
   bf16 *dx[3], *dx2[2], *du[2], *dqkv[2], *dh, *da;
+  bf16 *gin2 = nullptr, *gout2 = nullptr;  // backward pairs: gathered input / scattered output gradient
   float* attn;
   float* ws = nullptr;  // split-K workspace of the chain stream's bf16 GEMMs (gemm.cuh EpiArgs::ws)
   long long ws_elems = 0;
@@ -150,6 +151,8 @@ struct Trainer::Impl {
   // 2B-row pass (the recompute workspace holds 2M rows; fd_in / fd_out per rank gather the
   // two stage inputs and scatter the two outputs).  CK_FD_FUSE=0 disables.
   bool fd_fuse = false;
+  bool bwd_fuse = false;  // backward pairs under forward doubling (CK_BWD_FUSE=0 disables)
+  int fwd_pairs = 0, bwd_pairs = 0, bwd_tasks = 0;  // fused pairs / backward tasks issued (last iteration)
   std::vector<bf16*> fd_in, fd_out;
   std::vector<Stash> rscratch;  // per local rank
   float* loss_dummy = nullptr;  // sink for the recomputed last-stage loss
@@ -354,6 +357,8 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
   {
     const char* e = std::getenv("CK_FD_FUSE");
     I.fd_fuse = I.recompute && c.scaling == pipesim::ScalingStrategy::ForwardDoubling && !(e && e[0] == '0');
+    const char* b = std::getenv("CK_BWD_FUSE");
+    I.bwd_fuse = I.fd_fuse && !(b && b[0] == '0');
   }
   auto alloc_full = [&](Stash& st, bool embed, bool head, int Ls, int pairs = 1) {
       const int M = I.M * pairs;  // rows
@@ -391,7 +396,7 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
         I.fd_in.push_back(I.arena.alloc<bf16>((size_t)2 * M * h));
         I.fd_out.push_back(I.arena.alloc<bf16>((size_t)2 * M * h));
       }
-      st.layers.back().xo = I.arena.alloc<bf16>((size_t)M * h);
+      st.layers.back().xo = I.arena.alloc<bf16>((size_t)(I.fd_fuse ? 2 : 1) * M * h);  // pairs: 2M rows
       I.rscratch.push_back(std::move(st));
     }
     I.loss_dummy = I.arena.alloc<float>(1);
@@ -414,15 +419,20 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
   // ---- per-rank scratch and streams
   for (int k = 0; k < n_ranks; ++k) {
     Scratch sc;
-    for (auto& b : sc.dx) b = I.arena.alloc<bf16>((size_t)M * h);
+    const int pm = I.fd_fuse ? 2 : 1;  // backward pairs run on 2M rows
+    for (auto& b : sc.dx) b = I.arena.alloc<bf16>((size_t)pm * M * h);
     for (int j = 0; j < 2; ++j) {
-      sc.dx2[j] = I.arena.alloc<bf16>((size_t)M * h);
-      sc.du[j] = I.arena.alloc<bf16>((size_t)M * f);
-      sc.dqkv[j] = I.arena.alloc<bf16>((size_t)M * 3 * h);
+      sc.dx2[j] = I.arena.alloc<bf16>((size_t)pm * M * h);
+      sc.du[j] = I.arena.alloc<bf16>((size_t)pm * M * f);
+      sc.dqkv[j] = I.arena.alloc<bf16>((size_t)pm * M * 3 * h);
     }
-    sc.dh = I.arena.alloc<bf16>((size_t)M * h);
-    sc.da = I.arena.alloc<bf16>((size_t)M * h);
-    sc.attn = I.arena.alloc<float>(ops::attn_bwd_scratch_floats(I.B, shape.seq, H));
+    sc.dh = I.arena.alloc<bf16>((size_t)pm * M * h);
+    sc.da = I.arena.alloc<bf16>((size_t)pm * M * h);
+    if (I.fd_fuse) {
+      sc.gin2 = I.arena.alloc<bf16>((size_t)2 * M * h);
+      sc.gout2 = I.arena.alloc<bf16>((size_t)2 * M * h);
+    }
+    sc.attn = I.arena.alloc<float>(ops::attn_bwd_scratch_floats(pm * I.B, shape.seq, H));
     // split-K workspace: the widest chain GEMM output (fused forward pairs: 2M rows)
     sc.ws_elems = (long long)(I.fd_fuse ? 2 : 1) * M * std::max(3 * h, f);
     if (std::getenv("CK_GEMM_SPLIT_BF16") && std::string(std::getenv("CK_GEMM_SPLIT_BF16")) == "0") sc.ws_elems = 0;
@@ -682,28 +692,45 @@ void Trainer::stage_forward(int rank, int s, Stash& X, const bf16* x, bf16* out_
   }
 }
 
-void Trainer::backward_task(int rank, int p, int mb, int s) {
+// pairs = 2 (forward doubling, backward_pair): the backwards of micro-batches mb, mb+1 --
+// adjacent on the worker -- as ONE pass over 2B sequences: the two stashed stage inputs
+// are gathered for the recompute, the two incoming gradients gathered, every GEMM runs
+// on 2M rows (the weight gradients with K = 2M: one fp32 accumulate instead of two), and
+// the 2M-row input gradient is scattered to the two outgoing messages.
+void Trainer::backward_task(int rank, int p, int mb, int s, int pairs) {
   Impl& I = *d_;
   const ModelShape& m = I.m;
-  const int h = m.hidden, f = m.ffn, M = I.M, H = m.heads, r = rank / I.D;
+  const int h = m.hidden, f = m.ffn, M1 = I.M, M = I.M * pairs, H = m.heads, r = rank / I.D;
+  const size_t msg_bytes = (size_t)M1 * h * sizeof(bf16);
   cudaStream_t st = I.stream_of(rank);
   Copy& cp = I.copies.at({rank, p});
   StageState& S = I.stages.at(s);
   const StageLayout& L = S.L;
   const bf16* w = S.w16;
   float* gw = cp.grad;
-  const auto it = I.slot_of.find({rank, p, mb, s});
-  if (it == I.slot_of.end()) throw capi::InternalError("backward without stashed activation");
-  const int slot = it->second;
-  I.slot_of.erase(it);
-  Stash& Xslot = cp.slots[slot];
+  int slots[2] = {-1, -1};
+  for (int k = 0; k < pairs; ++k) {
+    const auto it = I.slot_of.find({rank, p, mb + k, s});
+    if (it == I.slot_of.end()) throw capi::InternalError("backward without stashed activation");
+    slots[k] = it->second;
+    I.slot_of.erase(it);
+  }
+  Stash& Xslot = cp.slots[slots[0]];
   Scratch& sc = I.scratch[rank - I.first];
   const size_t tok0 = (size_t)(r * I.N + mb) * I.B * m.seq;
   const bf16* stage_in = s == 0 ? Xslot.x0 : I.msgs.at(I.msg_key(r, mb, s - 1, 0)).buf;
+  if (pairs == 2) {  // gather the two stage inputs (kept until this task: stash / inbox)
+    bf16* xin2 = I.fd_in[rank - I.first];
+    for (int k = 0; k < 2; ++k) {
+      const bf16* src = s == 0 ? cp.slots[slots[k]].x0 : I.msgs.at(I.msg_key(r, mb + k, s - 1, 0)).buf;
+      CK_CUDA(cudaMemcpyAsync(xin2 + (size_t)k * M1 * h, src, msg_bytes, cudaMemcpyDeviceToDevice, st));
+    }
+    stage_in = xin2;
+  }
   Stash& X = I.recompute ? I.rscratch[rank - I.first] : Xslot;
   if (I.recompute) {  // rebuild the stage's activations from its stashed input
     Stash& Wk = I.rscratch[rank - I.first];
-    stage_forward(rank, s, Wk, stage_in, L.has_head ? Wk.xfinal : Wk.layers.back().xo, tok0, I.loss_dummy);
+    stage_forward(rank, s, Wk, stage_in, L.has_head ? Wk.xfinal : Wk.layers.back().xo, tok0, I.loss_dummy, pairs);
   }
 
   // Activation-gradient chain on the rank stream `st`; weight and bias gradients on the
@@ -738,14 +765,26 @@ void Trainer::backward_task(int rank, int p, int mb, int s) {
                        gw + L.lnf_b, gw + L.layers[L.n_layers - 1].b_fc2, M, h, st);
     dxo = d;
     I.launches_per_step += 3;
-  } else {
+  } else if (pairs == 1) {
     const Msg& in = I.msgs.at(I.msg_key(r, mb, s, 1));
     I.consume(in, st);
     dxo = in.buf;
+  } else {  // gather the two incoming gradients
+    for (int k = 0; k < 2; ++k) {
+      const Msg& in = I.msgs.at(I.msg_key(r, mb + k, s, 1));
+      I.consume(in, st);
+      CK_CUDA(cudaMemcpyAsync(sc.gin2 + (size_t)k * M1 * h, in.buf, msg_bytes, cudaMemcpyDeviceToDevice, st));
+    }
+    dxo = sc.gin2;
   }
-  const Msg* out_msg = (s > 0) ? &I.msgs.at(I.msg_key(r, mb, s - 1, 1)) : nullptr;
-  if (out_msg) out_msg->before_produce(st);
-  bf16* dx_stage = out_msg ? out_msg->buf : nullptr;
+  const Msg* out_msgs[2] = {nullptr, nullptr};
+  for (int k = 0; k < pairs && s > 0; ++k) {
+    out_msgs[k] = &I.msgs.at(I.msg_key(r, mb + k, s - 1, 1));
+    out_msgs[k]->before_produce(st);
+  }
+  const Msg* out_msg = out_msgs[0];
+  // a single message is produced in place; a pair's 2M rows go through scratch, then split
+  bf16* dx_stage = out_msg ? (pairs == 1 ? out_msg->buf : sc.gout2) : nullptr;
   for (int l = L.n_layers - 1; l >= 0; --l) {
     const LayerOffsets& o = L.layers[l];
     LayerStash& A = X.layers[l];
@@ -779,7 +818,7 @@ void Trainer::backward_task(int rank, int p, int mb, int s) {
     fork();
     gemm::gemm(gemm::kAccF32, true, true, h, h, M, dx2, h, A.a, h, epi(gw + o.w_o, h), ws);
     gemm::gemm(gemm::kStoreBF16, false, true, M, h, h, dx2, h, w + o.w_o, h, on_chain(epi(sc.da, h), sc), st);
-    ops::attn_bwd_tc(A.qkv, A.a, sc.da, A.lse, dqkv, sc.attn, I.B, m.seq, H, m.causal, st, gw + o.b_qkv);
+    ops::attn_bwd_tc(A.qkv, A.a, sc.da, A.lse, dqkv, sc.attn, I.B * pairs, m.seq, H, m.causal, st, gw + o.b_qkv);
     fork();
     gemm::gemm(gemm::kAccF32, true, true, 3 * h, h, M, dqkv, 3 * h, A.h1, h, epi(gw + o.w_qkv, h), ws);
     side_done(l);
@@ -794,16 +833,23 @@ void Trainer::backward_task(int rank, int p, int mb, int s) {
     ops::embed_bwd(I.tokens + tok0, dxo, gw + L.wte, gw + L.wpe, M, m.seq, h, st);
     I.launches_per_step += 1;
   } else {
-    out_msg->after_produce(st);  // the gradient leaves before the side stream is joined
+    for (int k = 0; k < pairs; ++k) {  // the gradient leaves before the side stream is joined
+      if (pairs == 2)
+        CK_CUDA(cudaMemcpyAsync(out_msgs[k]->buf, dx_stage + (size_t)k * M1 * h, msg_bytes, cudaMemcpyDeviceToDevice,
+                                st));
+      out_msgs[k]->after_produce(st);
+    }
   }
   if (side) {  // join: the side stream read the input message and the stash
     CK_CUDA(cudaEventRecord(sc.join[0], ws));
     CK_CUDA(cudaStreamWaitEvent(st, sc.join[0], 0));
   }
   // this task was the last reader of its input messages
-  if (s > 0) I.msgs.at(I.msg_key(r, mb, s - 1, 0)).after_last_use(st);
-  if (s + 1 < I.D) I.msgs.at(I.msg_key(r, mb, s, 1)).after_last_use(st);
-  cp.free_slots.push_back(slot);
+  for (int k = 0; k < pairs; ++k) {
+    if (s > 0) I.msgs.at(I.msg_key(r, mb + k, s - 1, 0)).after_last_use(st);
+    if (s + 1 < I.D) I.msgs.at(I.msg_key(r, mb + k, s, 1)).after_last_use(st);
+    cp.free_slots.push_back(slots[k]);
+  }
 }
 
 namespace {
@@ -928,6 +974,7 @@ void Trainer::begin_iteration() {
   if (I.it.open) throw pipesim::InvalidConfigError("iteration already open");
   if (I.coll_order.empty()) plan_sync(I);
   I.launches_per_step = 0;
+  I.fwd_pairs = I.bwd_pairs = I.bwd_tasks = 0;
   I.slot_of.clear();
   for (auto& kv : I.copies) {
     Copy& cp = kv.second;
@@ -998,7 +1045,7 @@ void Trainer::run_task(const pipesim::Task& t) {
       I.cur_span = &sp;
     }
     if (fwd) forward_task(rank, t.pipeline_id, t.micro_batch, t.stage);
-    else backward_task(rank, t.pipeline_id, t.micro_batch, t.stage);
+    else backward_task(rank, t.pipeline_id, t.micro_batch, t.stage), I.bwd_tasks++;
     I.cur_span = nullptr;
     if (I.profiling) {
       sp.b = I.timed_event();
@@ -1045,6 +1092,10 @@ void Trainer::issue_iteration() {
       fused.insert({w, i + 1});
       continue;
     }
+    if (I.bwd_fuse && i + 1 < int(wl.size()) && fuse_backward_pair(wl[i], wl[i + 1])) {
+      fused.insert({w, i + 1});
+      continue;
+    }
     run_task(wl[i]);
   }
   end_iteration();
@@ -1080,6 +1131,7 @@ bool Trainer::fuse_forward_pair(const pipesim::Task& t, const pipesim::Task& nex
       I.cur_span = &sp;
     }
     forward_pair(rank, t.pipeline_id, t.micro_batch, t.stage);
+    I.fwd_pairs++;
     I.cur_span = nullptr;
     if (I.profiling) {  // the pair's span goes to its first task, the second gets an empty one
       sp.b = I.timed_event();
@@ -1088,6 +1140,58 @@ bool Trainer::fuse_forward_pair(const pipesim::Task& t, const pipesim::Task& nex
       Impl::TaskSpan sp2{rank, int(next.kind), next.pipeline_id, next.micro_batch, next.stage, sp.b, sp.b, {}};
       I.spans.push_back(sp2);
     }
+  }
+  return true;
+}
+
+// Adjacent backwards of micro-batches (m, m+1) of the same copy (the forward-doubling
+// expansion, whose recompute workspace holds 2M rows) run as one backward pass over 2M
+// rows (backward_task with pairs = 2).  Fused only when both incoming gradients have
+// been issued already -- otherwise false and the two tasks run one by one -- so the
+// pair never waits on a producer the host has not enqueued.  Same checks and
+// bookkeeping as two run_task calls.
+bool Trainer::fuse_backward_pair(const pipesim::Task& t, const pipesim::Task& next) {
+  Impl& I = *d_;
+  Impl::IterState& S = I.it;
+  if (t.kind != TaskKind::Backward || next.kind != TaskKind::Backward || next.pipeline_id != t.pipeline_id ||
+      next.stage != t.stage || next.worker != t.worker || next.micro_batch != t.micro_batch + 1)
+    return false;
+  for (const pipesim::Task* u : {&t, &next}) {
+    const std::array<int, 4> self{1, u->pipeline_id, u->micro_batch, u->stage};
+    if (S.issued.count(self)) throw pipesim::InvalidConfigError("task issued twice in one iteration");
+    if (!S.issued.count({0, u->pipeline_id, u->micro_batch, u->stage}) ||
+        (u->stage < I.D - 1 && !S.issued.count({1, u->pipeline_id, u->micro_batch, u->stage + 1})))
+      return false;  // not both ready: issue them separately (run_task raises if truly missing)
+  }
+  S.issued.insert({1, t.pipeline_id, t.micro_batch, t.stage});
+  S.issued.insert({1, next.pipeline_id, next.micro_batch, next.stage});
+  for (int r = 0; r < I.W; ++r) {
+    const int rank = r * I.D + t.worker;
+    if (!I.local(rank)) continue;
+    Impl::TaskSpan sp{rank, int(t.kind), t.pipeline_id, t.micro_batch, t.stage, nullptr, nullptr, {}};
+    if (I.profiling) {
+      sp.a = I.timed_event();
+      CK_CUDA(cudaEventRecord(sp.a, I.stream_of(rank)));
+      I.cur_span = &sp;
+    }
+    backward_task(rank, t.pipeline_id, t.micro_batch, t.stage, 2);
+    I.bwd_pairs++;
+    I.bwd_tasks += 2;
+    I.cur_span = nullptr;
+    if (I.profiling) {  // the pair's span goes to its first task, the second gets an empty one
+      sp.b = I.timed_event();
+      CK_CUDA(cudaEventRecord(sp.b, I.stream_of(rank)));
+      I.spans.push_back(sp);
+      Impl::TaskSpan sp2{rank, int(next.kind), next.pipeline_id, next.micro_batch, next.stage, sp.b, sp.b, {}};
+      I.spans.push_back(sp2);
+    }
+    for (int k = 0; k < 2; ++k)
+      if (--S.copy_bwd_left[{rank, t.pipeline_id}] == 0) {
+        const int c = S.copy_done[t.stage]++;
+        CK_CUDA(cudaEventRecord(I.stage_done_ev.at(t.stage).at(c), I.stream_of(rank)));
+      }
+    S.bwd_left[t.stage] -= 2;
+    if (S.bwd_left[t.stage] == 0) drain_collectives(I, false);
   }
   return true;
 }
@@ -1466,6 +1570,9 @@ std::string Trainer::stats_json() const {
   }
   j.set("peak_stash_bytes_per_rank", std::move(sb));
   j.set("launches_per_step", Value::integer(I.graph_exec ? I.graph_kernels : I.launches_per_step));
+  j.set("fused_forward_pairs", Value::integer(I.fwd_pairs));
+  j.set("fused_backward_pairs", Value::integer(I.bwd_pairs));
+  j.set("backward_tasks", Value::integer(I.bwd_tasks));
   j.set("graph", Value::boolean(I.graph_exec != nullptr));
   j.set("steps", Value::integer(I.steps));
   return json::dump(j, -1);

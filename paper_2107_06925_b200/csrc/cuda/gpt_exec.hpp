@@ -66,12 +66,13 @@ class Trainer {
  private:
   void issue_iteration();
   void forward_task(int rank, int p, int mb, int s);
-  void backward_task(int rank, int p, int mb, int s);
+  void backward_task(int rank, int p, int mb, int s, int pairs = 1);
   void stage_forward(int rank, int s, Stash& X, const __nv_bfloat16* x, __nv_bfloat16* out_final,
                      size_t tok0, float* loss, int pairs = 1);
   // Forward doubling: micro-batches mb, mb+1 (adjacent forwards of one copy) as one 2B-row pass
   void forward_pair(int rank, int p, int mb, int s);
   bool fuse_forward_pair(const pipesim::Task& t, const pipesim::Task& next);
+  bool fuse_backward_pair(const pipesim::Task& t, const pipesim::Task& next);
   std::unique_ptr<Impl> d_;
 };
 

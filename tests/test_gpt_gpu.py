@@ -277,3 +277,54 @@ def test_adamw_two_steps_vs_numpy():
             assert cos >= 0.99 and rel <= 0.1, (it, s, cos, rel)
         params = after
     tr.close()
+
+
+def test_sync_plan_follows_dessim_on_the_given_profile():
+    """a24: eager-sync-opt decided by dessim::simulate on the CostProfile handed to the
+    trainer (normally the measured one, bench.py), per stage = every holder eager."""
+    shape = PRESETS["tiny"]
+    cfg = P.PipelineConfig("chimera", 4, 1, 8, 2, 1)
+    tr = Trainer(shape, cfg, lr=0.1)
+    prof = P.CostProfile(F_t=1.3, backward_ratio=2.2, alpha=0.05, beta=1e-4, L_grad=4000.0, L_act=8.0)
+    tr.set_sync_policy("eager-sync-opt")
+    tr.set_cost_profile(prof)
+    plan = tr.sync_plan()
+    sim = P.simulate(tr.schedule_text, prof, "eager-sync-opt")
+    want = {}
+    for ev in sim["allreduce_events"]:
+        want[ev["stage"]] = want.get(ev["stage"], True) and ev["eager"]
+    assert {e["stage"]: e["eager"] for e in plan["order"]} == want
+    assert plan["policy"] == "eager-sync-opt" and abs(plan["profile"]["F_t"] - 1.3) < 1e-12
+    # the plan changes the launch order only: one iteration still matches the oracle
+    tr.init_params(0)
+    params = [tr.get_params(s).astype(np.float64) for s in range(cfg.D)]
+    tok, lab = synthetic_batch(shape, cfg.mini_batch(), 4)
+    tr.set_batch(tok, lab)
+    tr.step()
+    _, _, g_ref, _ = O.run_iteration(json.loads(tr.schedule_text), _oshape(shape), params, tok, lab, 0.1)
+    for s in range(cfg.D):
+        g = (params[s] - tr.get_params(s).astype(np.float64)) / 0.1
+        assert np.linalg.norm(g - g_ref[s]) / np.linalg.norm(g_ref[s]) <= 3e-2
+    tr.close()
+
+
+def test_backward_pair_fusion_matches_unfused(monkeypatch):
+    """Forward doubling: the two backwards of a virtual micro-batch run as one 2B-row pass
+    (backward_pair) -- same results as two separate backwards (only the accumulation
+    order of the atomic gradient sums differs)."""
+    cfg = P.PipelineConfig("chimera", 4, 1, 8, 1, 1, "forward-doubling")
+    shape = PRESETS["tiny"]
+    out = {}
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("CK_BWD_FUSE", fuse)
+        tr = Trainer(shape, cfg, lr=0.5)
+        tr.init_params(0)
+        tok, lab = synthetic_batch(shape, cfg.mini_batch(), 9)
+        tr.set_batch(tok, lab)
+        losses = [tr.step() for _ in range(2)]
+        out[fuse] = (losses, [tr.get_params(s).astype(np.float64) for s in range(cfg.D)])
+        tr.close()
+    (l1, p1), (l0, p0) = out["1"], out["0"]
+    assert np.allclose(l1, l0, rtol=1e-5), (l1, l0)
+    for a, b in zip(p1, p0):
+        assert np.max(np.abs(a - b)) <= 1e-5 * max(1.0, np.max(np.abs(b)))
