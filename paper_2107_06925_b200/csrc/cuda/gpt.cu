@@ -21,6 +21,7 @@
 // slot pools whose live peak per worker equals analysis::memory_profile().act_counts.
 // The whole iteration is captured once into a CUDA graph and replayed.
 #include <algorithm>
+#include <cstdio>
 #include <array>
 #include <cstdlib>
 #include <cstring>
@@ -1084,10 +1085,20 @@ void Trainer::end_iteration() {
 void Trainer::issue_iteration() {
   Impl& I = *d_;
   begin_iteration();
+  // CK_TRACE_ISSUE=1 (debug): print every task as it is issued and synchronise after it,
+  // so a fault or a hang is pinned to one task
+  static const bool trace = std::getenv("CK_TRACE_ISSUE") != nullptr;
   std::set<std::pair<int, int>> fused;  // (worker, index) issued as the second of a pair
   for (const auto& [w, i] : I.order) {
     if (fused.count({w, i})) continue;
     const auto& wl = I.sched.per_worker[w];
+    if (trace) {
+      const Task& t = wl[i];
+      std::fprintf(stderr, "[issue] w%d i%d %s p%d m%d s%d\n", w, i, t.kind == TaskKind::Forward ? "F" : "B",
+                   t.pipeline_id, t.micro_batch, t.stage);
+      std::fflush(stderr);
+      CK_CUDA(cudaDeviceSynchronize());
+    }
     if (I.fd_fuse && i + 1 < int(wl.size()) && fuse_forward_pair(wl[i], wl[i + 1])) {
       fused.insert({w, i + 1});
       continue;
