@@ -38,6 +38,9 @@ CONFIGS = {
     # so the per-worker bubble is observable (closed form 1/4 at N=4, 1/9 at N=8)
     "gpt2-medium-d4": ("gpt2-medium", dict(scheme="chimera", D=4, W=1, N=4, B=4, f=1, scaling="direct"),
                        "GPT-2 medium Chimera D=4 N=4 W=1 B=4 (configs[1] model, one pipeline pair)"),
+    "gpt2-medium-d4-n8fd": ("gpt2-medium", dict(scheme="chimera", D=4, W=1, N=8, B=4, f=1,
+                                                scaling="forward-doubling"),
+                            "GPT-2 medium Chimera D=4 N=8 W=1 B=4 forward-doubling + recompute (configs[1] model)"),
     "gpt2-medium-d4-n8bh": ("gpt2-medium", dict(scheme="chimera", D=4, W=1, N=8, B=4, f=1,
                                                 scaling="backward-halving"),
                             "GPT-2 medium Chimera D=4 N=8 W=1 B=4 backward-halving (configs[1] model)"),

@@ -1312,7 +1312,12 @@ float Trainer::step() {
       long long kernels = 0;
       for (cudaGraphNode_t nd : nodes) {
         cudaGraphNodeType t;
-        CK_CUDA(cudaGraphNodeGetType(nd, &t));
+        // stream memory operations (cross-process flags) are driver-only node types the
+        // runtime enum cannot name: not kernels, and the query's error is not sticky
+        if (cudaGraphNodeGetType(nd, &t) != cudaSuccess) {
+          (void)cudaGetLastError();
+          continue;
+        }
         kernels += t == cudaGraphNodeTypeKernel;
       }
       I.graph_kernels = kernels;

@@ -1,5 +1,8 @@
 """Multi-process parity: the tiny GPT under Chimera D=4 W=2 on G processes (one GPU
-each) must produce the same loss and weights as the single-process run."""
+each) must produce the same loss and weights as the single-process run.
+MP_OPT=adamw: both runs use AdamW; MP_OPT=zero: the multi-process run shards the AdamW
+moments over each stage's holders (ZeRO-1: reduce-scatter, shard update, all-gather)
+while the single-process reference keeps them whole -- same mathematics."""
 import json, os, sys
 import numpy as np
 import torch
@@ -16,8 +19,12 @@ shape = PRESETS["tiny"]
 cfg = (P.PipelineConfig("chimera", 4, 1, 8, 1, 1, "forward-doubling") if os.environ.get("MP_CFG") == "fd"
        else P.PipelineConfig("chimera", 4, 2, 4, 2, 1))
 per = cfg.W * cfg.D // world
-tr = Trainer(shape, cfg, lr=0.5, first_rank=rank * per, n_ranks=per)
+LR = 0.5 if os.environ.get("MP_OPT", "sgd") == "sgd" else 1e-3
+tr = Trainer(shape, cfg, lr=LR, first_rank=rank * per, n_ranks=per)
 tr.connect()
+OPT = os.environ.get("MP_OPT", "sgd")
+if OPT != "sgd":
+    tr.set_optimizer("adamw", 0.9, 0.99, 1e-4, 0.01, zero=OPT == "zero")
 tr.init_params(0)
 losses = []
 for it in range(3):
@@ -36,7 +43,9 @@ if rank == 0:
             if s in merged:
                 assert np.array_equal(merged[s], v), f"stage {s} copies differ across processes"
             merged[s] = v
-    ref = Trainer(shape, cfg, lr=0.5)
+    ref = Trainer(shape, cfg, lr=LR)
+    if OPT != "sgd":
+        ref.set_optimizer("adamw", 0.9, 0.99, 1e-4, 0.01, zero=False)
     ref.init_params(0)
     rl = []
     for it in range(3):
@@ -44,7 +53,8 @@ if rank == 0:
         ref.set_batch(tok, lab)
         rl.append(ref.step())
     md = max(float(np.abs(merged[s] - ref.get_params(s)).max()) for s in range(cfg.D))
-    print(json.dumps({"world": world, "cfg": os.environ.get("MP_CFG", "direct"), "losses": losses, "ref_losses": rl,
+    print(json.dumps({"world": world, "cfg": os.environ.get("MP_CFG", "direct"), "opt": OPT, "losses": losses,
+                      "ref_losses": rl,
                       "max_abs_param_diff": md}))
     assert md < 1e-3 and all(abs(a - b) <= 1e-4 * abs(b) for a, b in zip(losses, rl)), "multi-process != single"
 dist.barrier()
