@@ -41,6 +41,8 @@ CONFIGS = {
     "gpt2-medium-d4-n8fd": ("gpt2-medium", dict(scheme="chimera", D=4, W=1, N=8, B=4, f=1,
                                                 scaling="forward-doubling"),
                             "GPT-2 medium Chimera D=4 N=8 W=1 B=4 forward-doubling + recompute (configs[1] model)"),
+    "gpt2-1.3b-d4": ("gpt2-1.3b", dict(scheme="chimera", D=4, W=1, N=16, B=2, f=1, scaling="forward-doubling"),
+                     "GPT-2 1.3B s=632 Chimera D=4 N=16 B=2 forward-doubling + recompute (configs[3] model, 4 stages)"),
     "gpt2-medium-d4-n8bh": ("gpt2-medium", dict(scheme="chimera", D=4, W=1, N=8, B=4, f=1,
                                                 scaling="backward-halving"),
                             "GPT-2 medium Chimera D=4 N=8 W=1 B=4 backward-halving (configs[1] model)"),
@@ -629,6 +631,11 @@ def main():
                     fh.write(text)
         # dessim::simulate (proj/src/dessim.cpp:60-181) on the measured F_t, B/F, alpha, beta:
         # per-worker idle / compute span, averaged -- the simulated counterpart of `measured`
+        replay_bubble = None
+        if one_rank_per_gpu:
+            from paper_2107_06925_b200.gpt import replay_measured
+            rp = replay_measured({"tasks": tasks}, sched, prof_b200.alpha + prof_b200.beta * prof_b200.L_act)
+            replay_bubble = round(rp["mean"], 4)
         sim = P.simulate(sched, prof_b200, "eager-sync")
         span = sim["compute_makespan"]
         dessim_bubble = round(sum(sim["per_worker_idle"]) / len(sim["per_worker_idle"]) / span, 4) if span else None
@@ -682,6 +689,7 @@ def main():
                        "measured_B/F": round(ratio, 3),
                        "reference_schedule_at_measured_B/F": str(bub_at_ratio),
                        "dessim_at_measured_profile": dessim_bubble,
+                       "list_schedule_at_measured_task_times": replay_bubble,
                        "note": (None if one_rank_per_gpu else
                                 f"{per} logical ranks share each GPU: per-rank bubble not observable")},
             "perfmodel": {"predicted_ms": round(pred, 3), "measured_ms": round(ms, 3),

@@ -197,6 +197,13 @@ struct Trainer::Impl {
   };
   std::vector<TaskSpan> spans;
   TaskSpan* cur_span = nullptr;  // the span being issued (profiling)
+  bool capturing_profile = false;  // profile_step captures its iteration into a graph
+  // A timing event: recorded as an event-record NODE when the profiled iteration is
+  // being captured (cudaEventRecordExternal), a plain record otherwise.
+  void mark(cudaEvent_t e, cudaStream_t st) {
+    if (capturing_profile) CK_CUDA(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+    else CK_CUDA(cudaEventRecord(e, st));
+  }
   // Stream wait for a message, bracketed by events while profiling: the bracket's
   // length is time the rank's stream sat idle inside the task (not busy), so the
   // measured bubble uses busy = span - stalls (dessim's busy = compute only).
@@ -542,9 +549,9 @@ Trainer::~Trainer() {
 void Trainer::Impl::consume(const Msg& in, cudaStream_t st) {
   if (!profiling || !cur_span) return in.before_consume(st);
   cudaEvent_t a = timed_event(), b = timed_event();
-  CK_CUDA(cudaEventRecord(a, st));
+  mark(a, st);
   in.before_consume(st);
-  CK_CUDA(cudaEventRecord(b, st));
+  mark(b, st);
   cur_span->stalls.emplace_back(a, b);
 }
 
@@ -912,10 +919,10 @@ void sync_stage_body(Trainer::Impl& I, int s);
 void sync_stage(Trainer::Impl& I, int s) {
   if (!I.profiling) return sync_stage_body(I, s);
   Trainer::Impl::CollSpan c{s, I.stage_eager.count(s) && I.stage_eager.at(s), I.timed_event(), nullptr};
-  CK_CUDA(cudaEventRecord(c.a, I.comm_stream));
+  I.mark(c.a, I.comm_stream);
   sync_stage_body(I, s);
   c.b = I.timed_event();
-  CK_CUDA(cudaEventRecord(c.b, I.comm_stream));
+  I.mark(c.b, I.comm_stream);
   I.coll_spans.push_back(c);
 }
 
@@ -1042,7 +1049,7 @@ void Trainer::run_task(const pipesim::Task& t) {
     Impl::TaskSpan sp{rank, int(t.kind), t.pipeline_id, t.micro_batch, t.stage, nullptr, nullptr, {}};
     if (I.profiling) {
       sp.a = I.timed_event();
-      CK_CUDA(cudaEventRecord(sp.a, I.stream_of(rank)));
+      I.mark(sp.a, I.stream_of(rank));
       I.cur_span = &sp;
     }
     if (fwd) forward_task(rank, t.pipeline_id, t.micro_batch, t.stage);
@@ -1050,7 +1057,7 @@ void Trainer::run_task(const pipesim::Task& t) {
     I.cur_span = nullptr;
     if (I.profiling) {
       sp.b = I.timed_event();
-      CK_CUDA(cudaEventRecord(sp.b, I.stream_of(rank)));
+      I.mark(sp.b, I.stream_of(rank));
       I.spans.push_back(sp);
     }
     if (!fwd) {
@@ -1138,7 +1145,7 @@ bool Trainer::fuse_forward_pair(const pipesim::Task& t, const pipesim::Task& nex
     Impl::TaskSpan sp{rank, int(t.kind), t.pipeline_id, t.micro_batch, t.stage, nullptr, nullptr, {}};
     if (I.profiling) {
       sp.a = I.timed_event();
-      CK_CUDA(cudaEventRecord(sp.a, I.stream_of(rank)));
+      I.mark(sp.a, I.stream_of(rank));
       I.cur_span = &sp;
     }
     forward_pair(rank, t.pipeline_id, t.micro_batch, t.stage);
@@ -1146,7 +1153,7 @@ bool Trainer::fuse_forward_pair(const pipesim::Task& t, const pipesim::Task& nex
     I.cur_span = nullptr;
     if (I.profiling) {  // the pair's span goes to its first task, the second gets an empty one
       sp.b = I.timed_event();
-      CK_CUDA(cudaEventRecord(sp.b, I.stream_of(rank)));
+      I.mark(sp.b, I.stream_of(rank));
       I.spans.push_back(sp);
       Impl::TaskSpan sp2{rank, int(next.kind), next.pipeline_id, next.micro_batch, next.stage, sp.b, sp.b, {}};
       I.spans.push_back(sp2);
@@ -1182,7 +1189,7 @@ bool Trainer::fuse_backward_pair(const pipesim::Task& t, const pipesim::Task& ne
     Impl::TaskSpan sp{rank, int(t.kind), t.pipeline_id, t.micro_batch, t.stage, nullptr, nullptr, {}};
     if (I.profiling) {
       sp.a = I.timed_event();
-      CK_CUDA(cudaEventRecord(sp.a, I.stream_of(rank)));
+      I.mark(sp.a, I.stream_of(rank));
       I.cur_span = &sp;
     }
     backward_task(rank, t.pipeline_id, t.micro_batch, t.stage, 2);
@@ -1191,7 +1198,7 @@ bool Trainer::fuse_backward_pair(const pipesim::Task& t, const pipesim::Task& ne
     I.cur_span = nullptr;
     if (I.profiling) {  // the pair's span goes to its first task, the second gets an empty one
       sp.b = I.timed_event();
-      CK_CUDA(cudaEventRecord(sp.b, I.stream_of(rank)));
+      I.mark(sp.b, I.stream_of(rank));
       I.spans.push_back(sp);
       Impl::TaskSpan sp2{rank, int(next.kind), next.pipeline_id, next.micro_batch, next.stage, sp.b, sp.b, {}};
       I.spans.push_back(sp2);
@@ -1333,19 +1340,39 @@ std::string Trainer::profile_step() {
   I.spans.clear();
   I.coll_spans.clear();
   I.ev_next = 0;
+  // Like step(): once a graph is in use the profiled iteration is captured (timing
+  // events become event-record nodes) and replayed, so the spans show the GPU running
+  // the iteration -- not the host issuing thousands of kernels into an idle device.
+  const bool graphed = I.use_graph && I.steps > 0;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  if (graphed) CK_CUDA(cudaStreamBeginCapture(I.main_stream, cudaStreamCaptureModeThreadLocal));
+  I.capturing_profile = graphed;
   cudaEvent_t t0 = I.timed_event();
-  CK_CUDA(cudaEventRecord(t0, I.main_stream));
+  I.mark(t0, I.main_stream);
   I.profiling = true;
   try {
     issue_iteration();
   } catch (...) {
     I.profiling = false;
+    I.capturing_profile = false;
+    if (graphed && cudaStreamEndCapture(I.main_stream, &g) == cudaSuccess && g) cudaGraphDestroy(g);
     throw;
   }
   I.profiling = false;
   cudaEvent_t t1 = I.timed_event();
-  CK_CUDA(cudaEventRecord(t1, I.main_stream));
+  I.mark(t1, I.main_stream);
+  I.capturing_profile = false;
+  if (graphed) {
+    CK_CUDA(cudaStreamEndCapture(I.main_stream, &g));
+    CK_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    CK_CUDA(cudaGraphLaunch(ge, I.main_stream));
+  }
   CK_CUDA(cudaStreamSynchronize(I.main_stream));
+  if (graphed) {
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+  }
   ++I.steps;
   using json::Value;
   Value arr = Value::array();

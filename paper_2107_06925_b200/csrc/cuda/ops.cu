@@ -497,7 +497,13 @@ void layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* 
 void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd, const bf16* g,
                    const bf16* dres, bf16* dx, float* dgamma, float* dbeta, float* dsum, int M, int h,
                    cudaStream_t st) {
-  const int grid = std::min(ceil_div(M, 8), cuda::num_sms());  // one 8-warp CTA per SM (255 registers)
+  // one 8-warp CTA per SM (255 registers); CK_LN_BWD_RPW=n: at least n rows per warp
+  // (fewer CTAs -> fewer column-partial reductions and atomics on small M)
+  static const int rpw = [] {
+    const char* e = std::getenv("CK_LN_BWD_RPW");
+    return e ? std::max(1, atoi(e)) : 1;
+  }();
+  const int grid = std::min(ceil_div(M, 8 * rpw), cuda::num_sms());
   const size_t smem = size_t(dsum ? 24 : 16) * h * sizeof(float);
   switch (h) {
 #define CK_LN(V)                                                                                   \

@@ -327,6 +327,59 @@ def timeline_json(profile: dict, schedule_text: str) -> str:
     return json.dumps(sched)
 
 
+def replay_measured(profile: dict, schedule_text: str, p2p_ms: float = 0.0) -> dict:
+    """The reference's list-scheduling semantics (proj/src/listsched.hpp:52-163: a task
+    starts when its worker is free and its data predecessors F(s-1) / B(s+1) / F(s) have
+    ended, + p2p on cross-worker edges) replayed with the MEASURED compute time of every
+    task (span minus message stalls) instead of uniform F_t / B_t: the bubble this
+    executor's schedule would have if it added no overhead beyond its own task times.
+    Measured bubble vs this isolates the executor's overhead from stage-cost imbalance
+    (which the uniform-cost prediction ignores).  Replica 0's ranks (rank = worker)."""
+    sched = json.loads(schedule_text)
+    D = sched["config"]["D"]
+    dur = {(t["rank"], t["kind"], t["pipeline"], t["micro"], t["stage"]):
+           max(0.0, t["end_ms"] - t["start_ms"] - t.get("stall_ms", 0.0)) for t in profile["tasks"] if t["rank"] < D}
+    pw = sched["per_worker"]
+    where = {}
+    for w, wl in enumerate(pw):
+        for t in wl:
+            where.setdefault((t["kind"], t["pipeline_id"], t["micro_batch"], t["stage"]), w)
+    end, free, head = {}, [0.0] * len(pw), [0] * len(pw)
+    left = sum(len(wl) for wl in pw)
+    while left:
+        progressed = False
+        for w, wl in enumerate(pw):
+            if head[w] >= len(wl):
+                continue
+            t = wl[head[w]]
+            k, p, m, st = t["kind"], t["pipeline_id"], t["micro_batch"], t["stage"]
+            deps = [("Forward", p, m, st - 1)] if k == "Forward" and st > 0 else \
+                   ([("Backward", p, m, st + 1)] if st + 1 < D else []) + [("Forward", p, m, st)] if k == "Backward" else []
+            ready, start = True, free[w]
+            for d in deps:
+                if d not in where:
+                    continue
+                if d not in end:
+                    ready = False
+                    break
+                start = max(start, end[d] + (p2p_ms if where[d] != w else 0.0))
+            if not ready:
+                continue
+            e = start + dur.get((w, k, p, m, st), 0.0)
+            end[(k, p, m, st)] = e
+            free[w] = e
+            head[w] += 1
+            left -= 1
+            progressed = True
+        if not progressed:
+            raise ValueError("replay_measured: dependency cycle")
+    span = max(free)
+    busy = [sum(dur.get((w, t["kind"], t["pipeline_id"], t["micro_batch"], t["stage"]), 0.0) for t in wl)
+            for w, wl in enumerate(pw)]
+    per = [(span - b) / span for b in busy]
+    return {"per_worker": per, "mean": sum(per) / len(per), "span_ms": span}
+
+
 def measured_timeline(profile: dict, schedule_text: str, policy: str = "eager-sync") -> str:
     """A profiled GPU iteration (Trainer.profile_step) as the reference's
     ``pipesim simulate -o`` timeline document (tools/main.cpp:134-170): replica 0's

@@ -1,4 +1,6 @@
-"""Microbenchmark of the non-GEMM stage kernels at the GPT-2-medium workload shapes."""
+"""Microbenchmark of the non-GEMM stage kernels (graph-timed).
+
+    python scripts/bench_small_ops.py [M h f]     (default: GPT-2 medium, 4096 1024 4096)"""
 import json
 import sys
 
@@ -29,7 +31,7 @@ def timeit(fn, it=50):
     return s.elapsed_time(e) / it * 1e3
 
 
-M, h, f = 4096, 1024, 4096
+M, h, f = (int(a) for a in sys.argv[1:4]) if len(sys.argv) > 3 else (4096, 1024, 4096)
 x = torch.randn(M, h, device="cuda").bfloat16()
 dy = torch.randn(M, h, device="cuda").bfloat16()
 dres = torch.randn(M, h, device="cuda").bfloat16()
@@ -50,9 +52,10 @@ for n in (h, 3 * h, f):
     d = torch.randn(M, n, device="cuda").bfloat16()
     bg = torch.zeros(n, device="cuda")
     res[f"bias_grad_{n}"] = timeit(lambda st: K.bias_grad(d, bg, stream=st))
-logits = torch.randn(M, 50304, device="cuda").bfloat16()
+logits = torch.randn(M, 50304, device="cuda").bfloat16()  # noqa: E305
 labels = torch.randint(0, 50257, (M,), device="cuda", dtype=torch.int32)
 ls = torch.zeros(1, device="cuda")
-res["xent_4096x50304"] = timeit(lambda st: K.xent(logits, labels, 50257, 1.0, 1.0, ls, stream=st), it=10)
+res[f"xent_{M}x50304"] = timeit(lambda st: K.xent(logits, labels, 50257, 1.0, 1.0, ls, stream=st), it=10)
+import os  # noqa: E402
 for k, v in res.items():
-    print(json.dumps({"op": k, "us": round(v, 2)}))
+    print(json.dumps({"op": k, "M": M, "h": h, "us": round(v, 2), "ln_bwd_rpw": os.environ.get("CK_LN_BWD_RPW", "1")}))
