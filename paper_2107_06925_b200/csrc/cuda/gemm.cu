@@ -579,8 +579,17 @@ inline int split_k(int epi, int tiles, int slots, int K, int chosen = 0) {
   }();
   if (chosen > 0) return chosen;
   if (epi == kAccF32 && force > 0) return force;
-  if (epi != kAccF32 || tiles >= slots) return 1;
+  if (epi != kAccF32) return 1;
   const int kb = (K + BK - 1) / BK;
+  if (tiles >= slots) {
+    // more than one wave: two slices when they cut the waves x depth product by >= 20 %
+    // (e.g. 75 or 100 CTA-pair tiles on 74 pairs: the weight gradients of GPT-2 1.3B's
+    // QKV / FC layers) -- more slices only add fp32 read-modify-write traffic to the
+    // HBM-resident gradient (graph-timed sweep, profiles/r02r_wgrad_sweep.jsonl)
+    const long long w1 = (long long)((tiles + slots - 1) / slots) * kb;
+    const long long w2 = (long long)((2LL * tiles + slots - 1) / slots) * ((kb + 1) / 2);
+    return (kb >= 16 && w2 * 5 <= w1 * 4) ? 2 : 1;
+  }
   // (more than 4 slices: the extra fp32 atomic traffic costs more than the wave it fills)
   const int kmax = kb / 8 < 1 ? 1 : (kb / 8 > 4 ? 4 : kb / 8);
   auto eff = [&](int ks) {
@@ -1173,7 +1182,7 @@ void gemm(Epi epi, bool a_mn, bool b_mn, int M, int N, int K, const __nv_bfloat1
     throw chimera::capi::InternalError("gemm: split-K epilogue not supported");
   }
   EpiArgs e2 = ep;
-  e2.ksplit = 0;
+  e2.ksplit = epi == kAccF32 ? ep.ksplit : 0;  // fp32 accumulate: a caller-forced slice count stands
   dispatch(plan.choice, epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, e2, st);
 }
 
