@@ -320,20 +320,29 @@ def gemm_roofline(stream_handle, peak_tflops, shape=None, cfg=None, workspace=Tr
     achieved = tot_flops / (tot_ms * 1e-3) / 1e12
     # DRAM bytes per launch of the same shapes from the committed `ncu --set full`
     # capture (scripts/roofline_shapes.py --config ...); null when not captured
-    traffic, tsrc = None, None
+    # (run-weighted like `achieved`: sum_i w_i dram_i / sum_i w_i, beside the algorithmic
+    # operand + output bytes with the same weights)
+    traffic, tsrc, alg = None, None, None
     root = os.path.dirname(os.path.abspath(__file__))
     for cand in (f"profiles/r02_gemm_roofline_ncu_{SHAPE_NAME}_B{cfg['B']}.json",
                  "profiles/r01y_gemm_roofline_ncu.json" if SHAPE_NAME == "gpt2-medium" and cfg["B"] == 4 else None):
         if cand and os.path.exists(os.path.join(root, cand)):
             with open(os.path.join(root, cand)) as fh:
-                traffic = json.load(fh)["avg_dram_bytes_per_launch"]
+                cap = json.load(fh)
+            by_shape = {tuple(l["shape"]): l for l in cap.get("launches", [])}
+            ws = [(w, by_shape.get((Mm, N, K, a, b))) for (Mm, N, K, a, b, w) in shapes]
+            if all(l is not None for _, l in ws):
+                traffic = sum(w * l["dram_bytes"] for w, l in ws) / sum(w for w, _ in ws)
+                alg = sum(w * l["algorithmic_bytes"] for w, l in ws) / sum(w for w, _ in ws)
+            else:
+                traffic = cap["avg_dram_bytes_per_launch"]
             tsrc = cand
             break
     return {"bound": "tensor", "kernel": "ck gemm_bf16 (tcgen05.mma kind::f16, TMA, TMEM; split-K + finalize "
                                         "where chosen), every stage-GEMM shape of the step, run-count weighted",
             "achieved": round(achieved, 1), "peak": peak_tflops, "unit": "TFLOP/s",
             "frac": round(achieved / peak_tflops, 4), "traffic": traffic, "traffic_unit": "bytes/launch",
-            "traffic_source": tsrc,
+            "traffic_source": tsrc, "algorithmic_bytes_per_launch": alg,
             "flops_per_launch_avg": tot_flops / wsum, "avg_launch_ms": tot_ms / wsum, "shapes": rows}
 
 

@@ -64,3 +64,23 @@ def test_gpt_executor_rejects_pipedream_before_touching_the_device():
     from paper_2107_06925_b200.gpt import PRESETS, Trainer
     with pytest.raises(P.InvalidConfigError):
         Trainer(PRESETS["tiny"], P.PipelineConfig("pipedream", 4, 1, 4), lr=0.1)
+
+
+def test_replay_measured_equals_reference_bubble_on_uniform_tasks():
+    """bench.py's `list_schedule_at_measured_task_times`: the reference list-scheduling
+    rule replayed with per-task times.  With uniform F = 1, B = 2 and no stalls it must
+    reproduce analysis::bubble_ratio exactly (proj/src/analysis.cpp:99-137)."""
+    import json
+    from fractions import Fraction
+    from paper_2107_06925_b200 import pipesim as P
+    from paper_2107_06925_b200.gpt import replay_measured
+    for cfg in (P.PipelineConfig("chimera", 4, 1, 4), P.PipelineConfig("chimera", 8, 1, 8),
+                P.PipelineConfig("chimera", 4, 1, 8, 2, 1, "forward-doubling"), P.PipelineConfig("dapple", 4, 1, 8)):
+        text = P.generate_json(cfg, None, -1)
+        sched = json.loads(text)
+        tasks = [{"rank": w, "kind": t["kind"], "pipeline": t["pipeline_id"], "micro": t["micro_batch"],
+                  "stage": t["stage"], "start_ms": 0.0, "end_ms": 1.0 if t["kind"] == "Forward" else 2.0}
+                 for w, wl in enumerate(sched["per_worker"]) for t in wl]
+        rp = replay_measured({"tasks": tasks}, text)
+        want = P.bubble_ratio(text)
+        assert abs(rp["per_worker"][0] - float(Fraction(str(want)))) < 1e-12, (cfg, rp, want)
