@@ -130,9 +130,14 @@ __global__ void __launch_bounds__(192, 2)
   ATTN_CTA(0);
   ATTN_CTA(1);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kSmemBar);
-  uint64_t *q_full = bar, *q_empty = bar + 2, *kv_full = bar + 4, *kv_empty = bar + 6, *s_full = bar + 8,
-           *p_full = bar + 9, *o_done = bar + 10, *s_free = bar + 11, *o_free = bar + 12;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
+  // K and V have separate full / empty barriers: K_j's slot frees when S_j's MMA is done
+  // (not after P_j V_j), so the producer loads K two tiles ahead and the S MMA never waits
+  // on the TMA (measured: with one K+V barrier pair ~570 of the ~2500 cycles per tile went
+  // to waiting for K, scripts/attn_trace.cu)
+  uint64_t *q_full = bar, *q_empty = bar + 2, *k_full = bar + 4, *k_empty = bar + 6, *s_full = bar + 8,
+           *p_full = bar + 9, *o_done = bar + 10, *s_free = bar + 11, *o_free = bar + 12, *v_full = bar + 13,
+           *v_empty = bar + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nq = (seq + kQ - 1) / kQ;
@@ -144,7 +149,8 @@ __global__ void __launch_bounds__(192, 2)
     ptx::tma_prefetch(&tqkv);
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&q_full[s], 1), ptx::mbar_init(&q_empty[s], 1);
-      ptx::mbar_init(&kv_full[s], 1), ptx::mbar_init(&kv_empty[s], 1);
+      ptx::mbar_init(&k_full[s], 1), ptx::mbar_init(&k_empty[s], 1);
+      ptx::mbar_init(&v_full[s], 1), ptx::mbar_init(&v_empty[s], 1);
     }
     ptx::mbar_init(s_full, 1);
     ptx::mbar_init(p_full, 128);
@@ -172,12 +178,14 @@ __global__ void __launch_bounds__(192, 2)
         const int n0 = q.n;
         while (q.valid() && q.n == n0) {
           const int st = g & 1;
-          ptx::mbar_wait_sleep(&kv_empty[st], ((g >> 1) & 1) ^ 1);
+          ptx::mbar_wait_sleep(&k_empty[st], ((g >> 1) & 1) ^ 1);
           ATTN_TRACE(true, g, 0);
-          ptx::mbar_arrive_expect_tx(&kv_full[st], 2 * kTileBytes);
-          ptx::tma_load_2d(smem + kSmemK + st * kTileBytes, &tqkv, &kv_full[st], H * kD + hd * kD,
+          ptx::mbar_arrive_expect_tx(&k_full[st], kTileBytes);
+          ptx::tma_load_2d(smem + kSmemK + st * kTileBytes, &tqkv, &k_full[st], H * kD + hd * kD,
                            row_base + q.j * kKV);
-          ptx::tma_load_2d(smem + kSmemV + st * kTileBytes, &tqkv, &kv_full[st], 2 * H * kD + hd * kD,
+          ptx::mbar_wait_sleep(&v_empty[st], ((g >> 1) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&v_full[st], kTileBytes);
+          ptx::tma_load_2d(smem + kSmemV + st * kTileBytes, &tqkv, &v_full[st], 2 * H * kD + hd * kD,
                            row_base + q.j * kKV);
           ++g;
           q.advance();
@@ -191,7 +199,7 @@ __global__ void __launch_bounds__(192, 2)
       auto issue_s = [&](int g, int n, bool first_of_item) {
         const int st = g & 1, qbuf = n & 1;
         if (first_of_item) mma_wait(&q_full[qbuf], (n >> 1) & 1);
-        mma_wait(&kv_full[st], (g >> 1) & 1);
+        mma_wait(&k_full[st], (g >> 1) & 1);
         ATTN_TRACE(true, g, 1);
         ptx::tc_fence_after();
         const uint32_t sq = ptx::smem_u32(smem + kSmemQ + qbuf * kTileBytes);
@@ -201,6 +209,7 @@ __global__ void __launch_bounds__(192, 2)
           ptx::umma_f16(tmem, ptx::smem_desc_sw128(sq + k * 32, 16, 1024), ptx::smem_desc_sw128(sk + k * 32, 16, 1024),
                         id_s, k > 0);
         ptx::umma_commit(s_full);
+        ptx::umma_commit(&k_empty[st]);  // K_g is read once: free its slot with S_g
       };
       issue_s(0, 0, true);
       int g = 0;
@@ -218,13 +227,14 @@ __global__ void __launch_bounds__(192, 2)
         mma_wait(p_full, g & 1);  // P_g in TMEM, O rescaled
         ATTN_TRACE(true, g, 3);
         if (j == 0 && n > 0) mma_wait(o_free, (n - 1) & 1);  // previous item's O read out
+        mma_wait(&v_full[g & 1], (g >> 1) & 1);
         ptx::tc_fence_after();
         const uint32_t sv = ptx::smem_u32(smem + kSmemV + (g & 1) * kTileBytes);
 #pragma unroll
         for (int k = 0; k < kKV / 16; ++k)  // A = P from TMEM cols [192, 256): 16 keys = 8 columns
           ptx::umma_f16_ts(tmem + 128, tmem + 192 + k * 8, ptx::smem_desc_sw128(sv + k * 2048, kTileBytes, 1024), id_o,
                            (j > 0 || k > 0) ? 1u : 0u);
-        ptx::umma_commit(&kv_empty[g & 1]);
+        ptx::umma_commit(&v_empty[g & 1]);
         ptx::umma_commit(o_done);
         if (last) ptx::umma_commit(&q_empty[n & 1]);
         q = nx;
