@@ -61,6 +61,12 @@ DEFAULT_CONFIG = "gpt2-1.3b"
 SHAPE_NAME, CFG, WORKLOAD = CONFIGS[DEFAULT_CONFIG]
 
 
+def progress(msg):
+    """Phase marks on stderr (the one JSON line stays alone on stdout)."""
+    if int(os.environ.get("RANK", "0")) == 0:
+        print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -139,7 +145,6 @@ class PortStages:
         self.np, self.O = np, O
         self.m = O.Shape(**shape.__dict__)
         self.D = CFG["D"]
-        self.params = O.init_params(self.m, self.D, 0)
         self.models = [O.StageModel(self.m, self.D, st) for st in range(self.D)]
         tok, lab = O.synthetic_tokens(self.m, 1, 1)
         self.tok, self.lab = tok, lab
@@ -154,7 +159,16 @@ class PortStages:
         import time as _t
         np, O, m = self.np, self.O, self.m
         sm = self.models[st]
-        P = O.unpack(self.params[st], sm.layout)
+        # this stage's parameters only (O.init_params' per-stage stream): the whole 1.3B
+        # model in fp64 would hold ~10 GB of host memory beside the GPU trainer
+        rng = np.random.default_rng([0, st])
+        flat = np.zeros(sm.total)
+        for _, o, r, c, init in sm.layout:
+            if init == "normal":
+                flat[o:o + r * c] = rng.standard_normal(r * c) * 0.02
+            elif init == "one":
+                flat[o:o + r * c] = 1.0
+        P = O.unpack(flat, sm.layout)
         x = self.tok if st == 0 else np.random.default_rng(st).standard_normal((m.seq, m.hidden))
         from threadpoolctl import threadpool_limits
         with threadpool_limits(limits=os.cpu_count()):  # torchrun exports OMP_NUM_THREADS=1
@@ -505,14 +519,17 @@ def main():
     tr = Trainer(shape, cfg, lr=1e-4, first_rank=rank * per, n_ranks=per)
     if world > 1:
         tr.connect()
+    progress("trainer created; init params")
     tr.init_params(seed=0)
     n_seq = cfg.mini_batch()
     tok, lab = synthetic_batch(shape, n_seq, seed=1)
     tr.set_batch(tok, lab)
+    progress("warm-up")
     for _ in range(args.warmup):
         loss = tr.step()
     stream = torch.cuda.ExternalStream(tr.stream_handle())
 
+    progress("timed steps")
     # ---- value: resident inputs, graph replay, CUDA events on the trainer stream
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -531,6 +548,7 @@ def main():
         ms = float(t)
     value = n_seq / (ms * 1e-3)
 
+    progress("e2e steps")
     # ---- e2e: public API per step: pinned H2D tokens+labels, step, D2H loss
     tok_h = torch.from_numpy(tok).pin_memory()
     lab_h = torch.from_numpy(lab).pin_memory()
@@ -553,6 +571,7 @@ def main():
     # ---- one profiled (eager) iteration: per-task GPU spans -> measured bubble
     if world > 1:
         dist.barrier()
+    progress("profiled iteration")
     prof = tr.profile_step()
     tasks, colls = prof["tasks"], prof.get("allreduce", [])
     if world > 1:  # per-process clocks, each relative to its own iteration start
@@ -669,9 +688,11 @@ def main():
         except Exception as e:  # the planner may find nothing feasible
             plans = {"error": str(e)[:200]}
         bt = stats.get("backward_tasks") or 0
+        progress("GEMM roofline")
         rl = gemm_roofline(tr.stream_handle(), peak, shape, CFG,
                            bwd_pair_frac=(2.0 * stats.get("fused_backward_pairs", 0) / bt) if bt else None)
         flops_seq = shape.flops_per_seq()
+        progress("CPU baseline")
         cpu = None if args.no_cpu_baseline else cpu_port_sample(shape)
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "seqs/s", "n_gpus": world,

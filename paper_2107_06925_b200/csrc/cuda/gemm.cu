@@ -689,6 +689,72 @@ __global__ void __launch_bounds__(128) k_splitk_finalize(float* __restrict__ ws,
   }
 }
 
+// ------------------------------------------------------------------ stream-K --
+// The CTA-pair kernel's work list.  Classic: output tiles pair, pair + npairs, ... (each
+// split into ksplit K-slices).  Stream-K (`sk` != 0): the tiles x K-blocks iteration
+// space is cut into npairs equal contiguous ranges, so no pair idles in a partial last
+// wave (50 tiles on 74 pairs: the N = 1280 stage GEMMs of GPT-2 1.3B at 2528 rows; 150
+// or 200 tiles: 2.03 / 2.7 waves).  A pair visits its range in DECREASING tile order:
+// its first item -- the head of the tile its range ends in -- is a PARTIAL (fp32 tile to
+// the workspace slot of this pair, then a per-CTA flag), its last item -- the tail of
+// the tile its range starts in -- OWNS that tile: it waits for the partials of the
+// lower-numbered pairs sharing the tile (already written: they were those pairs' first
+// items, and lower block indices are scheduled first), adds them and runs the fused
+// epilogue.  fp32 accumulate (weight gradients) needs no fix-up: every segment
+// reduce-adds its own part.
+struct SkItem {
+  int tile = 0, ks = 0, kb0 = 0, kb1 = 0;
+  bool partial = false;  // write the fp32 partial, no epilogue
+  bool fixup = false;    // add the partials of lower pairs before the epilogue
+};
+struct WorkList {
+  int pair, npairs, tiles, num_kb, kb_per, ksplit;
+  bool sk, acc;  // stream-K; fp32 accumulate (segments reduce-add, no fix-up)
+  long long b = 0, e = 0, cur = 0;
+  int next_tile = 0;
+  __device__ void init(int pair_, int npairs_, int base_tiles, int num_kb_, int ksplit_, bool sk_, bool acc_) {
+    pair = pair_, npairs = npairs_, num_kb = num_kb_, ksplit = ksplit_, sk = sk_, acc = acc_;
+    tiles = base_tiles * (sk ? 1 : ksplit);
+    kb_per = (num_kb + ksplit - 1) / ksplit;
+    if (sk) {
+      const long long T = (long long)base_tiles * num_kb;
+      b = T * pair / npairs, e = T * (pair + 1) / npairs, cur = e;
+    } else {
+      next_tile = pair;
+    }
+  }
+  __device__ bool next(SkItem& it) {
+    if (!sk) {
+      if (next_tile >= tiles) return false;
+      it.tile = next_tile % (tiles / ksplit);
+      it.ks = next_tile / (tiles / ksplit);
+      it.kb0 = it.ks * kb_per;
+      it.kb1 = min(num_kb, it.kb0 + kb_per);
+      it.partial = it.fixup = false;
+      next_tile += npairs;
+      return true;
+    }
+    if (cur <= b) return false;
+    const long long last = cur - 1;  // the highest remaining iteration
+    const int t = int(last / num_kb);
+    const long long t0 = (long long)t * num_kb;
+    const long long lo = t0 > b ? t0 : b;
+    it.tile = t, it.ks = 0, it.kb0 = int(lo - t0), it.kb1 = int(cur - t0);
+    it.partial = !acc && it.kb1 < num_kb;                  // lacks the tile's last K-block
+    it.fixup = !acc && !it.partial && it.kb0 > 0;          // has it, but not the first
+    cur = lo;
+    return true;
+  }
+  // the pairs (below `pair`) holding the other segments of the tile this pair owns
+  __device__ int first_producer(int t) const {  // lowest pair index whose range meets tile t
+    const long long T = (long long)tiles * num_kb, t0 = (long long)t * num_kb;
+    int q = pair;
+    while (q > 0 && T * q / npairs > t0) --q;  // range of q starts after t0 -> q-1 also in t
+    return q;
+  }
+};
+constexpr int kSkFlagInts = 2 * 160;  // per (pair, CTA) completion counters at the workspace tail
+
 // ---------------------------------------------------------- 2-SM variant ----
 // A CTA pair (cluster of 2 on one TPC) computes a 256 x PBN tile with
 // tcgen05.mma.cta_group::2 (M = 256): each CTA stages its 128 rows of A and PBN/2 of
@@ -721,7 +787,7 @@ template <int PBN, bool A_MN, bool B_MN, int EPI, bool TO>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiWarps, 1)
     k_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
             const __grid_constant__ CUtensorMap to, const __grid_constant__ CUtensorMap to2, const EpiArgs ep,
-            int M, int N, int K, int ksplit) {
+            int M, int N, int K, int ksplit, int sk) {
   static_assert(!TO || EPI != kStoreF32, "TMA-store epilogue: bf16 outputs / fp32 accumulate");
   constexpr bool AUX = TO && EPI == kBiasResid;  // residual block via TMA (tensor map `to2`)
   using C = PairCfg<PBN, AUX>;
@@ -742,8 +808,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
   const uint32_t cta = ptx::cluster_ctarank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int num_m = (M + 255) / 256, num_n = (N + PBN - 1) / PBN;
-  const int num_kb = (K + BK - 1) / BK, kb_per = (num_kb + ksplit - 1) / ksplit;
-  const int tiles = num_m * num_n * ksplit;
+  const int num_kb = (K + BK - 1) / BK;
+  WorkList wl0;  // this pair's work items (classic tiles or a stream-K range)
+  wl0.init(pair, npairs, num_m * num_n, num_kb, ksplit, sk != 0, EPI == kAccF32);
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&ta);
@@ -767,13 +834,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = pair; tile < tiles; tile += npairs) {
+      WorkList wl = wl0;
+      for (SkItem itm; wl.next(itm);) {
         int mb, nb;
-        tile_coords(tile, num_m, num_n, mb, nb);
-        const int ks = tile / (num_m * num_n);
+        tile_coords(itm.tile, num_m, num_n, mb, nb);
         const int m0 = mb * 256 + int(cta) * 128, n0 = nb * PBN + int(cta) * (PBN / 2);
-        const int kb1 = min(num_kb, (ks + 1) * kb_per);
-        for (int kb = ks * kb_per; kb < kb1; ++kb) {
+        for (int kb = itm.kb0; kb < itm.kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::kStageBytes;
           uint8_t* sb = sa + C::kABytes;
@@ -806,14 +872,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = pair; tile < tiles; tile += npairs, ++it) {
+      WorkList wl = wl0;
+      for (SkItem itm; wl.next(itm); ++it) {
         const int acc = it & 1;
         ptx::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         GEMM_TRACE(true, it, 0);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * PBN;
-        const int ks = tile / (num_m * num_n);
-        const int kb0 = ks * kb_per, kb1 = min(num_kb, (ks + 1) * kb_per);
+        const int kb0 = itm.kb0, kb1 = itm.kb1;
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
@@ -838,18 +904,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
     const int q = warp & 3, half = (warp - 4) >> 2;  // lane quarter, column half
     constexpr int NC = C::kChunks;
     uint8_t* stg = stg_base + (warp - 4) * C::kStgBytes;
-    int it = 0, nbuf = 0;
-    for (int tile = pair; tile < tiles; tile += npairs, ++it) {
+    int it = 0, nbuf = 0, aux_it = 0;
+    // stream-K fix-up state: this pair's fp32 partial slot (this CTA's 128 rows) and the
+    // per-(pair, CTA) completion counters at the workspace tail
+    float* const slot_base = ep.ws;
+    int* const flags = sk ? reinterpret_cast<int*>(ep.ws + ep.ws_elems) - kSkFlagInts : nullptr;
+    auto slot_of = [&](int pq) { return slot_base + (size_t(pq) * 2 + cta) * (128 * PBN); };
+    WorkList wl = wl0;
+    for (SkItem itm; wl.next(itm); ++it) {
       const int acc = it & 1;
       int mb, nb;
-      tile_coords(tile, num_m, num_n, mb, nb);
+      tile_coords(itm.tile, num_m, num_n, mb, nb);
+      if (itm.partial) {  // stream-K head / middle segment: fp32 partial -> workspace slot
+        ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t tp = tmem_base + (uint32_t(q * 32) << 16) + acc * PBN;
+        float* srow = slot_of(pair) + size_t(q * 32 + lane) * PBN;
+#pragma unroll 1
+        for (int c = half * NC; c < half * NC + NC; ++c) {
+          uint32_t r[32];
+          ptx::tmem_ld32(tp + c * 32, r);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<uint4*>(srow + c * 32 + 4 * k) = make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_leader_relaxed(&tempty[acc]);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(flags + pair * 2 + int(cta), 1);
+        continue;
+      }
+      int q_lo = pair;  // fix-up: partials of pairs [q_lo, pair) of this tile
+      if (itm.fixup) q_lo = wl.first_producer(itm.tile);
       EpiPre pre;  // this tile's first-chunk operands are fetched while the MMAs run
       uint4 auxn[4], auxn2[4];  // residual / U rows of the next two chunks (TMA epilogue), in
                                 // flight under the mainloop: their HBM latency is what the
                                 // single-wave shapes' exposed epilogue otherwise waits on
       if constexpr (!TO) {
         epilogue_prefetch<EPI>(ep, mb * 256 + int(cta) * 128 + q * 32, nb * PBN + half * (PBN / 2), M, N, lane,
-                               (ksplit > 1 || ep.atomic_acc), pre);
+                               (ksplit > 1 || sk || ep.atomic_acc), pre);
       } else if constexpr (AUX) {  // this warp's residual block, one TMA box per chunk
         ptx::fence_proxy_async();  // the previous tile's reads of the block precede the refill
         __syncwarp();
@@ -859,6 +955,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
           for (int c = 0; c < NC; ++c)
             ptx::tma_load_2d(stg + C::kAuxOff + c * 2048, &to2, &auxbar[warp - 4], c0 + 32 * c, rw);
         }
+        ++aux_it;
       } else {
         const int rr = mb * 256 + int(cta) * 128 + q * 32 + lane, c0 = nb * PBN + half * (PBN / 2);
         aux_row_prefetch<EPI>(ep, rr, c0, M, N, auxn);
@@ -869,6 +966,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
       GEMM_TRACE(warp == 4 && lane == 0, it, 2);
       GEMM_TRACE(warp == 11 && lane == 0, it, 4);
       ptx::tc_fence_after();
+      if (itm.fixup) {  // the lower pairs' partials of this tile have landed (8 warps each)
+        if (lane == 0)
+          for (int pq = q_lo; pq < pair; ++pq)
+            while (*reinterpret_cast<volatile int*>(flags + pq * 2 + int(cta)) < kPairEpiWarps) __nanosleep(32);
+        __syncwarp();
+        __threadfence();
+      }
       const int row0 = mb * 256 + int(cta) * 128 + q * 32;
       const uint32_t t0 = tmem_base + (uint32_t(q * 32) << 16) + acc * PBN;
 #pragma unroll 1
@@ -879,7 +983,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
         if constexpr (TO) {
           uint4 auxc[4];
           if constexpr (AUX) {  // this lane's row of the staged residual chunk
-            if (c == half * NC) ptx::mbar_wait(&auxbar[warp - 4], it & 1);
+            if (c == half * NC) ptx::mbar_wait(&auxbar[warp - 4], (aux_it - 1) & 1);
             const uint8_t* ab = stg + C::kAuxOff + (c - half * NC) * 2048;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
@@ -892,13 +996,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
           const uint32_t biasc = biasn;
           if (c + 1 < half * NC + NC) biasn = bias_prefetch(ep, col0 + 32, N, lane);
           ptx::tmem_ld_wait();
+          for (int pq = q_lo; pq < pair; ++pq) {  // stream-K fix-up: + the partial tiles
+            const float* prow = slot_of(pq) + size_t(q * 32 + lane) * PBN + c * 32;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const float4 v = *reinterpret_cast<const float4*>(prow + 4 * k);
+              r[4 * k] = __float_as_uint(__uint_as_float(r[4 * k]) + v.x);
+              r[4 * k + 1] = __float_as_uint(__uint_as_float(r[4 * k + 1]) + v.y);
+              r[4 * k + 2] = __float_as_uint(__uint_as_float(r[4 * k + 2]) + v.z);
+              r[4 * k + 3] = __float_as_uint(__uint_as_float(r[4 * k + 3]) + v.w);
+            }
+          }
           if (row0 < M && col0 < N)
             epilogue_chunk_tma<EPI>(ep, &to, &to2, row0, col0, r, stg, lane, nbuf, auxc, biasc);
         } else {
           EpiPre cur = pre;
-          if (c + 1 < half * NC + NC) epilogue_prefetch<EPI>(ep, row0, col0 + 32, M, N, lane, (ksplit > 1 || ep.atomic_acc), pre);
+          if (c + 1 < half * NC + NC)
+            epilogue_prefetch<EPI>(ep, row0, col0 + 32, M, N, lane, (ksplit > 1 || sk || ep.atomic_acc), pre);
           ptx::tmem_ld_wait();
-          if (row0 < M && col0 < N) epilogue_chunk<EPI>(ep, row0, col0, M, N, r, stg, lane, (ksplit > 1 || ep.atomic_acc), cur);
+          if (row0 < M && col0 < N)
+            epilogue_chunk<EPI>(ep, row0, col0, M, N, r, stg, lane, (ksplit > 1 || sk || ep.atomic_acc), cur);
         }
       }
       ptx::tc_fence_before();
@@ -906,6 +1023,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
       GEMM_TRACE(warp == 4 && lane == 0, it, 3);
       GEMM_TRACE(warp == 11 && lane == 0, it, 5);
       if (lane == 0) ptx::mbar_arrive_leader_relaxed(&tempty[acc]);
+      if (itm.fixup) {  // every epilogue warp of this CTA has read the partials: re-arm
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kPairEpiWarps) : "memory");
+        if (warp == 4 && lane == 0)
+          for (int pq = q_lo; pq < pair; ++pq) flags[pq * 2 + int(cta)] = 0;
+      }
     }
     if constexpr (TO)
       if (lane == 0) ptx::bulk_wait0();  // the bulk stores / reduces have completed
@@ -944,6 +1066,26 @@ bool tma_out(const EpiArgs& ep, int M, int N, CUtensorMap& to, CUtensorMap& to2)
   return true;
 }
 
+// Stream-K (the CTA-pair kernel's WorkList) pays when whole 256 x PBN tiles leave many
+// pairs idle in the last wave (efficiency tiles / (waves * pairs) < 0.85) and every pair
+// gets a few K-blocks.  bf16 epilogues need the caller's workspace for the fp32 partial
+// tiles (one 256 x PBN slot per pair) + the completion counters; fp32 accumulate needs
+// none.  CK_GEMM_STREAMK=0 disables it.
+inline bool stream_k_ok(int epi, const EpiArgs& ep, int base, int slots, int K, int pbn) {
+  static const bool on = [] {
+    const char* e = std::getenv("CK_GEMM_STREAMK");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || epi == kStoreF32 || ep.ksplit > 0) return false;
+  const int waves = (base + slots - 1) / slots;
+  if (double(base) / double(waves * slots) >= 0.85) return false;
+  const long long kb = (K + BK - 1) / BK;
+  if (kb * base / slots < 8) return false;
+  if (epi == kAccF32) return true;
+  return ep.ws && ep.ws_elems >= (long long)slots * 2 * 128 * pbn + kSkFlagInts &&
+         (reinterpret_cast<uintptr_t>(ep.ws) % 16) == 0;
+}
+
 template <int PBN, bool A_MN, bool B_MN, int EPI>
 void launch_pair(int M, int N, int K, const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B,
                  long long ldb, const EpiArgs& ep, cudaStream_t st) {
@@ -953,12 +1095,16 @@ void launch_pair(int M, int N, int K, const __nv_bfloat16* A, long long lda, con
   const CUtensorMap tb = B_MN ? cuda::make_map_2d_bf16(B, N, K, ldb, 64, BK)
                               : cuda::make_map_2d_bf16(B, K, N, ldb, 64, PBN / 2);
   const int base = ((M + 255) / 256) * ((N + PBN - 1) / PBN);
-  const int ks = split_k(EPI, base, cuda::num_sms() / 2, K, ep.ksplit);
-  const int tiles = base * ks;
-  const int pairs = tiles < cuda::num_sms() / 2 ? tiles : cuda::num_sms() / 2;
+  const int slots = cuda::num_sms() / 2;
+  int ks = split_k(EPI, base, slots, K, ep.ksplit);
+  int tiles = base * ks;
+  int pairs = tiles < slots ? tiles : slots;
   CUtensorMap to, to2;
   if constexpr (EPI != kStoreF32) {
     if (tma_out<EPI>(ep, M, N, to, to2)) {
+      // stream-K when whole tiles would leave >= 15 % of the pairs idle in the last wave
+      const int sk = stream_k_ok(EPI, ep, base, slots, K, PBN) ? 1 : 0;
+      if (sk) ks = 1, tiles = base, pairs = slots;
       using CT = PairCfg<PBN, EPI == kBiasResid>;
       if constexpr (EPI == kBiasResid)  // the residual, in the output's 32 x 32 swizzled chunk layout
         to2 = cuda::make_map_2d_bf16(ep.aux, N, M, ep.ld_aux, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
@@ -969,7 +1115,7 @@ void launch_pair(int M, int N, int K, const __nv_bfloat16* A, long long lda, con
         attr = true;
       }
       cuda::launch(kern, dim3(2 * pairs), dim3(128 + 32 * kPairEpiWarps), CT::kSmem, st, ta, tb, to, to2, ep, M, N,
-                   K, ks);
+                   K, ks, sk);
       CK_CUDA(cudaGetLastError());
       return;
     }
@@ -980,7 +1126,8 @@ void launch_pair(int M, int N, int K, const __nv_bfloat16* A, long long lda, con
     CK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr = true;
   }
-  cuda::launch(kern, dim3(2 * pairs), dim3(128 + 32 * kPairEpiWarps), C::kSmem, st, ta, tb, ta, ta, ep, M, N, K, ks);
+  cuda::launch(kern, dim3(2 * pairs), dim3(128 + 32 * kPairEpiWarps), C::kSmem, st, ta, tb, ta, ta, ep, M, N, K, ks,
+               0);
   CK_CUDA(cudaGetLastError());
 }
 

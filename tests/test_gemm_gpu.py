@@ -133,3 +133,52 @@ def test_split_k_bf16_epilogues(M, N, K, ks):
     assert _rel(cs, d.float().sum(0)) < 1e-4
     torch.cuda.synchronize()
     assert int(torch.count_nonzero(ws)) == 0  # the finalize pass leaves the workspace zeroed
+
+
+# stream-K (CTA-pair kernel): tiles that leave pairs idle in the last wave are cut into
+# equal K-block ranges per pair; bf16 epilogues fix up through the workspace
+SK_SHAPES = [(2528, 1280, 1280), (2528, 1280, 5120), (2528, 3840, 1280), (2528, 5120, 1280), (1264, 1280, 3840),
+             (600, 2000, 3000)]
+
+
+@pytest.mark.parametrize("M,N,K", SK_SHAPES)
+def test_stream_k_bf16_epilogues(M, N, K):
+    ws = torch.zeros(8 << 20, device="cuda")  # room for 74 pair slots of 256 x 256 fp32
+    A, B = _rand(M, K), _rand(N, K)
+    bias = _rand(N)
+    ref = A.float() @ B.float().t() + bias.float()
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    for _ in range(2):  # twice: the completion counters re-arm
+        ck.gemm("bf16", A, B, out, bias=bias, ws=ws)
+        assert _rel(out, ref) < 8e-3
+    resid = _rand(M, N)
+    ck.gemm("bias_resid", A, B, out, bias=bias, aux=resid, ws=ws)
+    assert _rel(out, ref + resid.float()) < 8e-3
+    g = torch.empty_like(out)
+    ck.gemm("bias_gelu", A, B, out, bias=bias, out2=g, ws=ws)
+    assert _rel(out, ref) < 8e-3
+    assert _rel(g, torch.nn.functional.gelu(out.float(), approximate="tanh")) < 8e-3
+    Wt = _rand(K, N)
+    dY = _rand(M, K)
+    U = _rand(M, N)
+    d = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    cs = torch.zeros(N, device="cuda")
+    ck.gemm("gelu_bwd", dY, Wt, d, b_mn=True, aux=U, colsum=cs, ws=ws)
+    u = U.float().requires_grad_()
+    (gp,) = torch.autograd.grad(torch.nn.functional.gelu(u, approximate="tanh").sum(), u)
+    assert _rel(d, (dY.float() @ Wt.float()) * gp) < 8e-3
+    assert _rel(cs, d.float().sum(0)) < 1e-4
+    torch.cuda.synchronize()
+    flags = ws[-320:].view(torch.int32)
+    assert int(torch.count_nonzero(flags)) == 0  # every counter re-armed
+
+
+@pytest.mark.parametrize("M,N,K", [(3840, 1280, 2528), (5120, 1280, 2528), (1280, 5120, 1264), (3000, 2000, 900)])
+def test_stream_k_weight_gradient(M, N, K):
+    """fp32 accumulate (MN-major operands, the weight-gradient layout): stream-K segments
+    reduce-add straight into the output."""
+    A, B = _rand(K, M), _rand(K, N)
+    ref = A.float().t() @ B.float()
+    acc = torch.ones(M, N, device="cuda")
+    ck.gemm("acc_f32", A, B, acc, a_mn=True, b_mn=True)
+    assert _rel(acc, ref + 1) < 1e-3
