@@ -34,9 +34,10 @@ namespace chimera::gemm {
 // clock64() stamps per tile of CTA 0 (scripts/gemm_trace.cu builds with CK_GEMM_TRACE)
 #ifdef CK_GEMM_TRACE
 __device__ long long g_gemm_trace[16][8];
-#define GEMM_TRACE(cond, t, ev)                                                  \
-  do {                                                                           \
-    if ((cond) && blockIdx.x == 0 && (t) < 16) g_gemm_trace[t][ev] = clock64(); \
+__device__ int g_gemm_trace_block = 0;
+#define GEMM_TRACE(cond, t, ev)                                                                   \
+  do {                                                                                            \
+    if ((cond) && int(blockIdx.x) == g_gemm_trace_block && (t) < 16) g_gemm_trace[t][ev] = clock64(); \
   } while (0)
 #else
 #define GEMM_TRACE(cond, t, ev) \
@@ -919,15 +920,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
         ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
         ptx::tc_fence_after();
         const uint32_t tp = tmem_base + (uint32_t(q * 32) << 16) + acc * PBN;
-        float* srow = slot_of(pair) + size_t(q * 32 + lane) * PBN;
+        // warp-interleaved layout: for each (chunk, 16-byte piece k) the 32 lanes' pieces
+        // are contiguous, so every store instruction writes 512 B in full sectors (a
+        // row-major slot made each instruction 32 partial-sector writes: ~10 us per tile)
+        float* sw = slot_of(pair) + size_t((q * 2 + half) * NC) * 32 * 32;
 #pragma unroll 1
         for (int c = half * NC; c < half * NC + NC; ++c) {
           uint32_t r[32];
           ptx::tmem_ld32(tp + c * 32, r);
           ptx::tmem_ld_wait();
+          float* sc = sw + size_t(c - half * NC) * 32 * 32;
 #pragma unroll
           for (int k = 0; k < 8; ++k)
-            *reinterpret_cast<uint4*>(srow + c * 32 + 4 * k) = make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+            *reinterpret_cast<uint4*>(sc + (k * 32 + lane) * 4) = make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
         }
         ptx::tc_fence_before();
         __syncwarp();
@@ -997,10 +1002,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
           if (c + 1 < half * NC + NC) biasn = bias_prefetch(ep, col0 + 32, N, lane);
           ptx::tmem_ld_wait();
           for (int pq = q_lo; pq < pair; ++pq) {  // stream-K fix-up: + the partial tiles
-            const float* prow = slot_of(pq) + size_t(q * 32 + lane) * PBN + c * 32;
+            const float* pc = slot_of(pq) + size_t((q * 2 + half) * NC + (c - half * NC)) * 32 * 32;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-              const float4 v = *reinterpret_cast<const float4*>(prow + 4 * k);
+              const float4 v = *reinterpret_cast<const float4*>(pc + (k * 32 + lane) * 4);
               r[4 * k] = __float_as_uint(__uint_as_float(r[4 * k]) + v.x);
               r[4 * k + 1] = __float_as_uint(__uint_as_float(r[4 * k + 1]) + v.y);
               r[4 * k + 2] = __float_as_uint(__uint_as_float(r[4 * k + 2]) + v.z);
@@ -1071,18 +1076,25 @@ bool tma_out(const EpiArgs& ep, int M, int N, CUtensorMap& to, CUtensorMap& to2)
 // gets a few K-blocks.  bf16 epilogues need the caller's workspace for the fp32 partial
 // tiles (one 256 x PBN slot per pair) + the completion counters; fp32 accumulate needs
 // none.  CK_GEMM_STREAMK=0 disables it.
+//
+// Measured (graph-timed, profiles/r02x_*, r02z_*): for the fp32 accumulate of the weight
+// gradients with more tiles than pairs (75 / 100 tiles on 74 pairs) it beats whole tiles
+// and two K-slices by 3-16 %; with fewer tiles than pairs two K-slices (split_k) stay
+// better.  For the bf16 epilogues the fix-up -- a 128 KB fp32 partial per CTA written and
+// read back through L2 before the epilogue -- costs more than the idle pairs it fills
+// (e.g. 2528 x 1280 x 1280: 17.8 vs 12.1 us), so it is only taken with CK_GEMM_STREAMK=2.
 inline bool stream_k_ok(int epi, const EpiArgs& ep, int base, int slots, int K, int pbn) {
-  static const bool on = [] {
+  static const int mode = [] {  // 0 off, 1 fp32 accumulate only (default), 2 also bf16
     const char* e = std::getenv("CK_GEMM_STREAMK");
-    return !(e && e[0] == '0');
+    return e ? atoi(e) : 1;
   }();
-  if (!on || epi == kStoreF32 || ep.ksplit > 0) return false;
+  if (mode == 0 || epi == kStoreF32 || ep.ksplit > 0) return false;
   const int waves = (base + slots - 1) / slots;
   if (double(base) / double(waves * slots) >= 0.85) return false;
   const long long kb = (K + BK - 1) / BK;
   if (kb * base / slots < 8) return false;
-  if (epi == kAccF32) return true;
-  return ep.ws && ep.ws_elems >= (long long)slots * 2 * 128 * pbn + kSkFlagInts &&
+  if (epi == kAccF32) return base >= slots;
+  return mode >= 2 && ep.ws && ep.ws_elems >= (long long)slots * 2 * 128 * pbn + kSkFlagInts &&
          (reinterpret_cast<uintptr_t>(ep.ws) % 16) == 0;
 }
 

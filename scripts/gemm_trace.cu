@@ -12,6 +12,12 @@
 int main(int argc, char** argv) {
   const int M = atoi(argv[1]), N = atoi(argv[2]), K = atoi(argv[3]), epi = atoi(argv[4]);
   const bool a_mn = atoi(argv[5]), b_mn = atoi(argv[6]);
+  const int block = argc > 7 ? atoi(argv[7]) : 0;  // CTA to trace
+  cudaMemcpyToSymbol(chimera::gemm::g_gemm_trace_block, &block, sizeof(int));
+  float* ws = nullptr;  // split-K / stream-K workspace (bf16 epilogues), zero-filled
+  const long long ws_elems = 8LL << 20;
+  cudaMalloc(&ws, ws_elems * 4);
+  cudaMemset(ws, 0, ws_elems * 4);
   __nv_bfloat16 *A, *B, *out, *aux, *out2, *bias;
   cudaMalloc(&A, size_t(M) * K * 2);
   cudaMalloc(&B, size_t(N) * K * 2);
@@ -31,6 +37,8 @@ int main(int argc, char** argv) {
   ep.ld_aux = N;
   ep.out2 = epi == 1 ? out2 : nullptr;
   ep.ld_out2 = N;
+  ep.ws = ws;
+  ep.ws_elems = ws_elems;
   auto run = [&] {
     chimera::gemm::gemm((chimera::gemm::Epi)epi, a_mn, b_mn, M, N, K, A, a_mn ? M : K, B, b_mn ? N : K, ep, 0);
   };
@@ -39,8 +47,8 @@ int main(int argc, char** argv) {
   static long long tr[16][8];
   cudaMemcpyFromSymbol(tr, chimera::gemm::g_gemm_trace, sizeof(tr));
   const long long c0 = tr[0][0];
-  printf("tile  mma_start  mma_issued  epi4_start  epi4_end  epi11_start epi11_end   (cycles from tile 0 start)\n");
-  printf("kernel entry -> tile0 mma start: %lld cycles\n", tr[0][0] - tr[0][6]);
+  printf("CTA %d: item  mma_start  mma_issued  epi4_start  epi4_end  epi11_start epi11_end   (cycles from item 0 start)\n", block);
+  printf("kernel entry -> item0 mma start: %lld cycles\n", tr[0][0] - tr[0][6]);
   for (int t = 0; t < 16 && tr[t][0]; ++t)
     printf("%4d %10lld %11lld %11lld %9lld %11lld %9lld\n", t, tr[t][0] - c0, tr[t][1] - c0, tr[t][2] - c0,
            tr[t][3] - c0, tr[t][4] - c0, tr[t][5] - c0);

@@ -182,3 +182,17 @@ def test_stream_k_weight_gradient(M, N, K):
     acc = torch.ones(M, N, device="cuda")
     ck.gemm("acc_f32", A, B, acc, a_mn=True, b_mn=True)
     assert _rel(acc, ref + 1) < 1e-3
+
+
+def test_stream_k_bf16_path_enabled():
+    """The bf16 stream-K fix-up is off by default (slower than whole tiles): run
+    the epilogue checks above with it forced on (CK_GEMM_STREAMK=2 is read once per
+    process, hence the subprocess)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, CK_GEMM_STREAMK="2")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.abspath(__file__) + "::test_stream_k_bf16_epilogues"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
