@@ -237,6 +237,7 @@ __global__ void __launch_bounds__(192, 2)
         ptx::umma_commit(&v_empty[g & 1]);
         ptx::umma_commit(o_done);
         if (last) ptx::umma_commit(&q_empty[n & 1]);
+        ATTN_TRACE(true, g, 13);  // PV_g issued
         q = nx;
       }
     }
@@ -263,6 +264,9 @@ __global__ void __launch_bounds__(192, 2)
       for (int c = 0; c < 4; ++c) ptx::tmem_ld32(trow + c * 32, r[c]);
       ptx::tmem_ld_wait();
       ATTN_TRACE(t == 0, g, 6);
+      ATTN_TRACE(t == 32, g, 10);  // the other softmax warps' S loads (s_free needs all 128)
+      ATTN_TRACE(t == 64, g, 11);
+      ATTN_TRACE(t == 96, g, 12);
       ptx::tc_fence_before();
       ptx::mbar_arrive(s_free);
       // masking only on the diagonal (causal) / sequence-tail tile (warp-uniform branch):

@@ -1343,7 +1343,10 @@ std::string Trainer::profile_step() {
   // Like step(): once a graph is in use the profiled iteration is captured (timing
   // events become event-record nodes) and replayed, so the spans show the GPU running
   // the iteration -- not the host issuing thousands of kernels into an idle device.
-  const bool graphed = I.use_graph && I.steps > 0;
+  // (single-process trainers only: there eight ranks' eager issue is host-bound.  A
+  // profile graph with cross-process flag waits hung with two processes time-sliced on
+  // one GPU (8-process emulation, r02); one rank per process issues eagerly fast enough)
+  const bool graphed = I.use_graph && I.steps > 0 && I.procs == 1;
   cudaGraph_t g = nullptr;
   cudaGraphExec_t ge = nullptr;
   if (graphed) CK_CUDA(cudaStreamBeginCapture(I.main_stream, cudaStreamCaptureModeThreadLocal));

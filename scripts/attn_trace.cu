@@ -49,14 +49,15 @@ int main(int argc, char** argv) {
   printf("CTA0 sm %lld start +%.2f us dur %.2f us\n", cta[0][0], (t0 - tmin) / 1e3, (cta[0][2] - cta[0][1]) / 1e3);
   // per-tile stamps relative to kv_full of tile 0 (cycles)
   const long long c0 = bwd ? tr[0][3] : tr[0][1];
-  const char* fnames[] = {"tma:kv_empty", "mma:kv_full", "mma:s_free", "mma:p_full", "sm:wait_s",
-                          "sm:s_full",    "sm:ld_done",  "sm:max_done", "sm:o_done", "sm:p_done"};
+  const char* fnames[] = {"tma:k_empty", "mma:k_full", "mma:s_free", "mma:p_full", "sm:wait_s",
+                          "sm:s_full",    "sm:ld_done",  "sm:max_done", "sm:o_done", "sm:p_done",
+                          "w1:ld_done",   "w2:ld_done",  "w3:ld_done",  "mma:pv_iss"};
   const char* bnames[] = {"mma:qd_full", "mma:ds_full", "mma:dq_free", "c:start", "c:lse_bar",
                           "c:s_full",    "c:ds_done",   "c:mm_done",   "c:dq_done", "tma:qd_empty",
                           "c:ld_done",   "c:math_done", "c:mm_wait"};
   const char** names = bwd ? bnames : fnames;
   printf("%-4s", "j");
-  const int nev = bwd ? 13 : 10;
+  const int nev = bwd ? 13 : 14;
   for (int e = 0; e < nev; ++e) printf(" %12s", names[e]);
   printf("\n");
   for (int j = 0; j < 16; ++j) {
