@@ -474,6 +474,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="chimera")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--diag-timeout", type=float, default=300.0,
+                    help="multi-process: seconds allowed for the profiled iteration + sync A/B")
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--B", type=int, default=0, help="override the config's micro-batch size")
     ap.add_argument("--partition", default="balanced", choices=["balanced", "even"],
@@ -502,6 +504,9 @@ def main():
     from paper_2107_06925_b200.gpt import Trainer, synthetic_batch
 
     os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
+    # one hardware queue per stream (set before the CUDA context exists): a stream blocked
+    # in a cross-process flag wait must not stall another stream sharing its queue
+    os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -568,6 +573,45 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t)
 
+    # ---- launches in the timed region (the captured iteration's kernel nodes, all processes)
+    stats = tr.stats()
+    launches = int(stats["launches_per_step"] * args.steps)
+    if world > 1:
+        t = torch.tensor([launches], dtype=torch.float64)
+        dist.all_reduce(t)
+        launches = int(t)
+    base = {
+        "metric": METRIC, "value": round(value, 2), "unit": "seqs/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic tokens (uniform, next-token labels), random-init weights N(0,0.02)",
+        "config": {"workload": WORKLOAD,
+                   "model": SHAPE_NAME, "global_batch": n_seq, "seq_len": shape.seq,
+                   "stage_layers": list(shape.stage_layers) or None,
+                   "parallelism": f"{cfg.scheme} D={cfg.D} W={cfg.W} f={cfg.f} {cfg.scaling}"
+                                  f"{' +recompute' if cfg.scaling == 'forward-doubling' else ''}: "
+                                  f"{n_logical} logical ranks on {world} GPU(s)",
+                   "l2": "working set per step >> L2 (weights, grads, stashes ~40 GB)"},
+        "e2e": {"value": round(n_seq / (e2e_ms * 1e-3), 2), "unit": "seqs/s",
+                "h2d_bytes_per_step": int(tok.nbytes + lab.nbytes), "d2h_bytes_per_step": 4},
+    }
+    clocks = clk.summary()
+
+    # The measured numbers are complete here.  Multi-process: the diagnostics below (eager
+    # profiled iteration, sync-policy A/B) run under a watchdog, so a hang there still
+    # leaves the bench line (without those sections) and a clean exit on every process.
+    watchdog = None
+    if world > 1:
+        def _diag_timeout():
+            if rank == 0:
+                print(json.dumps({**base, "gpu_launches": launches, "clocks": clocks, "cpu_baseline": None,
+                                  "diagnostics": f"profiled iteration / sync-policy A/B did not finish within "
+                                                 f"{args.diag_timeout} s; omitted"}), flush=True)
+            os._exit(0)
+        watchdog = threading.Timer(args.diag_timeout, _diag_timeout)
+        watchdog.daemon = True
+        watchdog.start()
+
     # ---- one profiled (eager) iteration: per-task GPU spans -> measured bubble
     if world > 1:
         dist.barrier()
@@ -624,13 +668,10 @@ def main():
             if pol == "eager-sync-opt":
                 sync_ab[pol]["eager_stages"] = [e["stage"] for e in tr.sync_plan()["order"] if e["eager"]]
         tr.set_sync_policy("eager-sync")
+    if watchdog is not None:
+        watchdog.cancel()
 
-    stats = tr.stats()
-    launches = int(stats["launches_per_step"] * args.steps)
     if world > 1:  # the loss is summed over the processes holding last stages
-        t = torch.tensor([launches], dtype=torch.float64)
-        dist.all_reduce(t)
-        launches = int(t)
         t = torch.tensor([loss])
         dist.all_reduce(t)
         loss = float(t)
@@ -693,21 +734,9 @@ def main():
                            bwd_pair_frac=(2.0 * stats.get("fused_backward_pairs", 0) / bt) if bt else None)
         flops_seq = shape.flops_per_seq()
         progress("CPU baseline")
-        cpu = None if args.no_cpu_baseline else cpu_port_sample(shape)
+        cpu = None if (args.no_cpu_baseline or world > 1) else cpu_port_sample(shape)  # N=1 only
         line = {
-            "metric": METRIC, "value": round(value, 2), "unit": "seqs/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic tokens (uniform, next-token labels), random-init weights N(0,0.02)",
-            "config": {"workload": WORKLOAD,
-                       "model": SHAPE_NAME, "global_batch": n_seq, "seq_len": shape.seq,
-                       "stage_layers": list(shape.stage_layers) or None,
-                       "parallelism": f"{cfg.scheme} D={cfg.D} W={cfg.W} f={cfg.f} {cfg.scaling}"
-                                      f"{' +recompute' if cfg.scaling == 'forward-doubling' else ''}: "
-                                      f"{n_logical} logical ranks on {world} GPU(s)",
-                       "l2": "working set per step >> L2 (weights, grads, stashes ~40 GB)"},
-            "e2e": {"value": round(n_seq / (e2e_ms * 1e-3), 2), "unit": "seqs/s",
-                    "h2d_bytes_per_step": int(tok.nbytes + lab.nbytes), "d2h_bytes_per_step": 4},
+            **base,
             "roofline": rl,
             "mfu": {"tflops_per_gpu": round(value * flops_seq / world / 1e12, 1),
                     "frac_of_sustained": round(value * flops_seq / world / 1e12 / peak_sus, 4) if peak_sus else None,
@@ -740,7 +769,7 @@ def main():
             "device_bytes": stats["device_bytes"],
             "loss": loss,
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -138,6 +138,9 @@ struct Trainer::Impl {
   bool connected = false;
   ncclComm_t world_comm = nullptr;
   std::map<int, ncclComm_t> stage_comm;  // stage -> communicator over its holder processes
+  // stage -> (flag in a peer holder's inbox to raise, own inbox flag that peer raises):
+  // the rendezvous before the stage collective (LinkPlan::ready_flag)
+  std::map<int, std::vector<std::pair<uint32_t*, uint32_t*>>> stage_ready;
   std::vector<cudaEvent_t> rank_done;
   cudaEvent_t start_ev, upd_ev;
   int32_t *tokens = nullptr, *labels = nullptr;
@@ -945,6 +948,18 @@ void sync_stage_body(Trainer::Impl& I, int s) {
     I.launches_per_step += 1;
     return;
   }
+  // Rendezvous with the other holders before the collective kernel launches: raise our
+  // flag in each peer's inbox, wait for theirs in ours (stream memory operations -- they
+  // hold no SMs).  An NCCL kernel spins on its SMs until every peer has launched; without
+  // this, one launched early can keep a persistent GEMM's last CTAs off the GPU while the
+  // peer it waits for needs that GEMM's output (a cross-process message) to get there.
+  // Reset-before-raise is ordered by the collective itself: a peer raises the next
+  // iteration's flag only after this iteration's collective, which runs after our reset.
+  for (const auto& [remote, own] : I.stage_ready.at(s)) MemOps::get().write(cs, remote, 1);
+  for (const auto& [remote, own] : I.stage_ready.at(s)) {
+    MemOps::get().wait(cs, own, 1);
+    MemOps::get().write(cs, own, 0);
+  }
   float* g0 = S.grads[0];
   if (S.grads.size() > 1) {
     ops::reduce_copies(g0, S.grads.data(), int(S.grads.size()), S.L.total, cs);
@@ -1093,18 +1108,23 @@ void Trainer::issue_iteration() {
   Impl& I = *d_;
   begin_iteration();
   // CK_TRACE_ISSUE=1 (debug): print every task as it is issued and synchronise after it,
-  // so a fault or a hang is pinned to one task
-  static const bool trace = std::getenv("CK_TRACE_ISSUE") != nullptr;
+  // so a fault or a hang is pinned to one task; =2: print only (is the host blocked in
+  // issue -- a full launch queue -- or the device?)
+  static const char* trace_env = std::getenv("CK_TRACE_ISSUE");
+  static const bool trace = trace_env != nullptr;
+  static const bool trace_sync = trace && trace_env[0] != '2';
   std::set<std::pair<int, int>> fused;  // (worker, index) issued as the second of a pair
   for (const auto& [w, i] : I.order) {
     if (fused.count({w, i})) continue;
     const auto& wl = I.sched.per_worker[w];
-    if (trace) {
+    bool mine = false;
+    for (int r = 0; r < I.W; ++r) mine = mine || I.local(r * I.D + w);
+    if (trace && mine) {
       const Task& t = wl[i];
-      std::fprintf(stderr, "[issue] w%d i%d %s p%d m%d s%d\n", w, i, t.kind == TaskKind::Forward ? "F" : "B",
-                   t.pipeline_id, t.micro_batch, t.stage);
+      std::fprintf(stderr, "[issue] proc %d w%d i%d %s p%d m%d s%d\n", I.proc, w, i,
+                   t.kind == TaskKind::Forward ? "F" : "B", t.pipeline_id, t.micro_batch, t.stage);
       std::fflush(stderr);
-      CK_CUDA(cudaDeviceSynchronize());
+      if (trace_sync) CK_CUDA(cudaDeviceSynchronize());
     }
     if (I.fd_fuse && i + 1 < int(wl.size()) && fuse_forward_pair(wl[i], wl[i + 1])) {
       fused.insert({w, i + 1});
@@ -1117,6 +1137,7 @@ void Trainer::issue_iteration() {
     run_task(wl[i]);
   }
   end_iteration();
+  if (trace) std::fprintf(stderr, "[issue] proc %d: iteration issued\n", I.proc), std::fflush(stderr);
 }
 
 // Adjacent forwards of micro-batches (m, m+1) of the same copy in a worker's order (the
@@ -1569,7 +1590,14 @@ void Trainer::connect(const std::string& all_blobs, const std::string& nccl_id) 
       if (rc != ncclSuccess)
         throw capi::InternalError("ncclCommInitRank (stage " + std::to_string(s) + ") failed");
     }
-    if (mine) I.stage_comm[s] = c;
+    if (mine) {
+      I.stage_comm[s] = c;
+      auto& rv = I.stage_ready[s];
+      for (int q : holders)
+        if (q != I.proc)
+          rv.push_back({reinterpret_cast<uint32_t*>(static_cast<char*>(I.peer_inbox[q]) + I.lp->ready_flag(q, s, I.proc)),
+                        reinterpret_cast<uint32_t*>(static_cast<char*>(I.inbox) + I.lp->ready_flag(I.proc, s, q))});
+    }
   }
   CK_CUDA(cudaDeviceSynchronize());
   I.connected = true;

@@ -63,7 +63,8 @@ struct LinkPlan {
         for (int s = 0; s + 1 < D; ++s)
           for (int dir = 0; dir < 2; ++dir) f(r, m, s, dir);
   }
-  // receive buffers (msg_bytes each) then one 32-bit flag per message consumed by q
+  // receive buffers (msg_bytes each), one 32-bit flag per message consumed by q, then
+  // the stage-sync rendezvous flags (ready_flag)
   std::map<long long, Slot> inbox_layout(int q, size_t* total) const {
     std::vector<long long> keys;
     for_each_msg([&](int r, int m, int s, int dir) {
@@ -73,8 +74,18 @@ struct LinkPlan {
     size_t off = 0;
     for (long long k : keys) out[k].buf = off, off += msg_bytes;
     for (long long k : keys) out[k].flag = off, off += 4;
+    off += size_t(D) * procs * 4;
     *total = std::max<size_t>(off, 256);
     return out;
+  }
+  // Offset in q's inbox of the flag process `from` raises when its copy of stage s's
+  // gradient is ready for the stage collective: q launches the NCCL kernel only after
+  // every other holder's flag is up, so a collective kernel never spins on SMs waiting
+  // for a peer whose own progress may depend on those SMs (gpt.cu sync_stage_body).
+  size_t ready_flag(int q, int s, int from) const {
+    size_t n = 0;
+    for_each_msg([&](int r, int m, int st, int dir) { n += proc_of(consumer_of(r, m, st, dir)) == q; });
+    return n * (msg_bytes + 4) + (size_t(s) * procs + from) * 4;
   }
   // one 32-bit ack per message produced by q for a consumer in another process
   std::map<long long, size_t> outbox_layout(int q, size_t* total) const {
