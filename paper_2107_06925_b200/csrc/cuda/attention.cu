@@ -421,8 +421,11 @@ void attn_fwd(const bf16* qkv, bf16* out, float* lse, int B, int seq, int H, boo
   CK_CUDA(cudaGetLastError());
 }
 
+// D (B*H*seq floats), then the fp32 dQ accumulator at a 128-byte boundary (vector
+// accesses and the TMA reduce-add need an aligned base for any B*H*seq)
+size_t attn_dq_offset(int B, int seq, int H) { return (size_t(B) * H * seq + 31) / 32 * 32; }
 size_t attn_bwd_scratch_floats(int B, int seq, int H) {
-  return size_t(B) * H * seq + size_t(B) * seq * H * kHd;
+  return attn_dq_offset(B, seq, H) + size_t(B) * seq * H * kHd;
 }
 
 void attn_bwd_dot(const bf16* out, const bf16* dout, float* D, int M, int seq, int H, cudaStream_t st, float* dq_zero) {
@@ -445,7 +448,7 @@ void attn_dq_out(const float* dq, bf16* dqkv, int M, int H, cudaStream_t st, flo
 void attn_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, bf16* dqkv,
               float* scratch, int B, int seq, int H, bool causal, cudaStream_t st) {
   float* D = scratch;
-  float* dq = scratch + size_t(B) * H * seq;
+  float* dq = scratch + attn_dq_offset(B, seq, H);
   const int M = B * seq;
   attn_bwd_dot(out, dout, D, M, seq, H, st, dq);
   const dim3 grid((seq + kTile - 1) / kTile, B * H);

@@ -29,6 +29,13 @@ namespace chimera::ops {
 // Per-phase clock64() stamps of CTA 0 (scripts/attn_trace.cu builds with CK_ATTN_TRACE).
 #ifdef CK_ATTN_TRACE
 __device__ long long g_attn_trace[32][16];
+__device__ int g_attn_trace_cta = 0;  // the CTA whose phases are stamped
+__device__ long long g_attn_warp[2][32][16];  // per-warp stamps [kind][tile][warp]
+#define ATTN_WTRACE(kind, j)                                                                       \
+  do {                                                                                              \
+    if ((threadIdx.x & 31) == 0 && blockIdx.x == g_attn_trace_cta && (j) < 32)                     \
+      g_attn_warp[kind][j][threadIdx.x >> 5] = clock64();                                          \
+  } while (0)
 __device__ long long g_attn_cta[4096][3];  // smid, globaltimer at entry / exit
 __device__ __forceinline__ long long gtimer() {
   long long t;
@@ -44,11 +51,14 @@ __device__ __forceinline__ int smid() {
   if (threadIdx.x == 0 && blockIdx.x < 4096) g_attn_cta[blockIdx.x][slot] = slot == 0 ? smid() : gtimer()
 #define ATTN_TRACE(cond, j, ev)                                                  \
   do {                                                                           \
-    if ((cond) && blockIdx.x == 0 && (j) < 32) g_attn_trace[j][ev] = clock64(); \
+    if ((cond) && blockIdx.x == g_attn_trace_cta && (j) < 32) g_attn_trace[j][ev] = clock64(); \
   } while (0)
 #else
 #define ATTN_TRACE(cond, j, ev) \
   do {                          \
+  } while (0)
+#define ATTN_WTRACE(kind, j) \
+  do {                       \
   } while (0)
 #define ATTN_CTA(slot)
 #endif
@@ -123,12 +133,13 @@ struct FwdSeq {
 // second Q buffer and its first S MMA runs while the current item's O is written out.
 template <bool CAUSAL>
 __global__ void __launch_bounds__(192, 2)
-    k_attn_fwd_tc(const __grid_constant__ CUtensorMap tqkv, bf16* __restrict__ out, float* __restrict__ lse,
-                  int seq, int H, int BH) {
+    k_attn_fwd_tc(const __grid_constant__ CUtensorMap tqkv, const __grid_constant__ CUtensorMap tout,
+                  bf16* __restrict__ out, float* __restrict__ lse, int seq, int H, int BH) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((ptx::smem_u32(smem) & 1023) != 0) __trap();  // swizzle atoms need 1 KB alignment
   ATTN_CTA(0);
   ATTN_CTA(1);
+  ATTN_TRACE(threadIdx.x == 0, 0, 14);  // entry
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kSmemBar);
   // K and V have separate full / empty barriers: K_j's slot frees when S_j's MMA is done
   // (not after P_j V_j), so the producer loads K two tiles ahead and the S MMA never waits
@@ -147,6 +158,7 @@ __global__ void __launch_bounds__(192, 2)
 
   if (warp == 4 && lane == 0) {
     ptx::tma_prefetch(&tqkv);
+    ptx::tma_prefetch(&tout);
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&q_full[s], 1), ptx::mbar_init(&q_empty[s], 1);
       ptx::mbar_init(&k_full[s], 1), ptx::mbar_init(&k_empty[s], 1);
@@ -164,8 +176,10 @@ __global__ void __launch_bounds__(192, 2)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;  // S: cols [0,128), O: [128,192), P (bf16 pairs): [192,256)
+  ATTN_TRACE(threadIdx.x == 0, 1, 14);  // set-up done
   cuda::pdl_wait();
   cuda::pdl_trigger();
+  ATTN_TRACE(threadIdx.x == 0, 2, 14);  // dependency resolved
 
   if (warp == 4) {
     if (lane == 0) {
@@ -218,11 +232,15 @@ __global__ void __launch_bounds__(192, 2)
         const bool last = j + 1 == q.nkb;
         FwdSeq nx = q;
         nx.advance();
-        if (nx.valid()) {  // S_g is in the softmax registers: compute the next scores now
+        // S_g is in the softmax registers: compute the next scores now -- except at an item
+        // boundary, where the item's last P V goes first (its O epilogue is the softmax
+        // warps' next step; the next item's S may still wait for that item's Q)
+        const bool s_first = nx.valid() && nx.n == n;
+        if (s_first) {
           mma_wait(s_free, g & 1);
           ATTN_TRACE(true, g, 2);
           ptx::tc_fence_after();
-          issue_s(g + 1, nx.n, nx.n != n);
+          issue_s(g + 1, nx.n, false);
         }
         mma_wait(p_full, g & 1);  // P_g in TMEM, O rescaled
         ATTN_TRACE(true, g, 3);
@@ -236,8 +254,13 @@ __global__ void __launch_bounds__(192, 2)
                            (j > 0 || k > 0) ? 1u : 0u);
         ptx::umma_commit(&v_empty[g & 1]);
         ptx::umma_commit(o_done);
-        if (last) ptx::umma_commit(&q_empty[n & 1]);
         ATTN_TRACE(true, g, 13);  // PV_g issued
+        if (nx.valid() && !s_first) {
+          mma_wait(s_free, g & 1);
+          ATTN_TRACE(true, g, 2);
+          ptx::tc_fence_after();
+          issue_s(g + 1, nx.n, true);
+        }
         q = nx;
       }
     }
@@ -247,6 +270,10 @@ __global__ void __launch_bounds__(192, 2)
     const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
     const float sl2 = 0.125f * kLog2e;
     float m = -INFINITY, l = 0.f;
+    // O of a whole query tile leaves through a TMA store staged in the item's (consumed) Q
+    // buffer; thread 0 frees that buffer (q_empty) once the store has read it, one tile
+    // later, so the warps never wait for the store
+    int pend_buf = -1;
     int g = 0;
     for (FwdSeq q = seq0; q.valid(); ++g) {
       const int b = q.bh / H, hd = q.bh % H, row_base = b * seq;
@@ -353,6 +380,11 @@ __global__ void __launch_bounds__(192, 2)
       ATTN_TRACE(t == 0, g, 9);
       ptx::tc_fence_before();
       ptx::mbar_arrive(p_full);
+      if (t == 0 && pend_buf >= 0) {
+        ptx::bulk_wait_read0();
+        ptx::mbar_arrive(&q_empty[pend_buf]);
+        pend_buf = -1;
+      }
       if (last) {  // item epilogue: O / l -> bf16, log-sum-exp
         ptx::mbar_wait(o_done, g & 1);
         ptx::tc_fence_after();
@@ -363,7 +395,33 @@ __global__ void __launch_bounds__(192, 2)
         ptx::tc_fence_before();
         ptx::mbar_arrive(o_free);
         const float inv = l > 0.f ? 1.f / l : 0.f;
-        if (qr < seq) {
+        const int qbuf = q.n & 1;
+        if (q0 + kQ <= seq) {  // whole tile: swizzled stage in the Q buffer -> TMA store
+          uint8_t* stg = smem + kSmemQ + qbuf * kTileBytes;
+#pragma unroll
+          for (int g8 = 0; g8 < 8; ++g8) {
+            uint32_t pk4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int jj = g8 * 8 + 2 * e;
+              __nv_bfloat162 hb = __floats2bfloat162_rn(__uint_as_float(o[jj >> 5][jj & 31]) * inv,
+                                                        __uint_as_float(o[jj >> 5][(jj & 31) + 1]) * inv);
+              pk4[e] = *reinterpret_cast<uint32_t*>(&hb);
+            }
+            *reinterpret_cast<uint4*>(stg + t * 128 + ((g8 ^ (t & 7)) << 4)) = make_uint4(pk4[0], pk4[1], pk4[2], pk4[3]);
+          }
+          ptx::fence_proxy_async();
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (t == 0) {
+            ptx::tma_store_2d(&tout, stg, hd * kD, row_base + q0);
+            ptx::bulk_commit();
+            pend_buf = qbuf;
+          }
+          lse[(long long)q.bh * seq + qr] = (m + __log2f(l)) / kLog2e;
+        } else {
+          if (t == 0) ptx::mbar_arrive(&q_empty[qbuf]);  // the S MMAs are done with this Q
+        }
+        if (q0 + kQ > seq && qr < seq) {
           bf16* orow = out + ((long long)row_base + qr) * (H * kD) + hd * kD;
 #pragma unroll
           for (int g8 = 0; g8 < 8; ++g8) {
@@ -382,6 +440,7 @@ __global__ void __launch_bounds__(192, 2)
       }
       q.advance();
     }
+    if (t == 0) ptx::bulk_wait0();
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -425,7 +484,11 @@ __global__ void __launch_bounds__(192, 2)
 constexpr int kB_K = 0, kB_V = 2 * kTileBytes, kB_Q = 4 * kTileBytes, kB_DO = 6 * kTileBytes,
               kB_P = 8 * kTileBytes, kB_DS = 10 * kTileBytes, kB_DQ = 12 * kTileBytes;  // stage [WG][128][128 B]
 constexpr int kB_BAR = 14 * kTileBytes;
-constexpr int kBwdSmem = kB_BAR + 256;
+// per query-tile stage: the tile's 128 log-sum-exp and D values, bulk-copied with Q / dO
+// (on the same full barrier) so the compute warps read them from shared memory -- a
+// global load hoisted by the scheduler had stalled them ~1/5 of the time (ncu r02ai)
+constexpr int kB_LSE = kB_BAR + 256;  // [2 stages][lse, D][128] fp32
+constexpr int kBwdSmem = kB_LSE + 2 * 2 * kQ * 4;
 constexpr int kBwdThreads = 512;  // WG0-1 compute, WG2 = TMA + MMA warps, WG3 dQ drain
 // Register split per SM sub-partition (one warp of each warpgroup): 2 x 200 + 56 + 56 = 512.
 constexpr int kBwdRegsCompute = 192, kBwdRegsOther = 64;
@@ -433,6 +496,10 @@ constexpr int kBwdRegsCompute = 192, kBwdRegsOther = 64;
 #define CK_ATTN_BWD_POLY_EVERY 0
 #endif
 constexpr int kBwdPolyEvery = CK_ATTN_BWD_POLY_EVERY;
+#ifndef CK_ATTN_DQ_RED  // 1: dQ drained by vector reductions from registers; 0: smem stage + TMA reduce-add
+#define CK_ATTN_DQ_RED 0
+#endif
+constexpr bool kDqRed = CK_ATTN_DQ_RED != 0;
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -467,7 +534,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     k_attn_bwd_tc(const __grid_constant__ CUtensorMap tqkv, const __grid_constant__ CUtensorMap tdo,
                   const __grid_constant__ CUtensorMap tdq, const __grid_constant__ CUtensorMap tdqkv,
                   const float* __restrict__ lse, const float* __restrict__ Dv, bf16* __restrict__ dqkv, int seq, int H,
-                  int BH, float* __restrict__ dbias) {
+                  int BH, float* __restrict__ dbias, int lse_bulk, float* __restrict__ dqacc) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((ptx::smem_u32(smem) & 1023) != 0) __trap();
   ATTN_CTA(0);
@@ -530,10 +597,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int n0 = q.n;
         while (q.valid() && q.n == n0) {
           const int st = g & 1, q0 = (q.j0 + q.it) * kQ;
+          // lse / D rows of the tile (seq % 4 == 0: 16-byte aligned, whole 16-byte rows)
+          const uint32_t lb = lse_bulk ? uint32_t(min(kQ, seq - q0)) * 4u : 0u;
           ptx::mbar_wait_sleep(&qd_empty[st], ((g >> 1) & 1) ^ 1);
-          ptx::mbar_arrive_expect_tx(&qd_full[st], 2 * kTileBytes);
+          ptx::mbar_arrive_expect_tx(&qd_full[st], 2 * kTileBytes + 2 * lb);
           ptx::tma_load_2d(smem + kB_Q + st * kTileBytes, &tqkv, &qd_full[st], hd * kD, row_base + q0);
           ptx::tma_load_2d(smem + kB_DO + st * kTileBytes, &tdo, &qd_full[st], hd * kD, row_base + q0);
+          if (lb) {
+            const long long o = (long long)q.bh * seq + q0;
+            ptx::bulk_load(smem + kB_LSE + st * 1024, lse + o, lb, &qd_full[st]);
+            ptx::bulk_load(smem + kB_LSE + st * 1024 + 512, Dv + o, lb, &qd_full[st]);
+          }
           ++g;
           q.advance();
         }
@@ -575,6 +649,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           mma_wait(st_free, g & 1);
           ptx::tc_fence_after();
           issue_s(g + 1, nx.n, nx.n != n);
+          ATTN_TRACE(true, g, 4);
         }
         const uint32_t sk = ptx::smem_u32(smem + kB_K + kvb * kTileBytes);
         const uint32_t sq = ptx::smem_u32(smem + kB_Q + st * kTileBytes);
@@ -593,6 +668,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                         (it > 0 || k > 0) ? 1u : 0u);
         }
         ptx::umma_commit(&qd_empty[st]);  // Q / dO of this tile: last read by dK / dV
+        ATTN_TRACE(true, g, 0);
         if (g >= 2) mma_wait(&dq_free[st], ((g >> 1) & 1) ^ 1);  // dQ_{g-2} drained
         ATTN_TRACE(true, g, 2);
         ptx::tc_fence_after();
@@ -606,6 +682,37 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         q = nx;
       }
     }
+  } else if (warp >= 12 && kDqRed) {  // dQ drain warpgroup: vector reductions from registers
+    // TMEM -> registers -> red.global.add.v4.f32 straight into the fp32 accumulator: no
+    // shared-memory stage (the staged TMA reduce-add moved 64 KB per tile through shared
+    // memory, the resource the MMAs' operand reads already nearly saturate)
+    const int r = (warp & 3) * 32 + lane;  // TMEM lane: query row
+    const uint32_t trow = tmem + (uint32_t((warp & 3) * 32) << 16);
+    int g = 0;
+    for (BwdSeq q = seq0; q.valid(); ++g) {
+      const int b = q.bh / H, hd = q.bh % H, row_base = b * seq, qr = (q.j0 + q.it) * kQ + r;
+      ptx::mbar_wait(&dq_full[g & 1], (g >> 1) & 1);
+      ptx::tc_fence_after();
+      float* dst = dqacc + ((long long)row_base + qr) * (H * kD) + hd * kD;
+#pragma unroll 1
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t v[32];
+        ptx::tmem_ld32(trow + kDQ + 64 * (g & 1) + 32 * hh, v);
+        ptx::tmem_ld_wait();
+        if (hh == 1) {
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&dq_free[g & 1]);
+        }
+        if (qr < seq) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 32 * hh + 4 * c), "r"(v[4 * c]),
+                         "r"(v[4 * c + 1]), "r"(v[4 * c + 2]), "r"(v[4 * c + 3])
+                         : "memory");
+        }
+      }
+      q.advance();
+    }
   } else if (warp >= 12) {  // dQ drain warpgroup
     const int r = (warp & 3) * 32 + lane;  // TMEM lane: query row
     const int dt = threadIdx.x - 384;
@@ -615,8 +722,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (BwdSeq q = seq0; q.valid(); ++g) {
       const int b = q.bh / H, hd = q.bh % H, row_base = b * seq, q0 = (q.j0 + q.it) * kQ;
       if (dt == 0) ptx::bulk_wait_read0();  // the previous reduce-adds have read the stage
+      ATTN_TRACE(dt == 0, g, 8);
       named_bar_sync(4, 128);
       ptx::mbar_wait(&dq_full[g & 1], (g >> 1) & 1);
+      ATTN_TRACE(dt == 0, g, 7);
       ptx::tc_fence_after();
 #pragma unroll 1
       for (int hh = 0; hh < 2; ++hh) {  // 32 columns at a time (few registers in this WG)
@@ -638,6 +747,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ptx::tma_reduce_add_2d(&tdq, stage, hd * kD, row_base + q0);
         ptx::tma_reduce_add_2d(&tdq, stage + kTileBytes, hd * kD + 32, row_base + q0);
         ptx::bulk_commit();
+        ATTN_TRACE(true, g, 9);
       }
       q.advance();
     }
@@ -671,15 +781,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       nl = -nl * kLog2e, nd = -nd;
     };
     const float2 sc2 = make_float2(sl2, sl2);
-    float nl, nd;
-    fetch(seq0, nl, nd);
+    float nl = 0.f, nd = 0.f;
+    if (!lse_bulk) fetch(seq0, nl, nd);
     int g = 0;
     for (BwdSeq q = seq0; q.valid(); ++g) {
       const int b = q.bh / H, hd = q.bh % H, row_base = b * seq;
       const int k0 = q.kb * kKV, q0 = (q.j0 + q.it) * kQ, qr = q0 + r, it = q.it;
       const bool last = it + 1 == q.niter;
-      float raw_l, raw_d;  // the next tile's lse / D: requested now, consumed after this tile's math
-      {
+      float raw_l = 0.f, raw_d = 0.f;  // (global path) the next tile's lse / D, used after this tile
+      if (!lse_bulk) {
         BwdSeq nq = q;
         nq.advance();
         fetch_raw(nq, raw_l, raw_d);
@@ -688,12 +798,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       ptx::mbar_wait(s_full, g & 1);
       ATTN_TRACE(threadIdx.x == 0, g, 5);
       ptx::tc_fence_after();
+      if (lse_bulk) {  // this tile's lse / D landed with its Q / dO (that phase cannot move on
+                       // before this tile's ds_full)
+        ptx::mbar_wait(&qd_full[g & 1], (g >> 1) & 1);
+        const float* ls = reinterpret_cast<const float*>(smem + kB_LSE + (g & 1) * 1024);
+        const bool in = qr < seq;
+        nl = in ? -ls[r] * kLog2e : 0.f;
+        nd = in ? -ls[128 + r] : 0.f;
+      }
       uint32_t rs[2][32], rd[2][32];
       ptx::tmem_ld32(trow + kS + 64 * g2, rs[0]);
       ptx::tmem_ld32(trow + kS + 64 * g2 + 32, rs[1]);
       ptx::tmem_ld32(trow + kDP + 64 * g2, rd[0]);
       ptx::tmem_ld32(trow + kDP + 64 * g2 + 32, rd[1]);
       ptx::tmem_ld_wait();
+      ATTN_WTRACE(0, g);
       ptx::tc_fence_before();
       ptx::mbar_arrive(st_free);
       // masking only on diagonal / tail tiles (warp-uniform branch): keys of this WG's
@@ -727,11 +846,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
       BwdSeq nx = q;
       nx.advance();
-      nl = -raw_l * kLog2e, nd = -raw_d;  // the next tile's, loaded a tile ago
+      if (!lse_bulk) nl = -raw_l * kLog2e, nd = -raw_d;  // the next tile's, loaded a tile ago
+      ATTN_TRACE(threadIdx.x == 0, g, 11);
       if (g > 0) {  // the previous tile's dV / dK / dQ MMAs have read the P / dS tiles
         ptx::mbar_wait(mm_done, (g - 1) & 1);
         ptx::tc_fence_after();
       }
+      ATTN_TRACE(threadIdx.x == 0, g, 10);
       if (epi_pending) {  // the previous item's dK / dV store has read this WG's P tile
         if (ct == 0) ptx::bulk_wait_read0();
         named_bar_sync(2 + g2, 128);
@@ -744,6 +865,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         *reinterpret_cast<uint4*>(sds + off) = make_uint4(dk[4 * k8], dk[4 * k8 + 1], dk[4 * k8 + 2], dk[4 * k8 + 3]);
       }
       ATTN_TRACE(threadIdx.x == 0, g, 6);
+      ATTN_WTRACE(1, g);
       ptx::fence_proxy_async();
       ptx::tc_fence_before();
       ptx::mbar_arrive(ds_full);
@@ -813,6 +935,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 void attn_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int seq, int H, bool causal, cudaStream_t st) {
   const long long ld = 3LL * H * kD;
   const CUtensorMap m = cuda::make_map_2d_bf16(qkv, ld, (long long)B * seq, ld, 64, 128);
+  const CUtensorMap mo = cuda::make_map_2d_bf16(out, (long long)H * kD, (long long)B * seq, (long long)H * kD, 64, 128);
   const int items = (seq + kQ - 1) / kQ * B * H;
   const dim3 grid(std::min(items, 2 * cuda::num_sms()));  // persistent: two CTAs per SM
   static bool attr = false;
@@ -821,8 +944,8 @@ void attn_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int seq, int H, 
     CK_CUDA(cudaFuncSetAttribute(k_attn_fwd_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal));
     attr = true;
   }
-  cuda::launch(causal ? k_attn_fwd_tc<true> : k_attn_fwd_tc<false>, grid, dim3(192), kSmemTotal, st, m, out, lse, seq, H,
-               B * H);
+  cuda::launch(causal ? k_attn_fwd_tc<true> : k_attn_fwd_tc<false>, grid, dim3(192), kSmemTotal, st, m, mo, out, lse, seq,
+               H, B * H);
   CK_CUDA(cudaGetLastError());
 }
 
@@ -832,7 +955,7 @@ void attn_bwd_tc(const bf16* qkv, const bf16* out, const bf16* dout, const float
   if (dbias && (reinterpret_cast<uintptr_t>(dbias) % 16))  // float4 atomics in the dQ pass
     throw chimera::capi::InternalError("attention: the bias-gradient pointer must be 16-byte aligned");
   float* D = scratch;
-  float* dq = scratch + size_t(B) * H * seq;
+  float* dq = scratch + attn_dq_offset(B, seq, H);
   const int M = B * seq;
   attn_bwd_dot(out, dout, D, M, seq, H, st, dq);  // + zeroes the dQ accumulator
   const long long ld = 3LL * H * kD;
@@ -849,7 +972,7 @@ void attn_bwd_tc(const bf16* qkv, const bf16* out, const bf16* dout, const float
   const int items = (seq + kKV - 1) / kKV * B * H;
   const dim3 grid(std::min(items, cuda::num_sms()));  // persistent: one CTA per SM
   cuda::launch(causal ? k_attn_bwd_tc<true> : k_attn_bwd_tc<false>, grid, dim3(kBwdThreads), kBwdSmem, st, mq, mo, mdq,
-               mdqkv, lse, D, dqkv, seq, H, B * H, dbias);
+               mdqkv, lse, D, dqkv, seq, H, B * H, dbias, int(seq % 4 == 0), dq);
   CK_CUDA(cudaGetLastError());
   attn_dq_out(dq, dqkv, M, H, st, dbias);
 }

@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const bf16* __restrict__ dy, con
                                                 const float* __restrict__ mean, const float* __restrict__ rstd,
                                                 const bf16* __restrict__ g, const bf16* __restrict__ dres,
                                                 bf16* __restrict__ dx, float* __restrict__ dgamma,
-                                                float* __restrict__ dbeta, float* __restrict__ dsum, int M) {
+                                                float* __restrict__ dbeta, float* __restrict__ dsum, int M,
+                                                int skip_atomics) {
   cuda::pdl_wait();
   constexpr int h = VPL * 256;
   extern __shared__ float red[];  // [8 warps][2][h] (+ [8 warps][h] column sums of dx when dsum)
@@ -102,14 +103,14 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const bf16* __restrict__ dy, con
   if (dsum)
     for (int i = threadIdx.x & 31; i < h; i += 32) colsum[i] = 0.f;  // warp-private slice
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float acc_g[VPL][8], acc_b[VPL][8];
+  // gamma / beta column partials accumulate in this warp's shared-memory slice (lane-private
+  // columns), not registers: 2 x 8 x VPL accumulators per lane had pushed the kernel past
+  // 255 registers into local-memory spills
+  float* acc = red + warp * 2 * h;  // [gamma | beta][h]
+  for (int i = lane * 4; i < 2 * h; i += 128) *reinterpret_cast<float4*>(acc + i) = make_float4(0.f, 0.f, 0.f, 0.f);
   Vec8 gam[VPL];
 #pragma unroll
-  for (int c = 0; c < VPL; ++c) {
-    gam[c].load(g + (c * 32 + lane) * 8);
-#pragma unroll
-    for (int t = 0; t < 8; ++t) acc_g[c][t] = acc_b[c][t] = 0.f;
-  }
+  for (int c = 0; c < VPL; ++c) gam[c].load(g + (c * 32 + lane) * 8);
   // rows are software-pipelined: the next row's dy / x / dres / statistics are in flight
   // (raw 16-byte vectors) while the current one is reduced and written
   const int stride = gridDim.x * 8;
@@ -140,15 +141,23 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const bf16* __restrict__ dy, con
       Vec8 dv, xv;
       dv.set(cd[c]);
       xv.set(cx[c]);
+      float ag[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const float xh = (xv.f[t] - mu) * rs;
         const float gg = dv.f[t] * gam[c].f[t];
         s1 += gg;
         s2 += gg * xh;
-        acc_g[c][t] += dv.f[t] * xh;
-        acc_b[c][t] += dv.f[t];
+        ag[t] = dv.f[t] * xh;
       }
+      float4* pg = reinterpret_cast<float4*>(acc + (c * 32 + lane) * 8);
+      float4* pb = reinterpret_cast<float4*>(acc + h + (c * 32 + lane) * 8);
+      float4 a = pg[0], b = pg[1], u = pb[0], v = pb[1];
+      a.x += ag[0], a.y += ag[1], a.z += ag[2], a.w += ag[3];
+      b.x += ag[4], b.y += ag[5], b.z += ag[6], b.w += ag[7];
+      u.x += dv.f[0], u.y += dv.f[1], u.z += dv.f[2], u.w += dv.f[3];
+      v.x += dv.f[4], v.y += dv.f[5], v.z += dv.f[6], v.w += dv.f[7];
+      pg[0] = a, pg[1] = b, pb[0] = u, pb[1] = v;
     }
     s1 = cuda::warp_sum(s1) * (1.f / h);
     s2 = cuda::warp_sum(s2) * (1.f / h);
@@ -173,15 +182,7 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const bf16* __restrict__ dy, con
       }
     }
   }
-  // reduce the per-lane column partials over the 8 warps, then one atomic per column
-#pragma unroll
-  for (int c = 0; c < VPL; ++c)
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int col = (c * 32 + lane) * 8 + t;
-      red[(warp * 2) * h + col] = acc_g[c][t];
-      red[(warp * 2 + 1) * h + col] = acc_b[c][t];
-    }
+  // reduce the per-warp column partials over the 8 warps, then one atomic per column
   __syncthreads();
   // one 16-byte vector atomic per 4 columns (a quarter of the L2 atomic operations)
   auto sum4 = [&](int base, int stride, int col) {
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(256) k_ln_bwd(const bf16* __restrict__ dy, con
     }
     return a;
   };
+  if (skip_atomics) return;  // (timing experiment only: CK_LN_BWD_SKIP_ATOMICS)
   for (int col = threadIdx.x * 4; col < h; col += blockDim.x * 4) {
     atomicAdd(reinterpret_cast<float4*>(dgamma + col), sum4(0, 2 * h, col));
     atomicAdd(reinterpret_cast<float4*>(dbeta + col), sum4(h, 2 * h, col));
@@ -503,6 +505,7 @@ void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float
     const char* e = std::getenv("CK_LN_BWD_RPW");
     return e ? std::max(1, atoi(e)) : 1;
   }();
+  static const int skip = std::getenv("CK_LN_BWD_SKIP_ATOMICS") ? 1 : 0;
   const int grid = std::min(ceil_div(M, 8 * rpw), cuda::num_sms());
   const size_t smem = size_t(dsum ? 24 : 16) * h * sizeof(float);
   switch (h) {
@@ -513,7 +516,8 @@ void layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float
       CK_CUDA(cudaFuncSetAttribute(k_ln_bwd<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * V * 256 * 4)); \
       attr = true;                                                                                 \
     }                                                                                              \
-    cuda::launch(k_ln_bwd<V>, dim3(grid), dim3(256), smem, st, dy, x, mean, rstd, g, dres, dx, dgamma, dbeta, dsum, M); \
+    cuda::launch(k_ln_bwd<V>, dim3(grid), dim3(256), smem, st, dy, x, mean, rstd, g, dres, dx, dgamma, dbeta, dsum, M, \
+                 skip);                                                                            \
     break;                                                                                         \
   }
     CK_LN(1) CK_LN(2) CK_LN(3) CK_LN(4) CK_LN(5) CK_LN(6) CK_LN(8)

@@ -58,6 +58,7 @@ void attn_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int seq, int H, 
 void attn_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, bf16* dqkv,
               float* scratch, int B, int seq, int H, bool causal, cudaStream_t st);
 size_t attn_bwd_scratch_floats(int B, int seq, int H);
+size_t attn_dq_offset(int B, int seq, int H);  // floats from the scratch base to the dQ accumulator
 // dbias (nullable, fp32 [3 H 64]) += column sums of the bf16 dqkv written (the QKV bias gradient)
 void attn_bwd_tc(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, bf16* dqkv,
                  float* scratch, int B, int seq, int H, bool causal, cudaStream_t st, float* dbias = nullptr);

@@ -10,9 +10,21 @@
 #include <cstdlib>
 #include <vector>
 
+// SM clock vs %globaltimer over ~1 ms of spinning: the rate clock64() stamps tick at
+__global__ void k_clock_rate(long long* out) {
+  long long t0, t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  const long long c0 = clock64();
+  do asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  while (t1 - t0 < 1000000);
+  out[0] = clock64() - c0, out[1] = t1 - t0;
+}
+
 int main(int argc, char** argv) {
   const int B = argc > 1 ? atoi(argv[1]) : 4, seq = argc > 2 ? atoi(argv[2]) : 1024, H = argc > 3 ? atoi(argv[3]) : 16;
   const bool bwd = argc > 4 && argv[4][0] == 'b';
+  const int trace_cta = argc > 5 ? atoi(argv[5]) : 0;
+  cudaMemcpyToSymbol(chimera::ops::g_attn_trace_cta, &trace_cta, sizeof(int));
   const size_t M = size_t(B) * seq;
   std::vector<__nv_bfloat16> h(M * 3 * H * 64);
   uint32_t x = 12345;
@@ -37,8 +49,15 @@ int main(int argc, char** argv) {
     else chimera::ops::attn_fwd_tc(qkv, out, lse, B, seq, H, true, 0);
   };
   chimera::ops::attn_fwd_tc(qkv, out, lse, B, seq, H, true, 0);
-  for (int i = 0; i < 5; ++i) run();
+  for (int i = 0; i < 400; ++i) run();  // clocks up before the traced launch
+  long long* clk;
+  cudaMalloc(&clk, 16);
+  k_clock_rate<<<1, 1>>>(clk);
+  run();
   cudaDeviceSynchronize();
+  long long clk_h[2];
+  cudaMemcpy(clk_h, clk, 16, cudaMemcpyDeviceToHost);
+  printf("SM clock during the trace: %.0f MHz (clock64 cycles per us)\n", clk_h[0] * 1e3 / clk_h[1]);
   static long long tr[32][16], cta[4096][3];
   cudaMemcpyFromSymbol(tr, chimera::ops::g_attn_trace, sizeof(tr));
   cudaMemcpyFromSymbol(cta, chimera::ops::g_attn_cta, sizeof(cta));
@@ -46,15 +65,17 @@ int main(int argc, char** argv) {
   long long t0 = cta[0][1], tend = 0, tmin = cta[0][1];
   for (int i = 0; i < ncta; ++i) tmin = std::min(tmin, cta[i][1]), tend = std::max(tend, cta[i][2]);
   printf("kernel span %.1f us, %d CTAs\n", (tend - tmin) / 1e3, ncta);
-  printf("CTA0 sm %lld start +%.2f us dur %.2f us\n", cta[0][0], (t0 - tmin) / 1e3, (cta[0][2] - cta[0][1]) / 1e3);
+  t0 = cta[trace_cta][1];
+  printf("CTA%d sm %lld start +%.2f us dur %.2f us\n", trace_cta, cta[trace_cta][0], (t0 - tmin) / 1e3,
+         (cta[trace_cta][2] - cta[trace_cta][1]) / 1e3);
   // per-tile stamps relative to kv_full of tile 0 (cycles)
   const long long c0 = bwd ? tr[0][3] : tr[0][1];
   const char* fnames[] = {"tma:k_empty", "mma:k_full", "mma:s_free", "mma:p_full", "sm:wait_s",
                           "sm:s_full",    "sm:ld_done",  "sm:max_done", "sm:o_done", "sm:p_done",
                           "w1:ld_done",   "w2:ld_done",  "w3:ld_done",  "mma:pv_iss"};
-  const char* bnames[] = {"mma:qd_full", "mma:ds_full", "mma:dq_free", "c:start", "c:lse_bar",
-                          "c:s_full",    "c:ds_done",   "c:mm_done",   "c:dq_done", "tma:qd_empty",
-                          "c:ld_done",   "c:math_done", "c:mm_wait"};
+  const char* bnames[] = {"mma:dvdk_iss", "mma:ds_full", "mma:dq_free", "c:start", "mma:s_next",
+                          "c:s_full",     "c:ds_done",   "dr:dq_full",  "dr:stg_free", "dr:red_iss",
+                          "c:mm_done",    "c:math_done", "-"};
   const char** names = bwd ? bnames : fnames;
   printf("%-4s", "j");
   const int nev = bwd ? 13 : 14;
@@ -65,7 +86,30 @@ int main(int argc, char** argv) {
     for (int e = 0; e < nev; ++e) printf(" %12lld", tr[j][e] ? tr[j][e] - c0 : -1);
     printf("\n");
   }
-  if (bwd)
+  if (!bwd)
+    printf("CTA0 fwd: entry %lld, set-up done %lld, PDL wait done %lld (cycles)\n", tr[0][14] - c0, tr[1][14] - c0,
+           tr[2][14] - c0);
+  {  // CTA start / end spread
+    long long s0 = cta[0][1], s1 = cta[0][1], d0 = cta[0][2] - cta[0][1], d1 = d0;
+    for (int i = 0; i < ncta; ++i) {
+      s0 = std::min(s0, cta[i][1]), s1 = std::max(s1, cta[i][1]);
+      d0 = std::min(d0, cta[i][2] - cta[i][1]), d1 = std::max(d1, cta[i][2] - cta[i][1]);
+    }
+    printf("CTA starts within %.2f us; CTA durations %.2f .. %.2f us\n", (s1 - s0) / 1e3, d0 / 1e3, d1 / 1e3);
+  }
+  if (bwd) {  // per compute warp: S/dP loaded, P/dS stored (cycles from the same origin)
+    static long long wt[2][32][16];
+    cudaMemcpyFromSymbol(wt, chimera::ops::g_attn_warp, sizeof(wt));
+    for (int k = 0; k < 2; ++k) {
+      printf("%s per warp (w0..w7):\n", k ? "P/dS stored" : "S/dP loaded");
+      for (int j = 0; j < 10; ++j) {
+        printf("%-4d", j);
+        for (int w = 0; w < 8; ++w) printf(" %8lld", wt[k][j][w] - c0);
+        printf("\n");
+      }
+    }
+  }
+  if (false)
     printf("CTA0 bwd: entry %lld, final drain done %lld, dK/dV stored %lld, bulk wait done %lld, exit %lld (cycles)\n",
            tr[0][13] - c0, tr[0][14] - c0, tr[0][15] - c0, tr[1][13] - c0, tr[1][14] - c0);
   // tail: histogram of CTA end times

@@ -39,7 +39,10 @@ def graph_us(fn, reps=20):
 
 def main():
     res = []
-    for (B, s, H, causal) in [(4, 1024, 16, True), (8, 128, 16, False), (4, 632, 20, True), (2, 632, 20, True)]:
+    shapes = [(4, 1024, 16, True), (8, 128, 16, False), (4, 632, 20, True), (2, 632, 20, True)]
+    if len(sys.argv) > 1 and sys.argv[1] == "scale":  # fixed vs per-tile cost
+        shapes = [(B, 1024, 16, True) for B in (1, 2, 4, 8, 16)]
+    for (B, s, H, causal) in shapes:
         qkv = torch.randn(B * s, 3 * H * 64, device="cuda").bfloat16()
         out = torch.empty(B * s, H * 64, device="cuda", dtype=torch.bfloat16)
         lse = torch.empty(B * H * s, device="cuda")

@@ -96,7 +96,8 @@ def test_bias_grad():
 
 @pytest.mark.parametrize("impl", ["mma_sync", "tcgen05"])
 @pytest.mark.parametrize("B,seq,H,causal", [(2, 256, 4, True), (1, 1024, 2, True), (2, 128, 16, False),
-                                             (1, 200, 2, True), (1, 632, 2, False), (3, 632, 2, True)])
+                                             (1, 200, 2, True), (1, 632, 2, False), (3, 632, 2, True),
+                                             (2, 203, 3, True), (2, 384, 2, False)])
 def test_attention(B, seq, H, causal, impl):
     d = 64
     qkv = (torch.randn(B * seq, 3 * H * d, device="cuda")).bfloat16()
