@@ -773,7 +773,8 @@ struct PairCfg {
   static constexpr int kABytes = 128 * BK * 2;               // this CTA's 128 rows of A
   static constexpr int kBBytes = (PBN / 2) * BK * 2;         // this CTA's PBN/2 rows of B
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = AUX ? 4 : PBN == 256 ? 5 : 7;
+  static constexpr int kStages = AUX ? 4 : PBN >= 192 ? 5 : 7;
+  static constexpr int kTmemCols = 2 * PBN <= 256 ? 256 : 512;  // two accumulators, power of 2
   // per-warp epilogue staging, 1 KB aligned for the swizzled TMA-store layouts: 2 x (U, G)
   // 2 KB bf16 chunk buffers; when AUX, 2 x 2 KB output buffers + the 8 KB residual block
   static constexpr int kAuxOff = 4096;
@@ -823,7 +824,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
     for (int w = 0; w < kPairEpiWarps; ++w) ptx::mbar_init(&auxbar[w], 1);
     ptx::fence_barrier_init();
   }
-  if (warp == 2) ptx::tmem_alloc2(tmem_slot, 2 * PBN);
+  if (warp == 2) ptx::tmem_alloc2(tmem_slot, C::kTmemCols);
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
@@ -918,6 +919,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
       tile_coords(itm.tile, num_m, num_n, mb, nb);
       if (itm.partial) {  // stream-K head / middle segment: fp32 partial -> workspace slot
         ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
+        GEMM_TRACE(warp == 4 && lane == 0, it, 2);  // partial: accumulator ready
         ptx::tc_fence_after();
         const uint32_t tp = tmem_base + (uint32_t(q * 32) << 16) + acc * PBN;
         // warp-interleaved layout: for each (chunk, 16-byte piece k) the 32 lanes' pieces
@@ -940,6 +942,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
         __threadfence();
         __syncwarp();
         if (lane == 0) atomicAdd(flags + pair * 2 + int(cta), 1);
+        GEMM_TRACE(warp == 4 && lane == 0, it, 3);  // partial stored + published
         continue;
       }
       int q_lo = pair;  // fix-up: partials of pairs [q_lo, pair) of this tile
@@ -977,9 +980,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
             while (*reinterpret_cast<volatile int*>(flags + pq * 2 + int(cta)) < kPairEpiWarps) __nanosleep(32);
         __syncwarp();
         __threadfence();
+        GEMM_TRACE(warp == 4 && lane == 0, it, 7);
       }
       const int row0 = mb * 256 + int(cta) * 128 + q * 32;
       const uint32_t t0 = tmem_base + (uint32_t(q * 32) << 16) + acc * PBN;
+      // fix-up: the first producer's partial of this warp's next chunk is loaded a chunk
+      // ahead (L2 latency under the current chunk's epilogue, not on its critical path)
+      auto partial_of = [&](int pq, int c) {
+        return slot_of(pq) + size_t((q * 2 + half) * NC + (c - half * NC)) * 32 * 32;
+      };
+      float4 pf[8];
+      if (TO && itm.fixup) {
+        const float* pc = partial_of(q_lo, half * NC);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pf[k] = *reinterpret_cast<const float4*>(pc + (k * 32 + lane) * 4);
+      }
 #pragma unroll 1
       for (int c = half * NC; c < half * NC + NC; ++c) {
         uint32_t r[32];
@@ -1000,12 +1015,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
           }
           const uint32_t biasc = biasn;
           if (c + 1 < half * NC + NC) biasn = bias_prefetch(ep, col0 + 32, N, lane);
+          float4 cur[8];
+          if (itm.fixup) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) cur[k] = pf[k];
+            if (c + 1 < half * NC + NC) {
+              const float* pn = partial_of(q_lo, c + 1);
+#pragma unroll
+              for (int k = 0; k < 8; ++k) pf[k] = *reinterpret_cast<const float4*>(pn + (k * 32 + lane) * 4);
+            }
+          }
           ptx::tmem_ld_wait();
           for (int pq = q_lo; pq < pair; ++pq) {  // stream-K fix-up: + the partial tiles
-            const float* pc = slot_of(pq) + size_t((q * 2 + half) * NC + (c - half * NC)) * 32 * 32;
+            if (pq > q_lo) {  // (a tile spanning three or more pairs: the later producers' here)
+              const float* pc = partial_of(pq, c);
+#pragma unroll
+              for (int k = 0; k < 8; ++k) cur[k] = *reinterpret_cast<const float4*>(pc + (k * 32 + lane) * 4);
+            }
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-              const float4 v = *reinterpret_cast<const float4*>(pc + (k * 32 + lane) * 4);
+              const float4 v = cur[k];
               r[4 * k] = __float_as_uint(__uint_as_float(r[4 * k]) + v.x);
               r[4 * k + 1] = __float_as_uint(__uint_as_float(r[4 * k + 1]) + v.y);
               r[4 * k + 2] = __float_as_uint(__uint_as_float(r[4 * k + 2]) + v.z);
@@ -1041,7 +1070,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
   ptx::cluster_sync();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc2(tmem_base, 2 * PBN);
+    ptx::tmem_dealloc2(tmem_base, C::kTmemCols);
   }
 }
 
@@ -1183,6 +1212,8 @@ template <int BN, bool A_MN, bool B_MN, int EPI>
 void launch_any(int M, int N, int K, const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B,
                 long long ldb, const EpiArgs& ep, cudaStream_t st) {
   if constexpr (BN == 0) launch_pair<256, A_MN, B_MN, EPI>(M, N, K, A, lda, B, ldb, ep, st);
+  else if constexpr (BN == 1 && !B_MN) launch_pair<192, A_MN, B_MN, EPI>(M, N, K, A, lda, B, ldb, ep, st);
+  else if constexpr (BN == 1) launch_pair<256, A_MN, B_MN, EPI>(M, N, K, A, lda, B, ldb, ep, st);  // K-major B only
   else launch<BN, A_MN, B_MN, EPI>(M, N, K, A, lda, B, ldb, ep, st);
 }
 
@@ -1227,18 +1258,34 @@ void by_layout(Epi epi, bool a_mn, bool b_mn, int M, int N, int K, const __nv_bf
 // >= 8 K-blocks deep); that variant pays the finalize pass: a launch plus M*N*(8+2)
 // bytes (+2 residual / gelu operand, +2 second output) at ~4 TB/s, and a per-wave
 // fixed cost for the shallower tiles.
+// Per-pair TFLOP/s of the 256 x 192 tile in the wave model (CK_GEMM_RATE192, e.g. 23).
+// Off by default: timed alone it is 6-8 % faster on the N = 1280 shapes (50 -> 70 busy
+// pairs), but in the one-GPU step, where eight ranks' kernels share the SMs, the idle
+// pairs of a 256-wide launch are used by the other ranks anyway and the narrower tile's
+// lower work per SM (operand feed) cost 3.6 % of throughput (profiles/r02ax_*).
+inline double rate192() {
+  static const double r = [] {
+    const char* e = std::getenv("CK_GEMM_RATE192");
+    return e ? atof(e) : 0.0;
+  }();
+  return r;
+}
+// CTA pair 256 x 192 (K-major B only: an MN-major B half of 96 rows is not whole 64-row
+// swizzle atoms): three quarters of the pair tile's work per output tile, for the N = 1280
+// shapes of GPT-2 1.3B where 256-wide tiles fill 50 of 74 pairs (70 with 192 columns).
 struct TilePlan {
-  int choice;  // 0 = CTA pair 256x256, else single-CTA 128 x choice
+  int choice;  // 0 = CTA pair 256x256, 1 = CTA pair 256x192, else single-CTA 128 x choice
   int ks;      // K-slices (bf16 epilogues through the workspace when > 1)
 };
 
-TilePlan pick_tile(Epi epi, int M, int N, int K, bool can_split) {
+TilePlan pick_tile(Epi epi, int M, int N, int K, bool can_split, bool b_mn) {
   struct Cand {
     int choice, bm, bn, slots;
     double rate;
   };
-  const Cand cands[] = {{0, 256, 256, cuda::num_sms() / 2, 24.6}, {256, BM, 256, cuda::num_sms(), 11.4},
-                        {128, BM, 128, cuda::num_sms(), 7.0}, {64, BM, 64, cuda::num_sms(), 3.6}};
+  const Cand cands[] = {{0, 256, 256, cuda::num_sms() / 2, 24.6}, {1, 256, 192, cuda::num_sms() / 2, rate192()},
+                        {256, BM, 256, cuda::num_sms(), 11.4}, {128, BM, 128, cuda::num_sms(), 7.0},
+                        {64, BM, 64, cuda::num_sms(), 3.6}};
   const int kb = (K + BK - 1) / BK;
   const int kmax = can_split ? std::max(1, std::min(4, kb / 8)) : 1;
   const double wave_fixed = 1.5e6;  // ps: prologue / fill / exposed epilogue per wave
@@ -1248,6 +1295,7 @@ TilePlan pick_tile(Epi epi, int M, int N, int K, bool can_split) {
   double best_t = 1e300;
   for (const Cand& c : cands) {
     if (c.choice == 0 && (M < 256 || N < 256)) continue;
+    if (c.choice == 1 && (M < 256 || N < 192 || b_mn || c.rate <= 0.0)) continue;
     if (c.choice == 256 && N <= 128) continue;
     const long long tiles = (long long)((M + c.bm - 1) / c.bm) * ((N + c.bn - 1) / c.bn);
     for (int kq = 1; kq <= (epi == kAccF32 ? 1 : kmax); ++kq) {
@@ -1262,14 +1310,15 @@ TilePlan pick_tile(Epi epi, int M, int N, int K, bool can_split) {
   return best;
 }
 
-int pick_tile(Epi epi, int M, int N, int K) { return pick_tile(epi, M, N, K, false).choice; }
+int pick_tile(Epi epi, int M, int N, int K) { return pick_tile(epi, M, N, K, false, false).choice; }
 
 namespace {
 
 void dispatch(int choice, Epi epi, bool a_mn, bool b_mn, int M, int N, int K, const __nv_bfloat16* A, long long lda,
               const __nv_bfloat16* B, long long ldb, const EpiArgs& ep, cudaStream_t st) {
-  if (choice == 0 && (M < 256 || N < 256)) choice = 128;
+  if ((choice == 0 && (M < 256 || N < 256)) || (choice == 1 && (M < 256 || N < 192))) choice = 128;
   if (choice == 0) by_layout<0>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
+  else if (choice == 1) by_layout<1>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
   else if (choice == 256) by_layout<256>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
   else if (choice == 64) by_layout<64>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
   else by_layout<128>(epi, a_mn, b_mn, M, N, K, A, lda, B, ldb, ep, st);
@@ -1304,10 +1353,10 @@ void gemm(Epi epi, bool a_mn, bool b_mn, int M, int N, int K, const __nv_bfloat1
     throw chimera::capi::InternalError("gemm: operands must be 16-byte aligned with ld % 8 == 0");
   // CTA-pair 256 x 256 or single-CTA 128 x {256, 128, 64} tiles, split-K slices (pick_tile).
   static const int force = [] {
-    const char* e = std::getenv("CK_GEMM_TILE");  // "pair" | "256" | "128" | "64" (benchmarks)
+    const char* e = std::getenv("CK_GEMM_TILE");  // "pair" | "pair192" | "256" | "128" | "64" (benchmarks)
     if (!e) return -1;
     const std::string v(e);
-    return v == "pair" ? 0 : v == "256" ? 256 : v == "64" ? 64 : 128;
+    return v == "pair" ? 0 : v == "pair192" ? 1 : v == "256" ? 256 : v == "64" ? 64 : 128;
   }();
   // The workspace route is OFF unless CK_GEMM_SPLIT_BF16=1 (wave model decides) or n > 1
   // (n slices), or a caller forces a slice count: graph-timed on B200 it never beat the
@@ -1319,7 +1368,7 @@ void gemm(Epi epi, bool a_mn, bool b_mn, int M, int N, int K, const __nv_bfloat1
     return e ? atoi(e) : 0;
   }();
   const bool can_split = (force_split != 0 || ep.ksplit >= 1) && split_ok(epi, M, N, ep);
-  TilePlan plan = pick_tile(epi, M, N, K, can_split);
+  TilePlan plan = pick_tile(epi, M, N, K, can_split, b_mn);
   if (force >= 0) plan.choice = force;
   if (ep.tile >= 0) plan.choice = ep.tile;
   if (can_split && force_split > 1) plan.ks = force_split;

@@ -45,13 +45,16 @@ int main(int argc, char** argv) {
   for (int i = 0; i < 5; ++i) run();
   cudaDeviceSynchronize();
   static long long tr[16][8];
+  cudaMemcpyToSymbol(chimera::gemm::g_gemm_trace, tr, sizeof(tr));  // clear stale stamps
+  run();
+  cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(tr, chimera::gemm::g_gemm_trace, sizeof(tr));
   const long long c0 = tr[0][0];
-  printf("CTA %d: item  mma_start  mma_issued  epi4_start  epi4_end  epi11_start epi11_end   (cycles from item 0 start)\n", block);
+  printf("CTA %d: item  mma_start  mma_issued  epi4_start  epi4_end  epi11_start epi11_end  fixup_waited (cycles from item 0 start)\n", block);
   printf("kernel entry -> item0 mma start: %lld cycles\n", tr[0][0] - tr[0][6]);
   for (int t = 0; t < 16 && tr[t][0]; ++t)
-    printf("%4d %10lld %11lld %11lld %9lld %11lld %9lld\n", t, tr[t][0] - c0, tr[t][1] - c0, tr[t][2] - c0,
-           tr[t][3] - c0, tr[t][4] - c0, tr[t][5] - c0);
+    printf("%4d %10lld %11lld %11lld %9lld %11lld %9lld %11lld\n", t, tr[t][0] - c0, tr[t][1] - c0, tr[t][2] - c0,
+           tr[t][3] - c0, tr[t][4] - c0, tr[t][5] - c0, tr[t][7] ? tr[t][7] - c0 : -1);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);

@@ -28,7 +28,9 @@ def main():
     name, cfg, _ = bench.CONFIGS[args.config]
     cfg = dict(cfg, B=args.B or cfg["B"])
     shapes = bench.roofline_shapes(PRESETS[name], cfg)
-    ws = torch.zeros(max(M * N for (M, N, K, a, b, w) in shapes if not (a and b)), device="cuda")
+    # the trainer's split-K / stream-K workspace is >= 74 pairs x 2 x 128 x 256 partial slots
+    ws = torch.zeros(max([M * N for (M, N, K, a, b, w) in shapes if not (a and b)] + [74 * 2 * 128 * 256 + 4096]),
+                     device="cuda")
     big = torch.zeros(256 << 20, device="cuda")
     tot = {"ours": 0.0, "cublas": 0.0, "w": 0.0}
     for (M, N, K, a, b, w) in shapes:
