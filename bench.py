@@ -474,6 +474,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="chimera")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--head-efficiency", type=float, default=None,
+                    help="balanced partition: LM head cost per FLOP relative to a layer's (default: measured)")
     ap.add_argument("--diag-timeout", type=float, default=300.0,
                     help="multi-process: seconds allowed for the profiled iteration + sync A/B")
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
@@ -494,7 +496,9 @@ def main():
         import dataclasses
         from paper_2107_06925_b200 import pipesim as P
         from paper_2107_06925_b200.gpt import balanced_partition
-        shape = dataclasses.replace(shape, stage_layers=balanced_partition(shape, P.PipelineConfig(**CFG)))
+        shape = dataclasses.replace(shape, stage_layers=balanced_partition(shape, P.PipelineConfig(**CFG),
+                                                                           *([args.head_efficiency]
+                                                                             if args.head_efficiency else [])))
     if args.impl == "reference":
         return run_reference(args, shape)
 

@@ -92,18 +92,25 @@ PRESETS = {
 }
 
 
-def balanced_partition(shape: GPTShape, config) -> tuple:
+# LM head + loss cost per FLOP relative to a transformer layer's, measured on B200: the
+# head stage's tasks of GPT-2 medium D=4 took 2.27 ms for 3 layers + head against 2.86 ms
+# for 7 layers (profiles/timelines/r02_d4n8fd_nobwdfuse_graph.*) -> the head costs 2.5
+# layers, 0.67 of its FLOP ratio (one large, efficient N = 50304 GEMM per pass)
+HEAD_EFFICIENCY = 0.67
+
+
+def balanced_partition(shape: GPTShape, config, head_efficiency: float = HEAD_EFFICIENCY) -> tuple:
     """Layers per stage minimising the busiest pipeline worker's load (then the busiest
-    stage), counting a layer as 1 and the LM head as its FLOP ratio
+    stage), counting a layer as 1 and the LM head as head_efficiency x its FLOP ratio
     V / (12 h + 2 s*causal_fraction) to a layer.  Chimera worker w holds stage w of the
     down pipelines and the mirrored stage of the up ones, so the stage carrying the
-    head should be shorter than the middle ones.  E.g. GPT-2 medium D=4: (5, 7, 7, 5) and
-    (7, 7, 7, 3) load the busiest worker equally (10 layers + head); the tie-break on the
-    busiest single stage (7 vs 5 + head = 8.8) picks (7, 7, 7, 3)."""
+    head should be shorter than the middle ones.  E.g. GPT-2 medium D=4 (head = 2.5
+    layers): (7, 6, 7, 4) loads worker 0 with 7 + 4 + 2.5 and worker 1 with 6 + 7, where
+    (7, 7, 7, 3) left worker 0 at 12.5 against worker 1's 14."""
     import itertools
     D, L = config.D, shape.n_layer
     attn = shape.seq * (0.5 if shape.causal else 1.0)
-    head = shape.vocab / (12.0 * shape.hidden + 2.0 * attn)
+    head = head_efficiency * shape.vocab / (12.0 * shape.hidden + 2.0 * attn)
     sched = json.loads(generate_json(config, None, -1))
     holds = [sorted({t["stage"] for t in wl}) for wl in sched["per_worker"]]
     best, best_key = None, None
