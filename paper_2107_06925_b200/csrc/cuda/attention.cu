@@ -378,22 +378,36 @@ __global__ void __launch_bounds__(128) k_attn_bwd(const bf16* __restrict__ qkv, 
 // per CTA: any head count), threadIdx.y <-> one of 4 rows in flight; CTAs stride over
 // row quads.
 constexpr int kDqGroups = 256;
+// kDqUnroll rows per thread in flight: one CTA per SM holds ~512 threads, so one row's
+// 32 bytes per thread left the SMs ~2 TB/s short of HBM on this pure stream
+constexpr int kDqUnroll = 4;
 __global__ void __launch_bounds__(1024) k_dq_out(const float* __restrict__ acc, bf16* __restrict__ dqkv, int n_rows,
                                                  int H, float* __restrict__ dbias) {
   cuda::pdl_wait();
   const int w = H * kHd, g = blockIdx.y * blockDim.x + threadIdx.x;  // w is a multiple of 64
   const bool live = g < w / 8;
+  const int rs = gridDim.x * 4;  // row stride between a thread's rows
   float cs[8] = {};
-  for (int r = blockIdx.x * 4 + threadIdx.y; live && r < n_rows; r += gridDim.x * 4) {
-    const float4* p = reinterpret_cast<const float4*>(acc + (long long)r * w) + 2 * g;
-    const float4 a = __ldcs(p), b = __ldcs(p + 1);
-    const uint4 q = make_uint4(pack(a.x * 0.125f, a.y * 0.125f), pack(a.z * 0.125f, a.w * 0.125f),
-                               pack(b.x * 0.125f, b.y * 0.125f), pack(b.z * 0.125f, b.w * 0.125f));
-    *reinterpret_cast<uint4*>(dqkv + (long long)r * 3 * w + 8 * g) = q;
-    if (dbias) {
-      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q);
+  for (int r0 = blockIdx.x * 4 + threadIdx.y; live && r0 < n_rows; r0 += kDqUnroll * rs) {
+    float4 a[kDqUnroll], b[kDqUnroll];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) cs[t] += __bfloat162float(h[t]);
+    for (int u = 0; u < kDqUnroll; ++u)
+      if (r0 + u * rs < n_rows) {
+        const float4* p = reinterpret_cast<const float4*>(acc + (long long)(r0 + u * rs) * w) + 2 * g;
+        a[u] = __ldcs(p), b[u] = __ldcs(p + 1);
+      }
+#pragma unroll
+    for (int u = 0; u < kDqUnroll; ++u) {
+      const int r = r0 + u * rs;
+      if (r >= n_rows) break;
+      const uint4 q = make_uint4(pack(a[u].x * 0.125f, a[u].y * 0.125f), pack(a[u].z * 0.125f, a[u].w * 0.125f),
+                                 pack(b[u].x * 0.125f, b[u].y * 0.125f), pack(b[u].z * 0.125f, b[u].w * 0.125f));
+      *reinterpret_cast<uint4*>(dqkv + (long long)r * 3 * w + 8 * g) = q;
+      if (dbias) {
+        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) cs[t] += __bfloat162float(h[t]);
+      }
     }
   }
   if (dbias) {  // reduce the 4 row lanes in shared memory: one atomic set per CTA and column group

@@ -60,5 +60,39 @@ def main():
             print(json.dumps(res[-1]), flush=True)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not (len(sys.argv) > 1 and sys.argv[1] == "breakdown"):
     main()
+
+
+def kernel_breakdown():
+    """Per-kernel device time of one attention backward (CUPTI via torch.profiler)."""
+    from torch.profiler import ProfilerActivity, profile
+    B, s, H = 4, 1024, 16
+    qkv = torch.randn(B * s, 3 * H * 64, device="cuda").bfloat16()
+    out = torch.empty(B * s, H * 64, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(B * H * s, device="cuda")
+    dout = torch.randn_like(out)
+    dqkv = torch.empty_like(qkv)
+    db = torch.zeros(3 * H * 64, device="cuda")
+    ck.attn_fwd_tc(qkv, out, lse, B, s, H, True)
+    for _ in range(3):
+        ck.attn_bwd(qkv, out, dout, lse, dqkv, B, s, H, True, impl="tcgen05", dbias=db)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(5):
+            ck.attn_bwd(qkv, out, dout, lse, dqkv, B, s, H, True, impl="tcgen05", dbias=db)
+        torch.cuda.synchronize()
+    agg = {}
+    for ev in prof.events():
+        if ev.device_type != torch.autograd.DeviceType.CUDA:
+            continue
+        import re
+        mk = re.search(r"(k_\w+)", ev.name)
+        k = mk.group(1) if mk else ev.name[:40]
+        agg.setdefault(k, []).append(ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total)
+    for k, v in agg.items():
+        print(json.dumps({"kernel": k, "n": len(v), "avg_us": round(sum(v) / len(v), 2)}), flush=True)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "breakdown":
+    kernel_breakdown()
