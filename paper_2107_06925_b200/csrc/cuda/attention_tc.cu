@@ -500,6 +500,16 @@ constexpr int kBwdPolyEvery = CK_ATTN_BWD_POLY_EVERY;
 #define CK_ATTN_DQ_RED 0
 #endif
 constexpr bool kDqRed = CK_ATTN_DQ_RED != 0;
+// 1: the dQ MMA takes dS from TMEM (compute warps tcgen05.st it beside the smem copy the
+// dK MMA reads transposed), the dQ accumulator single-buffered to make room: 32 KB less
+// shared-memory operand traffic per tile, the resource this kernel is bound by
+#ifndef CK_ATTN_DS_TMEM
+#define CK_ATTN_DS_TMEM 1
+#endif
+constexpr bool kDsTmem = CK_ATTN_DS_TMEM != 0;
+// dQ accumulator buffer / barrier slot of tile g and the parity of its full phase
+__device__ __forceinline__ int dq_slot(int g) { return kDsTmem ? 0 : (g & 1); }
+__device__ __forceinline__ uint32_t dq_full_parity(int g) { return kDsTmem ? (g & 1) : ((g >> 1) & 1); }
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -577,7 +587,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const uint32_t tmem = *tmem_slot;
   cuda::pdl_wait();
   cuda::pdl_trigger();
-  constexpr uint32_t kS = 0, kDP = 128, kDV = 256, kDK = 320, kDQ = 384;
+  constexpr uint32_t kS = 0, kDP = 128, kDV = 256, kDK = 320, kDQ = 384, kDS = 448;  // kDS: dS bf16 pairs (kDsTmem)
 
   // setmaxnreg is warpgroup-aligned: one instruction for warps 8-15 (TMA, MMA, two idle,
   // the drain warpgroup), one for the compute warpgroups, each heading its role block
@@ -669,15 +679,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         ptx::umma_commit(&qd_empty[st]);  // Q / dO of this tile: last read by dK / dV
         ATTN_TRACE(true, g, 0);
-        if (g >= 2) mma_wait(&dq_free[st], ((g >> 1) & 1) ^ 1);  // dQ_{g-2} drained
+        if (kDsTmem) {
+          if (g >= 1) mma_wait(&dq_free[0], (g - 1) & 1);  // dQ_{g-1} read out of TMEM
+        } else if (g >= 2) {
+          mma_wait(&dq_free[st], ((g >> 1) & 1) ^ 1);  // dQ_{g-2} drained
+        }
         ATTN_TRACE(true, g, 2);
         ptx::tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < kKV / 16; ++k)  // dQ = dS K: reduce over 16 keys per step
-          ptx::umma_f16(tmem + kDQ + 64 * st, ptx::smem_desc_sw128(sds + (k >> 2) * kTileBytes + (k & 3) * 32, 16, 1024),
-                        ptx::smem_desc_sw128(sk + k * 2048, kTileBytes, 1024), id_q, k > 0);
+        for (int k = 0; k < kKV / 16; ++k) {  // dQ = dS K: reduce over 16 keys per step
+          if (kDsTmem)  // A = dS from TMEM: 16 keys = 8 columns of bf16 pairs
+            ptx::umma_f16_ts(tmem + kDQ, tmem + kDS + k * 8, ptx::smem_desc_sw128(sk + k * 2048, kTileBytes, 1024), id_q,
+                             k > 0 ? 1u : 0u);
+          else
+            ptx::umma_f16(tmem + kDQ + 64 * st,
+                          ptx::smem_desc_sw128(sds + (k >> 2) * kTileBytes + (k & 3) * 32, 16, 1024),
+                          ptx::smem_desc_sw128(sk + k * 2048, kTileBytes, 1024), id_q, k > 0);
+        }
         ptx::umma_commit(mm_done);
-        ptx::umma_commit(&dq_full[st]);
+        ptx::umma_commit(&dq_full[dq_slot(g)]);
         if (last) ptx::umma_commit(&kv_empty[kvb]);  // this item's K / V no longer read
         q = nx;
       }
@@ -691,17 +711,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     int g = 0;
     for (BwdSeq q = seq0; q.valid(); ++g) {
       const int b = q.bh / H, hd = q.bh % H, row_base = b * seq, qr = (q.j0 + q.it) * kQ + r;
-      ptx::mbar_wait(&dq_full[g & 1], (g >> 1) & 1);
+      ptx::mbar_wait(&dq_full[dq_slot(g)], dq_full_parity(g));
       ptx::tc_fence_after();
       float* dst = dqacc + ((long long)row_base + qr) * (H * kD) + hd * kD;
 #pragma unroll 1
       for (int hh = 0; hh < 2; ++hh) {
         uint32_t v[32];
-        ptx::tmem_ld32(trow + kDQ + 64 * (g & 1) + 32 * hh, v);
+        ptx::tmem_ld32(trow + kDQ + 64 * dq_slot(g) + 32 * hh, v);
         ptx::tmem_ld_wait();
         if (hh == 1) {
           ptx::tc_fence_before();
-          ptx::mbar_arrive(&dq_free[g & 1]);
+          ptx::mbar_arrive(&dq_free[dq_slot(g)]);
         }
         if (qr < seq) {
 #pragma unroll
@@ -724,17 +744,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (dt == 0) ptx::bulk_wait_read0();  // the previous reduce-adds have read the stage
       ATTN_TRACE(dt == 0, g, 8);
       named_bar_sync(4, 128);
-      ptx::mbar_wait(&dq_full[g & 1], (g >> 1) & 1);
+      ptx::mbar_wait(&dq_full[dq_slot(g)], dq_full_parity(g));
       ATTN_TRACE(dt == 0, g, 7);
       ptx::tc_fence_after();
 #pragma unroll 1
       for (int hh = 0; hh < 2; ++hh) {  // 32 columns at a time (few registers in this WG)
         uint32_t v[32];
-        ptx::tmem_ld32(trow + kDQ + 64 * (g & 1) + 32 * hh, v);
+        ptx::tmem_ld32(trow + kDQ + 64 * dq_slot(g) + 32 * hh, v);
         ptx::tmem_ld_wait();
         if (hh == 1) {
           ptx::tc_fence_before();
-          ptx::mbar_arrive(&dq_free[g & 1]);
+          ptx::mbar_arrive(&dq_free[dq_slot(g)]);
         }
 #pragma unroll
         for (int c = 0; c < 8; ++c)
@@ -863,6 +883,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int off = r * 128 + ((k8 ^ (r & 7)) << 4);
         *reinterpret_cast<uint4*>(sp + off) = make_uint4(pk[4 * k8], pk[4 * k8 + 1], pk[4 * k8 + 2], pk[4 * k8 + 3]);
         *reinterpret_cast<uint4*>(sds + off) = make_uint4(dk[4 * k8], dk[4 * k8 + 1], dk[4 * k8 + 2], dk[4 * k8 + 3]);
+      }
+      if (kDsTmem) {  // this WG's 64 keys of dS -> TMEM columns [kDS + 32 g2, +32), the dQ MMA's A
+        tmem_st32(trow + kDS + 32 * g2, dk);
+        tmem_st_wait();
       }
       ATTN_TRACE(threadIdx.x == 0, g, 6);
       ATTN_WTRACE(1, g);
