@@ -37,6 +37,11 @@ extern "C" CK_API int ck_link_plan(const char* schedule_json, int ranks_per_proc
       Value ia = Value::object();
       ia.set("bytes", Value::integer((long long)ti));
       ia.set("slots", std::move(a));
+      // stage-collective rendezvous flags: [stage][from process] (LinkPlan::ready_flag)
+      Value rf = Value::array();
+      for (int st = 0; st < lp.D; ++st)
+        for (int from = 0; from < lp.procs; ++from) rf.push(Value::integer((long long)lp.ready_flag(q, st, from)));
+      ia.set("ready_flags", std::move(rf));
       Value ob = Value::object();
       ob.set("bytes", Value::integer((long long)to));
       ob.set("slots", std::move(b));

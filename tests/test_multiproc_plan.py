@@ -44,6 +44,13 @@ def test_plan_invariants(cfg):
             spans = sorted((v[0], v[0] + (8 << 20)) for v in pl["inbox"][q]["slots"].values())
             assert all(a[1] <= b[0] for a, b in zip(spans, spans[1:]))
             assert all(v[1] + 4 <= pl["inbox"][q]["bytes"] for v in pl["inbox"][q]["slots"].values())
+            # the stage-collective rendezvous flags: distinct, 4-byte aligned, past every
+            # message buffer and flag, inside the arena
+            rf = pl["inbox"][q]["ready_flags"]
+            assert len(rf) == cfg.D * G and len(set(rf)) == len(rf) and all(r % 4 == 0 for r in rf)
+            used = [v[0] + (8 << 20) for v in pl["inbox"][q]["slots"].values()] + \
+                   [v[1] + 4 for v in pl["inbox"][q]["slots"].values()]
+            assert min(rf) >= max(used, default=0) and max(rf) + 4 <= pl["inbox"][q]["bytes"]
         # every stage is held by 2f*W ranks (perfmodel::replicas_per_stage)
         if cfg.scheme == "chimera":
             holders = set()
