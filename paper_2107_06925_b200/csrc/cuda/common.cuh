@@ -100,6 +100,13 @@ inline bool pdl_enabled() {
   }();
   return on;
 }
+// Stream priorities (CK_STREAM_PRIO, see gpt.cu): when on, every launch carries its
+// stream's priority as a launch attribute so graph kernel nodes keep it (graphs are then
+// instantiated with cudaGraphInstantiateFlagUseNodePriority).
+inline bool& node_priority_flag() {
+  static bool on = false;
+  return on;
+}
 template <typename... KArgs, typename... Args>
 inline void launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -107,11 +114,21 @@ inline void launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, c
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (pdl_enabled()) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  if (node_priority_flag()) {
+    int prio = 0;
+    if (cudaStreamGetPriority(st, &prio) == cudaSuccess) {
+      at[n].id = cudaLaunchAttributePriority;
+      at[n++].val.priority = prio;
+    }
+  }
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = n;
   CK_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

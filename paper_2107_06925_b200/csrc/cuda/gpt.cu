@@ -452,17 +452,26 @@ Trainer::Trainer(const ModelShape& shape, const pipesim::Schedule& sched, float 
       CK_CUDA(cudaMemset(sc.ws, 0, (size_t)sc.ws_elems * sizeof(float)));
     }
     cudaStream_t s;
+    // CK_STREAM_PRIO=1: the activation / gradient chain streams at the highest priority,
+    // the weight-gradient side streams at the lowest (off the pipeline's critical path)
+    static const int prio_mode = [] {
+      const char* e = std::getenv("CK_STREAM_PRIO");
+      return e ? atoi(e) : 0;
+    }();
+    int prio_lo = 0, prio_hi = 0;
+    CK_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    if (prio_mode) cuda::node_priority_flag() = true;
     // CK_SERIALIZE=1: every rank issues on one stream (debug: rules out cross-stream races)
     const bool serial = std::getenv("CK_SERIALIZE") != nullptr;
     if (k > 0 && serial) s = I.streams[0];
-    else CK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    else CK_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, prio_mode ? prio_hi : 0));
     I.streams.push_back(s);
     // CK_WGRAD_SIDE=0: weight gradients stay on the rank stream (default under CK_SERIALIZE
     // unless CK_WGRAD_SIDE=1: one chain stream + side streams, the one-rank-per-GPU shape)
     const char* ws = std::getenv("CK_WGRAD_SIDE");
     const bool on = ws ? std::string(ws) != "0" : !serial;
     if (!on) sc.side = s;
-    else CK_CUDA(cudaStreamCreateWithFlags(&sc.side, cudaStreamNonBlocking));
+    else CK_CUDA(cudaStreamCreateWithPriority(&sc.side, cudaStreamNonBlocking, prio_mode ? prio_lo : 0));
     for (auto& e : sc.fork) CK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : sc.join) CK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     I.scratch.push_back(sc);
@@ -1330,7 +1339,8 @@ float Trainer::step() {
       CK_CUDA(cudaStreamBeginCapture(I.main_stream, cudaStreamCaptureModeThreadLocal));
       issue_iteration();
       CK_CUDA(cudaStreamEndCapture(I.main_stream, &I.graph));
-      CK_CUDA(cudaGraphInstantiate(&I.graph_exec, I.graph, 0));
+      CK_CUDA(cudaGraphInstantiate(&I.graph_exec, I.graph,
+                                   cuda::node_priority_flag() ? cudaGraphInstantiateFlagUseNodePriority : 0));
       // launches per step = the kernel nodes of the captured iteration (the issue-time
       // count above is an estimate: split-K finalize passes, NCCL kernels...)
       size_t n = 0;
@@ -1389,7 +1399,7 @@ std::string Trainer::profile_step() {
   I.capturing_profile = false;
   if (graphed) {
     CK_CUDA(cudaStreamEndCapture(I.main_stream, &g));
-    CK_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    CK_CUDA(cudaGraphInstantiate(&ge, g, cuda::node_priority_flag() ? cudaGraphInstantiateFlagUseNodePriority : 0));
     CK_CUDA(cudaGraphLaunch(ge, I.main_stream));
   }
   CK_CUDA(cudaStreamSynchronize(I.main_stream));
