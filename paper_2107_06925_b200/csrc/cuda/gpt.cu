@@ -1586,11 +1586,14 @@ void Trainer::connect(const std::string& all_blobs, const std::string& nccl_id) 
       if (Nccl::get().CommSplit(I.world_comm, mine ? s : NCCL_SPLIT_NOCOLOR, I.proc, &c, nullptr) != ncclSuccess)
         throw capi::InternalError("ncclCommSplit failed");
     } else if (mine) {
-      // the stage allreduces overlap compute: cap their CTAs (CK_NCCL_MAX_CTAS, default
-      // 16 of 148 SMs; 0 = NCCL's own choice) so the pipeline keeps its SMs
+      // CK_NCCL_MAX_CTAS=n caps the stage allreduces' CTAs (ncclConfig_t.maxCTAs).  Default
+      // 0 = NCCL's own choice: a cap of 16 of the 148 SMs, meant to leave the SMs to the
+      // pipeline, measured slower on every config (4 GPUs: configs[3] -1 %, GPT-2 1.3B D=4
+      // -2.3 %, configs[4] f=2 -11 %; profiles/r02bi_*, r02bj_*): the eager allreduce
+      // that ends the iteration is on the critical path
       ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
       const char* mc = std::getenv("CK_NCCL_MAX_CTAS");
-      const int max_ctas = mc ? atoi(mc) : 16;
+      const int max_ctas = mc ? atoi(mc) : 0;
       if (max_ctas > 0) cfg.maxCTAs = max_ctas, cfg.minCTAs = std::min(cfg.minCTAs > 0 ? cfg.minCTAs : 1, max_ctas);
       const ncclResult_t rc =
           Nccl::get().CommInitRankConfig
