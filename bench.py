@@ -476,7 +476,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--head-efficiency", type=float, default=None,
                     help="balanced partition: LM head cost per FLOP relative to a layer's (default: measured)")
-    ap.add_argument("--diag-timeout", type=float, default=300.0,
+    ap.add_argument("--diag-timeout", type=float, default=150.0,
                     help="multi-process: seconds allowed for the profiled iteration + sync A/B")
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--B", type=int, default=0, help="override the config's micro-batch size")
