@@ -229,7 +229,6 @@ __global__ void __launch_bounds__(192, 2)
       int g = 0;
       for (FwdSeq q = seq0; q.valid(); ++g) {
         const int n = q.n, j = q.j;
-        const bool last = j + 1 == q.nkb;
         FwdSeq nx = q;
         nx.advance();
         // S_g is in the softmax registers: compute the next scores now -- except at an item

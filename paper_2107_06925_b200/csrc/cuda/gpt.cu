@@ -592,7 +592,7 @@ EpiArgs on_chain(EpiArgs e, const Scratch& sc) {
 void Trainer::forward_task(int rank, int p, int mb, int s) {
   Impl& I = *d_;
   const ModelShape& m = I.m;
-  const int h = m.hidden, f = m.ffn, M = I.M, H = m.heads, r = rank / I.D;
+  const int h = m.hidden, M = I.M, r = rank / I.D;
   cudaStream_t st = I.stream_of(rank);
   Copy& cp = I.copies.at({rank, p});
   StageState& S = I.stages.at(s);
