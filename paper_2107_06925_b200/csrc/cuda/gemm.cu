@@ -984,17 +984,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
       }
       const int row0 = mb * 256 + int(cta) * 128 + q * 32;
       const uint32_t t0 = tmem_base + (uint32_t(q * 32) << 16) + acc * PBN;
-      // fix-up: the first producer's partial of this warp's next chunk is loaded a chunk
-      // ahead (L2 latency under the current chunk's epilogue, not on its critical path)
-      auto partial_of = [&](int pq, int c) {
-        return slot_of(pq) + size_t((q * 2 + half) * NC + (c - half * NC)) * 32 * 32;
-      };
-      float4 pf[8];
-      if (TO && itm.fixup) {
-        const float* pc = partial_of(q_lo, half * NC);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) pf[k] = *reinterpret_cast<const float4*>(pc + (k * 32 + lane) * 4);
-      }
 #pragma unroll 1
       for (int c = half * NC; c < half * NC + NC; ++c) {
         uint32_t r[32];
@@ -1015,26 +1004,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kPairEpiW
           }
           const uint32_t biasc = biasn;
           if (c + 1 < half * NC + NC) biasn = bias_prefetch(ep, col0 + 32, N, lane);
-          float4 cur[8];
-          if (itm.fixup) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) cur[k] = pf[k];
-            if (c + 1 < half * NC + NC) {
-              const float* pn = partial_of(q_lo, c + 1);
-#pragma unroll
-              for (int k = 0; k < 8; ++k) pf[k] = *reinterpret_cast<const float4*>(pn + (k * 32 + lane) * 4);
-            }
-          }
           ptx::tmem_ld_wait();
-          for (int pq = q_lo; pq < pair; ++pq) {  // stream-K fix-up: + the partial tiles
-            if (pq > q_lo) {  // (a tile spanning three or more pairs: the later producers' here)
-              const float* pc = partial_of(pq, c);
-#pragma unroll
-              for (int k = 0; k < 8; ++k) cur[k] = *reinterpret_cast<const float4*>(pc + (k * 32 + lane) * 4);
-            }
+          // stream-K fix-up: + the partial tiles (loads issued here, not a chunk ahead: the
+          // prefetch registers pushed the GELU'-epilogue instantiation into local-memory
+          // spills and cost it 30 % in the step, profiles/r02bq_launch_summary_cfg3_b2.txt)
+          for (int pq = q_lo; pq < pair; ++pq) {
+            const float* pc = slot_of(pq) + size_t((q * 2 + half) * NC + (c - half * NC)) * 32 * 32;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-              const float4 v = cur[k];
+              const float4 v = *reinterpret_cast<const float4*>(pc + (k * 32 + lane) * 4);
               r[4 * k] = __float_as_uint(__uint_as_float(r[4 * k]) + v.x);
               r[4 * k + 1] = __float_as_uint(__uint_as_float(r[4 * k + 1]) + v.y);
               r[4 * k + 2] = __float_as_uint(__uint_as_float(r[4 * k + 2]) + v.z);
