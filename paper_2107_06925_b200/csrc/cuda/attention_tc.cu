@@ -10,11 +10,13 @@
 //             into registers in one pass, which frees the S columns at once (s_free) so
 //             the MMA warp computes S_{j+1} underneath this tile's exp2s; P goes back to
 //             TMEM as bf16 pairs (tcgen05.st) for the PV MMA, running O is rescaled in
-//             TMEM only when a row max moves by more than 2^8; final O / l and the
-//             log-sum-exp go to HBM.
+//             TMEM only when a row max moves by more than 2^8; final O / l is staged
+//             in the item's consumed Q buffer and leaves by one TMA store (row tails:
+//             per-thread stores), the log-sum-exp per thread.
+// Persistent: (query tile, batch*head) items, heaviest first, dealt boustrophedon-wise.
 // The Q/K/V tiles come straight out of the packed [tokens, 3*H*64] QKV GEMM output via
 // one 2-D TMA map (no head split), so the kernel reads exactly Q, K, V once per tile.
-// ~80 KB smem and 256 TMEM columns per CTA: two CTAs per SM overlap one CTA's softmax
+// ~96 KB smem and 256 TMEM columns per CTA: two CTAs per SM overlap one CTA's softmax
 // with the other's MMAs.
 #include <cuda.h>
 
@@ -466,17 +468,18 @@ __global__ void __launch_bounds__(192, 2)
 //   S  = Q K^T, dP = dO V^T          (M128 q, N128 keys, K64)  TMEM [0,128), [128,256);
 //     issued as soon as the previous tile's S / dP sit in registers (st_free)
 //   P = exp2(S c - lse2), dS = P (dP - D) -> bf16, 128-byte-swizzled [q][key] smem tiles
-//     (each WG writes its own 64-key block)
+//     (each WG writes its own 64-key block); dS also -> TMEM [448,512) as bf16 pairs
 //   dV += P^T dO, dK += dS^T Q       (M128 keys, N64, K128 q)  TMEM [256,320), [320,384)
-//     -- P / dS read as MN-major A operands
-//   dQ_g = dS K                      (M128 q, N64, K128 keys)  TMEM [384 + 64 (g&1), ..)
-//     double-buffered so the MMA never waits for the drain
+//     -- P / dS read from smem as MN-major A operands
+//   dQ_g = dS K                      (M128 q, N64, K128 keys)  TMEM [384,448), A = dS
+//     from TMEM (kDsTmem; CK_ATTN_DS_TMEM=0: dS from smem, dQ double-buffered in
+//     [384 + 64 (g&1), ..)).  The tile's lse / D rows arrive with Q / dO (bulk copies).
 //   dQ_g is drained by a 4th warpgroup (warps 12-15, one per TMEM lane quarter) as soon
 //   as its MMA completes (dq_full), underneath the compute warpgroups' next tile:
 //   TMEM -> swizzled smem stage -> two TMA bulk tensor reduce-adds into the fp32 dQ
 //   accumulator (no per-thread atomics).  Draining it in the compute warps cost ~1.3 k
 //   of the ~3.6 k cycles per tile on their critical path.  setmaxnreg moves registers
-//   from the TMA/MMA and drain warpgroups (56) to the compute ones (200).
+//   from the TMA/MMA and drain warpgroups (64) to the compute ones (192).
 // Item epilogue: dK (x 1/sqrt(d)) / dV leave TMEM (acc_free lets the next item's MMAs
 // accumulate), are staged bf16 in the WG's P tile (free once the item's last MMAs are
 // done) and written by TMA stores.
@@ -489,7 +492,7 @@ constexpr int kB_BAR = 14 * kTileBytes;
 constexpr int kB_LSE = kB_BAR + 256;  // [2 stages][lse, D][128] fp32
 constexpr int kBwdSmem = kB_LSE + 2 * 2 * kQ * 4;
 constexpr int kBwdThreads = 512;  // WG0-1 compute, WG2 = TMA + MMA warps, WG3 dQ drain
-// Register split per SM sub-partition (one warp of each warpgroup): 2 x 200 + 56 + 56 = 512.
+// Register split per SM sub-partition (one warp of each warpgroup): 2 x 192 + 64 + 64 = 512.
 constexpr int kBwdRegsCompute = 192, kBwdRegsOther = 64;
 #ifndef CK_ATTN_BWD_POLY_EVERY  // backward: not MUFU-bound, the polynomial costs more than it saves
 #define CK_ATTN_BWD_POLY_EVERY 0
