@@ -437,6 +437,20 @@ def comm_report(world, msg_bytes):
     return rep or None
 
 
+def config_dict(shape, world):
+    """The `config` object of both arms' lines (same workload, same stage partition)."""
+    from paper_2107_06925_b200 import pipesim as P
+    cfg = P.PipelineConfig(**CFG)
+    n_logical = cfg.W * cfg.D
+    return {"workload": WORKLOAD,
+            "model": SHAPE_NAME, "global_batch": cfg.mini_batch(), "seq_len": shape.seq,
+            "stage_layers": list(shape.stage_layers) or None,
+            "parallelism": f"{cfg.scheme} D={cfg.D} W={cfg.W} f={cfg.f} {cfg.scaling}"
+                           f"{' +recompute' if cfg.scaling == 'forward-doubling' else ''}: "
+                           f"{n_logical} logical ranks on {world} GPU(s)",
+            "l2": "working set per step >> L2 (weights, grads, stashes ~40 GB)"}
+
+
 def run_reference(args, shape):
     """--impl reference: the reference path's CPU implementation (the numpy port of the
     reference Engine -- the reference itself has no transformer), all host threads, on
@@ -457,8 +471,7 @@ def run_reference(args, shape):
     line = {"metric": METRIC, "value": v, "unit": "seqs/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "model": SHAPE_NAME, "global_batch": CFG["B"] * CFG["N"] * CFG["W"],
-                       "seq_len": shape.seq},
+            "config": config_dict(shape, args.gpus),
             "cpu_baseline": {"value": v, "unit": "seqs/s", "cores": threads_used(), "kind": "port",
                              "cpu_model": cpu_model(),
                              "sample": f"numpy fp64 port of the reference Engine, one sequence per step through one "
@@ -492,7 +505,7 @@ def main():
 
     from paper_2107_06925_b200.gpt import PRESETS
     shape = PRESETS[SHAPE_NAME]
-    if args.impl != "reference" and args.partition == "balanced":
+    if args.partition == "balanced":  # both arms: the reference port times the same stages
         import dataclasses
         from paper_2107_06925_b200 import pipesim as P
         from paper_2107_06925_b200.gpt import balanced_partition
@@ -589,13 +602,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic tokens (uniform, next-token labels), random-init weights N(0,0.02)",
-        "config": {"workload": WORKLOAD,
-                   "model": SHAPE_NAME, "global_batch": n_seq, "seq_len": shape.seq,
-                   "stage_layers": list(shape.stage_layers) or None,
-                   "parallelism": f"{cfg.scheme} D={cfg.D} W={cfg.W} f={cfg.f} {cfg.scaling}"
-                                  f"{' +recompute' if cfg.scaling == 'forward-doubling' else ''}: "
-                                  f"{n_logical} logical ranks on {world} GPU(s)",
-                   "l2": "working set per step >> L2 (weights, grads, stashes ~40 GB)"},
+        "config": config_dict(shape, world),
         "e2e": {"value": round(n_seq / (e2e_ms * 1e-3), 2), "unit": "seqs/s",
                 "h2d_bytes_per_step": int(tok.nbytes + lab.nbytes), "d2h_bytes_per_step": 4},
     }
