@@ -80,3 +80,19 @@ def test_balanced_partition_prefers_short_head_stage():
     m = O.Shape(n_layer=4, hidden=128, heads=2, ffn=256, seq=16, vocab=50, vocab_padded=64, causal=True,
                 stage_layers=(2, 1, 1, 0 + 0) if False else (1, 1, 1, 1))
     assert O.stage_layout(m, 4, 3)[0][-1][0] == "lm_head"
+
+
+def test_balanced_partition_measured_head_cost():
+    """The LM head counted at its measured cost (gpt.HEAD_EFFICIENCY) moves a layer to the
+    head stage on GPT-2 medium D=4 (measured bubble 0.252 vs the reference's
+    0.253); counted at its FLOP ratio the old (7, 7, 7, 3) split comes back."""
+    from paper_2107_06925_b200.gpt import HEAD_EFFICIENCY, PRESETS, balanced_partition
+    cfg = P.PipelineConfig("chimera", 4, 1, 4, 4, 1)
+    assert 0.5 < HEAD_EFFICIENCY < 1.0
+    assert balanced_partition(PRESETS["gpt2-medium"], cfg) == (7, 6, 7, 4)
+    assert balanced_partition(PRESETS["gpt2-medium"], cfg, 1.0) == (7, 7, 7, 3)
+    for name in ("gpt2-medium", "gpt2-1.3b", "bert48"):
+        sh = PRESETS[name]
+        for D in (4, 8):
+            part = balanced_partition(sh, P.PipelineConfig("chimera", D, 1, 2 * D, 1, 1))
+            assert sum(part) == sh.n_layer and min(part) >= 1
