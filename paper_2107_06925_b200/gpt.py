@@ -243,7 +243,10 @@ class Trainer:
         return self.end_iteration()
 
     def profile_step(self) -> dict:
-        """One eager iteration with per-task GPU timestamps (see measured_bubble)."""
+        """One iteration with per-task GPU timestamps and message-wait brackets (see
+        measured_bubble): captured and replayed as a CUDA graph in a single-process
+        trainer once a graph exists (the GPU, not the host, paces the tasks), issued
+        eagerly when the trainer spans processes."""
         return json.loads(call_str(lib().ck_gpt_profile_step, self._h))
 
     def launch(self):
